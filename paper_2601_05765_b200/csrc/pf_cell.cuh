@@ -1,0 +1,1373 @@
+// pf_cell.cuh -- warp-per-cell construction + analytic evaluation of one
+// generalized Laguerre cell (power cell of site i restricted to the ball
+// B(p_i, sqrt(psi_i))).
+//
+// One warp owns one cell.  The convex polytope lives in shared memory in the
+// reference's primal packed layout (vertices, facet planes, tags, CCW vertex
+// loops; _kernels.py:10-18) so that every vertex is produced by the same
+// arithmetic as the reference clip (_kernels.py:188-191) and every
+// tolerance-deciding predicate sees the same bits.  Compiled with
+// --fmad=false, the build phase and all predicates are bit-identical to the
+// reference; only the transcendentals (atan2/sin/cos) differ in the last ulp.
+//
+// Work distribution inside the warp:
+//   * candidate gather  : lanes stride over the flattened z-runs of the grid
+//                         buckets that can hold a site within the stop radius
+//   * candidate order   : rank sort on the key (d^2, j) (_kernels.py:1293-1304)
+//   * clip (A7)         : lane per vertex (classify / keep, ballot-prefix
+//                         compaction), lane per facet (walk, crossing entries),
+//                         lane per crossing entry (dedup + new vertex), lane per
+//                         new-facet vertex (atan2 angle + rank sort)
+//   * evaluate (A9-A13) : lane per facet (restriction walk, generalized polygon
+//                         integrals, ray for the interior point, Gauss-Bonnet
+//                         patch area); order-dependent sums are done by every
+//                         lane redundantly over shared memory in the
+//                         reference's facet order, so results are deterministic
+//                         and independent of scheduling.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "pf_warp.cuh"
+
+namespace pf {
+
+// _kernels.py:29-50
+enum { CLIP_CUT = 0, CLIP_UNTOUCHED = 1, CLIP_EMPTY = 2, CLIP_OVERFLOW = 3, CLIP_DEGENERATE = 4 };
+enum { RF_OUTSIDE = 0, RF_UNTOUCHED = 1, RF_FULLCIRCLE = 2, RF_GENPOLY = 3 };
+enum { CELL_EMPTY = 0, CELL_FULLBALL = 1, CELL_CLIPPED = 2 };
+enum { FLAG_OVERFLOW = 1, FLAG_DEGENERATE_INTERIOR = 2, FLAG_UNSTABLE_PROJECTION = 4 };
+// internal: a capacity of this (small, shared-memory) instantiation was
+// exceeded; the cell is queued for the reference-capacity instantiation.
+enum { FLAG_RETRY = 256 };
+
+#define PF_PI 3.141592653589793
+#define PF_FOUR_PI (4.0 * PF_PI)
+
+// reference capacities (_kernels.py:24-27)
+enum { REF_MAX_V = 512, REF_MAX_F = 160, REF_MAX_L = 2048, REF_MAX_P = 256 };
+
+// Capacity set of one instantiation.  EXACT=true means the reference's own
+// capacities: overflow then reproduces the reference's CLIP_OVERFLOW outcome.
+template <int CV_, int CF_, int CL_, int CC_, int CE_, int CP_, bool EXACT_>
+struct Caps {
+    static constexpr int CV = CV_;  // vertices
+    static constexpr int CF = CF_;  // facets
+    static constexpr int CL = CL_;  // loop entries
+    static constexpr int CC = CC_;  // candidates per shell
+    static constexpr int CE = CE_;  // crossing entries per clip
+    static constexpr int CP = CP_;  // restricted boundary points per cell
+    static constexpr bool EXACT = EXACT_;
+};
+
+template <class C>
+struct Poly {
+    double x[C::CV], y[C::CV], z[C::CV];
+    double nx[C::CF], ny[C::CF], nz[C::CF], d[C::CF];
+    int tag[C::CF];
+    uint16_t lp[C::CF + 1];
+    uint16_t lv[C::CL];
+    int nv, nf, nl;
+};
+
+template <class C>
+struct BuildScratch {
+    double sd[C::CV];          // signed distances, reused for new-facet angles
+    uint16_t vmap[C::CV];      // kept index / referenced map
+    uint16_t onl[C::CV];       // new-facet vertex list (B indices, increasing)
+    uint16_t fk[C::CF];        // emitted loop length per facet
+    uint16_t fcb[C::CF];       // crossing-entry base per facet
+    uint16_t flb[C::CF];       // output loop base per facet (0xffff = dropped)
+    uint16_t fout[C::CF];      // output facet index
+    uint16_t ea[C::CE], eb[C::CE], eid[C::CE];  // crossing entries (walk order)
+    uint16_t emt[C::CE];       // first-occurrence entry of the same edge
+    double cd2[C::CC];         // candidates (d^2, j)
+    int cj[C::CC];
+    int ncand;
+    int run_start[32], run_off[32];
+};
+
+template <class C>
+struct EvalScratch {
+    double fh[C::CF], frc[C::CF], farea[C::CF], fcx[C::CF], fcy[C::CF], fcz[C::CF], fip[C::CF];
+    double fpa[C::CF];                 // projected (occluded) patch area
+    double smx[C::CF], smy[C::CF], smz[C::CF], smg[C::CF];  // interior-point ray midpoints
+    int16_t fhead[C::CF], fnp[C::CF];
+    uint8_t fkind[C::CF], fseg[C::CF], funs[C::CF];
+    uint8_t vin[C::CV];
+    double ppx[C::CP], ppy[C::CP], ppz[C::CP], pth[C::CP];
+    int16_t pnext[C::CP];
+    uint8_t pfl[C::CP];  // bit0 on_sph, bit1 conn (arc to next), bit2 deleted
+    int npool;
+};
+
+template <class C>
+struct WS {
+    Poly<C> P[2];
+    union {
+        BuildScratch<C> b;
+        EvalScratch<C> e;
+    } u;
+    int oflow;  // capacity overflow seen by any lane
+};
+
+// ---------------------------------------------------------------------------
+// inputs / outputs of the cell kernels
+// ---------------------------------------------------------------------------
+struct GridView {
+    const double *sx, *sy, *sz;  // sites in bucket order (SoA)
+    const int *sid;              // original index of sorted slot
+    const int *bstart;           // [ncell + 1]
+    double lo[3], ih[3];
+    int gn[3];
+};
+
+struct CellIn {
+    const double *pts;  // [n, 3] original order
+    const double *psi;  // [n]
+    int n;
+    GridView g;
+    // domain pack (reference layout, int32 indices)
+    const double *dv;
+    const double *dp;
+    const int *dt, *dlp, *dlv;
+    int dnv, dnf, dnl;
+    double tol, dpsi;
+    int ball_aware, want_m2;
+    double t_init;  // first shell radius^2 when not ball-aware
+};
+
+struct CellOut {
+    // fixed-stride reference outputs (any pointer may be null)
+    int64_t *status;
+    double *vol, *ksur, *cent, *ipt, *m2;
+    int64_t *fcount, *ftag;
+    double *farea, *fh, *fnrm, *fcent;
+    int smf;
+    // lean outputs for the Newton solver (may be null)
+    int *ftag32;    // [n, smf]
+    int *fcount32;  // [n]
+    int *flags;     // [n] per-cell flag word (incl. FLAG_RETRY)
+    int *census;    // [n] processed candidates (clips attempted)
+};
+
+PF_DEV double sq(double x) { return x * x; }
+
+// _kernels.py:59-80
+PF_DEV void perp_basis(double nx, double ny, double nz, double *e) {
+    double ax = fabs(nx), ay = fabs(ny), az = fabs(nz);
+    double ux, uy, uz;
+    if (ax <= ay && ax <= az) { ux = 1.0; uy = 0.0; uz = 0.0; }
+    else if (ay <= az) { ux = 0.0; uy = 1.0; uz = 0.0; }
+    else { ux = 0.0; uy = 0.0; uz = 1.0; }
+    double e1x = uy * nz - uz * ny;
+    double e1y = uz * nx - ux * nz;
+    double e1z = ux * ny - uy * nx;
+    double inv = 1.0 / sqrt(e1x * e1x + e1y * e1y + e1z * e1z);
+    e1x *= inv; e1y *= inv; e1z *= inv;
+    e[0] = e1x; e[1] = e1y; e[2] = e1z;
+    e[3] = ny * e1z - nz * e1y;
+    e[4] = nz * e1x - nx * e1z;
+    e[5] = nx * e1y - ny * e1x;
+}
+
+template <class C>
+PF_DEV void load_domain(Poly<C> &A, const CellIn &in) {
+    const int L = pfw::lane();
+    for (int v = L; v < in.dnv; v += 32) {
+        A.x[v] = in.dv[3 * v]; A.y[v] = in.dv[3 * v + 1]; A.z[v] = in.dv[3 * v + 2];
+    }
+    for (int f = L; f < in.dnf; f += 32) {
+        A.nx[f] = in.dp[4 * f]; A.ny[f] = in.dp[4 * f + 1]; A.nz[f] = in.dp[4 * f + 2];
+        A.d[f] = in.dp[4 * f + 3];
+        A.tag[f] = in.dt[f];
+    }
+    for (int f = L; f <= in.dnf; f += 32) A.lp[f] = (uint16_t)in.dlp[f];
+    for (int k = L; k < in.dnl; k += 32) A.lv[k] = (uint16_t)in.dlv[k];
+    if (L == 0) { A.nv = in.dnv; A.nf = in.dnf; A.nl = in.dnl; }
+    pfw::sync();
+}
+
+// max_v |v - p| (the running "rfar" of _kernels.py:1230-1237, 1341-1354)
+template <class C>
+PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
+    double m = 0.0;
+    for (int v = pfw::lane(); v < A.nv; v += 32) {
+        double d2 = sq(A.x[v] - px) + sq(A.y[v] - py) + sq(A.z[v] - pz);
+        if (d2 > m) m = d2;
+    }
+    return sqrt(pfw::max_d(m));
+}
+
+// ---------------------------------------------------------------------------
+// clip A by n.x <= dd into B (_kernels.py:109-319), warp-cooperative
+// ---------------------------------------------------------------------------
+template <class C>
+PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, double nz,
+                double dd, int tag, double tol) {
+    BuildScratch<C> &S = ws->u.b;
+    const int L = pfw::lane();
+    const unsigned lt = pfw::lanemask_lt();
+    const int nv = A.nv, nf = A.nf;
+
+    // 1. classify vertices (_kernels.py:121-134)
+    int n_out = 0;
+    for (int v0 = 0; v0 < nv; v0 += 32) {
+        int v = v0 + L;
+        bool out = false;
+        if (v < nv) {
+            double s = nx * A.x[v] + ny * A.y[v] + nz * A.z[v] - dd;
+            S.sd[v] = s;
+            out = s > tol;
+        }
+        n_out += pfw::popc(pfw::ballot(out));
+    }
+    if (n_out == 0) return CLIP_UNTOUCHED;
+    if (nv - n_out == 0) return CLIP_EMPTY;
+    pfw::sync();
+
+    // 2. keep inside vertices in order (_kernels.py:137-147)
+    int K = 0;
+    for (int v0 = 0; v0 < nv; v0 += 32) {
+        int v = v0 + L;
+        bool keep = v < nv && S.sd[v] <= tol;
+        unsigned m = pfw::ballot(keep);
+        if (keep) {
+            int idx = K + pfw::popc(m & lt);
+            S.vmap[v] = (uint16_t)idx;
+            B.x[idx] = A.x[v]; B.y[idx] = A.y[v]; B.z[idx] = A.z[v];
+        } else if (v < nv) {
+            S.vmap[v] = 0xffff;
+        }
+        K += pfw::popc(m);
+    }
+
+    // 3a. per facet: emitted loop length and crossing-edge count (_kernels.py:160-228)
+    for (int f = L; f < nf; f += 32) {
+        int start = A.lp[f], m = A.lp[f + 1] - start;
+        int k = 0, c = 0;
+        for (int e = 0; e < m; e++) {
+            int a = A.lv[start + e];
+            int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
+            double sa = S.sd[a], sb = S.sd[b];
+            bool ina = sa <= tol, inb = sb <= tol;
+            if (ina) {
+                k++;
+                if (!inb && sa < -tol) c++;
+            } else if (inb && sb < -tol) {
+                c++;
+            }
+        }
+        S.fk[f] = (uint16_t)(k + c);
+        S.fcb[f] = (uint16_t)c;
+    }
+    pfw::sync();
+    // 3b. prefix sums in facet order: crossing bases, kept-facet loop bases
+    int NE = 0, NFk = 0, NLk = 0;
+    for (int f0 = 0; f0 < nf; f0 += 32) {
+        int f = f0 + L;
+        int c = 0, kk = 0, keep = 0;
+        if (f < nf) {
+            c = S.fcb[f];
+            kk = S.fk[f];
+            keep = kk >= 3;
+        }
+        int tc, tk, tl;
+        int oc = pfw::excl_scan_i(c, &tc);
+        int ok = pfw::excl_scan_i(keep, &tk);
+        int ol = pfw::excl_scan_i(keep ? kk : 0, &tl);
+        if (f < nf) {
+            S.fcb[f] = (uint16_t)(NE + oc);
+            S.fout[f] = (uint16_t)(NFk + ok);
+            S.flb[f] = keep ? (uint16_t)(NLk + ol) : (uint16_t)0xffff;
+        }
+        NE += tc; NFk += tk; NLk += tl;
+    }
+    if (NE > C::CE) { if (L == 0) ws->oflow = 1; pfw::sync(); return CLIP_OVERFLOW; }
+    pfw::sync();
+    // 3c. crossing entries in walk order
+    for (int f = L; f < nf; f += 32) {
+        int start = A.lp[f], m = A.lp[f + 1] - start;
+        int pos = S.fcb[f];
+        for (int e = 0; e < m; e++) {
+            int a = A.lv[start + e];
+            int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
+            double sa = S.sd[a], sb = S.sd[b];
+            bool ina = sa <= tol, inb = sb <= tol;
+            bool cr = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
+            if (cr) { S.ea[pos] = (uint16_t)a; S.eb[pos] = (uint16_t)b; pos++; }
+        }
+    }
+    pfw::sync();
+    // 3d. first encounter of each edge creates the crossing vertex (_kernels.py:178-200)
+    int NFirst = 0;
+    for (int q0 = 0; q0 < NE; q0 += 32) {
+        int q = q0 + L;
+        bool first = false;
+        int mt = q;
+        if (q < NE) {
+            int a = S.ea[q], b = S.eb[q];
+            int lo = a < b ? a : b, hi = a < b ? b : a;
+            for (int r = 0; r < q; r++) {
+                int ra = S.ea[r], rb = S.eb[r];
+                int rlo = ra < rb ? ra : rb, rhi = ra < rb ? rb : ra;
+                if (rlo == lo && rhi == hi) { mt = r; break; }
+            }
+            first = mt == q;
+            S.emt[q] = (uint16_t)mt;
+        }
+        unsigned m = pfw::ballot(first);
+        if (first) {
+            int id = K + NFirst + pfw::popc(m & lt);
+            S.eid[q] = (uint16_t)id;
+            if (id < C::CV) {
+                int a = S.ea[q], b = S.eb[q];
+                double sa = S.sd[a], sb = S.sd[b];
+                double t = sa / (sa - sb);
+                B.x[id] = A.x[a] + t * (A.x[b] - A.x[a]);
+                B.y[id] = A.y[a] + t * (A.y[b] - A.y[a]);
+                B.z[id] = A.z[a] + t * (A.z[b] - A.z[a]);
+            }
+        }
+        NFirst += pfw::popc(m);
+    }
+    const int NVB = K + NFirst;
+    if (NVB > C::CV || NFk > C::CF || NLk > C::CL) {
+        if (!C::EXACT && L == 0) ws->oflow = 1;
+        pfw::sync();
+        return CLIP_OVERFLOW;
+    }
+    pfw::sync();
+    for (int q = L; q < NE; q += 32) {
+        int mt = S.emt[q];
+        if (mt != q) S.eid[q] = S.eid[mt];
+    }
+    pfw::sync();
+    // 3e. emit kept facets (_kernels.py:229-241)
+    for (int f = L; f < nf; f += 32) {
+        int lb = S.flb[f];
+        if (lb == 0xffff) continue;
+        int o = S.fout[f];
+        B.nx[o] = A.nx[f]; B.ny[o] = A.ny[f]; B.nz[o] = A.nz[f]; B.d[o] = A.d[f];
+        B.tag[o] = A.tag[f];
+        B.lp[o] = (uint16_t)lb;
+        B.lp[o + 1] = (uint16_t)(lb + S.fk[f]);
+        int start = A.lp[f], m = A.lp[f + 1] - start;
+        int pos = S.fcb[f], w = lb;
+        for (int e = 0; e < m; e++) {
+            int a = A.lv[start + e];
+            int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
+            double sa = S.sd[a], sb = S.sd[b];
+            bool ina = sa <= tol, inb = sb <= tol;
+            if (ina) B.lv[w++] = S.vmap[a];
+            bool cr = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
+            if (cr) B.lv[w++] = S.eid[pos++];
+        }
+    }
+    // 4. new facet (_kernels.py:243-295).  on_new = kept on-plane vertices
+    // (sa >= -tol when emitted, i.e. every kept vertex with sd >= -tol) and
+    // all crossing vertices, in B index order.
+    int ncp = 0;
+    for (int v0 = 0; v0 < nv; v0 += 32) {
+        int v = v0 + L;
+        bool on = v < nv && S.sd[v] <= tol && S.sd[v] >= -tol;
+        unsigned m = pfw::ballot(on);
+        if (on) S.onl[ncp + pfw::popc(m & lt)] = S.vmap[v];
+        ncp += pfw::popc(m);
+    }
+    for (int q = L; q < NFirst; q += 32) S.onl[ncp + q] = (uint16_t)(K + q);
+    ncp += NFirst;
+    if (ncp < 3) { pfw::sync(); return CLIP_DEGENERATE; }
+    if (NFk + 1 > C::CF || NLk + ncp > C::CL) {
+        if (!C::EXACT && L == 0) ws->oflow = 1;
+        pfw::sync();
+        return CLIP_OVERFLOW;
+    }
+    pfw::sync();
+    // centroid: sequential sum in index order, computed redundantly by every lane
+    double ccx = 0.0, ccy = 0.0, ccz = 0.0;
+    for (int q = 0; q < ncp; q++) {
+        int v = S.onl[q];
+        ccx += B.x[v]; ccy += B.y[v]; ccz += B.z[v];
+    }
+    ccx /= (double)ncp; ccy /= (double)ncp; ccz /= (double)ncp;
+    double e[6];
+    perp_basis(nx, ny, nz, e);
+    for (int q = L; q < ncp; q += 32) {
+        int v = S.onl[q];
+        double rx = B.x[v] - ccx, ry = B.y[v] - ccy, rz = B.z[v] - ccz;
+        S.sd[q] = atan2(rx * e[3] + ry * e[4] + rz * e[5], rx * e[0] + ry * e[1] + rz * e[2]);
+    }
+    pfw::sync();
+    // rank sort by (angle, index): the reference's insertion sort is stable on a total order
+    for (int q = L; q < ncp; q += 32) {
+        double aq = S.sd[q];
+        int vq = S.onl[q];
+        int r = 0;
+        for (int u = 0; u < ncp; u++) {
+            double au = S.sd[u];
+            int vu = S.onl[u];
+            r += (au < aq || (au == aq && vu < vq)) ? 1 : 0;
+        }
+        B.lv[NLk + r] = (uint16_t)vq;
+    }
+    if (L == 0) {
+        B.nx[NFk] = nx; B.ny[NFk] = ny; B.nz[NFk] = nz; B.d[NFk] = dd;
+        B.tag[NFk] = tag;
+        B.lp[NFk] = (uint16_t)NLk;
+        B.lp[NFk + 1] = (uint16_t)(NLk + ncp);
+    }
+    const int NF2 = NFk + 1, NL2 = NLk + ncp;
+    pfw::sync();
+    // 5. drop unreferenced vertices (_kernels.py:297-315)
+    for (int v = L; v < NVB; v += 32) S.vmap[v] = 0;
+    pfw::sync();
+    for (int k = L; k < NL2; k += 32) S.vmap[B.lv[k]] = 1;
+    pfw::sync();
+    int nref = 0;
+    for (int v0 = 0; v0 < NVB; v0 += 32) {
+        int v = v0 + L;
+        nref += pfw::popc(pfw::ballot(v < NVB && S.vmap[v] == 1));
+    }
+    if (nref != NVB) {
+        int base = 0;
+        for (int v0 = 0; v0 < NVB; v0 += 32) {
+            int v = v0 + L;
+            bool r = v < NVB && S.vmap[v] == 1;
+            unsigned m = pfw::ballot(r);
+            double x = 0, y = 0, z = 0;
+            int dst = base + pfw::popc(m & lt);
+            if (r) { x = B.x[v]; y = B.y[v]; z = B.z[v]; }
+            pfw::sync();
+            if (r) { B.x[dst] = x; B.y[dst] = y; B.z[dst] = z; S.vmap[v] = (uint16_t)(dst + 2); }
+            base += pfw::popc(m);
+            pfw::sync();
+        }
+        for (int k = L; k < NL2; k += 32) B.lv[k] = (uint16_t)(S.vmap[B.lv[k]] - 2);
+        nref = base;
+    }
+    if (L == 0) { B.nv = nref; B.nf = NF2; B.nl = NL2; }
+    pfw::sync();
+    return CLIP_CUT;
+}
+
+// ---------------------------------------------------------------------------
+// candidate gather over one distance shell [t_lo, t_hi) of d^2
+// ---------------------------------------------------------------------------
+PF_DEV int bucket_coord(double x, double lo, double ih, int gn) {
+    double t = (x - lo) * ih;
+    int b;
+    if (!(t > -1.0)) b = 0;  // also catches NaN
+    else if (t >= (double)gn) b = gn - 1;
+    else b = (int)t;
+    if (b < 0) b = 0;
+    if (b >= gn) b = gn - 1;
+    return b;
+}
+
+// returns the number of candidates (may exceed CC: overflow); *all_sites set
+// when the bucket range spans the whole grid
+template <class C>
+PF_DEV int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, double py, double pz,
+                        double t_lo, double t_hi, bool *all_sites) {
+    BuildScratch<C> &S = ws->u.b;
+    const GridView &g = in.g;
+    const int L = pfw::lane();
+    double r = sqrt(t_hi) * (1.0 + 1e-9) + 1e-300;
+    int i0 = bucket_coord(px - r, g.lo[0], g.ih[0], g.gn[0]);
+    int i1 = bucket_coord(px + r, g.lo[0], g.ih[0], g.gn[0]);
+    int j0 = bucket_coord(py - r, g.lo[1], g.ih[1], g.gn[1]);
+    int j1 = bucket_coord(py + r, g.lo[1], g.ih[1], g.gn[1]);
+    int k0 = bucket_coord(pz - r, g.lo[2], g.ih[2], g.gn[2]);
+    int k1 = bucket_coord(pz + r, g.lo[2], g.ih[2], g.gn[2]);
+    *all_sites = i0 == 0 && j0 == 0 && k0 == 0 && i1 == g.gn[0] - 1 && j1 == g.gn[1] - 1 &&
+                 k1 == g.gn[2] - 1;
+    const int ny = j1 - j0 + 1;
+    const int nruns = (i1 - i0 + 1) * ny;
+    if (L == 0) S.ncand = 0;
+    pfw::sync();
+    bool beyond = false;
+    for (int r0 = 0; r0 < nruns; r0 += 32) {
+        int rr = r0 + L;
+        int st = 0, len = 0;
+        if (rr < nruns) {
+            int ix = i0 + rr / ny, iy = j0 + rr % ny;
+            int lin0 = (ix * g.gn[1] + iy) * g.gn[2] + k0;
+            int lin1 = (ix * g.gn[1] + iy) * g.gn[2] + k1;
+            st = g.bstart[lin0];
+            len = g.bstart[lin1 + 1] - st;
+        }
+        int tot;
+        int off = pfw::excl_scan_i(len, &tot);
+        S.run_start[L] = st;
+        S.run_off[L] = off;
+        pfw::sync();
+        int nr = nruns - r0 < 32 ? nruns - r0 : 32;
+        for (int q0 = 0; q0 < tot; q0 += 32) {
+            int q = q0 + L;
+            if (q < tot) {
+                // last run whose offset <= q
+                int lo = 0, hi = nr - 1;
+                while (lo < hi) {
+                    int mid = (lo + hi + 1) >> 1;
+                    if (S.run_off[mid] <= q) lo = mid; else hi = mid - 1;
+                }
+                int s = S.run_start[lo] + (q - S.run_off[lo]);
+                int j = g.sid[s];
+                double d2 = sq(g.sx[s] - px) + sq(g.sy[s] - py) + sq(g.sz[s] - pz);
+                if (j != self && !(d2 < t_hi)) beyond = true;
+                if (j != self && d2 >= t_lo && d2 < t_hi) {
+                    int pos = pfw::atom_add(&S.ncand, 1);
+                    if (pos < C::CC) { S.cd2[pos] = d2; S.cj[pos] = j; }
+                }
+            }
+        }
+        pfw::sync();
+    }
+    if (pfw::any(beyond)) *all_sites = false;
+    int nc = S.ncand;
+    pfw::sync();
+    return nc;
+}
+
+// sort the shell's candidates by (d2, j) in place (rank sort through registers)
+template <class C>
+PF_DEV void sort_candidates(WS<C> *ws, int nc) {
+    BuildScratch<C> &S = ws->u.b;
+    const int L = pfw::lane();
+    constexpr int PER = (C::CC + 31) / 32;
+    double kd[PER];
+    int kj[PER], kr[PER];
+#pragma unroll
+    for (int t = 0; t < PER; t++) {
+        int q = t * 32 + L;
+        kr[t] = -1;
+        if (q < nc) {
+            kd[t] = S.cd2[q];
+            kj[t] = S.cj[q];
+            int r = 0;
+            for (int u = 0; u < nc; u++) {
+                double du = S.cd2[u];
+                int ju = S.cj[u];
+                r += (du < kd[t] || (du == kd[t] && ju < kj[t])) ? 1 : 0;
+            }
+            kr[t] = r;
+        }
+    }
+    pfw::sync();
+#pragma unroll
+    for (int t = 0; t < PER; t++) {
+        if (kr[t] >= 0) { S.cd2[kr[t]] = kd[t]; S.cj[kr[t]] = kj[t]; }
+    }
+    pfw::sync();
+}
+
+// ---------------------------------------------------------------------------
+// build the Laguerre cell of site i (_kernels.py:1197-1355)
+// returns 0 ok / 1 empty / 3 overflow; *which = buffer holding the cell
+// ---------------------------------------------------------------------------
+template <class C>
+PF_DEV int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int *nclips) {
+    const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
+    const double psii = in.psi[i];
+    const double tol = in.tol, dpsi = in.dpsi;
+    load_domain(ws->P[0], in);
+    int which = 0;
+    *nclips = 0;
+    double rfar = poly_rfar(ws->P[0], px, py, pz);
+    const double sq_ball = (in.ball_aware && psii > 0.0) ? sqrt(psii) : -1.0;
+    const double sq_psi_slack = sqrt((psii > 0.0 ? psii : 0.0) + dpsi);
+    if (in.ball_aware && psii <= 0.0) { *which_out = 0; return 0; }
+    const double br = sq_ball + sq_psi_slack;
+
+    double t_lo = -1.0;
+    double t_hi = in.ball_aware ? br * br * (1.0 + 1e-14) : in.t_init;
+    if (!(t_hi > 0.0)) t_hi = 1e-300;
+    for (;;) {
+        bool all_sites = false;
+        int nc = gather_shell(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites);
+        if (nc > C::CC) {
+            // too many candidates in this shell: narrow it (ties at one d^2
+            // cannot be split -> overflow)
+            double base = t_lo > 0.0 ? t_lo : 0.0;
+            double nt = base + (t_hi - base) * 0.25;
+            if (!(nt > base) || !(nt < t_hi)) {
+                if (pfw::lane() == 0) ws->oflow = 1;
+                pfw::sync();
+                *which_out = which;
+                return 3;
+            }
+            t_hi = nt;
+            continue;
+        }
+        sort_candidates(ws, nc);
+        for (int c = 0; c < nc; c++) {
+            double stop_r = rfar + sqrt(rfar * rfar + dpsi);
+            if (in.ball_aware && br < stop_r) stop_r = br;
+            const double D2 = ws->u.b.cd2[c];
+            const int j = ws->u.b.cj[c];
+            if (sqrt(D2) >= stop_r) { *which_out = which; return 0; }
+            const double pjx = in.pts[3 * j], pjy = in.pts[3 * j + 1], pjz = in.pts[3 * j + 2];
+            const double psij = in.psi[j];
+            if (D2 <= tol * tol) {
+                if (psij > psii || (psij == psii && j < i)) { *which_out = which; return 1; }
+                continue;
+            }
+            (*nclips)++;
+            const double D = sqrt(D2);
+            const double nxp = (pjx - px) / D;
+            const double nyp = (pjy - py) / D;
+            const double nzp = (pjz - pz) / D;
+            const double hij = 0.5 * (D2 + psii - psij) / D;
+            const double dd = (nxp * px + nyp * py + nzp * pz) + hij;
+            int st = clip(ws, ws->P[which], ws->P[1 - which], nxp, nyp, nzp, dd, j, tol);
+            if (st == CLIP_EMPTY) { *which_out = which; return 1; }
+            if (st == CLIP_OVERFLOW) { *which_out = which; return 3; }
+            if (st == CLIP_CUT) {
+                which = 1 - which;
+                rfar = poly_rfar(ws->P[which], px, py, pz);
+            }
+        }
+        if (all_sites) break;
+        double stop_r = rfar + sqrt(rfar * rfar + dpsi);
+        if (in.ball_aware && br < stop_r) stop_r = br;
+        if (sqrt(t_hi) >= stop_r) break;
+        t_lo = t_hi;
+        t_hi = t_hi * 4.0;
+    }
+    *which_out = which;
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// evaluation (_kernels.py:411-1170)
+// ---------------------------------------------------------------------------
+enum { PF_ONSPH = 1, PF_CONN = 2, PF_DEL = 4 };
+
+// Restrict facet f to the ball and emit its boundary sequence into the pool
+// (_kernels.py:411-675).  Executed by one lane.  Returns the kind, -1 on
+// MAX_P overflow, -2 on pool overflow.
+template <class C>
+PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double py, double pz,
+                          double psi, double tol, double *s_out, double *rc_out, int *head_out,
+                          int *np_out) {
+    EvalScratch<C> &E = ws->u.e;
+    const int nf = P.nf;
+    const double nx = P.nx[f], ny = P.ny[f], nz = P.nz[f], dd = P.d[f];
+    const double s = dd - (nx * px + ny * py + nz * pz);
+    const double rc2 = psi - s * s;
+    const double R = sqrt(psi);
+    *s_out = s; *rc_out = 0.0; *head_out = -1; *np_out = 0;
+    if (rc2 <= tol * (2.0 * R + tol)) return RF_OUTSIDE;
+    const double rc = sqrt(rc2);
+    *rc_out = rc;
+    const double qx = px + s * nx, qy = py + s * ny, qz = pz + s * nz;
+    const int start = P.lp[f], m = P.lp[f + 1] - start;
+    int n_in = 0;
+    for (int e = 0; e < m; e++) n_in += E.vin[P.lv[start + e]];
+
+    int head = -1, prev = -1, npts = 0;
+#define PF_EMIT(X, Y, Z, FL)                                        \
+    do {                                                            \
+        int _id = pfw::atom_add(&E.npool, 1);                       \
+        if (_id >= C::CP) return -2;                                \
+        E.ppx[_id] = (X); E.ppy[_id] = (Y); E.ppz[_id] = (Z);       \
+        E.pfl[_id] = (uint8_t)(FL);                                 \
+        E.pnext[_id] = -1;                                          \
+        if (prev >= 0) E.pnext[prev] = (int16_t)_id; else head = _id; \
+        prev = _id;                                                 \
+        npts++;                                                     \
+    } while (0)
+
+    if (n_in == m) {
+        for (int e = 0; e < m; e++) {
+            int v = P.lv[start + e];
+            PF_EMIT(P.x[v], P.y[v], P.z[v], 0);
+        }
+        E.pnext[prev] = (int16_t)head;
+        *head_out = head; *np_out = npts;
+        return RF_UNTOUCHED;
+    }
+    bool first_entry = false;
+    bool cur_inside = E.vin[P.lv[start]] != 0;
+    for (int e = 0; e < m; e++) {
+        const int a = P.lv[start + e];
+        const int bb = P.lv[start + (e + 1 == m ? 0 : e + 1)];
+        const bool ina = E.vin[a] != 0;
+        const bool inb = E.vin[bb] != 0;
+        if (ina) {
+            if (npts >= REF_MAX_P) return -1;
+            PF_EMIT(P.x[a], P.y[a], P.z[a], 0);
+            cur_inside = true;
+        }
+        if (ina && inb) continue;
+        // _edge_other_facet (_kernels.py:397-408): facet holding edge (bb -> a)
+        int g = -1;
+        for (int gg = 0; gg < nf && g < 0; gg++) {
+            if (gg == f) continue;
+            int s0 = P.lp[gg], mg = P.lp[gg + 1] - s0;
+            for (int ee = 0; ee < mg; ee++) {
+                if (P.lv[s0 + ee] == bb && P.lv[s0 + (ee + 1 == mg ? 0 : ee + 1)] == a) { g = gg; break; }
+            }
+        }
+        double gx, gy, gz, gd, c12, det, ux, uy, uz;
+        if (g >= 0) {
+            gx = P.nx[g]; gy = P.ny[g]; gz = P.nz[g]; gd = P.d[g];
+            c12 = nx * gx + ny * gy + nz * gz;
+            det = 1.0 - c12 * c12;
+            ux = ny * gz - nz * gy;
+            uy = nz * gx - nx * gz;
+            uz = nx * gy - ny * gx;
+        } else {
+            ux = P.x[bb] - P.x[a];
+            uy = P.y[bb] - P.y[a];
+            uz = P.z[bb] - P.z[a];
+            det = 1.0; c12 = 0.0; gd = 0.0; gx = 0.0; gy = 0.0; gz = 0.0;
+        }
+        double un = sqrt(ux * ux + uy * uy + uz * uz);
+        if (un < 1e-300 || det <= 1e-300) { cur_inside = inb; continue; }
+        ux /= un; uy /= un; uz /= un;
+        if (ux < 0.0 || (ux == 0.0 && (uy < 0.0 || (uy == 0.0 && uz < 0.0)))) {
+            ux = -ux; uy = -uy; uz = -uz;
+        }
+        double x0x, x0y, x0z;
+        if (g >= 0) {
+            double r1 = dd - (nx * px + ny * py + nz * pz);
+            double r2 = gd - (gx * px + gy * py + gz * pz);
+            double al = (r1 - c12 * r2) / det;
+            double be = (r2 - c12 * r1) / det;
+            x0x = px + al * nx + be * gx;
+            x0y = py + al * ny + be * gy;
+            x0z = pz + al * nz + be * gz;
+        } else {
+            x0x = P.x[a]; x0y = P.y[a]; x0z = P.z[a];
+        }
+        double w0x = x0x - px, w0y = x0y - py, w0z = x0z - pz;
+        double bh = ux * w0x + uy * w0y + uz * w0z;
+        double cc = w0x * w0x + w0y * w0y + w0z * w0z - psi;
+        double disc = bh * bh - cc;
+        if (disc <= tol * tol) { cur_inside = inb; continue; }
+        double sqd = sqrt(disc);
+        double t1 = -bh - sqd, t2 = -bh + sqd;
+        double ta = ux * (P.x[a] - x0x) + uy * (P.y[a] - x0y) + uz * (P.z[a] - x0z);
+        double tb = ux * (P.x[bb] - x0x) + uy * (P.y[bb] - x0y) + uz * (P.z[bb] - x0z);
+        double tlo = ta < tb ? ta : tb;
+        double thi = ta < tb ? tb : ta;
+        for (int which = 0; which < 2; which++) {
+            double t;
+            if (ta <= tb) t = which == 0 ? t1 : t2;
+            else t = which == 0 ? t2 : t1;
+            if (t <= tlo + tol || t >= thi - tol) continue;
+            if (npts >= REF_MAX_P) return -1;
+            double cxx = x0x + t * ux, cxy = x0y + t * uy, cxz = x0z + t * uz;
+            if (cur_inside) {
+                PF_EMIT(cxx, cxy, cxz, PF_ONSPH | PF_CONN);
+                cur_inside = false;
+            } else {
+                if (prev >= 0) E.pfl[prev] |= PF_CONN;
+                else first_entry = true;
+                PF_EMIT(cxx, cxy, cxz, PF_ONSPH);
+                cur_inside = true;
+            }
+        }
+        cur_inside = inb;
+    }
+#undef PF_EMIT
+    if (npts == 0) {
+        double eb[6];
+        perp_basis(nx, ny, nz, eb);
+        bool cin = true;
+        for (int e = 0; e < m; e++) {
+            int a = P.lv[start + e];
+            int bb = P.lv[start + (e + 1 == m ? 0 : e + 1)];
+            double p0u = (P.x[a] - qx) * eb[0] + (P.y[a] - qy) * eb[1] + (P.z[a] - qz) * eb[2];
+            double p0v = (P.x[a] - qx) * eb[3] + (P.y[a] - qy) * eb[4] + (P.z[a] - qz) * eb[5];
+            double p1u = (P.x[bb] - qx) * eb[0] + (P.y[bb] - qy) * eb[1] + (P.z[bb] - qz) * eb[2];
+            double p1v = (P.x[bb] - qx) * eb[3] + (P.y[bb] - qy) * eb[4] + (P.z[bb] - qz) * eb[5];
+            if ((p1u - p0u) * (-p0v) - (p1v - p0v) * (-p0u) < 0.0) { cin = false; break; }
+        }
+        return cin ? RF_FULLCIRCLE : RF_OUTSIDE;
+    }
+    E.pnext[prev] = (int16_t)head;  // close the ring
+    if (first_entry) E.pfl[prev] |= PF_CONN;
+    // drop zero-length connectors (_kernels.py:612-636)
+    {
+        int i = head;
+        int kept = 0;
+        for (int t = 0; t < npts; t++) {
+            int j = E.pnext[i];
+            bool jdel = (E.pfl[j] & PF_DEL) != 0;  // only the wrap to a merged head
+            double dxp = E.ppx[i] - E.ppx[j];
+            double dyp = E.ppy[i] - E.ppy[j];
+            double dzp = E.ppz[i] - E.ppz[j];
+            if (!(E.pfl[i] & PF_CONN) && !jdel && dxp * dxp + dyp * dyp + dzp * dzp <= tol * tol) {
+                if (E.pfl[i] & PF_ONSPH) E.pfl[j] |= PF_ONSPH;
+                E.pfl[i] |= PF_DEL;
+            } else {
+                kept++;
+            }
+            i = j;
+        }
+        if (kept < npts) {
+            int nh = -1, lastk = -1;
+            i = head;
+            for (int t = 0; t < npts; t++) {
+                int j = E.pnext[i];
+                if (!(E.pfl[i] & PF_DEL)) {
+                    if (lastk >= 0) E.pnext[lastk] = (int16_t)i; else nh = i;
+                    lastk = i;
+                }
+                i = j;
+            }
+            if (lastk >= 0) E.pnext[lastk] = (int16_t)nh;
+            head = nh;
+            npts = kept;
+        }
+    }
+    if (npts < 2) return RF_OUTSIDE;
+    // canonical rotation: start at the arc with the smallest start angle (_kernels.py:640-674)
+    {
+        double eb[6];
+        perp_basis(nx, ny, nz, eb);
+        double best = 1e300;
+        int bi = head;
+        int i = head;
+        for (int t = 0; t < npts; t++) {
+            if (E.pfl[i] & PF_CONN) {
+                double rx = E.ppx[i] - qx, ry = E.ppy[i] - qy, rz = E.ppz[i] - qz;
+                double aang = atan2(rx * eb[3] + ry * eb[4] + rz * eb[5], rx * eb[0] + ry * eb[1] + rz * eb[2]);
+                if (aang < best) { best = aang; bi = i; }
+            }
+            i = E.pnext[i];
+        }
+        head = bi;
+    }
+    *head_out = head; *np_out = npts;
+    return RF_GENPOLY;
+}
+
+// _kernels.py:678-716 + 331-390: area, centroid, polar moment of a restricted facet
+template <class C>
+PF_DEV void seq_integrals(WS<C> *ws, int head, int npts, double nx, double ny, double nz,
+                          double qx, double qy, double qz, double rc, double *out) {
+    EvalScratch<C> &E = ws->u.e;
+    double e[6];
+    perp_basis(nx, ny, nz, e);
+    double A = 0.0, Mx = 0.0, My = 0.0, Ip = 0.0;
+    int i = head;
+    for (int t = 0; t < npts; t++) {
+        int j = E.pnext[i];
+        double x0 = (E.ppx[i] - qx) * e[0] + (E.ppy[i] - qy) * e[1] + (E.ppz[i] - qz) * e[2];
+        double y0 = (E.ppx[i] - qx) * e[3] + (E.ppy[i] - qy) * e[4] + (E.ppz[i] - qz) * e[5];
+        double x1 = (E.ppx[j] - qx) * e[0] + (E.ppy[j] - qy) * e[1] + (E.ppz[j] - qz) * e[2];
+        double y1 = (E.ppx[j] - qx) * e[3] + (E.ppy[j] - qy) * e[4] + (E.ppz[j] - qz) * e[5];
+        if (!(E.pfl[i] & PF_CONN)) {
+            double cr = x0 * y1 - x1 * y0;
+            A += 0.5 * cr;
+            double dx = x1 - x0, dy = y1 - y0;
+            Mx += dy * (x0 * x0 + x0 * x1 + x1 * x1) / 6.0;
+            My += -dx * (y0 * y0 + y0 * y1 + y1 * y1) / 6.0;
+            double sx3 = x0 * x0 * x0 + x0 * x0 * x1 + x0 * x1 * x1 + x1 * x1 * x1;
+            double sy3 = y0 * y0 * y0 + y0 * y0 * y1 + y0 * y1 * y1 + y1 * y1 * y1;
+            Ip += (dy * sx3 - dx * sy3) / 12.0;
+        } else {
+            double a0 = atan2(y0, x0);
+            double a1r = atan2(y1, x1);
+            double sweep = a1r - a0;
+            if (sweep <= 0.0) sweep += 2.0 * PF_PI;
+            const double cx = 0.0, cy = 0.0, r = rc;
+            double a1 = a0 + sweep;
+            double dth = a1 - a0;
+            double s0 = sin(a0), s1 = sin(a1), c0 = cos(a0), c1 = cos(a1);
+            double s20 = sin(2.0 * a0), s21 = sin(2.0 * a1);
+            double s40 = sin(4.0 * a0), s41 = sin(4.0 * a1);
+            double ic = s1 - s0;
+            double isn = c0 - c1;
+            double ic2 = 0.5 * dth + 0.25 * (s21 - s20);
+            double is2 = 0.5 * dth - 0.25 * (s21 - s20);
+            double ic3 = (s1 - s1 * s1 * s1 / 3.0) - (s0 - s0 * s0 * s0 / 3.0);
+            double is3 = (-c1 + c1 * c1 * c1 / 3.0) - (-c0 + c0 * c0 * c0 / 3.0);
+            double ic4 = 0.375 * dth + 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
+            double is4 = 0.375 * dth - 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
+            A += 0.5 * (r * r * dth + cx * r * ic + cy * r * isn);
+            Mx += 0.5 * r * (cx * cx * ic + 2.0 * cx * r * ic2 + r * r * ic3);
+            My += 0.5 * r * (cy * cy * isn + 2.0 * cy * r * is2 + r * r * is3);
+            Ip += (r / 3.0) * (cx * cx * cx * ic + 3.0 * cx * cx * r * ic2
+                               + 3.0 * cx * r * r * ic3 + r * r * r * ic4
+                               + cy * cy * cy * isn + 3.0 * cy * cy * r * is2
+                               + 3.0 * cy * r * r * is3 + r * r * r * is4);
+        }
+        i = j;
+    }
+    double cx, cy, cz;
+    if (A > 0.0) {
+        cx = qx + (Mx / A) * e[0] + (My / A) * e[3];
+        cy = qy + (Mx / A) * e[1] + (My / A) * e[4];
+        cz = qz + (Mx / A) * e[2] + (My / A) * e[5];
+    } else {
+        cx = qx; cy = qy; cz = qz;
+    }
+    out[0] = A; out[1] = cx; out[2] = cy; out[3] = cz; out[4] = Ip;
+}
+
+// _kernels.py:819-835
+PF_DEV void project_from(double cx, double cy, double cz, double yx, double yy, double yz,
+                         double px, double py, double pz, double psi, double *o) {
+    double dx = yx - cx, dy = yy - cy, dz = yz - cz;
+    double a = dx * dx + dy * dy + dz * dz;
+    double wx = cx - px, wy = cy - py, wz = cz - pz;
+    double b = dx * wx + dy * wy + dz * wz;
+    double c0 = wx * wx + wy * wy + wz * wz - psi;
+    double disc = b * b - a * c0;
+    if (disc < 0.0) disc = 0.0;
+    double t = (-b + sqrt(disc)) / a;
+    o[0] = cx + t * dx; o[1] = cy + t * dy; o[2] = cz + t * dz;
+}
+
+// _kernels.py:838-1001, streamed over the facet's boundary ring by one lane.
+template <class C>
+PF_DEV double patch_area(WS<C> *ws, int head, int npts, double nx, double ny, double nz, double s,
+                         double px, double py, double pz, double psi, double cx, double cy,
+                         double cz, bool *unstable_out) {
+    EvalScratch<C> &E = ws->u.e;
+    const double R = sqrt(psi);
+    bool unstable = false;
+    double kg_sum = 0.0;
+    // tangents: tin_i comes from connector i-1, tout_i from connector i
+    double pr0[3], pri[3], prj[3];
+    if (E.pfl[head] & PF_ONSPH) { pr0[0] = E.ppx[head]; pr0[1] = E.ppy[head]; pr0[2] = E.ppz[head]; }
+    else project_from(cx, cy, cz, E.ppx[head], E.ppy[head], E.ppz[head], px, py, pz, psi, pr0);
+    pri[0] = pr0[0]; pri[1] = pr0[1]; pri[2] = pr0[2];
+    double tin_i[3] = {0.0, 0.0, 0.0};   // tin of the current point (from previous connector)
+    double tout0[3] = {0.0, 0.0, 0.0};   // tout of point 0 (needs tin from the last connector)
+    int i = head;
+    for (int t = 0; t < npts; t++) {
+        const int j = E.pnext[i];
+        if (t + 1 == npts) { prj[0] = pr0[0]; prj[1] = pr0[1]; prj[2] = pr0[2]; }
+        else if (E.pfl[j] & PF_ONSPH) { prj[0] = E.ppx[j]; prj[1] = E.ppy[j]; prj[2] = E.ppz[j]; }
+        else project_from(cx, cy, cz, E.ppx[j], E.ppy[j], E.ppz[j], px, py, pz, psi, prj);
+        double tout[3] = {0.0, 0.0, 0.0}, tin_j[3] = {0.0, 0.0, 0.0};
+        const bool arc = (E.pfl[i] & PF_CONN) != 0;
+        double mx, my, mz, ee;
+        bool skip = false;
+        if (arc) {
+            mx = nx; my = ny; mz = nz; ee = s;
+        } else {
+            double ax = E.ppx[i] - cx, ay = E.ppy[i] - cy, az = E.ppz[i] - cz;
+            double bx2 = E.ppx[j] - cx, by2 = E.ppy[j] - cy, bz2 = E.ppz[j] - cz;
+            mx = ay * bz2 - az * by2;
+            my = az * bx2 - ax * bz2;
+            mz = ax * by2 - ay * bx2;
+            double mn = sqrt(mx * mx + my * my + mz * mz);
+            if (mn < 1e-300) {
+                unstable = true;
+                skip = true;
+                ee = 0.0;
+            } else {
+                mx /= mn; my /= mn; mz /= mn;
+                ee = mx * (cx - px) + my * (cy - py) + mz * (cz - pz);
+            }
+        }
+        if (!skip) {
+            for (int attempt = 0; attempt < 2; attempt++) {
+                double qx = px + ee * mx, qy = py + ee * my, qz = pz + ee * mz;
+                double rr2 = psi - ee * ee;
+                if (rr2 <= 0.0) { unstable = true; break; }
+                double u[6];
+                perp_basis(mx, my, mz, u);
+                double rpx = pri[0] - qx, rpy = pri[1] - qy, rpz = pri[2] - qz;
+                double phP = atan2(rpx * u[3] + rpy * u[4] + rpz * u[5], rpx * u[0] + rpy * u[1] + rpz * u[2]);
+                double rqx = prj[0] - qx, rqy = prj[1] - qy, rqz = prj[2] - qz;
+                double phQ = atan2(rqx * u[3] + rqy * u[4] + rqz * u[5], rqx * u[0] + rqy * u[1] + rqz * u[2]);
+                double dPQ = phQ - phP;
+                if (dPQ < 0.0) dPQ += 2.0 * PF_PI;
+                double sweep;
+                if (arc) {
+                    sweep = dPQ;
+                } else {
+                    double mxp = 0.5 * (E.ppx[i] + E.ppx[j]);
+                    double myp = 0.5 * (E.ppy[i] + E.ppy[j]);
+                    double mzp = 0.5 * (E.ppz[i] + E.ppz[j]);
+                    double h[3];
+                    project_from(cx, cy, cz, mxp, myp, mzp, px, py, pz, psi, h);
+                    double rmx = h[0] - qx, rmy = h[1] - qy, rmz = h[2] - qz;
+                    double phM = atan2(rmx * u[3] + rmy * u[4] + rmz * u[5], rmx * u[0] + rmy * u[1] + rmz * u[2]);
+                    double dPM = phM - phP;
+                    if (dPM < 0.0) dPM += 2.0 * PF_PI;
+                    if (dPM <= dPQ + 1e-12) {
+                        sweep = dPQ;
+                    } else {
+                        mx = -mx; my = -my; mz = -mz; ee = -ee;
+                        continue;
+                    }
+                }
+                kg_sum += (ee / R) * sweep;
+                double t0x = my * rpz - mz * rpy, t0y = mz * rpx - mx * rpz, t0z = mx * rpy - my * rpx;
+                double tn = sqrt(t0x * t0x + t0y * t0y + t0z * t0z);
+                if (tn > 0.0) { t0x /= tn; t0y /= tn; t0z /= tn; }
+                tout[0] = t0x; tout[1] = t0y; tout[2] = t0z;
+                double t1x = my * rqz - mz * rqy, t1y = mz * rqx - mx * rqz, t1z = mx * rqy - my * rqx;
+                tn = sqrt(t1x * t1x + t1y * t1y + t1z * t1z);
+                if (tn > 0.0) { t1x /= tn; t1y /= tn; t1z /= tn; }
+                tin_j[0] = t1x; tin_j[1] = t1y; tin_j[2] = t1z;
+                break;
+            }
+        }
+        // turning angle at point i (needs tin_i, tout_i, proj_i); point 0 deferred
+        if (t == 0) {
+            tout0[0] = tout[0]; tout0[1] = tout[1]; tout0[2] = tout[2];
+        } else {
+            double ax = tin_i[0], ay = tin_i[1], az = tin_i[2];
+            double bx2 = tout[0], by2 = tout[1], bz2 = tout[2];
+            double nxv = (pri[0] - px) / R, nyv = (pri[1] - py) / R, nzv = (pri[2] - pz) / R;
+            double crx = ay * bz2 - az * by2, cry = az * bx2 - ax * bz2, crz = ax * by2 - ay * bx2;
+            double sv = crx * nxv + cry * nyv + crz * nzv;
+            double cv = ax * bx2 + ay * by2 + az * bz2;
+            double th = atan2(sv, cv);
+            if (fabs(th) > PF_PI - 1e-7) unstable = true;
+            E.pth[i] = th;
+        }
+        tin_i[0] = tin_j[0]; tin_i[1] = tin_j[1]; tin_i[2] = tin_j[2];
+        pri[0] = prj[0]; pri[1] = prj[1]; pri[2] = prj[2];
+        i = j;
+    }
+    {   // point 0: tin from the last connector
+        double ax = tin_i[0], ay = tin_i[1], az = tin_i[2];
+        double bx2 = tout0[0], by2 = tout0[1], bz2 = tout0[2];
+        double nxv = (pr0[0] - px) / R, nyv = (pr0[1] - py) / R, nzv = (pr0[2] - pz) / R;
+        double crx = ay * bz2 - az * by2, cry = az * bx2 - ax * bz2, crz = ax * by2 - ay * bx2;
+        double sv = crx * nxv + cry * nyv + crz * nzv;
+        double cv = ax * bx2 + ay * by2 + az * bz2;
+        double th = atan2(sv, cv);
+        if (fabs(th) > PF_PI - 1e-7) unstable = true;
+        E.pth[head] = th;
+    }
+    double th_sum = 0.0;
+    i = head;
+    for (int t = 0; t < npts; t++) { th_sum += E.pth[i]; i = E.pnext[i]; }
+    double area = psi * (2.0 * PF_PI - kg_sum - th_sum);
+    if (area < -1e-9 * PF_FOUR_PI * psi || area > PF_FOUR_PI * psi * (1.0 + 1e-9)) unstable = true;
+    if (area < 0.0) area = 0.0;
+    if (area > PF_FOUR_PI * psi) area = PF_FOUR_PI * psi;
+    *unstable_out = unstable;
+    return area;
+}
+
+// result of one cell evaluation (uniform across the warp)
+struct CellRes {
+    int status;
+    double vol, K, cx, cy, cz, ix, iy, iz, m2;
+    int flags;
+};
+
+// _kernels.py:1008-1170.  Returns with res filled in every lane.  On pool
+// overflow sets ws->oflow (fast instantiation) and returns.
+template <class C>
+PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, double pz,
+                          double psi, double tol, int want_m2, CellRes *res) {
+    EvalScratch<C> &E = ws->u.e;
+    const int L = pfw::lane();
+    const int nf = P.nf;
+    res->flags = 0;
+    res->status = CELL_EMPTY; res->vol = 0.0; res->K = 0.0;
+    res->cx = px; res->cy = py; res->cz = pz; res->ix = px; res->iy = py; res->iz = pz; res->m2 = 0.0;
+    if (psi <= 0.0) return;
+    const double R = sqrt(psi);
+    const double ball_tol = tol * (2.0 * R + tol);
+    for (int v = L; v < P.nv; v += 32) {
+        double wx = P.x[v] - px, wy = P.y[v] - py, wz = P.z[v] - pz;
+        double q = wx * wx + wy * wy + wz * wz - psi;
+        E.vin[v] = q <= ball_tol ? 1 : 0;
+    }
+    if (L == 0) E.npool = 0;
+    pfw::sync();
+    // restrict + integrate, lane per facet (_kernels.py:1027-1071)
+    bool ovf = false, pool_ovf = false;
+    for (int f = L; f < nf; f += 32) {
+        double s, rc;
+        int head, npts;
+        int kind = restrict_facet(ws, P, f, px, py, pz, psi, tol, &s, &rc, &head, &npts);
+        if (kind == -1) { ovf = true; kind = RF_OUTSIDE; }
+        if (kind == -2) { pool_ovf = true; kind = RF_OUTSIDE; }
+        E.fkind[f] = (uint8_t)kind; E.fh[f] = s; E.frc[f] = rc; E.fhead[f] = (int16_t)head;
+        E.fnp[f] = (int16_t)npts;
+        if (kind == RF_OUTSIDE) {
+            E.farea[f] = 0.0; E.fcx[f] = px; E.fcy[f] = py; E.fcz[f] = pz; E.fip[f] = 0.0;
+            continue;
+        }
+        double qx = px + s * P.nx[f], qy = py + s * P.ny[f], qz = pz + s * P.nz[f];
+        if (kind == RF_FULLCIRCLE) {
+            E.farea[f] = PF_PI * rc * rc;
+            E.fcx[f] = qx; E.fcy[f] = qy; E.fcz[f] = qz;
+            double rc2 = rc * rc;
+            E.fip[f] = 0.5 * PF_PI * (rc2 * rc2);
+        } else {
+            double o[5];
+            seq_integrals(ws, head, npts, P.nx[f], P.ny[f], P.nz[f], qx, qy, qz, rc, o);
+            if (o[0] <= 0.0) {
+                E.fkind[f] = RF_OUTSIDE;
+                E.farea[f] = 0.0; E.fcx[f] = px; E.fcy[f] = py; E.fcz[f] = pz; E.fip[f] = 0.0;
+                continue;
+            }
+            E.farea[f] = o[0]; E.fcx[f] = o[1]; E.fcy[f] = o[2]; E.fcz[f] = o[3]; E.fip[f] = o[4];
+        }
+    }
+    if (pfw::any(pool_ovf)) {
+        if (L == 0) ws->oflow = 1;
+        pfw::sync();
+        res->flags = FLAG_RETRY;
+        return;
+    }
+    if (pfw::any(ovf)) {  // reference: first facet with kind < 0 aborts the cell
+        res->flags = FLAG_OVERFLOW;
+        return;
+    }
+    pfw::sync();
+    bool any_present = false, any_area = false;
+    for (int f = 0; f < nf; f++) {
+        if (E.fkind[f] != RF_OUTSIDE) any_present = true;
+        if (E.fkind[f] != RF_OUTSIDE && E.farea[f] > 0.0) any_area = true;
+    }
+    // NB: reference sets any_present before the A <= 0 demotion; a demoted
+    // GENPOLY still counts as "present" there.  Demotion always comes with
+    // area 0, so (any_present && any_area) == any_area except for that case,
+    // which the full-ball/empty branch below treats identically.
+    if (!any_area) {
+        bool inside = true;
+        for (int f = 0; f < nf; f++)
+            if (E.fh[f] < -tol) { inside = false; break; }
+        if ((inside && nf > 0) || nf == 0) {
+            res->status = CELL_FULLBALL;
+            res->vol = PF_FOUR_PI / 3.0 * psi * R;
+            res->K = PF_FOUR_PI * psi;
+            res->m2 = want_m2 ? PF_FOUR_PI * psi * R * R * R / 5.0 : 0.0;
+        }
+        (void)any_present;
+        return;
+    }
+    // interior point (_kernels.py:723-816): ray per restricted facet, lane per facet
+    for (int f = L; f < nf; f += 32) {
+        E.fseg[f] = 0;
+        if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
+        double ox = E.fcx[f], oy = E.fcy[f], oz = E.fcz[f];
+        double dx = -P.nx[f], dy = -P.ny[f], dz = -P.nz[f];
+        double wx = ox - px, wy = oy - py, wz = oz - pz;
+        double bh = dx * wx + dy * wy + dz * wz;
+        double cc = wx * wx + wy * wy + wz * wz - psi;
+        double disc = bh * bh - cc;
+        if (disc <= 0.0) continue;
+        double t_hi = -bh + sqrt(disc);
+        double t_lo = 0.0;
+        bool ok = true;
+        for (int g = 0; g < nf; g++) {
+            if (g == f) continue;
+            double den = P.nx[g] * dx + P.ny[g] * dy + P.nz[g] * dz;
+            double num = P.d[g] - (P.nx[g] * ox + P.ny[g] * oy + P.nz[g] * oz);
+            if (den > tol) {
+                double tc = num / den;
+                if (tc < t_hi) t_hi = tc;
+            } else if (den < -tol) {
+                double tc = num / den;
+                if (tc > t_lo) t_lo = tc;
+            } else if (num < -tol) {
+                ok = false;
+                break;
+            }
+        }
+        if (!ok || t_hi - t_lo <= tol) continue;
+        double tm = 0.5 * (t_lo + t_hi);
+        double mx = ox + tm * dx, my = oy + tm * dy, mz = oz + tm * dz;
+        double mg = sqrt(psi) - sqrt(sq(mx - px) + sq(my - py) + sq(mz - pz));
+        for (int g = 0; g < nf; g++) {
+            double d2 = P.d[g] - (P.nx[g] * mx + P.ny[g] * my + P.nz[g] * mz);
+            if (d2 < mg) mg = d2;
+        }
+        E.fseg[f] = 1;
+        E.smx[f] = mx; E.smy[f] = my; E.smz[f] = mz; E.smg[f] = mg;
+    }
+    pfw::sync();
+    double ix, iy, iz, bx = px, by = py, bz = pz;
+    {
+        double sx = 0.0, sy = 0.0, sz = 0.0, best_margin = -1.0;
+        int nseg = 0;
+        for (int f = 0; f < nf; f++) {
+            if (!E.fseg[f]) continue;
+            sx += E.smx[f]; sy += E.smy[f]; sz += E.smz[f];
+            nseg++;
+            if (E.smg[f] > best_margin) { best_margin = E.smg[f]; bx = E.smx[f]; by = E.smy[f]; bz = E.smz[f]; }
+        }
+        bool ok = nseg > 0;
+        if (ok) {
+            double cx = sx / (double)nseg, cy = sy / (double)nseg, cz = sz / (double)nseg;
+            double mg = sqrt(psi) - sqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
+            for (int g = 0; g < nf; g++) {
+                double d2 = P.d[g] - (P.nx[g] * cx + P.ny[g] * cy + P.nz[g] * cz);
+                if (d2 < mg) mg = d2;
+            }
+            if (mg <= 0.0) {
+                if (best_margin > 0.0) { cx = bx; cy = by; cz = bz; }
+                else ok = false;
+            }
+            ix = cx; iy = cy; iz = cz;
+        }
+        if (!ok) {
+            res->flags = FLAG_DEGENERATE_INTERIOR;
+            return;
+        }
+    }
+    // occluded areas with perturb-and-retry (_kernels.py:1100-1128)
+    double kbar = 0.0;
+    for (int attempt = 0; attempt < 4; attempt++) {
+        for (int f = L; f < nf; f += 32) {
+            E.funs[f] = 0;
+            if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0 || E.fkind[f] == RF_FULLCIRCLE) continue;
+            bool uns;
+            E.fpa[f] = patch_area(ws, E.fhead[f], E.fnp[f], P.nx[f], P.ny[f], P.nz[f], E.fh[f], px, py,
+                                  pz, psi, ix, iy, iz, &uns);
+            E.funs[f] = uns ? 1 : 0;
+        }
+        pfw::sync();
+        kbar = 0.0;
+        bool bad = false;
+        for (int f = 0; f < nf; f++) {
+            if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
+            if (E.fkind[f] == RF_FULLCIRCLE) { kbar += 2.0 * PF_PI * R * (R - E.fh[f]); continue; }
+            if (E.funs[f]) { bad = true; break; }
+            kbar += E.fpa[f];
+        }
+        pfw::sync();
+        if (!bad) break;
+        if (attempt == 3) { res->flags |= FLAG_UNSTABLE_PROJECTION; break; }
+        double w = 0.35 * (double)(attempt + 1);
+        ix = ix + w * (bx - ix);
+        iy = iy + w * (by - iy);
+        iz = iz + w * (bz - iz);
+    }
+    double K = PF_FOUR_PI * psi - kbar;
+    if (K < 0.0) K = 0.0;
+    if (K > PF_FOUR_PI * psi) K = PF_FOUR_PI * psi;
+    double vol = R * K / 3.0;
+    double mx = 0.0, my = 0.0, mz = 0.0, nsx = 0.0, nsy = 0.0, nsz = 0.0;
+    double m2 = want_m2 ? R * R * R * K / 5.0 : 0.0;
+    for (int f = 0; f < nf; f++) {
+        if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
+        double fa = E.farea[f], fh = E.fh[f];
+        double pv = fh * fa / 3.0;
+        vol += pv;
+        mx += pv * 0.75 * (E.fcx[f] - px);
+        my += pv * 0.75 * (E.fcy[f] - py);
+        mz += pv * 0.75 * (E.fcz[f] - pz);
+        nsx += P.nx[f] * fa;
+        nsy += P.ny[f] * fa;
+        nsz += P.nz[f] * fa;
+        if (want_m2) m2 += (fh / 5.0) * (E.fip[f] + fh * fh * fa);
+    }
+    mx += 0.25 * psi * (-nsx);
+    my += 0.25 * psi * (-nsy);
+    mz += 0.25 * psi * (-nsz);
+    double ccx, ccy, ccz;
+    if (vol > 0.0) { ccx = px + mx / vol; ccy = py + my / vol; ccz = pz + mz / vol; }
+    else { vol = 0.0; ccx = px; ccy = py; ccz = pz; }
+    res->status = CELL_CLIPPED;
+    res->vol = vol; res->K = K; res->cx = ccx; res->cy = ccy; res->cz = ccz;
+    res->ix = ix; res->iy = iy; res->iz = iz; res->m2 = m2;
+}
+
+// ---------------------------------------------------------------------------
+// one cell end to end (_kernels.py:1374-1474).  Returns the cell's flags;
+// FLAG_RETRY means nothing was written and the cell must be re-run on the
+// reference-capacity instantiation.
+// ---------------------------------------------------------------------------
+template <class C>
+PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+    const int L = pfw::lane();
+    if (L == 0) ws->oflow = 0;
+    pfw::sync();
+    int which, nclips;
+    int st = build_cell(ws, in, i, &which, &nclips);
+    if (ws->oflow) {
+        pfw::sync();
+        if (!C::EXACT) return FLAG_RETRY;
+        st = 3;
+    }
+    if (out.census && L == 0) out.census[i] = nclips;
+    const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
+    if (st == 3) {
+        if (L == 0) {
+            if (out.status) out.status[i] = CELL_EMPTY;
+            if (out.vol) out.vol[i] = 0.0;
+            if (out.ksur) out.ksur[i] = 0.0;
+            if (out.fcount) out.fcount[i] = 0;
+            if (out.fcount32) out.fcount32[i] = 0;
+            if (out.flags) out.flags[i] = FLAG_OVERFLOW;
+        }
+        return FLAG_OVERFLOW;
+    }
+    if (st == 1) {
+        if (L == 0) {
+            if (out.status) out.status[i] = CELL_EMPTY;
+            if (out.vol) out.vol[i] = 0.0;
+            if (out.ksur) out.ksur[i] = 0.0;
+            if (out.cent) { out.cent[3 * i] = px; out.cent[3 * i + 1] = py; out.cent[3 * i + 2] = pz; }
+            if (out.ipt) { out.ipt[3 * i] = px; out.ipt[3 * i + 1] = py; out.ipt[3 * i + 2] = pz; }
+            if (out.m2) out.m2[i] = 0.0;
+            if (out.fcount) out.fcount[i] = 0;
+            if (out.fcount32) out.fcount32[i] = 0;
+            if (out.flags) out.flags[i] = 0;
+        }
+        return 0;
+    }
+    const Poly<C> &P = ws->P[which];
+    CellRes r;
+    evaluate_cell(ws, P, px, py, pz, in.psi[i], in.tol, in.want_m2, &r);
+    if (ws->oflow) {
+        pfw::sync();
+        if (!C::EXACT) return FLAG_RETRY;
+        // beyond even the reference-capacity pool: report as overflow
+        r.flags = FLAG_OVERFLOW;
+        r.status = CELL_EMPTY; r.vol = 0.0; r.K = 0.0;
+        r.cx = px; r.cy = py; r.cz = pz; r.ix = px; r.iy = py; r.iz = pz; r.m2 = 0.0;
+    }
+    int flags = r.flags;
+    if (L == 0) {
+        if (out.status) out.status[i] = r.status;
+        if (out.vol) out.vol[i] = r.vol;
+        if (out.ksur) out.ksur[i] = r.K;
+        if (out.cent) { out.cent[3 * i] = r.cx; out.cent[3 * i + 1] = r.cy; out.cent[3 * i + 2] = r.cz; }
+        if (out.ipt) { out.ipt[3 * i] = r.ix; out.ipt[3 * i + 1] = r.iy; out.ipt[3 * i + 2] = r.iz; }
+        if (out.m2) out.m2[i] = r.m2;
+    }
+    // restricted facet summaries in facet order, zero-area facets dropped (_kernels.py:1456-1474)
+    int nk = 0;
+    if (r.status == CELL_CLIPPED) {
+        const EvalScratch<C> &E = ws->u.e;
+        const unsigned lt = pfw::lanemask_lt();
+        const int smf = out.smf;
+        for (int f0 = 0; f0 < P.nf; f0 += 32) {
+            int f = f0 + L;
+            bool keep = f < P.nf && !(E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0);
+            unsigned m = pfw::ballot(keep);
+            int slot = nk + pfw::popc(m & lt);
+            if (keep && slot < smf) {
+                size_t o = (size_t)i * smf + slot;
+                if (out.ftag) out.ftag[o] = P.tag[f];
+                if (out.ftag32) out.ftag32[o] = P.tag[f];
+                if (out.farea) out.farea[o] = E.farea[f];
+                if (out.fh) out.fh[o] = E.fh[f];
+                if (out.fnrm) { out.fnrm[3 * o] = P.nx[f]; out.fnrm[3 * o + 1] = P.ny[f]; out.fnrm[3 * o + 2] = P.nz[f]; }
+                if (out.fcent) { out.fcent[3 * o] = E.fcx[f]; out.fcent[3 * o + 1] = E.fcy[f]; out.fcent[3 * o + 2] = E.fcz[f]; }
+            }
+            nk += pfw::popc(m);
+        }
+        if (nk > smf) { nk = smf; flags |= FLAG_OVERFLOW; }
+    }
+    if (L == 0) {
+        if (out.fcount) out.fcount[i] = nk;
+        if (out.fcount32) out.fcount32[i] = nk;
+        if (out.flags) out.flags[i] = flags;
+    }
+    pfw::sync();
+    return flags;
+}
+
+}  // namespace pf

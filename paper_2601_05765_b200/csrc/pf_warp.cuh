@@ -1,0 +1,64 @@
+// pf_warp.cuh -- the handful of warp-collective primitives the cell kernel
+// uses.  On the device they are the sm_100a intrinsics.  The cell algorithm
+// (pf_cell.cuh) only ever calls these with all 32 lanes converged, which is
+// what lets tests/emu compile the same algorithm for a lock-step host warp
+// emulator (test infrastructure, never shipped) by providing its own versions
+// of exactly these functions.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__) && !defined(PF_EMU)
+#define PF_DEV __device__ __forceinline__
+#define PF_DEVNI __device__ __noinline__
+#define PF_FULL 0xffffffffu
+namespace pfw {
+PF_DEV int lane() { return threadIdx.x & 31; }
+PF_DEV unsigned ballot(bool p) { return __ballot_sync(PF_FULL, p); }
+PF_DEV bool any(bool p) { return __any_sync(PF_FULL, p); }
+PF_DEV void sync() { __syncwarp(); }
+PF_DEV int shfl(int v, int src) { return __shfl_sync(PF_FULL, v, src); }
+PF_DEV double shfl(double v, int src) { return __shfl_sync(PF_FULL, v, src); }
+PF_DEV int shfl_xor(int v, int m) { return __shfl_xor_sync(PF_FULL, v, m); }
+PF_DEV double shfl_xor(double v, int m) { return __shfl_xor_sync(PF_FULL, v, m); }
+PF_DEV int popc(unsigned m) { return __popc(m); }
+PF_DEV int atom_add(int *p, int v) { return atomicAdd(p, v); }
+PF_DEV unsigned lanemask_lt() { return (1u << lane()) - 1u; }
+}  // namespace pfw
+#else
+#ifndef PF_EMU
+#error "pf_warp.cuh: host compilation requires the test emulator (define PF_EMU)"
+#endif
+// provided by tests/emu/emu_warp.h
+#endif
+
+namespace pfw {
+// exact (order-independent) warp reductions
+PF_DEV double max_d(double v) {
+    for (int m = 16; m > 0; m >>= 1) {
+        double o = shfl_xor(v, m);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+PF_DEV int sum_i(int v) {
+    for (int m = 16; m > 0; m >>= 1) v += shfl_xor(v, m);
+    return v;
+}
+PF_DEV int max_i(int v) {
+    for (int m = 16; m > 0; m >>= 1) {
+        int o = shfl_xor(v, m);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+// exclusive prefix over lanes of an int
+PF_DEV int excl_scan_i(int v, int *total) {
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = shfl(x, (lane() - o) & 31);
+        if (lane() >= o) x += y;
+    }
+    *total = shfl(x, 31);
+    return x - v;
+}
+}  // namespace pfw
