@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the partial-OT hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric (BASELINE.json): "generalized Laguerre cells/sec (vol+areas) and ms per
+Newton solve at 2M cells".  Workload at N=1: C4, the 2M-cell droplet scene
+(paper teaser scale), weights psi at convergence of the
+config's first (cold-start) Newton solve, which is computed in the untimed
+set-up and itself timed once as ``newton.ms_per_solve``.
+
+One step = one full evaluation of the restricted Laguerre cells (bucket grid
+counting sort + dpsi reduction + candidate gather + clip + restriction +
+volumes / free-surface / facet areas / centroids), fp64, ball-aware, outputs
+in the reference's fixed-stride layout (smf=32) resident in HBM.  L2 is
+flushed (a 256 MiB write) before every timed step.  `e2e` repeats the step
+through the reference-facing drop-in (`_kernels._batch_evaluate` on host numpy
+arrays): host->device copy of (pts, psi) and device->host copy of all twelve
+outputs inside the timed region.
+
+N>1 (torchrun): the domain is partitioned into x-slabs; rank r evaluates the
+cells it owns using owned + ghost sites (ghost margin = largest ball-aware
+search radius, with the global dpsi), so per-cell results are identical to
+N=1 and there is no data-path collective during the evaluation.  Total work
+is fixed (strong scaling).  `--impl reference` times the CPU oracle port of
+the reference kernel (oracle/, bit-identical to the numba reference) on the
+host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "generalized Laguerre cells/sec (vol+areas)"
+UNIT = "cells/s"
+
+# S_cell = sum of census terms x DP-pipe slots (census slot order)
+S_WEIGHTS = np.array([29, 3, 16, 19, 6, 8, 6, 74, 70, 15, 160, 170, 60, 37, 20, 0], np.float64)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--smf", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-newton", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_scene(name):
+    from paper_2601_05765_b200 import scenes
+
+    return scenes.make(name)
+
+
+def workload_desc(name, sc):
+    return {"C1": "C1 10k random seeds (30% fill), unit box",
+            "C2": "C2 100k dam break (46^3 jittered lattice)",
+            "C3": "C3 500k chocs (ball of radius 1/4)",
+            "C4": "C4 2M-cell droplet (pool z<0.08 + drop r=0.12), paper teaser scale",
+            "C5": "C5 1M two-fluid (spacing h / 2h)"}[name] + f", n={sc.n}"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"pf_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows]
+        mx = float(rows[0][1])
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 4 + k and "Active" in r[4 + k] and "Not" not in r[4 + k]:
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def slab_partition(pts, psi, dpsi, ws, rank):
+    """Owned cells of rank r (x-slab) + ghost sites within the largest search radius."""
+    x = pts[:, 0]
+    lo, hi = rank / ws, (rank + 1) / ws
+    own = (x >= lo) & ((x < hi) if rank < ws - 1 else (x <= 1.0 + 1e-12))
+    br = np.sqrt(np.maximum(psi, 0)) + np.sqrt(np.maximum(psi, 0) + dpsi)
+    W = float(br[own].max()) * (1 + 1e-9) if own.any() else 0.0
+    keep = (x >= lo - W) & (x <= hi + W)
+    idx = np.nonzero(keep)[0]  # global order preserved (ties break on index)
+    owned_local = np.nonzero(own[idx])[0].astype(np.int32)
+    return idx, owned_local
+
+
+def converged_psi(sc, dom):
+    import torch
+
+    from paper_2601_05765_b200 import solver
+
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = solver.newton_solve(torch.as_tensor(sc.pts, device="cuda"),
+                              torch.as_tensor(sc.nu, device="cuda"), dom)
+    e1.record()
+    torch.cuda.synchronize()
+    return res.psi, float(e0.elapsed_time(e1)), res.stats
+
+
+def cpu_reference_run(sc, psi, steps, warmup, sample_cells, threads):
+    """CPU oracle port of _kernels._batch_evaluate on the host cores."""
+    from oracle import pyoracle as O
+    from paper_2601_05765_b200 import geom, laguerre
+
+    O.set_threads(threads)
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    dpk = laguerre.domain_pack(dom)
+    rng = np.random.default_rng(0)
+    cells = np.sort(rng.choice(sc.n, size=min(sample_cells, sc.n), replace=False)).astype(np.int64)
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        g = O.SpatialGrid(sc.pts, [0, 0, 0], [1, 1, 1], dpk.volume)
+        o = O.evaluate(sc.pts, psi, dpk.args(), dpk.tol, g, ball_aware=True, want_m2=True, smf=32,
+                       i0=0, i1=len(cells), cells=cells)
+        t1 = time.perf_counter()
+        if it >= warmup:
+            times.append(t1 - t0)
+    return len(cells) / (sum(times) / len(times)), O.num_threads(), o["err"]
+
+
+def main():
+    a = parse()
+    ws, rank, local = dist_env()
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        sc = make_scene(a.config)
+        # converged weights need the device solve; the CPU arm uses the same
+        # weights when a GPU is present, else the cold-start weights
+        psi = sc.psi_cold()
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                from paper_2601_05765_b200 import geom
+
+                psi = converged_psi(sc, geom.box_domain([0, 0, 0], [1, 1, 1]))[0].cpu().numpy()
+        except Exception:
+            pass
+        threads = os.cpu_count() or 1
+        sample = 400_000 if sc.n > 400_000 else sc.n
+        v, cores, err = cpu_reference_run(sc, psi, a.steps, a.warmup, sample, threads)
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": 1e3 * sample / v, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "impl": "reference",
+                "config": {"workload": workload_desc(a.config, sc), "ball_aware": True, "smf": 32},
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                 "sample": f"{sample} random cells of the workload per step "
+                                           "(full neighbourhoods), grid build included"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "flags": err}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_05765_b200 import _kernels, _lib, geom, laguerre, restricted
+
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    sc = make_scene(a.config)
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    dpk = laguerre.domain_pack(dom)
+    L = _lib.lib()
+    c = _lib.ctx()
+    laguerre.upload_domain(c, *dpk.args(), dpk.tol)
+
+    # ---- set-up (untimed): converged weights from the config's first solve
+    newton = None
+    if a.no_newton:
+        psi_g = torch.as_tensor(sc.psi_cold(), device="cuda")
+    else:
+        psi_g, newton_ms, nst = converged_psi(sc, dom)
+        newton = {"ms_per_solve": newton_ms, "iterations": nst["iterations"],
+                  "evaluations": nst["evaluations"], "cg_iterations": nst["cg_iterations"],
+                  "worst_initial": nst["worst_initial"], "worst_final": nst["worst_final"],
+                  "status": nst["status_name"], "start": "cold (kappa (3 nu/4 pi)^(2/3))",
+                  "eps_vol": 0.01, "n": sc.n}
+    psi_h = psi_g.cpu().numpy()
+    dpsi = float(max(psi_h.max() - psi_h.min(), 0.0))
+
+    if ws > 1:
+        idx, owned = slab_partition(sc.pts, psi_h, dpsi, ws, rank)
+    else:
+        idx, owned = np.arange(sc.n), None
+    pts_l = torch.as_tensor(np.ascontiguousarray(sc.pts[idx]), device="cuda")
+    psi_l = torch.as_tensor(np.ascontiguousarray(psi_h[idx]), device="cuda")
+    owned_t = None if owned is None else torch.as_tensor(owned, device="cuda")
+    n_l = len(idx)
+    n_eval = n_l if owned is None else len(owned)
+    smf = a.smf
+    outs = restricted.alloc(n_l, smf)
+    census = torch.zeros((n_l, 16), dtype=torch.int32, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step(cen=None):
+        err = L.pf_batch_evaluate_ex(c, n_l, _lib.ptr(pts_l), _lib.ptr(psi_l), float(dpk.tol), dpsi, 1,
+                                     1, smf, *[_lib.ptr(t) for t in outs],
+                                     _lib.ptr(owned_t), 0 if owned_t is None else len(owned),
+                                     None, _lib.ptr(cen), 1, _lib.stream_ptr())
+        return _lib.check(err, "pf_batch_evaluate_ex")
+
+    # census pass (untimed) -> algorithmic FP64 work of this workload
+    step(census)
+    torch.cuda.synchronize()
+    cen = census[owned_t.long()] if owned_t is not None else census
+    s_cell = float((cen.double().cpu().numpy() @ S_WEIGHTS).sum())  # DP slots, all owned cells
+    mean_clips = float(cen[:, 0].double().mean())
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    fl = 0
+    tot_ms = 0.0
+    cells_ms = 0.0
+    launches0 = L.pf_launch_count()
+    with ClockSampler(dev) as clk:
+        for _ in range(a.steps):
+            flush.fill_(1.0)
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fl |= step()
+            e1.record()
+            torch.cuda.synchronize()
+            tot_ms += e0.elapsed_time(e1)
+            import ctypes
+
+            ms = ctypes.c_double(0.0)
+            _lib.check(L.pf_last_cells_ms(c, ctypes.byref(ms)), "pf_last_cells_ms")
+            cells_ms += ms.value
+    launches = int(L.pf_launch_count() - launches0)
+    t_step = tot_ms / a.steps
+    t_cells = cells_ms / a.steps
+    if ws > 1:
+        tt = torch.tensor([t_step, t_cells], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_cells = float(tt[0]), float(tt[1])
+        s_all = torch.tensor([s_cell], dtype=torch.float64, device="cuda")
+        dist.all_reduce(s_all)
+        s_cell_total = float(s_all[0])
+    else:
+        s_cell_total = s_cell
+    value = sc.n / (t_step * 1e-3)
+
+    # ---- end to end through the drop-in numpy API (N=1)
+    e2e = None
+    if not a.no_e2e and ws == 1:
+        from oracle import pyoracle as O  # only for the output allocator shapes
+
+        host = O.alloc_outputs(sc.n, smf)
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
+        pts_p, psi_p = pin(sc.pts), pin(psi_h)
+        host = {k: pin(v) for k, v in host.items()}
+        gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
+        times = []
+        for it in range(2 + a.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _kernels._batch_evaluate(pts_p, psi_p, *dpk.args(), *gargs, dpk.tol, dpsi, True, True, smf,
+                                     *[host[k] for k in O.OUT_ORDER])
+            torch.cuda.synchronize()
+            if it >= 2:
+                times.append(time.perf_counter() - t0)
+        t_e2e = sum(times) / len(times)
+        h2d = sc.pts.nbytes + psi_h.nbytes
+        d2h = sum(host[k].nbytes for k in O.OUT_ORDER)
+        e2e = {"value": sc.n / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * t_e2e,
+               "api": "paper_2601_05765_b200._kernels._batch_evaluate (numpy, pinned host buffers)"}
+
+    # ---- FP64 roofline of the dominant kernel (k_cells_fast + exact tier)
+    import ctypes
+
+    peak = ctypes.c_double(0.0)
+    _lib.check(L.pf_fp64_peak(ctypes.byref(peak), None), "pf_fp64_peak")
+    achieved = 2.0 * s_cell_total / (t_cells * 1e-3) / 1e12  # slot = FMA-equivalent (2 flop)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(a.config)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                "frac": achieved / peak.value if peak.value > 0 else None, "traffic": traffic,
+                "kernel": "k_cells_fast+k_cells_exact",
+                "kernel_ms": t_cells, "kernel_share_of_step": t_cells / t_step,
+                "algorithmic": f"census S_cell (SURVEY.md §8(d)) = {s_cell_total / sc.n:.0f} DP slots/cell,"
+                               f" x2 flop/slot; mean processed candidates {mean_clips:.1f}/cell",
+                "peak_source": "measured in-run by pf_fp64_peak (DFMA chains; MEASURED_PEAKS.json has no FP64 entry)"}
+
+    # ---- CPU baseline: oracle port on the host cores (rank 0, N=1)
+    cpu = None
+    if not a.no_cpu and ws == 1 and rank == 0:
+        threads = os.cpu_count() or 1
+        sample = 200_000 if sc.n > 200_000 else sc.n
+        v, cores, _ = cpu_reference_run(sc, psi_h, 1, 0, sample, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{sample} random cells of the same workload (full neighbourhoods), one pass, "
+                         "grid build included; oracle/potflow_oracle.c is bit-identical to the numba reference"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_desc(a.config, sc), "ball_aware": True, "smf": smf,
+                           "psi": "converged (first cold-start Newton solve, eps_vol=1%)"
+                           if newton else "cold start",
+                           "l2": "256 MiB flush write before every timed step",
+                           "parallelism": f"x-slab spatial partition over {ws} GPU(s), ghosts by search radius"
+                           if ws > 1 else "1 GPU"},
+                "flags": fl, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline, "cpu_baseline": cpu, "newton": newton,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

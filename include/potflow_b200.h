@@ -1,0 +1,157 @@
+/*
+ * potflow_b200.h -- C ABI of the B200 (sm_100a) partial-optimal-transport hot
+ * path.  Plain pointers and sizes only; every array argument is a DEVICE
+ * pointer unless its name ends in _host.  `stream` is a cudaStream_t passed as
+ * void* (0 = legacy default stream).  Functions return 0 on success and a
+ * negative code on error (message via pf_last_error()); functions that mirror
+ * a reference kernel returning a flag word return that word (>= 0).
+ *
+ * Reference interfaces replaced (all under /root/reference/pkg/src/potflow):
+ *   pf_set_domain       laguerre._DomainPack / domain_pack     laguerre.py:113-139
+ *   pf_grid_build       laguerre.SpatialGrid.__init__          laguerre.py:52-80
+ *   pf_grid_export      SpatialGrid.bucket_start/bucket_sites  laguerre.py:78-79
+ *   pf_dpsi_max         laguerre._dpsi_max                     laguerre.py:142-145
+ *   pf_batch_evaluate   _kernels._batch_evaluate               _kernels.py:1362-1478
+ *   pf_knn              _kernels._knn / laguerre.knn            _kernels.py:1562-1620, laguerre.py:90-96
+ *   pf_newton_*         ot_solver.newton_solve (spec only)
+ *   pf_fluid_*          fluid_sim.step (spec only)
+ */
+#ifndef POTFLOW_B200_H
+#define POTFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pf_ctx pf_ctx; /* opaque: device domain, grid, scratch */
+
+/* cell status (_kernels.py:43-45) and flag bits (_kernels.py:48-50) */
+#define PF_CELL_EMPTY 0
+#define PF_CELL_FULLBALL 1
+#define PF_CELL_CLIPPED 2
+#define PF_FLAG_OVERFLOW 1
+#define PF_FLAG_DEGENERATE_INTERIOR 2
+#define PF_FLAG_UNSTABLE_PROJECTION 4
+
+const char *pf_version(void);
+const char *pf_last_error(void);
+/* number of kernels this library has launched so far (benchmark evidence) */
+unsigned long long pf_launch_count(void);
+/* measured FP64 FMA throughput of the current device, TFLOP/s (FMA = 2 flops) */
+int pf_fp64_peak(double *tflops_host, double *ms_host);
+
+/* context lifetime; device = CUDA ordinal the context's buffers live on */
+int pf_ctx_create(pf_ctx **out, int device);
+int pf_ctx_destroy(pf_ctx *ctx);
+
+/* Domain polytope in the reference packed layout (geom.pack_cell,
+ * geom.py:353-375): dv[512*3], dc[3], dp[160*4], dt[160], dlp[161],
+ * dlv[2048] (host arrays), tol = DEFAULT_REL_TOL * diagonal
+ * (laguerre.py:120). */
+int pf_set_domain(pf_ctx *ctx, const double *dv_host, const int64_t *dc_host,
+                  const double *dp_host, const int64_t *dt_host, const int64_t *dlp_host,
+                  const int64_t *dlv_host, double tol);
+
+/* Uniform bucket grid over the domain bounding box by counting sort.
+ * cell_size <= 0 picks the bucket edge from the weights (half the mean
+ * ball-aware search radius, psi may be NULL -> (|domain|/n)^(1/3)/2).
+ * Sites are stored bucket-sorted (SoA) for coalesced candidate gathers. */
+int pf_grid_build(pf_ctx *ctx, int64_t n, const double *pts, const double *psi,
+                  double cell_size, void *stream);
+/* same with explicit bucket counts per axis (dims_host int[3]), as the
+ * reference's SpatialGrid chooses them (laguerre.py:63-64) */
+int pf_grid_build_dims(pf_ctx *ctx, int64_t n, const double *pts, const int *dims_host, void *stream);
+/* grid dims (int[3]), origin (double[3]) and edge (double[3]) of the last build */
+int pf_grid_info(pf_ctx *ctx, int *dims_host, double *lo_host, double *h_host);
+/* reference-layout CSR of the last grid (int64 bucket_start[ncell+1],
+ * bucket_sites[n]; within a bucket sites are in increasing index order) */
+int pf_grid_export(pf_ctx *ctx, int64_t *bucket_start, int64_t *bucket_sites, void *stream);
+
+/* dpsi = max(psi) - min(psi) (>= 0) into the context's device scalar;
+ * dpsi_host (optional) receives it synchronously. */
+int pf_dpsi_max(pf_ctx *ctx, int64_t n, const double *psi, double *dpsi_host, void *stream);
+
+/* _kernels._batch_evaluate.  Outputs are caller-allocated device arrays with
+ * the reference shapes: status i64[n], vol f64[n], ksur f64[n], cent f64[n,3],
+ * ipt f64[n,3], m2 f64[n], fcount i64[n], ftag i64[n,smf], farea f64[n,smf],
+ * fh f64[n,smf], fnrm f64[n,smf,3], fcent f64[n,smf,3].  Any output may be
+ * NULL (skipped).  dpsi_max < 0 uses the device value of pf_dpsi_max.
+ * rebuild_grid != 0 rebuilds the bucket grid from pts first.
+ * Returns the OR of the per-cell flag words (synchronises the stream). */
+int64_t pf_batch_evaluate(pf_ctx *ctx, int64_t n, const double *pts, const double *psi,
+                          double tol, double dpsi_max, int ball_aware, int want_m2, int64_t smf,
+                          int64_t *status, double *vol, double *ksur, double *cent, double *ipt,
+                          double *m2, int64_t *fcount, int64_t *ftag, double *farea, double *fh,
+                          double *fnrm, double *fcent, int rebuild_grid, void *stream);
+
+/* Extended form: optional subset of cells to evaluate (cells int32[ncells],
+ * original indices; NULL = all), per-cell flag words (cell_flags int32[n],
+ * optional) and the algorithmic-work census (census16 int32[n,16], optional;
+ * slots = SURVEY.md §8(d) S_cell terms). */
+int64_t pf_batch_evaluate_ex(pf_ctx *ctx, int64_t n, const double *pts, const double *psi,
+                             double tol, double dpsi_max, int ball_aware, int want_m2, int64_t smf,
+                             int64_t *status, double *vol, double *ksur, double *cent, double *ipt,
+                             double *m2, int64_t *fcount, int64_t *ftag, double *farea, double *fh,
+                             double *fnrm, double *fcent, const int32_t *cells, int64_t ncells,
+                             int32_t *cell_flags, int32_t *census16, int rebuild_grid, void *stream);
+
+/* Asynchronous lean variant used by the Newton solver: writes vol, ksur and
+ * the restricted facet list (int32 tags / f64 areas, stride smf) and ORs the
+ * flag word into *flags (device int64).  No host synchronisation. */
+int pf_evaluate_lean(pf_ctx *ctx, int64_t n, const double *pts, const double *psi,
+                     int ball_aware, int64_t smf, double *vol, double *ksur, int32_t *fcount,
+                     int32_t *ftag, double *farea, double *cent, int64_t *flags, void *stream);
+
+/* per-cell processed-candidate census of the last evaluation (int32[n]) */
+int pf_last_census(pf_ctx *ctx, int32_t *census, void *stream);
+/* device time (ms) of the cell kernels (both tiers) of the last evaluation */
+int pf_last_cells_ms(pf_ctx *ctx, double *ms_host);
+/* number of cells that overflowed the shared-memory tier in the last evaluation */
+int pf_last_retry_count(pf_ctx *ctx, int64_t *count_host);
+
+/* _kernels._knn for a batch of queries: out_idx i64[nq,k] holds the k
+ * nearest sites (by (d^2, index)) of each query (queries f64[nq,3]); uses the
+ * grid of the last pf_grid_build on pts.  Returns min(k, n). */
+int64_t pf_knn(pf_ctx *ctx, int64_t n, const double *pts, int64_t nq, const double *queries,
+               int64_t k, int64_t *out_idx, void *stream);
+
+/* ---- damped Newton solve for the weights ---------------- */
+typedef struct {
+    int status;           /* 0 converged, 1 max_newton reached, 2 DampingStall, 3 InitFailure */
+    int iterations;       /* accepted Newton steps */
+    int evaluations;      /* cell evaluations (init + every damping trial) */
+    int cg_iterations;    /* total Jacobi-PCG iterations */
+    int damping_halvings; /* rejected KMT trials */
+    int init_doublings;   /* kappa doublings of the cold start */
+    double worst_initial; /* max_i |V_i - nu_i| / nu_i before the first step */
+    double worst_final;
+    double last_alpha;
+    int64_t flags;        /* OR of cell flag words of the last evaluation */
+} pf_newton_stats;
+
+/* g = nu - vol; stats_host[3] = (max |vol-nu|/nu, min vol, min nu) */
+int pf_newton_gradient(int64_t n, const double *nu, const double *vol, double *g,
+                       double *stats_host, void *stream);
+/* ELL Hessian rows from a lean evaluation: H_ij = -|B_ij|/(2 D_ij) (site facets only,
+ * compacted to hcnt[i] entries), diag = sum_j |B_ij|/(2 D_ij) + |K_i|/(2 sqrt(max(psi, tau))) */
+int pf_newton_hessian(int64_t n, int smf, const double *pts, const double *psi, const int32_t *fcount,
+                      const int32_t *ftag, const double *farea, const double *ksur, double tau_psi,
+                      int32_t *hcnt, int32_t *hcol, double *hval, double *diag, void *stream);
+/* Jacobi-PCG, x = H^-1 b to ||r|| <= rtol ||b||; returns the iteration count */
+int pf_pcg(int64_t n, int smf, const int32_t *hcnt, const int32_t *hcol, const double *hval,
+           const double *diag, const double *b, double *x, double rtol, int max_iter, void *stream);
+/* full solve: psi (device, in/out) to max_i |V_i - nu_i|/nu_i <= eps_vol;
+ * cold_start != 0 initialises psi = kappa (3 nu / 4 pi)^(2/3) (kappa doubling) */
+int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const double *nu, double *psi,
+                    int cold_start, double eps_vol, int max_newton, int smf, double tau_psi,
+                    int ball_aware, pf_newton_stats *stats, void *stream);
+/* vol / ksur / restricted facets of the solve's final evaluation */
+int pf_newton_last_state(double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
+                         int64_t n, int smf, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POTFLOW_B200_H */

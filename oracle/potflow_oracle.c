@@ -1039,8 +1039,9 @@ i64 pfo_batch_evaluate(i64 n, const double *pts, const double *psi,
                        int ball_aware, int want_m2, i64 smf,
                        i64 *status, double *vol, double *ksur, double *cent, double *ipt, double *m2,
                        i64 *fcount, i64 *ftag, double *farea_o, double *fh_o, double *fnrm,
-                       double *fcent_o, i64 i0, i64 i1, i64 *clip_count) {
-    if (i1 <= i0) { i0 = 0; i1 = n; }
+                       double *fcent_o, i64 i0, i64 i1, i64 *clip_count, const i64 *cells) {
+    /* cells != NULL: evaluate only cells[i0..i1) (a bounded sample) */
+    if (i1 <= i0) { i0 = 0; i1 = cells ? 0 : n; }
     Domain *D = (Domain *)malloc(sizeof(Domain));
     domain_load(D, dv, dc, dp, dt, dlp, dlv);
     Grid G = {grid_start, grid_sites, lox, loy, loz, ihx, ihy, ihz, gnx, gny, gnz, h_min};
@@ -1051,11 +1052,12 @@ i64 pfo_batch_evaluate(i64 n, const double *pts, const double *psi,
         w->cand_d2 = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
         w->cand_j = (i64 *)malloc(sizeof(i64) * (size_t)(n > 0 ? n : 1));
 #pragma omp for schedule(dynamic, 64)
-        for (i64 i = i0; i < i1; i++) {
+        for (i64 ii = i0; ii < i1; ii++) {
+            const i64 i = cells ? cells[ii] : ii;
             int which;
             int st = build_cell(i, n, pts, psi, dpsi_max, ball_aware, D, &G, tol, w, &which);
             if (clip_count) clip_count[i] = w->n_clips;
-            i64 li = i - i0;
+            i64 li = ii - i0;
             if (st == 3) {
                 flags_all[li] = FLAG_OVERFLOW;
                 status[i] = CELL_EMPTY; vol[i] = 0.0; ksur[i] = 0.0; fcount[i] = 0;

@@ -42,7 +42,7 @@ def lib():
         L.pfo_batch_evaluate.argtypes = (
             [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
              d, d, d, d, d, d, i64, i64, i64, d, d, d, C.c_int, C.c_int, i64]
-            + [vp] * 12 + [i64, i64, vp])
+            + [vp] * 12 + [i64, i64, vp, vp])
         L.pfo_batch_build.restype = i64
         L.pfo_batch_build.argtypes = (
             [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
@@ -138,8 +138,9 @@ def batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
                    gnx, gny, gnz, h_min, tol, dpsi_max_, ball_aware, want_m2, smf,
                    status, vol, ksur, cent, ipt, m2,
                    fcount, ftag, farea_o, fh_o, fnrm, fcent_o,
-                   i0=0, i1=0, clip_count=None):
-    """_kernels._batch_evaluate (_kernels.py:1362-1478); optional [i0, i1) cell range."""
+                   i0=0, i1=0, clip_count=None, cells=None):
+    """_kernels._batch_evaluate (_kernels.py:1362-1478); optional [i0, i1) cell range
+    (of ``cells`` when given: a bounded sample of cell indices)."""
     f8, i8 = np.float64, np.int64
     n = len(pts)
     args = [_chk(pts, f8), _chk(psi, f8), _chk(dv, f8), _chk(dc, i8), _chk(dp, f8),
@@ -153,7 +154,8 @@ def batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
     return int(lib().pfo_batch_evaluate(
         n, *[_p(a) for a in args], lox, loy, loz, ihx, ihy, ihz, gnx, gny, gnz, h_min, tol,
         dpsi_max_, int(bool(ball_aware)), int(bool(want_m2)), int(smf),
-        *[_p(a) for a in outs], int(i0), int(i1), _p(clip_count)))
+        *[_p(a) for a in outs], int(i0), int(i1), _p(clip_count),
+        _p(None if cells is None else _chk(np.ascontiguousarray(cells, np.int64), i8))))
 
 
 def batch_build(pts, psi, dv, dc, dp, dt, dlp, dlv,
@@ -214,7 +216,7 @@ OUT_ORDER = ("status", "vol", "ksur", "cent", "ipt", "m2",
 
 
 def evaluate(pts, psi, domain_pack_args, tol, grid: SpatialGrid, ball_aware=True,
-             want_m2=True, smf=32, dpsi=None, i0=0, i1=0, clip_count=None):
+             want_m2=True, smf=32, dpsi=None, i0=0, i1=0, clip_count=None, cells=None):
     """Convenience wrapper: allocate outputs and run batch_evaluate."""
     pts = np.ascontiguousarray(pts, np.float64)
     psi = np.ascontiguousarray(psi, np.float64)
@@ -224,6 +226,6 @@ def evaluate(pts, psi, domain_pack_args, tol, grid: SpatialGrid, ball_aware=True
         dpsi = dpsi_max(psi)
     err = batch_evaluate(pts, psi, *domain_pack_args, *grid.kernel_args(), tol, dpsi,
                          ball_aware, want_m2, smf, *[o[k] for k in OUT_ORDER],
-                         i0=i0, i1=i1, clip_count=clip_count)
+                         i0=i0, i1=i1, clip_count=clip_count, cells=cells)
     o["err"] = err
     return o

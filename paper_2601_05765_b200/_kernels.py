@@ -1,0 +1,132 @@
+"""Drop-in replacement of the reference's ``potflow._kernels`` batch entry points.
+
+Same function names, same positional arguments, same output arrays and the
+same returned flag word as /root/reference/pkg/src/potflow/_kernels.py, but
+the work runs on the B200 through libpotflow_b200.so:
+
+* ``_batch_evaluate``  _kernels.py:1362-1478 -> pf_batch_evaluate
+* ``_knn``             _kernels.py:1562-1620 -> pf_knn
+
+Arrays may be numpy (copied to the device and back, as a drop-in for the numba
+call) or torch CUDA tensors (used in place, no host round trip).  The host
+grid arguments (grid_start ... h_min) are accepted for signature
+compatibility; the device builds its own bucket grid from ``pts`` because the
+processed-candidate order is the global (d^2, j) order either way
+(_kernels.py:1293-1304), so results do not depend on the bucket layout.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .laguerre import upload_domain
+
+MAX_V, MAX_F, MAX_L, MAX_P = 512, 160, 2048, 256
+CLIP_CUT, CLIP_UNTOUCHED, CLIP_EMPTY, CLIP_OVERFLOW, CLIP_DEGENERATE = 0, 1, 2, 3, 4
+RF_OUTSIDE, RF_UNTOUCHED, RF_FULLCIRCLE, RF_GENPOLY = 0, 1, 2, 3
+CELL_EMPTY, CELL_FULLBALL, CELL_CLIPPED = 0, 1, 2
+FLAG_OVERFLOW, FLAG_DEGENERATE_INTERIOR, FLAG_UNSTABLE_PROJECTION = 1, 2, 4
+
+
+def _is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _to_dev(x, dtype):
+    import torch
+
+    if _is_torch(x):
+        if x.device.type != "cuda" or x.dtype != dtype or not x.is_contiguous():
+            raise TypeError("torch inputs must be contiguous CUDA tensors of the reference dtype")
+        return x
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+def _host(x):
+    if _is_torch(x):
+        return x.detach().cpu().numpy()
+    return np.asarray(x)
+
+
+def _batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
+                    grid_start, grid_sites, lox, loy, loz, ihx, ihy, ihz,
+                    gnx, gny, gnz, h_min, tol, dpsi_max, ball_aware, want_m2,
+                    smf,
+                    status, vol, ksur, cent, ipt, m2,
+                    fcount, ftag, farea_o, fh_o, fnrm, fcent_o):
+    """Build and evaluate every restricted cell (see module docstring)."""
+    import torch
+
+    f8, i8 = torch.float64, torch.int64
+    outs_host = [status, vol, ksur, cent, ipt, m2, fcount, ftag, farea_o, fh_o, fnrm, fcent_o]
+    dtypes = [i8, f8, f8, f8, f8, f8, i8, i8, f8, f8, f8, f8]
+    on_device = _is_torch(pts)
+    c = _lib.ctx()
+    upload_domain(c, _host(dv), _host(dc), _host(dp), _host(dt), _host(dlp), _host(dlv), float(tol))
+    if on_device:
+        p = _to_dev(pts, f8)
+        w = _to_dev(psi, f8)
+        outs = [_to_dev(o, t) for o, t in zip(outs_host, dtypes)]
+    else:
+        p = torch.from_numpy(np.ascontiguousarray(pts, np.float64)).to("cuda", non_blocking=True)
+        w = torch.from_numpy(np.ascontiguousarray(psi, np.float64)).to("cuda", non_blocking=True)
+        outs = [torch.empty(o.shape, dtype=t, device="cuda") for o, t in zip(outs_host, dtypes)]
+    n = int(p.shape[0])
+    cflags = torch.empty(n, dtype=torch.int32, device="cuda")
+    err = int(_lib.lib().pf_batch_evaluate_ex(
+        c, n, _lib.ptr(p), _lib.ptr(w), float(tol), float(dpsi_max), int(bool(ball_aware)),
+        int(bool(want_m2)), int(smf), *[_lib.ptr(o) for o in outs], None, 0, _lib.ptr(cflags),
+        None, 1, _lib.stream_ptr()))
+    _lib.check(err, "pf_batch_evaluate_ex")
+    if not on_device:
+        # the reference leaves cent/ipt/m2 of capacity-overflowed cells
+        # untouched (_kernels.py:1393-1399): keep the caller's values there
+        keep = None
+        if err & FLAG_OVERFLOW:
+            keep = ((cflags & 512) != 0).cpu().numpy()  # FLAG_BUILD_OVERFLOW (pf_cell.cuh)
+        for k, (h, d) in enumerate(zip(outs_host, outs)):
+            if keep is not None and k in (3, 4, 5) and keep.any():
+                src = d.cpu().numpy().reshape(h.shape)
+                src[keep] = h[keep]
+                h[...] = src
+            elif isinstance(h, np.ndarray) and h.flags.c_contiguous and h.flags.writeable:
+                torch.from_numpy(h).copy_(d.view(h.shape))  # straight D2H into the caller's buffer
+            else:
+                h[...] = d.cpu().numpy().reshape(h.shape)
+    return err
+
+
+def _knn(pts, grid_start, grid_sites, lox, loy, loz, ihx, ihy, ihz,
+         gnx, gny, gnz, h_min, qx, qy, qz, k, out_idx):
+    """Exact k nearest sites of one query (writes out_idx, returns the count)."""
+    import torch
+
+    from .geom import box_domain
+
+    p = _to_dev(pts, torch.float64)
+    n = int(p.shape[0])
+    kk = min(int(k), n)
+    if kk <= 0:
+        return 0
+    lo = np.array([lox, loy, loz], dtype=np.float64)
+    hi = lo + np.array([gnx / ihx, gny / ihy, gnz / ihz])
+    from .laguerre import domain_pack
+
+    dom = box_domain(lo, hi)
+    dpk = domain_pack(dom)
+    c = _lib.ctx()
+    upload_domain(c, *dpk.args(), dpk.tol)
+    q = torch.tensor([[qx, qy, qz]], dtype=torch.float64, device="cuda")
+    res = torch.empty((1, kk), dtype=torch.int64, device="cuda")
+    got = _lib.check(_lib.lib().pf_knn(c, n, _lib.ptr(p), 1, _lib.ptr(q), kk, _lib.ptr(res),
+                                       _lib.stream_ptr()), "pf_knn")
+    vals = res[0, :got]
+    if _is_torch(out_idx):
+        out_idx[:got] = vals
+    else:
+        out_idx[:got] = vals.cpu().numpy()
+    return int(got)

@@ -40,6 +40,9 @@ enum { FLAG_OVERFLOW = 1, FLAG_DEGENERATE_INTERIOR = 2, FLAG_UNSTABLE_PROJECTION
 // internal: a capacity of this (small, shared-memory) instantiation was
 // exceeded; the cell is queued for the reference-capacity instantiation.
 enum { FLAG_RETRY = 256 };
+// per-cell flag only: the Laguerre cell itself overflowed (build status 3);
+// the reference then writes status/vol/ksur/fcount but not cent/ipt/m2
+enum { FLAG_BUILD_OVERFLOW = 512 };
 
 #define PF_PI 3.141592653589793
 #define PF_FOUR_PI (4.0 * PF_PI)
@@ -109,6 +112,14 @@ struct WS {
         EvalScratch<C> e;
     } u;
     int oflow;  // capacity overflow seen by any lane
+    int cen_on;   // census requested for this cell
+    int cen[16];  // algorithmic-work census (SURVEY.md §8(d) S_cell terms)
+};
+
+// census slots:
+enum {
+    CEN_CLIPS = 0, CEN_TESTS, CEN_NEWV, CEN_NFV, CEN_RFAR, CEN_CUTS, CEN_LOOP, CEN_CROSS,
+    CEN_RFAC, CEN_RFAC_NF, CEN_SEG, CEN_ARC, CEN_BPTS, CEN_PROJ, CEN_FULLC, CEN_N
 };
 
 // ---------------------------------------------------------------------------
@@ -133,8 +144,11 @@ struct CellIn {
     const int *dt, *dlp, *dlv;
     int dnv, dnf, dnl;
     double tol, dpsi;
+    const double *dpsi_ptr;  // when set, dpsi is read from device memory
     int ball_aware, want_m2;
     double t_init;  // first shell radius^2 when not ball-aware
+    const int *cells;  // optional: evaluate only these cells (original indices)
+    int ncells;
 };
 
 struct CellOut {
@@ -149,6 +163,7 @@ struct CellOut {
     int *fcount32;  // [n]
     int *flags;     // [n] per-cell flag word (incl. FLAG_RETRY)
     int *census;    // [n] processed candidates (clips attempted)
+    int *census16;  // [n, 16] full census (CEN_*), optional
 };
 
 PF_DEV double sq(double x) { return x * x; }
@@ -209,6 +224,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     const int L = pfw::lane();
     const unsigned lt = pfw::lanemask_lt();
     const int nv = A.nv, nf = A.nf;
+    if (ws->cen_on && L == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += nv; }
 
     // 1. classify vertices (_kernels.py:121-134)
     int n_out = 0;
@@ -332,6 +348,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
         NFirst += pfw::popc(m);
     }
     const int NVB = K + NFirst;
+    if (ws->cen_on && L == 0) ws->cen[CEN_NEWV] += NFirst;
     if (NVB > C::CV || NFk > C::CF || NLk > C::CL) {
         if (!C::EXACT && L == 0) ws->oflow = 1;
         pfw::sync();
@@ -446,7 +463,10 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
         for (int k = L; k < NL2; k += 32) B.lv[k] = (uint16_t)(S.vmap[B.lv[k]] - 2);
         nref = base;
     }
-    if (L == 0) { B.nv = nref; B.nf = NF2; B.nl = NL2; }
+    if (L == 0) {
+        B.nv = nref; B.nf = NF2; B.nl = NL2;
+        if (ws->cen_on) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += nref; }
+    }
     pfw::sync();
     return CLIP_CUT;
 }
@@ -570,7 +590,7 @@ template <class C>
 PF_DEV int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int *nclips) {
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const double psii = in.psi[i];
-    const double tol = in.tol, dpsi = in.dpsi;
+    const double tol = in.tol, dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
     load_domain(ws->P[0], in);
     int which = 0;
     *nclips = 0;
@@ -1118,6 +1138,29 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         res->flags = FLAG_RETRY;
         return;
     }
+    if (ws->cen_on) {
+        int cross = 0, seg = 0, arc = 0, bp = 0, proj = 0, fc = 0;
+        for (int f = L; f < nf; f += 32) {
+            int k = E.fkind[f];
+            if (k == RF_FULLCIRCLE) fc++;
+            if ((k == RF_GENPOLY || k == RF_UNTOUCHED) && E.fnp[f] > 0) {
+                int i = E.fhead[f];
+                for (int t = 0; t < E.fnp[f]; t++) {
+                    bp++;
+                    if (E.pfl[i] & PF_ONSPH) cross++; else proj++;
+                    if (E.pfl[i] & PF_CONN) arc++; else seg++;
+                    i = E.pnext[i];
+                }
+            }
+        }
+        cross = pfw::sum_i(cross); seg = pfw::sum_i(seg); arc = pfw::sum_i(arc);
+        bp = pfw::sum_i(bp); proj = pfw::sum_i(proj); fc = pfw::sum_i(fc);
+        if (L == 0) {
+            ws->cen[CEN_LOOP] += P.nl; ws->cen[CEN_CROSS] += cross; ws->cen[CEN_SEG] += seg;
+            ws->cen[CEN_ARC] += arc; ws->cen[CEN_BPTS] += bp; ws->cen[CEN_PROJ] += proj;
+            ws->cen[CEN_FULLC] += fc;
+        }
+    }
     if (pfw::any(ovf)) {  // reference: first facet with kind < 0 aborts the cell
         res->flags = FLAG_OVERFLOW;
         return;
@@ -1279,9 +1322,13 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
 // reference-capacity instantiation.
 // ---------------------------------------------------------------------------
 template <class C>
-PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
     const int L = pfw::lane();
-    if (L == 0) ws->oflow = 0;
+    if (L == 0) {
+        ws->oflow = 0;
+        ws->cen_on = out.census16 != nullptr;
+        for (int k = 0; k < 16; k++) ws->cen[k] = 0;
+    }
     pfw::sync();
     int which, nclips;
     int st = build_cell(ws, in, i, &which, &nclips);
@@ -1299,9 +1346,8 @@ PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
             if (out.ksur) out.ksur[i] = 0.0;
             if (out.fcount) out.fcount[i] = 0;
             if (out.fcount32) out.fcount32[i] = 0;
-            if (out.flags) out.flags[i] = FLAG_OVERFLOW;
         }
-        return FLAG_OVERFLOW;
+        return FLAG_OVERFLOW | FLAG_BUILD_OVERFLOW;
     }
     if (st == 1) {
         if (L == 0) {
@@ -1359,8 +1405,10 @@ PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
             }
             nk += pfw::popc(m);
         }
+        if (ws->cen_on && L == 0) { ws->cen[CEN_RFAC] += nk; ws->cen[CEN_RFAC_NF] += nk * P.nf; }
         if (nk > smf) { nk = smf; flags |= FLAG_OVERFLOW; }
     }
+
     if (L == 0) {
         if (out.fcount) out.fcount[i] = nk;
         if (out.fcount32) out.fcount32[i] = nk;
@@ -1368,6 +1416,18 @@ PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
     }
     pfw::sync();
     return flags;
+}
+
+template <class C>
+PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+    int r = run_cell_impl(ws, in, out, i);
+    if (!(r & FLAG_RETRY) && pfw::lane() == 0) {
+        if (out.census16)
+            for (int k = 0; k < 16; k++) out.census16[(size_t)i * 16 + k] = k < CEN_N ? ws->cen[k] : 0;
+        if (out.flags) out.flags[i] = r;
+    }
+    pfw::sync();
+    return r;
 }
 
 }  // namespace pf

@@ -1,0 +1,481 @@
+// pf_newton.cu -- damped Newton (KMT) solve for the Laguerre weights on the
+// device (the reference ships the
+// algorithm only as specification).
+//
+//   g_i  = nu_i - |V_i|
+//   H    = -grad^2 K:  H_ij = -1/2 |B_ij| / |p_j - p_i|        (PAPER Eq. 2)
+//          H_ii = sum_j 1/2 |B_ij| / |p_j - p_i| + 1/2 |K_i| / sqrt(max(psi_i, tau_psi))
+//   H u = g by Jacobi-preconditioned CG, rtol 1e-3 (1e-4 once worst < 10 eps)
+//   psi <- psi + alpha u, alpha halved until min_i |V_i| >= 1/2 min(min nu, min |V(psi0)|)
+//
+// Matrix layout: the cell kernel's restricted-facet list is an ELL matrix
+// (row = cell, stride smf, int32 columns, f64 values); assembly compacts each
+// row to its site facets.  All reductions are two-level with a fixed block
+// count, so every number is bitwise reproducible run to run.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/potflow_b200.h"
+
+extern unsigned long long pf_internal_launches_add(unsigned long long k);
+extern int pf_internal_set_err(const char *msg);
+
+namespace {
+
+constexpr int RB = 256;      // threads per block for vector kernels
+constexpr int NPART = 1024;  // fixed number of partial sums (deterministic reductions)
+
+#define NCK(x)                                                                       \
+    do {                                                                             \
+        cudaError_t _e = (x);                                                        \
+        if (_e != cudaSuccess) {                                                     \
+            char _b[256];                                                            \
+            snprintf(_b, sizeof _b, "%s:%d %s: %s", __FILE__, __LINE__, #x,         \
+                     cudaGetErrorString(_e));                                        \
+            return pf_internal_set_err(_b);                                          \
+        }                                                                            \
+    } while (0)
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++) s += sh[k];
+    __syncthreads();
+    return s;
+}
+__device__ __forceinline__ double block_max(double v, double *sh) {
+    for (int m = 16; m > 0; m >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, m));
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double s = -INFINITY;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++) s = fmax(s, sh[k]);
+    __syncthreads();
+    return s;
+}
+__device__ __forceinline__ double block_min(double v, double *sh) {
+    return -block_max(-v, sh);
+}
+
+// gradient, worst relative volume error, min volume (partials per block)
+__global__ void __launch_bounds__(RB) k_grad(int64_t n, const double *__restrict__ nu,
+                                            const double *__restrict__ vol, double *__restrict__ g,
+                                            double *__restrict__ part) {
+    __shared__ double sh[32];
+    double worst = 0.0, vmin = INFINITY, nmin = INFINITY;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        double v = vol[i], t = nu[i];
+        if (g) g[i] = t - v;
+        worst = fmax(worst, fabs(v - t) / t);
+        vmin = fmin(vmin, v);
+        nmin = fmin(nmin, t);
+    }
+    double a = block_max(worst, sh), b = block_min(vmin, sh), c = block_min(nmin, sh);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = a;
+        part[NPART + blockIdx.x] = b;
+        part[2 * NPART + blockIdx.x] = c;
+    }
+}
+
+// final reduce of the three partial arrays -> out[0]=worst, out[1]=min vol, out[2]=min nu
+__global__ void k_grad_fin(const double *__restrict__ part, int nb, double *out) {
+    __shared__ double sh[32];
+    double a = 0.0, b = INFINITY, c = INFINITY;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        a = fmax(a, part[k]);
+        b = fmin(b, part[NPART + k]);
+        c = fmin(c, part[2 * NPART + k]);
+    }
+    a = block_max(a, sh);
+    b = block_min(b, sh);
+    c = block_min(c, sh);
+    if (threadIdx.x == 0) { out[0] = a; out[1] = b; out[2] = c; }
+}
+
+// Hessian rows: compact site facets of each cell's restricted-facet list
+__global__ void __launch_bounds__(RB) k_hessian(int64_t n, int smf, const double *__restrict__ pts,
+                                               const double *__restrict__ psi,
+                                               const int *__restrict__ fcount,
+                                               const int *__restrict__ ftag,
+                                               const double *__restrict__ farea,
+                                               const double *__restrict__ ksur, double tau_psi,
+                                               int *__restrict__ hcnt, int *__restrict__ hcol,
+                                               double *__restrict__ hval, double *__restrict__ diag) {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        const double px = pts[3 * i], py = pts[3 * i + 1], pz = pts[3 * i + 2];
+        int c = fcount[i];
+        if (c > smf) c = smf;
+        double d = 0.0;
+        int k = 0;
+        for (int s = 0; s < c; s++) {
+            int j = ftag[i * smf + s];
+            if (j < 0) continue;
+            double dx = pts[3 * j] - px, dy = pts[3 * j + 1] - py, dz = pts[3 * j + 2] - pz;
+            double w = 0.5 * farea[i * smf + s] / sqrt(dx * dx + dy * dy + dz * dz);
+            hcol[i * smf + k] = j;
+            hval[i * smf + k] = -w;
+            d += w;
+            k++;
+        }
+        double ps = psi[i] > tau_psi ? psi[i] : tau_psi;
+        d += 0.5 * ksur[i] / sqrt(ps);
+        // an empty cell has no volume derivative; regularise with the free
+        // ball's d|V|/dpsi = 2 pi sqrt(psi) so Jacobi/CG stay defined
+        if (!(d > 0.0)) d = 2.0 * 3.141592653589793 * sqrt(ps);
+        diag[i] = d;
+        hcnt[i] = k;
+    }
+}
+
+// ---- Jacobi PCG (device scalars; `done` short-circuits after convergence) ----
+// sc: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] bb, [6] rr_new, [7] rz_new
+// ic: [0] done flag, [1] iterations
+
+__global__ void __launch_bounds__(RB) k_pcg_init(int64_t n, const double *__restrict__ b,
+                                                const double *__restrict__ diag, double *__restrict__ x,
+                                                double *__restrict__ r, double *__restrict__ z,
+                                                double *__restrict__ p, double *__restrict__ part) {
+    __shared__ double sh[32];
+    double rz = 0.0, bb = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        double bi = b[i], zi = bi / diag[i];
+        x[i] = 0.0;
+        r[i] = bi;
+        z[i] = zi;
+        p[i] = zi;
+        rz += bi * zi;
+        bb += bi * bi;
+    }
+    double a = block_sum(rz, sh), c = block_sum(bb, sh);
+    if (threadIdx.x == 0) { part[blockIdx.x] = a; part[NPART + blockIdx.x] = c; }
+}
+
+__global__ void k_sum2(const double *__restrict__ part, int nb, double *out0, double *out1) {
+    __shared__ double sh[32];
+    double a = 0.0, b = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) { a += part[k]; b += part[NPART + k]; }
+    a = block_sum(a, sh);
+    b = block_sum(b, sh);
+    if (threadIdx.x == 0) { *out0 = a; if (out1) *out1 = b; }
+}
+
+// Ap = H p and partial p.Ap
+__global__ void __launch_bounds__(RB) k_spmv(int64_t n, int smf, const int *__restrict__ hcnt,
+                                            const int *__restrict__ hcol, const double *__restrict__ hval,
+                                            const double *__restrict__ diag, const double *__restrict__ p,
+                                            double *__restrict__ Ap, double *__restrict__ part,
+                                            const int *__restrict__ ic) {
+    if (ic[0]) return;
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        double s = diag[i] * p[i];
+        const int c = hcnt[i];
+        const int *col = hcol + i * smf;
+        const double *val = hval + i * smf;
+        for (int k = 0; k < c; k++) s += val[k] * p[col[k]];
+        Ap[i] = s;
+        acc += p[i] * s;
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void k_alpha(const double *__restrict__ part, int nb, double *sc, const int *ic) {
+    if (ic[0]) return;
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) a += part[k];
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) {
+        sc[1] = a;
+        sc[3] = a != 0.0 ? sc[0] / a : 0.0;
+    }
+}
+
+// x += alpha p ; r -= alpha Ap ; z = r / diag ; partial r.z and r.r
+__global__ void __launch_bounds__(RB) k_update(int64_t n, const double *__restrict__ diag,
+                                              double *__restrict__ x, double *__restrict__ r,
+                                              double *__restrict__ z, const double *__restrict__ p,
+                                              const double *__restrict__ Ap, const double *__restrict__ sc,
+                                              double *__restrict__ part, const int *__restrict__ ic) {
+    if (ic[0]) return;
+    __shared__ double sh[32];
+    const double alpha = sc[3];
+    double rz = 0.0, rr = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        double xi = x[i] + alpha * p[i];
+        double ri = r[i] - alpha * Ap[i];
+        double zi = ri / diag[i];
+        x[i] = xi;
+        r[i] = ri;
+        z[i] = zi;
+        rz += ri * zi;
+        rr += ri * ri;
+    }
+    double a = block_sum(rz, sh), c = block_sum(rr, sh);
+    if (threadIdx.x == 0) { part[blockIdx.x] = a; part[NPART + blockIdx.x] = c; }
+}
+
+// beta, convergence test ||r|| <= rtol ||b||, iteration count
+__global__ void k_beta(const double *__restrict__ part, int nb, double *sc, int *ic, double rtol,
+                       int max_iter) {
+    if (ic[0]) return;
+    __shared__ double sh[32];
+    double a = 0.0, b = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) { a += part[k]; b += part[NPART + k]; }
+    a = block_sum(a, sh);
+    b = block_sum(b, sh);
+    if (threadIdx.x == 0) {
+        sc[4] = sc[0] != 0.0 ? a / sc[0] : 0.0;
+        sc[0] = a;
+        sc[2] = b;
+        ic[1] += 1;
+        if (sqrt(b) <= rtol * sqrt(sc[5]) || ic[1] >= max_iter || !(a == a)) ic[0] = 1;
+    }
+}
+
+__global__ void __launch_bounds__(RB) k_pdir(int64_t n, const double *__restrict__ z, double *__restrict__ p,
+                                            const double *__restrict__ sc, const int *__restrict__ ic) {
+    if (ic[0]) return;
+    const double beta = sc[4];
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        p[i] = z[i] + beta * p[i];
+}
+
+__global__ void __launch_bounds__(RB) k_axpy_to(int64_t n, const double *__restrict__ a, double s,
+                                               const double *__restrict__ b, double *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        out[i] = a[i] + s * b[i];
+}
+
+__global__ void __launch_bounds__(RB) k_cold_psi(int64_t n, const double *__restrict__ nu, double kappa,
+                                                double *__restrict__ psi) {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        psi[i] = kappa * pow(3.0 * nu[i] / (4.0 * 3.141592653589793), 2.0 / 3.0);
+}
+
+template <class T>
+int dalloc(T **p, size_t *cap, size_t n) {
+    if (*p && *cap >= n) return 0;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    NCK(cudaMalloc((void **)p, std::max<size_t>(n, 16) * sizeof(T)));
+    *cap = n;
+    return 0;
+}
+
+struct NewtonWS {
+    double *g = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr;
+    double *diag = nullptr, *hval = nullptr, *farea = nullptr, *vol = nullptr, *ksur = nullptr;
+    double *psi_t = nullptr, *vol_t = nullptr, *ksur_t = nullptr, *farea_t = nullptr;
+    int *hcnt = nullptr, *hcol = nullptr, *fcount = nullptr, *ftag = nullptr;
+    int *fcount_t = nullptr, *ftag_t = nullptr;
+    double *part = nullptr, *sc = nullptr, *red = nullptr;
+    int *ic = nullptr;
+    int64_t *flags = nullptr;
+    size_t c[24] = {0};
+};
+NewtonWS g_ws;
+
+int ws_alloc(int64_t n, int smf) {
+    NewtonWS &w = g_ws;
+    size_t N = n, E = (size_t)n * smf;
+    int rc = 0;
+    rc |= dalloc(&w.g, &w.c[0], N); rc |= dalloc(&w.x, &w.c[1], N); rc |= dalloc(&w.r, &w.c[2], N);
+    rc |= dalloc(&w.z, &w.c[3], N); rc |= dalloc(&w.p, &w.c[4], N); rc |= dalloc(&w.Ap, &w.c[5], N);
+    rc |= dalloc(&w.diag, &w.c[6], N); rc |= dalloc(&w.hval, &w.c[7], E); rc |= dalloc(&w.farea, &w.c[8], E);
+    rc |= dalloc(&w.vol, &w.c[9], N); rc |= dalloc(&w.ksur, &w.c[10], N); rc |= dalloc(&w.psi_t, &w.c[11], N);
+    rc |= dalloc(&w.vol_t, &w.c[12], N); rc |= dalloc(&w.ksur_t, &w.c[13], N);
+    rc |= dalloc(&w.farea_t, &w.c[14], E); rc |= dalloc(&w.hcnt, &w.c[15], N);
+    rc |= dalloc(&w.hcol, &w.c[16], E); rc |= dalloc(&w.fcount, &w.c[17], N); rc |= dalloc(&w.ftag, &w.c[18], E);
+    rc |= dalloc(&w.fcount_t, &w.c[19], N); rc |= dalloc(&w.ftag_t, &w.c[20], E);
+    rc |= dalloc(&w.part, &w.c[21], 3 * NPART); rc |= dalloc(&w.sc, &w.c[22], 16);
+    rc |= dalloc(&w.red, &w.c[23], 16);
+    if (!w.ic) NCK(cudaMalloc(&w.ic, 4 * sizeof(int)));
+    if (!w.flags) NCK(cudaMalloc(&w.flags, sizeof(int64_t)));
+    return rc;
+}
+
+int nblocks(int64_t n) { return (int)std::min<int64_t>(NPART, std::max<int64_t>(1, (n + RB - 1) / RB)); }
+
+// (worst, min vol, min nu) of the current evaluation
+int grad_stats(int64_t n, const double *nu, const double *vol, double *g, double *out_host,
+               cudaStream_t st) {
+    int nb = nblocks(n);
+    pf_internal_launches_add(2);
+    k_grad<<<nb, RB, 0, st>>>(n, nu, vol, g, g_ws.part);
+    k_grad_fin<<<1, 1024, 0, st>>>(g_ws.part, nb, g_ws.red);
+    NCK(cudaMemcpyAsync(out_host, g_ws.red, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    NCK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_newton_gradient(int64_t n, const double *nu, const double *vol, double *g, double *stats_host,
+                       void *stream) {
+    if (ws_alloc(n, 1)) return -1;
+    return grad_stats(n, nu, vol, g, stats_host, (cudaStream_t)stream);
+}
+
+int pf_newton_hessian(int64_t n, int smf, const double *pts, const double *psi, const int32_t *fcount,
+                      const int32_t *ftag, const double *farea, const double *ksur, double tau_psi,
+                      int32_t *hcnt, int32_t *hcol, double *hval, double *diag, void *stream) {
+    pf_internal_launches_add(1);
+    k_hessian<<<nblocks(n), RB, 0, (cudaStream_t)stream>>>(n, smf, pts, psi, fcount, ftag, farea, ksur,
+                                                            tau_psi, hcnt, hcol, hval, diag);
+    NCK(cudaGetLastError());
+    return 0;
+}
+
+// Jacobi-PCG on the ELL Hessian; returns the iteration count (>= 0)
+int pf_pcg(int64_t n, int smf, const int32_t *hcnt, const int32_t *hcol, const double *hval,
+           const double *diag, const double *b, double *x, double rtol, int max_iter, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ws_alloc(n, smf)) return -1;
+    NewtonWS &w = g_ws;
+    int nb = nblocks(n);
+    NCK(cudaMemsetAsync(w.ic, 0, 4 * sizeof(int), st));
+    pf_internal_launches_add(2);
+    k_pcg_init<<<nb, RB, 0, st>>>(n, b, diag, x, w.r, w.z, w.p, w.part);
+    k_sum2<<<1, 1024, 0, st>>>(w.part, nb, w.sc + 0, w.sc + 5);
+    int host_ic[2] = {0, 0};
+    double bb = 0.0;
+    NCK(cudaMemcpyAsync(&bb, w.sc + 5, sizeof(double), cudaMemcpyDeviceToHost, st));
+    NCK(cudaStreamSynchronize(st));
+    if (!(bb > 0.0)) return 0;
+    const int batch = 8;
+    while (true) {
+        for (int t = 0; t < batch; t++) {
+            pf_internal_launches_add(5);
+            k_spmv<<<nb, RB, 0, st>>>(n, smf, hcnt, hcol, hval, diag, w.p, w.Ap, w.part, w.ic);
+            k_alpha<<<1, 1024, 0, st>>>(w.part, nb, w.sc, w.ic);
+            k_update<<<nb, RB, 0, st>>>(n, diag, x, w.r, w.z, w.p, w.Ap, w.sc, w.part, w.ic);
+            k_beta<<<1, 1024, 0, st>>>(w.part, nb, w.sc, w.ic, rtol, max_iter);
+            k_pdir<<<nb, RB, 0, st>>>(n, w.z, w.p, w.sc, w.ic);
+        }
+        NCK(cudaMemcpyAsync(host_ic, w.ic, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        NCK(cudaStreamSynchronize(st));
+        if (host_ic[0]) break;
+    }
+    NCK(cudaGetLastError());
+    return host_ic[1];
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// full solve
+// ---------------------------------------------------------------------------
+extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const double *nu, double *psi,
+                               int cold_start, double eps_vol, int max_newton, int smf, double tau_psi,
+                               int ball_aware, pf_newton_stats *stats, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    pf_newton_stats S;
+    memset(&S, 0, sizeof S);
+    if (n <= 0) { if (stats) *stats = S; return 0; }
+    if (ws_alloc(n, smf)) return -1;
+    NewtonWS &w = g_ws;
+    if (pf_grid_build(ctx, n, pts, cold_start ? nullptr : psi, 0.0, stream)) return -1;
+    auto evaluate = [&](const double *ps, double *vol, double *ksur, int *fcount, int *ftag,
+                        double *farea) -> int {
+        S.evaluations++;
+        return pf_evaluate_lean(ctx, n, pts, ps, ball_aware, smf, vol, ksur, fcount, ftag, farea, nullptr,
+                                w.flags, stream);
+    };
+    double stats3[3];
+    // init_weights: cold kappa doubling until no cell is empty
+    if (cold_start) {
+        double kappa = 1.0;
+        for (;;) {
+            pf_internal_launches_add(1);
+            k_cold_psi<<<nblocks(n), RB, 0, st>>>(n, nu, kappa, psi);
+            if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea)) return -1;
+            if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
+            if (stats3[1] > 0.0) break;
+            kappa *= 2.0;
+            S.init_doublings++;
+            if (kappa > 1024.0) { S.status = 3; if (stats) *stats = S; return 0; }  // InitFailure
+        }
+    } else {
+        if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea)) return -1;
+        if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
+    }
+    const double floor_v = 0.5 * std::min(stats3[2], stats3[1]);
+    S.worst_initial = stats3[0];
+    double worst = stats3[0];
+    for (int it = 0; it < max_newton; it++) {
+        if (worst <= eps_vol) break;
+        // H from the current evaluation, solve H u = g
+        if (pf_newton_hessian(n, smf, pts, psi, w.fcount, w.ftag, w.farea, w.ksur, tau_psi, w.hcnt, w.hcol,
+                              w.hval, w.diag, stream))
+            return -1;
+        double rtol = worst < 10.0 * eps_vol ? 1e-4 : 1e-3;
+        int cg = pf_pcg(n, smf, w.hcnt, w.hcol, w.hval, w.diag, w.g, w.x, rtol, 10000, stream);
+        if (cg < 0) return -1;
+        S.cg_iterations += cg;
+        // KMT damping
+        double alpha = 1.0;
+        bool accepted = false;
+        while (alpha >= 0x1p-20) {
+            pf_internal_launches_add(1);
+            k_axpy_to<<<nblocks(n), RB, 0, st>>>(n, psi, alpha, w.x, w.psi_t);
+            if (evaluate(w.psi_t, w.vol_t, w.ksur_t, w.fcount_t, w.ftag_t, w.farea_t)) return -1;
+            if (grad_stats(n, nu, w.vol_t, w.g, stats3, st)) return -1;
+            if (stats3[1] >= floor_v) { accepted = true; break; }
+            alpha *= 0.5;
+            S.damping_halvings++;
+        }
+        if (!accepted) { S.status = 2; break; }  // DampingStall
+        NCK(cudaMemcpyAsync(psi, w.psi_t, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        std::swap(w.vol, w.vol_t);
+        std::swap(w.ksur, w.ksur_t);
+        std::swap(w.fcount, w.fcount_t);
+        std::swap(w.ftag, w.ftag_t);
+        std::swap(w.farea, w.farea_t);
+        std::swap(w.c[9], w.c[12]);
+        std::swap(w.c[10], w.c[13]);
+        std::swap(w.c[17], w.c[19]);
+        std::swap(w.c[18], w.c[20]);
+        std::swap(w.c[8], w.c[14]);
+        S.iterations++;
+        S.last_alpha = alpha;
+        worst = stats3[0];
+    }
+    S.worst_final = worst;
+    if (S.status == 0 && worst > eps_vol) S.status = 1;  // not converged within max_newton
+    int64_t fl = 0;
+    NCK(cudaMemcpyAsync(&fl, w.flags, sizeof fl, cudaMemcpyDeviceToHost, st));
+    NCK(cudaStreamSynchronize(st));
+    S.flags = fl;
+    if (stats) *stats = S;
+    return 0;
+}
+
+extern "C" int pf_newton_last_state(double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
+                                    int64_t n, int smf, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    NewtonWS &w = g_ws;
+    if (vol) NCK(cudaMemcpyAsync(vol, w.vol, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (ksur) NCK(cudaMemcpyAsync(ksur, w.ksur, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (fcount) NCK(cudaMemcpyAsync(fcount, w.fcount, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    if (ftag) NCK(cudaMemcpyAsync(ftag, w.ftag, (size_t)n * smf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    if (farea) NCK(cudaMemcpyAsync(farea, w.farea, (size_t)n * smf * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return 0;
+}

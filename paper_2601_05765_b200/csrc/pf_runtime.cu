@@ -1,0 +1,762 @@
+// pf_runtime.cu -- device runtime of the partial-OT hot path for sm_100a:
+// grid build (counting sort), weight reductions, the two-tier warp-per-cell
+// evaluation kernels, batched kNN, and the C ABI of include/potflow_b200.h.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "pf_tiers.cuh"
+#include "../../include/potflow_b200.h"
+
+using namespace pf;
+
+namespace {
+
+thread_local std::string g_err;
+unsigned long long g_launches = 0;  // kernels launched by this library (bench evidence)
+
+int set_err(const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return -1;
+}
+
+#define CK(x)                                                                       \
+    do {                                                                            \
+        cudaError_t _e = (x);                                                       \
+        if (_e != cudaSuccess)                                                      \
+            return set_err("%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(_e)); \
+    } while (0)
+
+inline cudaStream_t S(void *s) { return (cudaStream_t)s; }
+
+template <class T>
+int ensure(T **p, size_t *cap, size_t count) {
+    if (*cap >= count && *p) return 0;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    size_t c = count < 16 ? 16 : count + count / 4;
+    CK(cudaMalloc((void **)p, c * sizeof(T)));
+    *cap = c;
+    return 0;
+}
+
+}  // namespace
+
+struct pf_ctx {
+    int device = 0;
+    int nsm = 148;
+    // domain (device copies, reference layout with int32 indices)
+    double *dv = nullptr, *dp = nullptr;
+    int *dt = nullptr, *dlp = nullptr, *dlv = nullptr;
+    int dnv = 0, dnf = 0, dnl = 0;
+    double tol = 0.0;
+    double dlo[3] = {0, 0, 0}, dhi[3] = {1, 1, 1};
+    double dvol = 1.0;
+    bool has_domain = false;
+    // grid
+    double *sx = nullptr, *sy = nullptr, *sz = nullptr;
+    size_t sx_cap = 0, sy_cap = 0, sz_cap = 0;
+    int *sid = nullptr, *bid = nullptr;
+    size_t sid_cap = 0, bid_cap = 0;
+    int *bcount = nullptr, *bstart = nullptr;
+    size_t bcount_cap = 0, bstart_cap = 0;
+    int *scan_tmp = nullptr;
+    size_t scan_tmp_cap = 0;
+    int64_t grid_n = -1;
+    const double *grid_pts = nullptr;
+    int gn[3] = {1, 1, 1};
+    double glo[3] = {0, 0, 0}, gh[3] = {1, 1, 1}, gih[3] = {1, 1, 1};
+    // reductions / scalars (device): [0] dpsi, [1..2] ordered min/max, [3] sum
+    double *dscal = nullptr;
+    unsigned long long *mm = nullptr;
+    // evaluation scratch
+    int *retry_list = nullptr;
+    size_t retry_cap = 0;
+    int *counters = nullptr;  // [0] retry count
+    unsigned long long *err = nullptr;
+    int *census = nullptr;
+    size_t census_cap = 0;
+    WS<ExactCaps> *exact_ws = nullptr;
+    int exact_warps = 0;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool ev_valid = false;
+    int fast_blocks = 0;
+    bool attr_set = false;
+};
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int FAST_WARPS = 4;
+constexpr int EXACT_WARPS = 2;
+
+__device__ __forceinline__ unsigned long long ord_bits(double x) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long o) {
+    unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+    return __longlong_as_double((long long)b);
+}
+
+__global__ void k_minmax(const double *__restrict__ v, int64_t n, unsigned long long *mm) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double x = v[i];
+        lo = x < lo ? x : lo;
+        hi = x > hi ? x : hi;
+    }
+    for (int m = 16; m > 0; m >>= 1) {
+        double a = __shfl_xor_sync(0xffffffffu, lo, m), b = __shfl_xor_sync(0xffffffffu, hi, m);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], ord_bits(lo));
+        atomicMax(&mm[1], ord_bits(hi));
+    }
+}
+
+// dpsi = max(hi - lo, 0) (laguerre.py:142-145); empty -> 0
+__global__ void k_dpsi_finish(const unsigned long long *mm, int64_t n, double *dscal) {
+    double lo = ord_val(mm[0]), hi = ord_val(mm[1]);
+    double d = n > 0 ? hi - lo : 0.0;
+    dscal[0] = d > 0.0 ? d : 0.0;
+    dscal[1] = lo;
+    dscal[2] = hi;
+}
+
+__global__ void k_sum_sqrt(const double *__restrict__ v, int64_t n, double *out) {
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        s += v[i] > 0.0 ? sqrt(v[i]) : 0.0;
+    for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+__global__ void k_grid_bucket(const double *__restrict__ pts, int64_t n, double lo0, double lo1,
+                              double lo2, double ih0, double ih1, double ih2, int g0, int g1, int g2,
+                              int *__restrict__ bid, int *__restrict__ bcount) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int a = bucket_coord(pts[3 * i], lo0, ih0, g0);
+        int b = bucket_coord(pts[3 * i + 1], lo1, ih1, g1);
+        int c = bucket_coord(pts[3 * i + 2], lo2, ih2, g2);
+        int l = (a * g1 + b) * g2 + c;
+        bid[i] = l;
+        atomicAdd(&bcount[l], 1);
+    }
+}
+
+// exclusive scan, block-local (1024 threads x 4 items); block sums to `sums`
+constexpr int SCAN_T = 1024, SCAN_I = 4, SCAN_B = SCAN_T * SCAN_I;
+
+__device__ __forceinline__ int block_excl_scan(int v, int *total) {
+    __shared__ int wsum[32];
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int s = wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        wsum[lane] = s;
+    }
+    __syncthreads();
+    int base = w > 0 ? wsum[w - 1] : 0;
+    *total = wsum[31];
+    __syncthreads();
+    return base + x - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_blocks(const int *__restrict__ in, int *__restrict__ out,
+                                                        int64_t n, int *__restrict__ sums) {
+    int64_t b0 = (int64_t)blockIdx.x * SCAN_B + (int64_t)threadIdx.x * SCAN_I;
+    int v[SCAN_I], s = 0;
+    for (int k = 0; k < SCAN_I; k++) {
+        v[k] = b0 + k < n ? in[b0 + k] : 0;
+        s += v[k];
+    }
+    int tot;
+    int off = block_excl_scan(s, &tot);
+    for (int k = 0; k < SCAN_I; k++) {
+        if (b0 + k < n) out[b0 + k] = off;
+        off += v[k];
+    }
+    if (threadIdx.x == 0 && sums) sums[blockIdx.x] = tot;
+}
+
+__global__ void k_scan_add(int *__restrict__ out, int64_t n, const int *__restrict__ sums) {
+    int64_t b0 = (int64_t)blockIdx.x * SCAN_B;
+    int add = sums[blockIdx.x];
+    for (int64_t k = threadIdx.x; k < SCAN_B && b0 + k < n; k += blockDim.x) out[b0 + k] += add;
+}
+
+__global__ void k_grid_scatter(const int *__restrict__ bid, int64_t n, const int *__restrict__ bstart,
+                               int *__restrict__ fill, int *__restrict__ sid) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int l = bid[i];
+        int s = bstart[l] + atomicAdd(&fill[l], 1);
+        sid[s] = (int)i;
+    }
+}
+
+// order each bucket by site index (== numpy's stable argsort) and lay out SoA
+__global__ void k_grid_finish(int ncell, const int *__restrict__ bstart, int *__restrict__ sid,
+                              const double *__restrict__ pts, double *__restrict__ sx,
+                              double *__restrict__ sy, double *__restrict__ sz) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        int a = bstart[c], b = bstart[c + 1];
+        for (int k = a + 1; k < b; k++) {
+            int v = sid[k], j = k - 1;
+            while (j >= a && sid[j] > v) { sid[j + 1] = sid[j]; j--; }
+            sid[j + 1] = v;
+        }
+        for (int k = a; k < b; k++) {
+            int i = sid[k];
+            sx[k] = pts[3 * i];
+            sy[k] = pts[3 * i + 1];
+            sz[k] = pts[3 * i + 2];
+        }
+    }
+}
+
+__global__ void k_grid_export(const int *__restrict__ bstart, int ncell, const int *__restrict__ sid,
+                              int64_t n, int64_t *__restrict__ bs64, int64_t *__restrict__ sid64) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = t; c <= ncell; c += st) bs64[c] = bstart[c];
+    for (int64_t i = t; i < n; i += st) sid64[i] = sid[i];
+}
+
+// cells of the fast tier: shared-memory workspace, one warp per cell, cells
+// visited in bucket order (neighbouring warps share candidates through L1/L2)
+__global__ void __launch_bounds__(FAST_WARPS * 32)
+    k_cells_fast(CellIn in, CellOut out, int count, int *__restrict__ retry_list,
+                 int *__restrict__ counters, unsigned long long *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WS<FastCaps> *ws = (WS<FastCaps> *)(smem + (size_t)wid * sizeof(WS<FastCaps>));
+    const int nw = gridDim.x * FAST_WARPS;
+    int fl = 0;
+    for (int t = blockIdx.x * FAST_WARPS + wid; t < count; t += nw) {
+        const int i = in.cells ? in.cells[t] : in.g.sid[t];
+        int r = run_cell<FastCaps>(ws, in, out, i);
+        if (r & FLAG_RETRY) {
+            if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
+        } else {
+            fl |= r & 7;
+        }
+    }
+    if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
+}
+
+// cells that overflowed the fast tier, with the reference's capacities
+__global__ void __launch_bounds__(EXACT_WARPS * 32)
+    k_cells_exact(CellIn in, CellOut out, const int *__restrict__ list, const int *__restrict__ counters,
+                  WS<ExactCaps> *__restrict__ wsbase, unsigned long long *__restrict__ err) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WS<ExactCaps> *ws = wsbase + (size_t)blockIdx.x * EXACT_WARPS + wid;
+    const int count = counters[0];
+    const int nw = gridDim.x * EXACT_WARPS;
+    int fl = 0;
+    for (int t = blockIdx.x * EXACT_WARPS + wid; t < count; t += nw) {
+        int r = run_cell<ExactCaps>(ws, in, out, list[t]);
+        fl |= r & 7;
+    }
+    if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
+}
+
+// exact k nearest of each query by (d^2, j) (_kernels.py:1562-1620), warp per query
+__global__ void __launch_bounds__(EXACT_WARPS * 32)
+    k_knn(CellIn in, int64_t nq, const double *__restrict__ q, int k, double t0,
+          WS<ExactCaps> *__restrict__ wsbase, int64_t *__restrict__ out_idx) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WS<ExactCaps> *ws = wsbase + (size_t)blockIdx.x * EXACT_WARPS + wid;
+    const int nw = gridDim.x * EXACT_WARPS;
+    for (int64_t t = blockIdx.x * EXACT_WARPS + wid; t < nq; t += nw) {
+        const double qx = q[3 * t], qy = q[3 * t + 1], qz = q[3 * t + 2];
+        double tlo = -1.0, thi = t0;
+        int got = 0;
+        for (;;) {
+            bool all = false;
+            int nc = gather_shell(ws, in, -1, qx, qy, qz, tlo, thi, &all);
+            if (nc > ExactCaps::CC) {
+                double base = tlo > 0.0 ? tlo : 0.0;
+                double nt = base + (thi - base) * 0.25;
+                if (!(nt > base) || !(nt < thi)) {  // > CC sites tied at one distance
+                    for (int c = got + lane; c < k; c += 32) out_idx[t * k + c] = -1;
+                    break;
+                }
+                thi = nt;
+                continue;
+            }
+            sort_candidates(ws, nc);
+            // emit the shell's candidates in order
+            int take = nc < k - got ? nc : k - got;
+            for (int c = lane; c < take; c += 32) out_idx[t * k + got + c] = ws->u.b.cj[c];
+            got += take;
+            __syncwarp();
+            if (got >= k || all) break;
+            tlo = thi;
+            thi = thi * 4.0;
+        }
+    }
+}
+
+void fill_cellin(pf_ctx *c, CellIn &in, int64_t n, const double *pts, const double *psi, double tol,
+                 double dpsi, int ball_aware, int want_m2) {
+    memset(&in, 0, sizeof in);
+    in.pts = pts;
+    in.psi = psi;
+    in.n = (int)n;
+    in.g.sx = c->sx; in.g.sy = c->sy; in.g.sz = c->sz; in.g.sid = c->sid; in.g.bstart = c->bstart;
+    for (int a = 0; a < 3; a++) { in.g.lo[a] = c->glo[a]; in.g.ih[a] = c->gih[a]; in.g.gn[a] = c->gn[a]; }
+    in.dv = c->dv; in.dp = c->dp; in.dt = c->dt; in.dlp = c->dlp; in.dlv = c->dlv;
+    in.dnv = c->dnv; in.dnf = c->dnf; in.dnl = c->dnl;
+    in.tol = tol;
+    in.dpsi = dpsi >= 0.0 ? dpsi : 0.0;
+    in.dpsi_ptr = dpsi >= 0.0 ? nullptr : c->dscal;
+    in.ball_aware = ball_aware;
+    in.want_m2 = want_m2;
+    // first shell of the non-ball-aware search: a few bucket edges
+    double h = std::max(c->gh[0], std::max(c->gh[1], c->gh[2]));
+    in.t_init = (3.0 * h) * (3.0 * h);
+}
+
+int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cudaStream_t st) {
+    if (!c->attr_set) {
+        CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cells_fast, FAST_WARPS * 32,
+                                                         FAST_WARPS * sizeof(WS<FastCaps>)));
+        if (nb < 1) return set_err("fast cell kernel cannot be resident");
+        c->fast_blocks = nb * c->nsm;
+        c->exact_warps = c->nsm * EXACT_WARPS;
+        CK(cudaMalloc(&c->exact_ws, (size_t)c->exact_warps * sizeof(WS<ExactCaps>)));
+        c->attr_set = true;
+    }
+    if (ensure(&c->retry_list, &c->retry_cap, (size_t)n + 1)) return -1;
+    CK(cudaMemsetAsync(c->counters, 0, 4 * sizeof(int), st));
+    CK(cudaMemsetAsync(c->err, 0, sizeof(unsigned long long), st));
+    const int64_t count = in.cells ? in.ncells : n;
+    int64_t blocks = std::min<int64_t>(c->fast_blocks, (count + FAST_WARPS - 1) / FAST_WARPS);
+    if (blocks < 1) blocks = 1;
+    if (!c->ev[0]) {
+        CK(cudaEventCreate(&c->ev[0]));
+        CK(cudaEventCreate(&c->ev[1]));
+    }
+    CK(cudaEventRecord(c->ev[0], st));
+    g_launches++;
+    k_cells_fast<<<(int)blocks, FAST_WARPS * 32, FAST_WARPS * sizeof(WS<FastCaps>), st>>>(
+        in, out, (int)count, c->retry_list, c->counters, c->err);
+    CK(cudaGetLastError());
+    g_launches++;
+    k_cells_exact<<<c->exact_warps / EXACT_WARPS, EXACT_WARPS * 32, 0, st>>>(
+        in, out, c->retry_list, c->counters, c->exact_ws, c->err);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev[1], st));
+    c->ev_valid = true;
+    return 0;
+}
+
+int grid_build(pf_ctx *c, int64_t n, const double *pts, const double *psi, double cell_size,
+               cudaStream_t st, const int *dims = nullptr) {
+    if (!c->has_domain) return set_err("pf_grid_build: no domain set");
+    double ext[3];
+    for (int a = 0; a < 3; a++) ext[a] = std::max(c->dhi[a] - c->dlo[a], 1e-300);
+    double H = cell_size;
+    if (!(H > 0.0)) {
+        H = 0.0;
+        if (psi && n > 0) {
+            CK(cudaMemsetAsync(c->dscal + 3, 0, sizeof(double), st));
+            g_launches++;
+            k_sum_sqrt<<<c->nsm * 4, 256, 0, st>>>(psi, n, c->dscal + 3);
+            double sum = 0.0;
+            CK(cudaMemcpyAsync(&sum, c->dscal + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            H = sum / (double)n;  // mean ball radius ~ half the ball-aware search radius
+        }
+        if (!(H > 0.0)) H = 0.5 * std::cbrt(c->dvol / (double)std::max<int64_t>(n, 1));
+    }
+    // bound the bucket count (memory and scan cost): <= 512 per axis, <= 2^24 total
+    int g[3];
+    for (;;) {
+        for (int a = 0; a < 3; a++) g[a] = (int)std::min(512.0, std::max(1.0, std::ceil(ext[a] / H)));
+        if ((double)g[0] * g[1] * g[2] <= 16777216.0) break;
+        H *= 1.25;
+    }
+    if (dims)
+        for (int a = 0; a < 3; a++) g[a] = std::max(1, dims[a]);
+    for (int a = 0; a < 3; a++) {
+        c->gn[a] = g[a];
+        c->glo[a] = c->dlo[a];
+        c->gh[a] = ext[a] / g[a];
+        c->gih[a] = 1.0 / c->gh[a];
+    }
+    const int64_t ncell = (int64_t)g[0] * g[1] * g[2];
+    if (ensure(&c->sx, &c->sx_cap, n) || ensure(&c->sy, &c->sy_cap, n) || ensure(&c->sz, &c->sz_cap, n) ||
+        ensure(&c->sid, &c->sid_cap, n) || ensure(&c->bid, &c->bid_cap, n) ||
+        ensure(&c->bcount, &c->bcount_cap, ncell + 1) || ensure(&c->bstart, &c->bstart_cap, ncell + 1))
+        return -1;
+    int64_t nblk = (ncell + 1 + SCAN_B - 1) / SCAN_B;
+    if (nblk > SCAN_B) return set_err("grid too large for the two-level scan");
+    if (ensure(&c->scan_tmp, &c->scan_tmp_cap, 2 * nblk + 2)) return -1;
+    CK(cudaMemsetAsync(c->bcount, 0, (ncell + 1) * sizeof(int), st));
+    int gb = (int)std::min<int64_t>(c->nsm * 8, (n + 255) / 256 + 1);
+    if (n > 0)
+        g_launches++;
+        k_grid_bucket<<<gb, 256, 0, st>>>(pts, n, c->glo[0], c->glo[1], c->glo[2], c->gih[0], c->gih[1],
+                                          c->gih[2], g[0], g[1], g[2], c->bid, c->bcount);
+    g_launches++;
+    k_scan_blocks<<<(int)nblk, SCAN_T, 0, st>>>(c->bcount, c->bstart, ncell + 1, c->scan_tmp);
+    if (nblk > 1) {
+        g_launches++;
+        k_scan_blocks<<<1, SCAN_T, 0, st>>>(c->scan_tmp, c->scan_tmp + nblk + 1, nblk, nullptr);
+        g_launches++;
+        k_scan_add<<<(int)nblk, 256, 0, st>>>(c->bstart, ncell + 1, c->scan_tmp + nblk + 1);
+    }
+    CK(cudaMemsetAsync(c->bcount, 0, (ncell + 1) * sizeof(int), st));
+    if (n > 0) {
+        g_launches++;
+        k_grid_scatter<<<gb, 256, 0, st>>>(c->bid, n, c->bstart, c->bcount, c->sid);
+        g_launches++;
+        k_grid_finish<<<(int)std::min<int64_t>(c->nsm * 8, (ncell + 255) / 256), 256, 0, st>>>(
+            (int)ncell, c->bstart, c->sid, pts, c->sx, c->sy, c->sz);
+    }
+    CK(cudaGetLastError());
+    c->grid_n = n;
+    c->grid_pts = pts;
+    return 0;
+}
+
+int dpsi_dev(pf_ctx *c, int64_t n, const double *psi, cudaStream_t st) {
+    unsigned long long init[2] = {~0ull, 0ull};
+    CK(cudaMemcpyAsync(c->mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+    g_launches++;
+    if (n > 0) k_minmax<<<c->nsm * 4, 256, 0, st>>>(psi, n, c->mm);
+    g_launches++;
+    k_dpsi_finish<<<1, 1, 0, st>>>(c->mm, n, c->dscal);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// FP64 pipe peak: independent DFMA chains, 8 per thread, no memory traffic
+__global__ void __launch_bounds__(256) k_dfma_peak(double *out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-9, x2 = x0 + 2e-9, x3 = x0 + 3e-9;
+    double x4 = x0 + 4e-9, x5 = x0 + 5e-9, x6 = x0 + 6e-9, x7 = x0 + 7e-9;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    double r = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (r == 1234.5) out[0] = r;  // keep the chains alive
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *pf_version(void) { return "potflow-b200 0.1.0 (sm_100a)"; }
+
+unsigned long long pf_launch_count(void) { return g_launches; }
+
+// measured FP64 FMA throughput of this device (TFLOP/s, FMA = 2 flops)
+int pf_fp64_peak(double *tflops_host, double *ms_host) {
+    const int iters = 4096, threads = 256;
+    int dev = 0, nsm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    int blocks = nsm * 8;
+    double *buf = nullptr;
+    CK(cudaMalloc(&buf, sizeof(double)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    g_launches++;
+    k_dfma_peak<<<blocks, threads>>>(buf, 64, 0.999999, 1e-7);  // warm
+    CK(cudaEventRecord(e0));
+    g_launches++;
+    k_dfma_peak<<<blocks, threads>>>(buf, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    if (tflops_host) *tflops_host = flops / (ms * 1e-3) / 1e12;
+    if (ms_host) *ms_host = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    return 0;
+}
+const char *pf_last_error(void) { return g_err.c_str(); }
+
+int pf_ctx_create(pf_ctx **out, int device) {
+    if (!out) return set_err("pf_ctx_create: null out");
+    CK(cudaSetDevice(device));
+    pf_ctx *c = new pf_ctx();
+    c->device = device;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        delete c;
+        return set_err("pf_ctx_create: device %d is sm_%d%d, this build targets sm_100a", device,
+                       prop.major, prop.minor);
+    }
+    c->nsm = prop.multiProcessorCount;
+    CK(cudaMalloc(&c->dscal, 8 * sizeof(double)));
+    CK(cudaMalloc(&c->mm, 2 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&c->counters, 4 * sizeof(int)));
+    CK(cudaMalloc(&c->err, sizeof(unsigned long long)));
+    CK(cudaMemset(c->dscal, 0, 8 * sizeof(double)));
+    *out = c;
+    return 0;
+}
+
+int pf_ctx_destroy(pf_ctx *c) {
+    if (!c) return 0;
+    void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
+                    c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
+                    c->err, c->census, c->exact_ws};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    delete c;
+    return 0;
+}
+
+int pf_set_domain(pf_ctx *c, const double *dv, const int64_t *dc, const double *dp, const int64_t *dt,
+                  const int64_t *dlp, const int64_t *dlv, double tol) {
+    int nv = (int)dc[0], nf = (int)dc[1], nl = (int)dc[2];
+    if (nv <= 0 || nf <= 0 || nl <= 0 || nv > FastCaps::CV || nf > FastCaps::CF || nl > FastCaps::CL)
+        return set_err("pf_set_domain: domain (%d verts, %d facets, %d loop entries) exceeds the "
+                       "shared-memory cell capacity", nv, nf, nl);
+    int dti[REF_MAX_F], dlpi[REF_MAX_F + 1], dlvi[REF_MAX_L];
+    for (int f = 0; f < nf; f++) dti[f] = (int)dt[f];
+    for (int f = 0; f <= nf; f++) dlpi[f] = (int)dlp[f];
+    for (int k = 0; k < nl; k++) dlvi[k] = (int)dlv[k];
+    void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    CK(cudaMalloc(&c->dv, 3 * nv * sizeof(double)));
+    CK(cudaMalloc(&c->dp, 4 * nf * sizeof(double)));
+    CK(cudaMalloc(&c->dt, nf * sizeof(int)));
+    CK(cudaMalloc(&c->dlp, (nf + 1) * sizeof(int)));
+    CK(cudaMalloc(&c->dlv, nl * sizeof(int)));
+    CK(cudaMemcpy(c->dv, dv, 3 * nv * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dp, dp, 4 * nf * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dt, dti, nf * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dlp, dlpi, (nf + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dlv, dlvi, nl * sizeof(int), cudaMemcpyHostToDevice));
+    c->dnv = nv; c->dnf = nf; c->dnl = nl;
+    c->tol = tol;
+    for (int a = 0; a < 3; a++) { c->dlo[a] = INFINITY; c->dhi[a] = -INFINITY; }
+    for (int v = 0; v < nv; v++)
+        for (int a = 0; a < 3; a++) {
+            c->dlo[a] = std::min(c->dlo[a], dv[3 * v + a]);
+            c->dhi[a] = std::max(c->dhi[a], dv[3 * v + a]);
+        }
+    // polytope volume by apex fan (geom.cell_volume_convex, geom.py:506-518)
+    double ap[3] = {0, 0, 0};
+    for (int v = 0; v < nv; v++)
+        for (int a = 0; a < 3; a++) ap[a] += dv[3 * v + a] / nv;
+    double vol = 0.0;
+    for (int f = 0; f < nf; f++) {
+        const double *p0 = dv + 3 * dlv[dlp[f]];
+        for (int k = (int)dlp[f] + 1; k + 1 < (int)dlp[f + 1]; k++) {
+            const double *p1 = dv + 3 * dlv[k], *p2 = dv + 3 * dlv[k + 1];
+            double u[3] = {p1[0] - p0[0], p1[1] - p0[1], p1[2] - p0[2]};
+            double w[3] = {p2[0] - p0[0], p2[1] - p0[1], p2[2] - p0[2]};
+            double cr[3] = {u[1] * w[2] - u[2] * w[1], u[2] * w[0] - u[0] * w[2], u[0] * w[1] - u[1] * w[0]};
+            vol += cr[0] * (p0[0] - ap[0]) + cr[1] * (p0[1] - ap[1]) + cr[2] * (p0[2] - ap[2]);
+        }
+    }
+    c->dvol = std::fabs(vol) / 6.0;
+    c->has_domain = true;
+    return 0;
+}
+
+int pf_grid_build(pf_ctx *c, int64_t n, const double *pts, const double *psi, double cell_size,
+                  void *stream) {
+    return grid_build(c, n, pts, psi, cell_size, S(stream));
+}
+
+int pf_grid_build_dims(pf_ctx *c, int64_t n, const double *pts, const int *dims_host, void *stream) {
+    return grid_build(c, n, pts, nullptr, 1.0, S(stream), dims_host);
+}
+
+int pf_grid_info(pf_ctx *c, int *dims, double *lo, double *h) {
+    for (int a = 0; a < 3; a++) {
+        if (dims) dims[a] = c->gn[a];
+        if (lo) lo[a] = c->glo[a];
+        if (h) h[a] = c->gh[a];
+    }
+    return 0;
+}
+
+int pf_grid_export(pf_ctx *c, int64_t *bucket_start, int64_t *bucket_sites, void *stream) {
+    if (c->grid_n < 0) return set_err("pf_grid_export: no grid");
+    int ncell = c->gn[0] * c->gn[1] * c->gn[2];
+    g_launches++;
+    k_grid_export<<<c->nsm * 4, 256, 0, S(stream)>>>(c->bstart, ncell, c->sid, c->grid_n, bucket_start,
+                                                     bucket_sites);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int pf_dpsi_max(pf_ctx *c, int64_t n, const double *psi, double *dpsi_host, void *stream) {
+    if (dpsi_dev(c, n, psi, S(stream))) return -1;
+    if (dpsi_host) {
+        CK(cudaMemcpyAsync(dpsi_host, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+        CK(cudaStreamSynchronize(S(stream)));
+    }
+    return 0;
+}
+
+int64_t pf_batch_evaluate(pf_ctx *c, int64_t n, const double *pts, const double *psi, double tol,
+                          double dpsi_max, int ball_aware, int want_m2, int64_t smf, int64_t *status,
+                          double *vol, double *ksur, double *cent, double *ipt, double *m2,
+                          int64_t *fcount, int64_t *ftag, double *farea, double *fh, double *fnrm,
+                          double *fcent, int rebuild_grid, void *stream) {
+    return pf_batch_evaluate_ex(c, n, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, status, vol,
+                                ksur, cent, ipt, m2, fcount, ftag, farea, fh, fnrm, fcent, nullptr, 0,
+                                nullptr, nullptr, rebuild_grid, stream);
+}
+
+int64_t pf_batch_evaluate_ex(pf_ctx *c, int64_t n, const double *pts, const double *psi, double tol,
+                             double dpsi_max, int ball_aware, int want_m2, int64_t smf, int64_t *status,
+                             double *vol, double *ksur, double *cent, double *ipt, double *m2,
+                             int64_t *fcount, int64_t *ftag, double *farea, double *fh, double *fnrm,
+                             double *fcent, const int32_t *cells, int64_t ncells, int32_t *cell_flags,
+                             int32_t *census16, int rebuild_grid, void *stream) {
+    cudaStream_t st = S(stream);
+    if (!c->has_domain) return set_err("pf_batch_evaluate: no domain set");
+    if (n < 0 || n > 0x7fffffff) return set_err("pf_batch_evaluate: bad n");
+    if (rebuild_grid || c->grid_n != n || c->grid_pts != pts) {
+        if (grid_build(c, n, pts, psi, 0.0, st)) return -1;
+    }
+    if (dpsi_max < 0.0 && dpsi_dev(c, n, psi, st)) return -1;
+    if (ensure(&c->census, &c->census_cap, (size_t)n + 1)) return -1;
+    CellIn in;
+    fill_cellin(c, in, n, pts, psi, tol, dpsi_max, ball_aware, want_m2);
+    CellOut out;
+    memset(&out, 0, sizeof out);
+    out.status = status; out.vol = vol; out.ksur = ksur; out.cent = cent; out.ipt = ipt; out.m2 = m2;
+    out.fcount = fcount; out.ftag = ftag; out.farea = farea; out.fh = fh; out.fnrm = fnrm;
+    out.fcent = fcent; out.smf = (int)smf; out.census = c->census;
+    out.flags = cell_flags;
+    out.census16 = census16;
+    in.cells = cells;
+    in.ncells = (int)ncells;
+    if (n > 0 && (!cells || ncells > 0) && launch_cells(c, in, out, n, st)) return -1;
+    unsigned long long e = 0;
+    if (n > 0) {
+        CK(cudaMemcpyAsync(&e, c->err, sizeof e, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return (int64_t)e;
+}
+
+int pf_evaluate_lean(pf_ctx *c, int64_t n, const double *pts, const double *psi, int ball_aware,
+                     int64_t smf, double *vol, double *ksur, int32_t *fcount, int32_t *ftag,
+                     double *farea, double *cent, int64_t *flags, void *stream) {
+    cudaStream_t st = S(stream);
+    if (!c->has_domain) return set_err("pf_evaluate_lean: no domain set");
+    if (c->grid_n != n || c->grid_pts != pts) return set_err("pf_evaluate_lean: build the grid first");
+    if (dpsi_dev(c, n, psi, st)) return -1;
+    CellIn in;
+    fill_cellin(c, in, n, pts, psi, c->tol, -1.0, ball_aware, 0);
+    CellOut out;
+    memset(&out, 0, sizeof out);
+    out.vol = vol; out.ksur = ksur; out.cent = cent; out.fcount32 = fcount; out.ftag32 = ftag;
+    out.farea = farea; out.smf = (int)smf;
+    if (n > 0 && launch_cells(c, in, out, n, st)) return -1;
+    if (flags) {
+        CK(cudaMemcpyAsync(flags, c->err, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
+    return 0;
+}
+
+int pf_last_census(pf_ctx *c, int32_t *census, void *stream) {
+    if (!c->census || c->grid_n < 0) return set_err("pf_last_census: nothing evaluated");
+    CK(cudaMemcpyAsync(census, c->census, c->grid_n * sizeof(int32_t), cudaMemcpyDeviceToDevice, S(stream)));
+    return 0;
+}
+
+int pf_last_cells_ms(pf_ctx *c, double *ms) {
+    if (!c->ev_valid) return set_err("pf_last_cells_ms: no evaluation recorded");
+    CK(cudaEventSynchronize(c->ev[1]));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[1]));
+    *ms = f;
+    return 0;
+}
+
+int pf_last_retry_count(pf_ctx *c, int64_t *count) {
+    int v = 0;
+    CK(cudaMemcpy(&v, c->counters, sizeof(int), cudaMemcpyDeviceToHost));
+    *count = v;
+    return 0;
+}
+
+int64_t pf_knn(pf_ctx *c, int64_t n, const double *pts, int64_t nq, const double *queries, int64_t k,
+               int64_t *out_idx, void *stream) {
+    cudaStream_t st = S(stream);
+    if (!c->has_domain) return set_err("pf_knn: no domain set");
+    if (k > n) k = n;
+    if (k <= 0 || nq <= 0) return k > 0 ? k : 0;
+    if (c->grid_n != n || c->grid_pts != pts) {
+        if (grid_build(c, n, pts, nullptr, 0.0, st)) return -1;
+    }
+    if (!c->attr_set) {
+        CellIn dummy;
+        CellOut dout;
+        memset(&dummy, 0, sizeof dummy);
+        memset(&dout, 0, sizeof dout);
+        // allocates the exact-tier workspace (no cells launched)
+        if (launch_cells(c, dummy, dout, 0, st)) return -1;
+    }
+    CellIn in;
+    fill_cellin(c, in, n, pts, nullptr, c->tol, 0.0, 1, 0);
+    double h = std::max(c->gh[0], std::max(c->gh[1], c->gh[2]));
+    double r0 = h * std::cbrt((double)k);
+    g_launches++;
+    k_knn<<<c->exact_warps / EXACT_WARPS, EXACT_WARPS * 32, 0, st>>>(in, nq, queries, (int)k, r0 * r0,
+                                                                   c->exact_ws, out_idx);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return k;
+}
+
+}  // extern "C"
+
+unsigned long long pf_internal_launches_add(unsigned long long k) { return g_launches += k; }
+int pf_internal_set_err(const char *msg) { return set_err("%s", msg); }

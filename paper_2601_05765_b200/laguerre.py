@@ -1,0 +1,202 @@
+"""Laguerre-diagram plumbing on the B200: domain pack, bucket grid, kNN.
+
+Mirrors the reference's ``potflow.laguerre`` host API
+(/root/reference/pkg/src/potflow/laguerre.py) with the per-site work moved to
+the device:
+
+* ``Site`` / ``sites_to_arrays``     laguerre.py:20-42   (host, unchanged semantics)
+* ``SpatialGrid``                    laguerre.py:45-87   counting sort on the GPU (pf_grid_build)
+* ``knn``                            laguerre.py:90-96   batched warp-per-query kernel (pf_knn)
+* ``bisector_plane``                 laguerre.py:99-110
+* ``domain_pack`` / ``_DomainPack``  laguerre.py:113-139
+* ``_dpsi_max``                      laguerre.py:142-145 (device min/max reduction)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .geom import DEFAULT_REL_TOL, ConvexCell, Plane, cell_volume_convex, pack_cell
+
+
+@dataclass
+class Site:
+    p: np.ndarray
+    psi: float = 0.0
+    nu: float = 1.0
+    phase: int = 0
+
+    def __post_init__(self):
+        self.p = np.asarray(self.p, dtype=np.float64)
+        if self.psi < 0.0:
+            raise ValueError("site weight must be non-negative")
+        if self.nu <= 0.0:
+            raise ValueError("prescribed volume must be positive")
+
+
+def sites_to_arrays(sites: list):
+    pts = np.array([s.p for s in sites], dtype=np.float64).reshape(-1, 3)
+    return (pts, np.array([s.psi for s in sites], dtype=np.float64),
+            np.array([s.nu for s in sites], dtype=np.float64),
+            np.array([s.phase for s in sites], dtype=np.int64))
+
+
+def bisector_plane(p_i, psi_i, p_j, psi_j) -> Plane:
+    """Power bisector of (p_i, psi_i), (p_j, psi_j), cell i inside (laguerre.py:99-110)."""
+    p_i = np.asarray(p_i, dtype=np.float64)
+    p_j = np.asarray(p_j, dtype=np.float64)
+    diff = p_j - p_i
+    D2 = float(diff @ diff)
+    if D2 == 0.0:
+        raise ValueError("coincident sites have no bisector")
+    D = np.sqrt(D2)
+    n = diff / D
+    return Plane(n, float(n @ p_i) + 0.5 * (D2 + psi_i - psi_j) / D)
+
+
+class _DomainPack:
+    """Packed domain + tolerance + volume (laguerre.py:113-129)."""
+
+    def __init__(self, domain: ConvexCell):
+        self.cell = domain
+        self.verts, self.cnt, self.planes, self.tags, self.lp, self.lv = pack_cell(domain)
+        self.tol = DEFAULT_REL_TOL * domain.diagonal()
+        self.volume = cell_volume_convex(domain)
+
+    def args(self):
+        return (self.verts, self.cnt, self.planes, self.tags, self.lp, self.lv)
+
+
+_pack_cache: dict[int, _DomainPack] = {}
+
+
+def domain_pack(domain: ConvexCell) -> _DomainPack:
+    dp = _pack_cache.get(id(domain))
+    if dp is None or dp.cell is not domain:
+        dp = _DomainPack(domain)
+        _pack_cache.clear()
+        _pack_cache[id(domain)] = dp
+    return dp
+
+
+# which packed domain is resident in each device context
+_resident: dict[int, tuple] = {}
+
+
+def upload_domain(ctx, dv, dc, dp, dt, dlp, dlv, tol: float) -> None:
+    """Make the packed domain resident in the device context (pf_set_domain)."""
+    arrs = [np.ascontiguousarray(np.asarray(a), dtype=t) for a, t in
+            ((dv, np.float64), (dc, np.int64), (dp, np.float64), (dt, np.int64),
+             (dlp, np.int64), (dlv, np.int64))]
+    nv, nf, nl = (int(x) for x in arrs[1][:3])
+    key = (float(tol), arrs[0][:nv].tobytes(), arrs[2][:nf].tobytes(), arrs[3][:nf].tobytes(),
+           arrs[4][:nf + 1].tobytes(), arrs[5][:nl].tobytes())
+    if _resident.get(ctx.value) == key:
+        return
+    _lib.check(_lib.lib().pf_set_domain(ctx, *[a.ctypes.data for a in arrs], float(tol)),
+               "pf_set_domain")
+    _resident[ctx.value] = key
+
+
+def _dev(x, dtype):
+    import torch
+
+    if isinstance(x, torch.Tensor):
+        if x.device.type != "cuda":
+            x = x.cuda()
+        return x.to(dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+def _dpsi_max(psi) -> float:
+    """max(psi) - min(psi), >= 0 (laguerre.py:142-145), reduced on the device."""
+    import torch
+
+    t = _dev(psi, torch.float64)
+    if t.numel() == 0:
+        return 0.0
+    out = C.c_double(0.0)
+    _lib.check(_lib.lib().pf_dpsi_max(_lib.ctx(), t.numel(), _lib.ptr(t), C.byref(out),
+                                      _lib.stream_ptr()), "pf_dpsi_max")
+    return float(out.value)
+
+
+class SpatialGrid:
+    """Uniform bucket grid over the domain bounding box, built on the GPU.
+
+    ``target_cell_size=None`` reproduces the reference's bucket edge
+    (|domain|/n)^(1/3) with dims clipped to [1, 128] (laguerre.py:59-64), so
+    ``bucket_start`` / ``bucket_sites`` / ``kernel_args()`` equal the
+    reference's arrays (sites ordered by bucket, then index, as numpy's stable
+    argsort gives).  The evaluation kernels build their own, finer grid.
+    """
+
+    def __init__(self, points, domain: ConvexCell, target_cell_size: float | None = None):
+        import torch
+
+        pts = _dev(points, torch.float64).reshape(-1, 3)
+        n = pts.shape[0]
+        lo, hi = domain.bbox()
+        extent = np.maximum(hi - lo, 1e-300)
+        if target_cell_size is None:
+            target_cell_size = (cell_volume_convex(domain) / max(n, 1)) ** (1.0 / 3.0)
+        dims = np.clip(np.ceil(extent / max(target_cell_size, 1e-300)).astype(np.int64), 1, 128)
+        h = extent / dims
+        self.lo = lo.copy()
+        self.dims = dims
+        self.h = h
+        self.inv_h = 1.0 / h
+        self.h_min = float(h.min())
+        self.points = pts
+        dpk = domain_pack(domain)
+        c = _lib.ctx()
+        upload_domain(c, *dpk.args(), dpk.tol)
+        gdims = (C.c_int * 3)(*[int(x) for x in dims])
+        _lib.check(_lib.lib().pf_grid_build_dims(c, n, _lib.ptr(pts), gdims, _lib.stream_ptr()),
+                   "pf_grid_build_dims")
+        ncell = int(dims.prod())
+        self.bucket_start = torch.empty(ncell + 1, dtype=torch.int64, device="cuda")
+        self.bucket_sites = torch.empty(n, dtype=torch.int64, device="cuda")
+        _lib.check(_lib.lib().pf_grid_export(c, _lib.ptr(self.bucket_start),
+                                             _lib.ptr(self.bucket_sites), _lib.stream_ptr()),
+                   "pf_grid_export")
+
+    def kernel_args(self):
+        return (self.bucket_start, self.bucket_sites,
+                float(self.lo[0]), float(self.lo[1]), float(self.lo[2]),
+                float(self.inv_h[0]), float(self.inv_h[1]), float(self.inv_h[2]),
+                int(self.dims[0]), int(self.dims[1]), int(self.dims[2]), self.h_min)
+
+
+def knn_batch(points, queries, k: int, domain: ConvexCell):
+    """k nearest sites of every query, ordered by (distance, index); int64 [nq, min(k, n)]."""
+    import torch
+
+    pts = _dev(points, torch.float64).reshape(-1, 3)
+    q = _dev(queries, torch.float64).reshape(-1, 3)
+    n = pts.shape[0]
+    kk = min(int(k), n)
+    out = torch.empty((q.shape[0], max(kk, 0)), dtype=torch.int64, device="cuda")
+    if kk <= 0 or q.shape[0] == 0:
+        return out
+    c = _lib.ctx()
+    dpk = domain_pack(domain)
+    upload_domain(c, *dpk.args(), dpk.tol)
+    got = _lib.check(_lib.lib().pf_knn(c, n, _lib.ptr(pts), q.shape[0], _lib.ptr(q), kk,
+                                       _lib.ptr(out), _lib.stream_ptr()), "pf_knn")
+    return out[:, :got]
+
+
+def knn(grid: SpatialGrid, q, k: int, domain: ConvexCell | None = None) -> np.ndarray:
+    """Indices of the k nearest sites to q by increasing distance (laguerre.py:90-96)."""
+    if domain is None:
+        lo = grid.lo
+        hi = grid.lo + grid.h * grid.dims
+        from .geom import box_domain
+
+        domain = box_domain(lo, hi)
+    return knn_batch(grid.points, np.asarray(q, dtype=np.float64).reshape(1, 3), k,
+                     domain)[0].cpu().numpy()

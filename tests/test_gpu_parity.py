@@ -1,0 +1,150 @@
+"""On-device parity of the sm_100a path (libpotflow_b200.so) against the
+reference's golden outputs and the CPU oracle.
+
+Bar (BASELINE.json north star): status / facet adjacency (ftag lists in
+order) / facet counts bit-exact; volumes, free-surface and facet areas within
+1e-9 relative (areas relative to the sphere area 4 pi psi when the reference
+value is ~0); centroids within 1e-9 of the domain diagonal.
+"""
+import numpy as np
+import pytest
+
+from conftest import OUT_KEYS, golden_domain, golden_scene
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ["sparse", "sparse_varpsi", "sparse_full", "dense", "twofluid", "lattice_ties"]
+REL = 1e-9
+
+
+def _close(a, b, scale):
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), scale))) if a.size else 0.0
+
+
+def _check(o, r, psi_max):
+    for k in ("status", "fcount", "ftag"):
+        assert np.array_equal(o[k], r[k]), k
+    sph = 4 * np.pi * psi_max
+    assert _close(o["vol"], r["vol"], sph ** 1.5 * 1e-6) <= REL
+    assert _close(o["ksur"], r["ksur"], sph) <= REL
+    assert _close(o["farea"], r["farea"], sph) <= REL
+    assert np.max(np.abs(o["cent"] - r["cent"])) <= REL
+    assert np.max(np.abs(o["fcent"] - r["fcent"])) <= REL
+    assert np.array_equal(o["fnrm"], r["fnrm"])  # bisector normals: same arithmetic
+    assert np.array_equal(o["fh"], r["fh"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_dropin_numpy_matches_reference(golden, name):
+    """The numpy drop-in `_kernels._batch_evaluate` with the reference's 37 arguments."""
+    from oracle import pyoracle as O
+    from paper_2601_05765_b200 import _kernels
+
+    s = golden_scene(golden, name)
+    n, smf = len(s["pts"]), int(golden["ev_smf"])
+    g = O.SpatialGrid(s["pts"], [0, 0, 0], [1, 1, 1], float(golden["dom_unit_vol"]))
+    o = O.alloc_outputs(n, smf)
+    err = _kernels._batch_evaluate(s["pts"], s["psi"], *golden_domain(golden), *g.kernel_args(),
+                                   float(golden["dom_unit_tol"]), float(s["dpsi"]),
+                                   bool(s["ball_aware"]), True, smf, *[o[k] for k in OUT_KEYS])
+    assert err == int(s["err"])
+    _check(o, s, float(s["psi"].max()))
+
+
+def _scene_large(kind):
+    from paper_2601_05765_b200 import scenes
+
+    if kind == "C1-100k":
+        sc = scenes.c1_random(n=100_000)
+        return sc.pts, sc.psi_cold(), True
+    if kind == "C2":
+        sc = scenes.c2_dam_break()
+        return sc.pts, np.full(sc.n, (0.85 * sc.meta["h"]) ** 2), True
+    if kind == "C5-50k":
+        sc = scenes.c5_two_fluid(n_target=50_000)
+        h = sc.meta["h"]
+        return sc.pts, np.where(sc.nu > 1.5 * h ** 3, (1.7 * h) ** 2, (0.85 * h) ** 2), True
+    if kind == "C1-full":
+        sc = scenes.c1_random(n=5000)
+        return sc.pts, sc.psi_cold() * 2, False
+    raise KeyError(kind)
+
+
+@pytest.mark.parametrize("kind", ["C1-100k", "C2", "C5-50k", "C1-full"])
+def test_device_matches_oracle(kind):
+    """Torch-resident path vs the CPU oracle on the paper-scale scenes."""
+    import torch
+
+    from oracle import pyoracle as O
+    from paper_2601_05765_b200 import geom, laguerre, restricted
+
+    pts, psi, ba = _scene_large(kind)
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    dpk = laguerre.domain_pack(dom)
+    d = restricted.evaluate(torch.as_tensor(pts, device="cuda"), torch.as_tensor(psi, device="cuda"),
+                            dom, ball_aware=ba, smf=32)
+    o = {k: getattr(d, k).cpu().numpy() for k in OUT_KEYS}
+    g = O.SpatialGrid(pts, [0, 0, 0], [1, 1, 1], 1.0)
+    r = O.evaluate(pts, psi, dpk.args(), dpk.tol, g, ball_aware=ba, smf=32)
+    assert d.flags == r["err"]
+    _check(o, r, float(psi.max()))
+
+
+def test_partition_and_symmetry_properties():
+    """Size-independent properties at full C2 size: facet symmetry i<->j and
+    areas agreeing from both sides; run-to-run determinism."""
+    import torch
+
+    from paper_2601_05765_b200 import geom, restricted
+
+    pts, psi, _ = _scene_large("C2")
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    tp, tw = torch.as_tensor(pts, device="cuda"), torch.as_tensor(psi, device="cuda")
+    a = restricted.evaluate(tp, tw, dom)
+    b = restricted.evaluate(tp, tw, dom)
+    for k in OUT_KEYS:
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    ft, fa, fc = a.ftag.cpu().numpy(), a.farea.cpu().numpy(), a.fcount.cpu().numpy()
+    n = len(fc)
+    area = {}
+    for i in range(n):
+        for s in range(fc[i]):
+            if ft[i, s] >= 0:
+                area[(i, int(ft[i, s]))] = fa[i, s]
+    worst = 0.0
+    for (i, j), v in area.items():
+        assert (j, i) in area
+        worst = max(worst, abs(v - area[(j, i)]) / max(v, 1e-300))
+    assert worst < 1e-8
+
+
+def test_spatial_grid_and_knn_match_reference(golden):
+    import torch
+
+    from paper_2601_05765_b200 import geom, laguerre
+
+    s = golden_scene(golden, "sparse")
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    g = laguerre.SpatialGrid(s["pts"], dom)
+    assert np.array_equal(g.dims, golden["grid_dims"])
+    assert np.array_equal(g.bucket_start.cpu().numpy(), golden["grid_bucket_start"])
+    assert np.array_equal(g.bucket_sites.cpu().numpy(), golden["grid_bucket_sites"])
+    out = laguerre.knn_batch(s["pts"], golden["knn_q"], 30, dom).cpu().numpy()
+    for t, k in enumerate(golden["knn_k"]):
+        assert np.array_equal(out[t, :k], golden["knn_idx"][t, :k])
+    # drop-in _knn with the reference argument list
+    from paper_2601_05765_b200 import _kernels
+
+    idx = np.empty(int(golden["knn_k"][0]), np.int64)
+    got = _kernels._knn(torch.as_tensor(s["pts"], device="cuda"), *g.kernel_args(),
+                        *golden["knn_q"][0], int(golden["knn_k"][0]), idx)
+    assert got == len(idx) and np.array_equal(idx, golden["knn_idx"][0, :got])
+
+
+def test_dpsi_max_matches():
+    from paper_2601_05765_b200 import laguerre
+
+    rng = np.random.default_rng(0)
+    psi = rng.random(100_003) * 1e-3 - 2e-4
+    assert laguerre._dpsi_max(psi) == float(max(psi.max() - psi.min(), 0.0))
+    assert laguerre._dpsi_max(np.array([])) == 0.0
