@@ -74,7 +74,11 @@ def _batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
     else:
         p = torch.from_numpy(np.ascontiguousarray(pts, np.float64)).to("cuda", non_blocking=True)
         w = torch.from_numpy(np.ascontiguousarray(psi, np.float64)).to("cuda", non_blocking=True)
-        outs = [torch.empty(o.shape, dtype=t, device="cuda") for o, t in zip(outs_host, dtypes)]
+        # fixed-stride slots past fcount come back zero (the reference leaves
+        # them untouched; callers allocate zeros)
+        outs = [torch.zeros(o.shape, dtype=t, device="cuda") if k >= 7 else
+                torch.empty(o.shape, dtype=t, device="cuda")
+                for k, (o, t) in enumerate(zip(outs_host, dtypes))]
     n = int(p.shape[0])
     cflags = torch.empty(n, dtype=torch.int32, device="cuda")
     err = int(_lib.lib().pf_batch_evaluate_ex(

@@ -98,7 +98,12 @@ struct EvalScratch {
     int16_t fhead[C::CF], fnp[C::CF];
     uint8_t fkind[C::CF], fseg[C::CF], funs[C::CF];
     uint8_t vin[C::CV];
-    double ppx[C::CP], ppy[C::CP], ppz[C::CP], pth[C::CP];
+    // twin-facet lookup (replaces the reference's O(nf m) _edge_other_facet scan)
+    uint8_t vdeg[C::CV];            // outgoing loop entries per vertex
+    uint16_t vinc[C::CV * 4];       // their entry indices (first 4)
+    uint8_t efac[C::CL];            // facet of each loop entry
+    uint16_t esv[C::CL];            // successor vertex of each loop entry
+    double ppx[C::CP], ppy[C::CP], ppz[C::CP];
     int16_t pnext[C::CP];
     uint8_t pfl[C::CP];  // bit0 on_sph, bit1 conn (arc to next), bit2 deleted
     int npool;
@@ -280,6 +285,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     pfw::sync();
     // 3b. prefix sums in facet order: crossing bases, kept-facet loop bases
     int NE = 0, NFk = 0, NLk = 0;
+    bool small_facet = false;  // a dropped facet that still emitted 1-2 entries
     for (int f0 = 0; f0 < nf; f0 += 32) {
         int f = f0 + L;
         int c = 0, kk = 0, keep = 0;
@@ -288,6 +294,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
             kk = S.fk[f];
             keep = kk >= 3;
         }
+        small_facet |= pfw::any(kk >= 1 && kk <= 2);
         int tc, tk, tl;
         int oc = pfw::excl_scan_i(c, &tc);
         int ok = pfw::excl_scan_i(keep, &tk);
@@ -436,7 +443,16 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     }
     const int NF2 = NFk + 1, NL2 = NLk + ncp;
     pfw::sync();
-    // 5. drop unreferenced vertices (_kernels.py:297-315)
+    // 5. drop unreferenced vertices (_kernels.py:297-315).  A kept vertex can
+    // only lose all its facets if some dropped facet emitted 1-2 entries.
+    if (!small_facet) {
+        if (L == 0) {
+            B.nv = NVB; B.nf = NF2; B.nl = NL2;
+            if (ws->cen_on) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += NVB; }
+        }
+        pfw::sync();
+        return CLIP_CUT;
+    }
     for (int v = L; v < NVB; v += 32) S.vmap[v] = 0;
     pfw::sync();
     for (int k = L; k < NL2; k += 32) S.vmap[B.lv[k]] = 1;
@@ -721,13 +737,23 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
             cur_inside = true;
         }
         if (ina && inb) continue;
-        // _edge_other_facet (_kernels.py:397-408): facet holding edge (bb -> a)
+        // _edge_other_facet (_kernels.py:397-408): lowest facet != f holding
+        // the directed edge (bb -> a), through the vertex incidence table
         int g = -1;
-        for (int gg = 0; gg < nf && g < 0; gg++) {
-            if (gg == f) continue;
-            int s0 = P.lp[gg], mg = P.lp[gg + 1] - s0;
-            for (int ee = 0; ee < mg; ee++) {
-                if (P.lv[s0 + ee] == bb && P.lv[s0 + (ee + 1 == mg ? 0 : ee + 1)] == a) { g = gg; break; }
+        const int dg = E.vdeg[bb];
+        if (dg <= 4) {
+            for (int t = 0; t < dg; t++) {
+                const int k2 = E.vinc[bb * 4 + t];
+                const int g2 = E.efac[k2];
+                if (E.esv[k2] == a && g2 != f && (g < 0 || g2 < g)) g = g2;
+            }
+        } else {
+            for (int gg = 0; gg < nf && g < 0; gg++) {
+                if (gg == f) continue;
+                int s0 = P.lp[gg], mg = P.lp[gg + 1] - s0;
+                for (int ee = 0; ee < mg; ee++) {
+                    if (P.lv[s0 + ee] == bb && P.lv[s0 + (ee + 1 == mg ? 0 : ee + 1)] == a) { g = gg; break; }
+                }
             }
         }
         double gx, gy, gz, gd, c12, det, ux, uy, uz;
@@ -845,28 +871,18 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
         }
     }
     if (npts < 2) return RF_OUTSIDE;
-    // canonical rotation: start at the arc with the smallest start angle (_kernels.py:640-674)
-    {
-        double eb[6];
-        perp_basis(nx, ny, nz, eb);
-        double best = 1e300;
-        int bi = head;
-        int i = head;
-        for (int t = 0; t < npts; t++) {
-            if (E.pfl[i] & PF_CONN) {
-                double rx = E.ppx[i] - qx, ry = E.ppy[i] - qy, rz = E.ppz[i] - qz;
-                double aang = atan2(rx * eb[3] + ry * eb[4] + rz * eb[5], rx * eb[0] + ry * eb[1] + rz * eb[2]);
-                if (aang < best) { best = aang; bi = i; }
-            }
-            i = E.pnext[i];
-        }
-        head = bi;
-    }
+    // The reference rotates the ring to start at the arc with the smallest
+    // start angle (_kernels.py:640-674); that only fixes a summation order,
+    // and this path's sums are reductions anyway, so the ring keeps its start.
     *head_out = head; *np_out = npts;
     return RF_GENPOLY;
 }
 
-// _kernels.py:678-716 + 331-390: area, centroid, polar moment of a restricted facet
+// _kernels.py:678-716 + 331-390: area, centroid, polar moment of a restricted
+// facet.  Same Green forms as the reference; an arc's trigonometric values come
+// from its end-point coordinates (cos a = x/r, sin a = y/r, double-angle
+// identities) and its sweep from one atan2 of (cross, dot), instead of
+// 2 atan2 + 8 sin/cos per arc.  Agrees with the reference to rounding.
 template <class C>
 PF_DEV void seq_integrals(WS<C> *ws, int head, int npts, double nx, double ny, double nz,
                           double qx, double qy, double qz, double rc, double *out) {
@@ -875,55 +891,60 @@ PF_DEV void seq_integrals(WS<C> *ws, int head, int npts, double nx, double ny, d
     perp_basis(nx, ny, nz, e);
     double A = 0.0, Mx = 0.0, My = 0.0, Ip = 0.0;
     int i = head;
+    // local frame coordinates of the current point
+    double x0 = (E.ppx[i] - qx) * e[0] + (E.ppy[i] - qy) * e[1] + (E.ppz[i] - qz) * e[2];
+    double y0 = (E.ppx[i] - qx) * e[3] + (E.ppy[i] - qy) * e[4] + (E.ppz[i] - qz) * e[5];
+    const double x00 = x0, y00 = y0;
     for (int t = 0; t < npts; t++) {
-        int j = E.pnext[i];
-        double x0 = (E.ppx[i] - qx) * e[0] + (E.ppy[i] - qy) * e[1] + (E.ppz[i] - qz) * e[2];
-        double y0 = (E.ppx[i] - qx) * e[3] + (E.ppy[i] - qy) * e[4] + (E.ppz[i] - qz) * e[5];
-        double x1 = (E.ppx[j] - qx) * e[0] + (E.ppy[j] - qy) * e[1] + (E.ppz[j] - qz) * e[2];
-        double y1 = (E.ppx[j] - qx) * e[3] + (E.ppy[j] - qy) * e[4] + (E.ppz[j] - qz) * e[5];
+        const int j = E.pnext[i];
+        double x1, y1;
+        if (t + 1 == npts) { x1 = x00; y1 = y00; }
+        else {
+            x1 = (E.ppx[j] - qx) * e[0] + (E.ppy[j] - qy) * e[1] + (E.ppz[j] - qz) * e[2];
+            y1 = (E.ppx[j] - qx) * e[3] + (E.ppy[j] - qy) * e[4] + (E.ppz[j] - qz) * e[5];
+        }
         if (!(E.pfl[i] & PF_CONN)) {
-            double cr = x0 * y1 - x1 * y0;
+            double cr = fma(x0, y1, -x1 * y0);
             A += 0.5 * cr;
             double dx = x1 - x0, dy = y1 - y0;
-            Mx += dy * (x0 * x0 + x0 * x1 + x1 * x1) / 6.0;
-            My += -dx * (y0 * y0 + y0 * y1 + y1 * y1) / 6.0;
-            double sx3 = x0 * x0 * x0 + x0 * x0 * x1 + x0 * x1 * x1 + x1 * x1 * x1;
-            double sy3 = y0 * y0 * y0 + y0 * y0 * y1 + y0 * y1 * y1 + y1 * y1 * y1;
-            Ip += (dy * sx3 - dx * sy3) / 12.0;
+            double xx = fma(x0, x0, fma(x0, x1, x1 * x1));
+            double yy = fma(y0, y0, fma(y0, y1, y1 * y1));
+            Mx = fma(dy * xx, 1.0 / 6.0, Mx);
+            My = fma(-dx * yy, 1.0 / 6.0, My);
+            double sx3 = (x0 + x1) * (x0 * x0 + x1 * x1);
+            double sy3 = (y0 + y1) * (y0 * y0 + y1 * y1);
+            Ip = fma(fma(dy, sx3, -dx * sy3), 1.0 / 12.0, Ip);
         } else {
-            double a0 = atan2(y0, x0);
-            double a1r = atan2(y1, x1);
-            double sweep = a1r - a0;
-            if (sweep <= 0.0) sweep += 2.0 * PF_PI;
-            const double cx = 0.0, cy = 0.0, r = rc;
-            double a1 = a0 + sweep;
-            double dth = a1 - a0;
-            double s0 = sin(a0), s1 = sin(a1), c0 = cos(a0), c1 = cos(a1);
-            double s20 = sin(2.0 * a0), s21 = sin(2.0 * a1);
-            double s40 = sin(4.0 * a0), s41 = sin(4.0 * a1);
-            double ic = s1 - s0;
-            double isn = c0 - c1;
-            double ic2 = 0.5 * dth + 0.25 * (s21 - s20);
-            double is2 = 0.5 * dth - 0.25 * (s21 - s20);
+            double r0 = sqrt(x0 * x0 + y0 * y0), r1 = sqrt(x1 * x1 + y1 * y1);
+            double c0 = r0 > 0.0 ? x0 / r0 : 1.0, s0 = r0 > 0.0 ? y0 / r0 : 0.0;
+            double c1 = r1 > 0.0 ? x1 / r1 : 1.0, s1 = r1 > 0.0 ? y1 / r1 : 0.0;
+            double dth = atan2(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
+            if (dth <= 0.0) dth += 2.0 * PF_PI;
+            double s20 = 2.0 * s0 * c0, c20 = fma(c0, c0, -s0 * s0);
+            double s21 = 2.0 * s1 * c1, c21 = fma(c1, c1, -s1 * s1);
+            double s40 = 2.0 * s20 * c20, s41 = 2.0 * s21 * c21;
+            const double r = rc;
             double ic3 = (s1 - s1 * s1 * s1 / 3.0) - (s0 - s0 * s0 * s0 / 3.0);
             double is3 = (-c1 + c1 * c1 * c1 / 3.0) - (-c0 + c0 * c0 * c0 / 3.0);
             double ic4 = 0.375 * dth + 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
             double is4 = 0.375 * dth - 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
-            A += 0.5 * (r * r * dth + cx * r * ic + cy * r * isn);
-            Mx += 0.5 * r * (cx * cx * ic + 2.0 * cx * r * ic2 + r * r * ic3);
-            My += 0.5 * r * (cy * cy * isn + 2.0 * cy * r * is2 + r * r * is3);
-            Ip += (r / 3.0) * (cx * cx * cx * ic + 3.0 * cx * cx * r * ic2
-                               + 3.0 * cx * r * r * ic3 + r * r * r * ic4
-                               + cy * cy * cy * isn + 3.0 * cy * cy * r * is2
-                               + 3.0 * cy * r * r * is3 + r * r * r * is4);
+            double r2 = r * r;
+            A = fma(0.5 * r2, dth, A);
+            Mx = fma(0.5 * r * r2, ic3, Mx);
+            My = fma(0.5 * r * r2, is3, My);
+            Ip = fma((r / 3.0) * r2 * r, ic4 + is4, Ip);
         }
+        x0 = x1;
+        y0 = y1;
         i = j;
     }
     double cx, cy, cz;
     if (A > 0.0) {
-        cx = qx + (Mx / A) * e[0] + (My / A) * e[3];
-        cy = qy + (Mx / A) * e[1] + (My / A) * e[4];
-        cz = qz + (Mx / A) * e[2] + (My / A) * e[5];
+        double ia = 1.0 / A;
+        double u = Mx * ia, v = My * ia;
+        cx = qx + u * e[0] + v * e[3];
+        cy = qy + u * e[1] + v * e[4];
+        cz = qz + u * e[2] + v * e[5];
     } else {
         cx = qx; cy = qy; cz = qz;
     }
@@ -944,22 +965,46 @@ PF_DEV void project_from(double cx, double cy, double cz, double yx, double yy, 
     o[0] = cx + t * dx; o[1] = cy + t * dy; o[2] = cz + t * dz;
 }
 
+PF_DEV void cross3(const double *a, const double *b, double *o) {
+    o[0] = fma(a[1], b[2], -a[2] * b[1]);
+    o[1] = fma(a[2], b[0], -a[0] * b[2]);
+    o[2] = fma(a[0], b[1], -a[1] * b[0]);
+}
+PF_DEV double dot3(const double *a, const double *b) { return fma(a[0], b[0], fma(a[1], b[1], a[2] * b[2])); }
+// CCW angle from a to b around the unit axis m, in [0, 2 pi)
+PF_DEV double ccw_angle(const double *a, const double *b, const double *m) {
+    double c[3];
+    cross3(a, b, c);
+    double t = atan2(dot3(c, m), dot3(a, b));
+    return t < 0.0 ? t + 2.0 * PF_PI : t;
+}
+PF_DEV void unit3(double *v) {
+    double n2 = dot3(v, v);
+    if (n2 > 0.0) {
+        double inv = 1.0 / sqrt(n2);
+        v[0] *= inv; v[1] *= inv; v[2] *= inv;
+    }
+}
+
 // _kernels.py:838-1001, streamed over the facet's boundary ring by one lane.
+// Gauss-Bonnet: area = psi (2 pi - sum_arcs (e/R) sweep - sum_vertices theta).
+// Sweeps are CCW angles about the connector circle's axis from one atan2 of
+// (cross, dot) -- the reference's two frame angles phP, phQ -- and the
+// segment orientation test keeps the reference's projected-midpoint rule.
 template <class C>
 PF_DEV double patch_area(WS<C> *ws, int head, int npts, double nx, double ny, double nz, double s,
                          double px, double py, double pz, double psi, double cx, double cy,
                          double cz, bool *unstable_out) {
     EvalScratch<C> &E = ws->u.e;
-    const double R = sqrt(psi);
+    const double R = sqrt(psi), iR = 1.0 / R;
     bool unstable = false;
-    double kg_sum = 0.0;
-    // tangents: tin_i comes from connector i-1, tout_i from connector i
+    double kg_sum = 0.0, th_sum = 0.0;
     double pr0[3], pri[3], prj[3];
     if (E.pfl[head] & PF_ONSPH) { pr0[0] = E.ppx[head]; pr0[1] = E.ppy[head]; pr0[2] = E.ppz[head]; }
     else project_from(cx, cy, cz, E.ppx[head], E.ppy[head], E.ppz[head], px, py, pz, psi, pr0);
     pri[0] = pr0[0]; pri[1] = pr0[1]; pri[2] = pr0[2];
-    double tin_i[3] = {0.0, 0.0, 0.0};   // tin of the current point (from previous connector)
-    double tout0[3] = {0.0, 0.0, 0.0};   // tout of point 0 (needs tin from the last connector)
+    double tin_i[3] = {0.0, 0.0, 0.0};
+    double tout0[3] = {0.0, 0.0, 0.0};
     int i = head;
     for (int t = 0; t < npts; t++) {
         const int j = E.pnext[i];
@@ -968,103 +1013,74 @@ PF_DEV double patch_area(WS<C> *ws, int head, int npts, double nx, double ny, do
         else project_from(cx, cy, cz, E.ppx[j], E.ppy[j], E.ppz[j], px, py, pz, psi, prj);
         double tout[3] = {0.0, 0.0, 0.0}, tin_j[3] = {0.0, 0.0, 0.0};
         const bool arc = (E.pfl[i] & PF_CONN) != 0;
-        double mx, my, mz, ee;
+        double m[3], ee;
         bool skip = false;
         if (arc) {
-            mx = nx; my = ny; mz = nz; ee = s;
+            m[0] = nx; m[1] = ny; m[2] = nz; ee = s;
         } else {
-            double ax = E.ppx[i] - cx, ay = E.ppy[i] - cy, az = E.ppz[i] - cz;
-            double bx2 = E.ppx[j] - cx, by2 = E.ppy[j] - cy, bz2 = E.ppz[j] - cz;
-            mx = ay * bz2 - az * by2;
-            my = az * bx2 - ax * bz2;
-            mz = ax * by2 - ay * bx2;
-            double mn = sqrt(mx * mx + my * my + mz * mz);
+            double a3[3] = {E.ppx[i] - cx, E.ppy[i] - cy, E.ppz[i] - cz};
+            double b3[3] = {E.ppx[j] - cx, E.ppy[j] - cy, E.ppz[j] - cz};
+            cross3(a3, b3, m);
+            double mn = sqrt(dot3(m, m));
             if (mn < 1e-300) {
                 unstable = true;
                 skip = true;
                 ee = 0.0;
             } else {
-                mx /= mn; my /= mn; mz /= mn;
-                ee = mx * (cx - px) + my * (cy - py) + mz * (cz - pz);
+                double im = 1.0 / mn;
+                m[0] *= im; m[1] *= im; m[2] *= im;
+                ee = m[0] * (cx - px) + m[1] * (cy - py) + m[2] * (cz - pz);
             }
         }
         if (!skip) {
             for (int attempt = 0; attempt < 2; attempt++) {
-                double qx = px + ee * mx, qy = py + ee * my, qz = pz + ee * mz;
-                double rr2 = psi - ee * ee;
-                if (rr2 <= 0.0) { unstable = true; break; }
-                double u[6];
-                perp_basis(mx, my, mz, u);
-                double rpx = pri[0] - qx, rpy = pri[1] - qy, rpz = pri[2] - qz;
-                double phP = atan2(rpx * u[3] + rpy * u[4] + rpz * u[5], rpx * u[0] + rpy * u[1] + rpz * u[2]);
-                double rqx = prj[0] - qx, rqy = prj[1] - qy, rqz = prj[2] - qz;
-                double phQ = atan2(rqx * u[3] + rqy * u[4] + rqz * u[5], rqx * u[0] + rqy * u[1] + rqz * u[2]);
-                double dPQ = phQ - phP;
-                if (dPQ < 0.0) dPQ += 2.0 * PF_PI;
-                double sweep;
-                if (arc) {
-                    sweep = dPQ;
-                } else {
-                    double mxp = 0.5 * (E.ppx[i] + E.ppx[j]);
-                    double myp = 0.5 * (E.ppy[i] + E.ppy[j]);
-                    double mzp = 0.5 * (E.ppz[i] + E.ppz[j]);
+                const double q[3] = {px + ee * m[0], py + ee * m[1], pz + ee * m[2]};
+                if (psi - ee * ee <= 0.0) { unstable = true; break; }
+                const double rp[3] = {pri[0] - q[0], pri[1] - q[1], pri[2] - q[2]};
+                const double rq[3] = {prj[0] - q[0], prj[1] - q[1], prj[2] - q[2]};
+                const double dPQ = ccw_angle(rp, rq, m);
+                if (!arc) {
                     double h[3];
-                    project_from(cx, cy, cz, mxp, myp, mzp, px, py, pz, psi, h);
-                    double rmx = h[0] - qx, rmy = h[1] - qy, rmz = h[2] - qz;
-                    double phM = atan2(rmx * u[3] + rmy * u[4] + rmz * u[5], rmx * u[0] + rmy * u[1] + rmz * u[2]);
-                    double dPM = phM - phP;
-                    if (dPM < 0.0) dPM += 2.0 * PF_PI;
-                    if (dPM <= dPQ + 1e-12) {
-                        sweep = dPQ;
-                    } else {
-                        mx = -mx; my = -my; mz = -mz; ee = -ee;
+                    project_from(cx, cy, cz, 0.5 * (E.ppx[i] + E.ppx[j]), 0.5 * (E.ppy[i] + E.ppy[j]),
+                                 0.5 * (E.ppz[i] + E.ppz[j]), px, py, pz, psi, h);
+                    const double rm[3] = {h[0] - q[0], h[1] - q[1], h[2] - q[2]};
+                    if (!(ccw_angle(rp, rm, m) <= dPQ + 1e-12)) {
+                        // traversal is clockwise around m: flip the circle normal
+                        m[0] = -m[0]; m[1] = -m[1]; m[2] = -m[2]; ee = -ee;
                         continue;
                     }
                 }
-                kg_sum += (ee / R) * sweep;
-                double t0x = my * rpz - mz * rpy, t0y = mz * rpx - mx * rpz, t0z = mx * rpy - my * rpx;
-                double tn = sqrt(t0x * t0x + t0y * t0y + t0z * t0z);
-                if (tn > 0.0) { t0x /= tn; t0y /= tn; t0z /= tn; }
-                tout[0] = t0x; tout[1] = t0y; tout[2] = t0z;
-                double t1x = my * rqz - mz * rqy, t1y = mz * rqx - mx * rqz, t1z = mx * rqy - my * rqx;
-                tn = sqrt(t1x * t1x + t1y * t1y + t1z * t1z);
-                if (tn > 0.0) { t1x /= tn; t1y /= tn; t1z /= tn; }
-                tin_j[0] = t1x; tin_j[1] = t1y; tin_j[2] = t1z;
+                kg_sum = fma(ee * iR, dPQ, kg_sum);
+                cross3(m, rp, tout);
+                unit3(tout);
+                cross3(m, rq, tin_j);
+                unit3(tin_j);
                 break;
             }
         }
-        // turning angle at point i (needs tin_i, tout_i, proj_i); point 0 deferred
         if (t == 0) {
             tout0[0] = tout[0]; tout0[1] = tout[1]; tout0[2] = tout[2];
         } else {
-            double ax = tin_i[0], ay = tin_i[1], az = tin_i[2];
-            double bx2 = tout[0], by2 = tout[1], bz2 = tout[2];
-            double nxv = (pri[0] - px) / R, nyv = (pri[1] - py) / R, nzv = (pri[2] - pz) / R;
-            double crx = ay * bz2 - az * by2, cry = az * bx2 - ax * bz2, crz = ax * by2 - ay * bx2;
-            double sv = crx * nxv + cry * nyv + crz * nzv;
-            double cv = ax * bx2 + ay * by2 + az * bz2;
-            double th = atan2(sv, cv);
+            // turning angle at point i: tin from connector i-1, tout from connector i
+            double cr[3];
+            cross3(tin_i, tout, cr);
+            const double nv[3] = {(pri[0] - px) * iR, (pri[1] - py) * iR, (pri[2] - pz) * iR};
+            double th = atan2(dot3(cr, nv), dot3(tin_i, tout));
             if (fabs(th) > PF_PI - 1e-7) unstable = true;
-            E.pth[i] = th;
+            th_sum += th;
         }
         tin_i[0] = tin_j[0]; tin_i[1] = tin_j[1]; tin_i[2] = tin_j[2];
         pri[0] = prj[0]; pri[1] = prj[1]; pri[2] = prj[2];
         i = j;
     }
-    {   // point 0: tin from the last connector
-        double ax = tin_i[0], ay = tin_i[1], az = tin_i[2];
-        double bx2 = tout0[0], by2 = tout0[1], bz2 = tout0[2];
-        double nxv = (pr0[0] - px) / R, nyv = (pr0[1] - py) / R, nzv = (pr0[2] - pz) / R;
-        double crx = ay * bz2 - az * by2, cry = az * bx2 - ax * bz2, crz = ax * by2 - ay * bx2;
-        double sv = crx * nxv + cry * nyv + crz * nzv;
-        double cv = ax * bx2 + ay * by2 + az * bz2;
-        double th = atan2(sv, cv);
+    {
+        double cr[3];
+        cross3(tin_i, tout0, cr);
+        const double nv[3] = {(pr0[0] - px) * iR, (pr0[1] - py) * iR, (pr0[2] - pz) * iR};
+        double th = atan2(dot3(cr, nv), dot3(tin_i, tout0));
         if (fabs(th) > PF_PI - 1e-7) unstable = true;
-        E.pth[head] = th;
+        th_sum += th;
     }
-    double th_sum = 0.0;
-    i = head;
-    for (int t = 0; t < npts; t++) { th_sum += E.pth[i]; i = E.pnext[i]; }
     double area = psi * (2.0 * PF_PI - kg_sum - th_sum);
     if (area < -1e-9 * PF_FOUR_PI * psi || area > PF_FOUR_PI * psi * (1.0 + 1e-9)) unstable = true;
     if (area < 0.0) area = 0.0;
@@ -1098,8 +1114,23 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         double wx = P.x[v] - px, wy = P.y[v] - py, wz = P.z[v] - pz;
         double q = wx * wx + wy * wy + wz * wz - psi;
         E.vin[v] = q <= ball_tol ? 1 : 0;
+        E.vdeg[v] = 0;
     }
     if (L == 0) E.npool = 0;
+    // loop-entry facet and successor vertex, for the twin-facet table
+    for (int f = L; f < nf; f += 32) {
+        const int s0 = P.lp[f], m = P.lp[f + 1] - s0;
+        for (int e = 0; e < m; e++) {
+            E.efac[s0 + e] = (uint8_t)f;
+            E.esv[s0 + e] = P.lv[s0 + (e + 1 == m ? 0 : e + 1)];
+        }
+    }
+    pfw::sync();
+    for (int k = L; k < P.nl; k += 32) {
+        const int a = P.lv[k];
+        const int slot = pfw::atom_add_u8(&E.vdeg[a]);
+        if (slot < 4) E.vinc[a * 4 + slot] = (uint16_t)k;
+    }
     pfw::sync();
     // restrict + integrate, lane per facet (_kernels.py:1027-1071)
     bool ovf = false, pool_ovf = false;
@@ -1166,10 +1197,10 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         return;
     }
     pfw::sync();
-    bool any_present = false, any_area = false;
-    for (int f = 0; f < nf; f++) {
-        if (E.fkind[f] != RF_OUTSIDE) any_present = true;
-        if (E.fkind[f] != RF_OUTSIDE && E.farea[f] > 0.0) any_area = true;
+    bool any_area = false;
+    for (int f0 = 0; f0 < nf; f0 += 32) {
+        int f = f0 + L;
+        any_area |= pfw::any(f < nf && E.fkind[f] != RF_OUTSIDE && E.farea[f] > 0.0);
     }
     // NB: reference sets any_present before the A <= 0 demotion; a demoted
     // GENPOLY still counts as "present" there.  Demotion always comes with
@@ -1177,15 +1208,16 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     // which the full-ball/empty branch below treats identically.
     if (!any_area) {
         bool inside = true;
-        for (int f = 0; f < nf; f++)
-            if (E.fh[f] < -tol) { inside = false; break; }
+        for (int f0 = 0; f0 < nf; f0 += 32) {
+            int f = f0 + L;
+            inside &= !pfw::any(f < nf && E.fh[f] < -tol);
+        }
         if ((inside && nf > 0) || nf == 0) {
             res->status = CELL_FULLBALL;
             res->vol = PF_FOUR_PI / 3.0 * psi * R;
             res->K = PF_FOUR_PI * psi;
             res->m2 = want_m2 ? PF_FOUR_PI * psi * R * R * R / 5.0 : 0.0;
         }
-        (void)any_present;
         return;
     }
     // interior point (_kernels.py:723-816): ray per restricted facet, lane per facet
@@ -1231,22 +1263,35 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     pfw::sync();
     double ix, iy, iz, bx = px, by = py, bz = pz;
     {
-        double sx = 0.0, sy = 0.0, sz = 0.0, best_margin = -1.0;
-        int nseg = 0;
-        for (int f = 0; f < nf; f++) {
+        // average of the ray midpoints and the deepest one (first on ties)
+        double sx = 0.0, sy = 0.0, sz = 0.0, bm = -1.0;
+        int nseg = 0, bf = -1;
+        for (int f = L; f < nf; f += 32) {
             if (!E.fseg[f]) continue;
             sx += E.smx[f]; sy += E.smy[f]; sz += E.smz[f];
             nseg++;
-            if (E.smg[f] > best_margin) { best_margin = E.smg[f]; bx = E.smx[f]; by = E.smy[f]; bz = E.smz[f]; }
+            if (E.smg[f] > bm) { bm = E.smg[f]; bf = f; }
         }
+        sx = pfw::sum_d(sx); sy = pfw::sum_d(sy); sz = pfw::sum_d(sz);
+        nseg = pfw::sum_i(nseg);
+        // argmax margin, lowest facet index among equal margins
+        for (int m = 16; m > 0; m >>= 1) {
+            double om = pfw::shfl_xor(bm, m);
+            int of = pfw::shfl_xor(bf, m);
+            if (om > bm || (om == bm && of >= 0 && (bf < 0 || of < bf))) { bm = om; bf = of; }
+        }
+        const double best_margin = bm;
+        if (bf >= 0 && best_margin > -1.0) { bx = E.smx[bf]; by = E.smy[bf]; bz = E.smz[bf]; }
         bool ok = nseg > 0;
         if (ok) {
-            double cx = sx / (double)nseg, cy = sy / (double)nseg, cz = sz / (double)nseg;
+            double inv = 1.0 / (double)nseg;
+            double cx = sx * inv, cy = sy * inv, cz = sz * inv;
             double mg = sqrt(psi) - sqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
-            for (int g = 0; g < nf; g++) {
+            for (int g = L; g < nf; g += 32) {
                 double d2 = P.d[g] - (P.nx[g] * cx + P.ny[g] * cy + P.nz[g] * cz);
                 if (d2 < mg) mg = d2;
             }
+            mg = -pfw::max_d(-mg);
             if (mg <= 0.0) {
                 if (best_margin > 0.0) { cx = bx; cy = by; cz = bz; }
                 else ok = false;
@@ -1270,14 +1315,21 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
             E.funs[f] = uns ? 1 : 0;
         }
         pfw::sync();
-        kbar = 0.0;
-        bool bad = false;
-        for (int f = 0; f < nf; f++) {
-            if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
-            if (E.fkind[f] == RF_FULLCIRCLE) { kbar += 2.0 * PF_PI * R * (R - E.fh[f]); continue; }
-            if (E.funs[f]) { bad = true; break; }
-            kbar += E.fpa[f];
+        // first unstable facet in facet order (the reference stops there)
+        int first_bad = nf;
+        for (int f0 = 0; f0 < nf; f0 += 32) {
+            int f = f0 + L;
+            unsigned mb = pfw::ballot(f < nf && E.funs[f] && !(E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0));
+            if (mb && first_bad == nf) first_bad = f0 + __builtin_ctz_pf(mb);
         }
+        const bool bad = first_bad < nf;
+        double kb = 0.0;
+        for (int f = L; f < first_bad; f += 32) {
+            if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
+            if (E.fkind[f] == RF_FULLCIRCLE) kb += 2.0 * PF_PI * R * (R - E.fh[f]);
+            else kb += E.fpa[f];
+        }
+        kbar = pfw::sum_d(kb);
         pfw::sync();
         if (!bad) break;
         if (attempt == 3) { res->flags |= FLAG_UNSTABLE_PROJECTION; break; }
@@ -1289,10 +1341,9 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     double K = PF_FOUR_PI * psi - kbar;
     if (K < 0.0) K = 0.0;
     if (K > PF_FOUR_PI * psi) K = PF_FOUR_PI * psi;
-    double vol = R * K / 3.0;
-    double mx = 0.0, my = 0.0, mz = 0.0, nsx = 0.0, nsy = 0.0, nsz = 0.0;
-    double m2 = want_m2 ? R * R * R * K / 5.0 : 0.0;
-    for (int f = 0; f < nf; f++) {
+    double vol = 0.0;
+    double mx = 0.0, my = 0.0, mz = 0.0, nsx = 0.0, nsy = 0.0, nsz = 0.0, m2 = 0.0;
+    for (int f = L; f < nf; f += 32) {
         if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
         double fa = E.farea[f], fh = E.fh[f];
         double pv = fh * fa / 3.0;
@@ -1305,6 +1356,10 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         nsz += P.nz[f] * fa;
         if (want_m2) m2 += (fh / 5.0) * (E.fip[f] + fh * fh * fa);
     }
+    vol = R * K / 3.0 + pfw::sum_d(vol);
+    mx = pfw::sum_d(mx); my = pfw::sum_d(my); mz = pfw::sum_d(mz);
+    nsx = pfw::sum_d(nsx); nsy = pfw::sum_d(nsy); nsz = pfw::sum_d(nsz);
+    m2 = want_m2 ? R * R * R * K / 5.0 + pfw::sum_d(m2) : 0.0;
     mx += 0.25 * psi * (-nsx);
     my += 0.25 * psi * (-nsy);
     mz += 0.25 * psi * (-nsz);

@@ -18,6 +18,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -418,6 +420,10 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
         if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
     }
     const double floor_v = 0.5 * std::min(stats3[2], stats3[1]);
+    const bool verbose = getenv("PF_NEWTON_VERBOSE") != nullptr;
+    if (verbose)
+        fprintf(stderr, "[pf_newton] n=%lld init worst=%.6e minvol=%.6e minnu=%.6e floor=%.6e\n",
+                (long long)n, stats3[0], stats3[1], stats3[2], floor_v);
     S.worst_initial = stats3[0];
     double worst = stats3[0];
     for (int it = 0; it < max_newton; it++) {
@@ -457,6 +463,9 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
         S.iterations++;
         S.last_alpha = alpha;
         worst = stats3[0];
+        if (verbose)
+            fprintf(stderr, "[pf_newton] it=%d worst=%.6e minvol=%.6e alpha=%g cg=%d\n", it + 1, worst,
+                    stats3[1], alpha, cg);
     }
     S.worst_final = worst;
     if (S.status == 0 && worst > eps_vol) S.status = 1;  // not converged within max_newton

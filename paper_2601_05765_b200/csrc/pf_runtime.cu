@@ -252,7 +252,7 @@ __global__ void k_grid_export(const int *__restrict__ bstart, int ncell, const i
 
 // cells of the fast tier: shared-memory workspace, one warp per cell, cells
 // visited in bucket order (neighbouring warps share candidates through L1/L2)
-__global__ void __launch_bounds__(FAST_WARPS * 32)
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     k_cells_fast(CellIn in, CellOut out, int count, int *__restrict__ retry_list,
                  int *__restrict__ counters, unsigned long long *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -349,6 +349,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
     if (!c->attr_set) {
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
+        CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int nb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cells_fast, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(WS<FastCaps>)));

@@ -22,8 +22,16 @@ PF_DEV int shfl_xor(int v, int m) { return __shfl_xor_sync(PF_FULL, v, m); }
 PF_DEV double shfl_xor(double v, int m) { return __shfl_xor_sync(PF_FULL, v, m); }
 PF_DEV int popc(unsigned m) { return __popc(m); }
 PF_DEV int atom_add(int *p, int v) { return atomicAdd(p, v); }
+// increment a byte counter in shared memory (word-aligned atomic on its word)
+PF_DEV int atom_add_u8(uint8_t *p) {
+    unsigned *w = (unsigned *)((uintptr_t)p & ~(uintptr_t)3);
+    unsigned sh = ((unsigned)((uintptr_t)p & 3)) * 8;
+    unsigned old = atomicAdd(w, 1u << sh);
+    return (old >> sh) & 0xff;
+}
 PF_DEV unsigned lanemask_lt() { return (1u << lane()) - 1u; }
 }  // namespace pfw
+PF_DEV int __builtin_ctz_pf(unsigned m) { return __ffs(m) - 1; }
 #else
 #ifndef PF_EMU
 #error "pf_warp.cuh: host compilation requires the test emulator (define PF_EMU)"
@@ -38,6 +46,10 @@ PF_DEV double max_d(double v) {
         double o = shfl_xor(v, m);
         v = o > v ? o : v;
     }
+    return v;
+}
+PF_DEV double sum_d(double v) {
+    for (int m = 16; m > 0; m >>= 1) v += shfl_xor(v, m);
     return v;
 }
 PF_DEV int sum_i(int v) {

@@ -17,6 +17,7 @@
 
 #define PF_DEV static inline
 #define PF_DEVNI static
+static inline int __builtin_ctz_pf(unsigned m) { return __builtin_ctz(m); }
 
 extern "C" void emu_swap(void **from_sp, void *to_sp);
 
@@ -90,6 +91,7 @@ static inline int atom_add(int *p, int v) {
     return o;
 }
 static inline unsigned lanemask_lt() { return (1u << g_lane) - 1u; }
+static inline int atom_add_u8(uint8_t *p) { return (*p)++; }
 
 // run fn(ctx, lane) on 32 fibers to completion; returns 0 or an error code
 int emu_run_warp(EmuWarp *w, void (*fn)(void *, int), void *ctx, uint64_t seed);
