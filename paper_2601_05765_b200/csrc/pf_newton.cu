@@ -56,14 +56,15 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     __syncthreads();
     return s;
 }
+__device__ __forceinline__ double nanmax(double a, double b) { return (a != a || b != b) ? NAN : fmax(a, b); }
 __device__ __forceinline__ double block_max(double v, double *sh) {
-    for (int m = 16; m > 0; m >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, m));
+    for (int m = 16; m > 0; m >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, m));
     int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     if (l == 0) sh[w] = v;
     __syncthreads();
     double s = -INFINITY;
     if (threadIdx.x == 0)
-        for (int k = 0; k < (int)(blockDim.x >> 5); k++) s = fmax(s, sh[k]);
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++) s = nanmax(s, sh[k]);
     __syncthreads();
     return s;
 }
@@ -80,8 +81,9 @@ __global__ void __launch_bounds__(RB) k_grad(int64_t n, const double *__restrict
     for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
         double v = vol[i], t = nu[i];
         if (g) g[i] = t - v;
-        worst = fmax(worst, fabs(v - t) / t);
-        vmin = fmin(vmin, v);
+        double e = fabs(v - t) / t;
+        if (!(e <= worst)) worst = e;  // NaN-propagating max / min
+        if (!(v >= vmin)) vmin = v;
         nmin = fmin(nmin, t);
     }
     double a = block_max(worst, sh), b = block_min(vmin, sh), c = block_min(nmin, sh);
@@ -97,8 +99,8 @@ __global__ void k_grad_fin(const double *__restrict__ part, int nb, double *out)
     __shared__ double sh[32];
     double a = 0.0, b = INFINITY, c = INFINITY;
     for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-        a = fmax(a, part[k]);
-        b = fmin(b, part[NPART + k]);
+        a = nanmax(a, part[k]);
+        b = -nanmax(-b, -part[NPART + k]);
         c = fmin(c, part[2 * NPART + k]);
     }
     a = block_max(a, sh);
