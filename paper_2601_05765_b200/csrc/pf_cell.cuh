@@ -804,6 +804,14 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
             if (ta <= tb) t = which == 0 ? t1 : t2;
             else t = which == 0 ? t2 : t1;
             if (t <= tlo + tol || t >= thi - tol) continue;
+            // The first root in walk order is where the edge enters the ball.
+            // After a vertex classified inside (cur_inside == ina here) it can
+            // only pass the range test if that vertex lies outside the sphere
+            // by less than the tolerance; the reference then labels the entry
+            // an exit and closes the facet with a spurious arc (a whole
+            // circular segment too much).  It coincides with the vertex to
+            // ~tol: drop it.  Never fires on consistent geometry.
+            if (which == 0 && cur_inside) continue;
             if (npts >= REF_MAX_P) return -1;
             double cxx = x0x + t * ux, cxy = x0y + t * uy, cxz = x0z + t * uz;
             if (cur_inside) {
@@ -878,14 +886,39 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
     return RF_GENPOLY;
 }
 
+// Degenerate arcs.  When a loop vertex sits within tolerance of the sphere,
+// the reference can emit an arc connector whose two end points coincide to
+// ~tol but come out in clockwise order; its sweep then wraps from ~-1e-9 to
+// ~2 pi (_kernels.py:696-700 and 919-921), adding a whole disk / cap to the
+// facet.  A long arc must pass through the antipode of its start point on the
+// facet circle, so when that antipode lies outside the cell the arc can only
+// be the short one.  This test only fires for end points closer than
+// PF_ARC_CHORD * tol and only flips sweeps the geometry proves impossible
+// (see tests/test_degenerate_arcs.py: Monte-Carlo volumes of such cells).
+#define PF_ARC_CHORD 100.0
+template <class C>
+PF_DEV bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
+                                double dx, double dy, double dz, double rc, double tol) {
+    double dn = sqrt(dx * dx + dy * dy + dz * dz);
+    if (!(dn > 0.0)) return false;
+    double k = rc / dn;
+    double mx = qx - k * dx, my = qy - k * dy, mz = qz - k * dz;
+    for (int g = 0; g < P.nf; g++) {
+        if (g == f) continue;
+        if (P.nx[g] * mx + P.ny[g] * my + P.nz[g] * mz - P.d[g] > tol) return true;
+    }
+    return false;
+}
+
 // _kernels.py:678-716 + 331-390: area, centroid, polar moment of a restricted
 // facet.  Same Green forms as the reference; an arc's trigonometric values come
 // from its end-point coordinates (cos a = x/r, sin a = y/r, double-angle
 // identities) and its sweep from one atan2 of (cross, dot), instead of
 // 2 atan2 + 8 sin/cos per arc.  Agrees with the reference to rounding.
 template <class C>
-PF_DEV void seq_integrals(WS<C> *ws, int head, int npts, double nx, double ny, double nz,
-                          double qx, double qy, double qz, double rc, double *out) {
+PF_DEV void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
+                          double nx, double ny, double nz, double qx, double qy, double qz,
+                          double rc, double *out) {
     EvalScratch<C> &E = ws->u.e;
     double e[6];
     perp_basis(nx, ny, nz, e);
@@ -919,7 +952,14 @@ PF_DEV void seq_integrals(WS<C> *ws, int head, int npts, double nx, double ny, d
             double c0 = r0 > 0.0 ? x0 / r0 : 1.0, s0 = r0 > 0.0 ? y0 / r0 : 0.0;
             double c1 = r1 > 0.0 ? x1 / r1 : 1.0, s1 = r1 > 0.0 ? y1 / r1 : 0.0;
             double dth = atan2(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
-            if (dth <= 0.0) dth += 2.0 * PF_PI;
+            if (dth <= 0.0) {
+                dth += 2.0 * PF_PI;
+                double ch2 = (x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0);
+                if (ch2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
+                    long_arc_impossible(P, f, qx, qy, qz, x0 * e[0] + y0 * e[3], x0 * e[1] + y0 * e[4],
+                                        x0 * e[2] + y0 * e[5], rc, tol))
+                    dth -= 2.0 * PF_PI;
+            }
             double s20 = 2.0 * s0 * c0, c20 = fma(c0, c0, -s0 * s0);
             double s21 = 2.0 * s1 * c1, c21 = fma(c1, c1, -s1 * s1);
             double s40 = 2.0 * s20 * c20, s41 = 2.0 * s21 * c21;
@@ -992,9 +1032,10 @@ PF_DEV void unit3(double *v) {
 // (cross, dot) -- the reference's two frame angles phP, phQ -- and the
 // segment orientation test keeps the reference's projected-midpoint rule.
 template <class C>
-PF_DEV double patch_area(WS<C> *ws, int head, int npts, double nx, double ny, double nz, double s,
-                         double px, double py, double pz, double psi, double cx, double cy,
-                         double cz, bool *unstable_out) {
+PF_DEV double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
+                         double nx, double ny, double nz, double s, double px, double py,
+                         double pz, double psi, double cx, double cy, double cz,
+                         bool *unstable_out) {
     EvalScratch<C> &E = ws->u.e;
     const double R = sqrt(psi), iR = 1.0 / R;
     bool unstable = false;
@@ -1038,7 +1079,14 @@ PF_DEV double patch_area(WS<C> *ws, int head, int npts, double nx, double ny, do
                 if (psi - ee * ee <= 0.0) { unstable = true; break; }
                 const double rp[3] = {pri[0] - q[0], pri[1] - q[1], pri[2] - q[2]};
                 const double rq[3] = {prj[0] - q[0], prj[1] - q[1], prj[2] - q[2]};
-                const double dPQ = ccw_angle(rp, rq, m);
+                double dPQ = ccw_angle(rp, rq, m);
+                if (arc && dPQ > PF_PI) {
+                    const double d0 = rp[0] - rq[0], d1 = rp[1] - rq[1], d2 = rp[2] - rq[2];
+                    if (d0 * d0 + d1 * d1 + d2 * d2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
+                        long_arc_impossible(P, f, q[0], q[1], q[2], rp[0], rp[1], rp[2],
+                                            sqrt(psi - ee * ee), tol))
+                        dPQ -= 2.0 * PF_PI;
+                }
                 if (!arc) {
                     double h[3];
                     project_from(cx, cy, cz, 0.5 * (E.ppx[i] + E.ppx[j]), 0.5 * (E.ppy[i] + E.ppy[j]),
@@ -1154,7 +1202,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
             E.fip[f] = 0.5 * PF_PI * (rc2 * rc2);
         } else {
             double o[5];
-            seq_integrals(ws, head, npts, P.nx[f], P.ny[f], P.nz[f], qx, qy, qz, rc, o);
+            seq_integrals(ws, P, f, tol, head, npts, P.nx[f], P.ny[f], P.nz[f], qx, qy, qz, rc, o);
             if (o[0] <= 0.0) {
                 E.fkind[f] = RF_OUTSIDE;
                 E.farea[f] = 0.0; E.fcx[f] = px; E.fcy[f] = py; E.fcz[f] = pz; E.fip[f] = 0.0;
@@ -1310,8 +1358,8 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
             E.funs[f] = 0;
             if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0 || E.fkind[f] == RF_FULLCIRCLE) continue;
             bool uns;
-            E.fpa[f] = patch_area(ws, E.fhead[f], E.fnp[f], P.nx[f], P.ny[f], P.nz[f], E.fh[f], px, py,
-                                  pz, psi, ix, iy, iz, &uns);
+            E.fpa[f] = patch_area(ws, P, f, tol, E.fhead[f], E.fnp[f], P.nx[f], P.ny[f], P.nz[f], E.fh[f],
+                                  px, py, pz, psi, ix, iy, iz, &uns);
             E.funs[f] = uns ? 1 : 0;
         }
         pfw::sync();
