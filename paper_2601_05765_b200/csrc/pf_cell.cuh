@@ -172,9 +172,11 @@ struct CellOut {
 };
 
 PF_DEV double sq(double x) { return x * x; }
+// one out-of-line copy of the (long) double-precision atan2
+PF_NOINL double atan2_ool(double y, double x) { return atan2(y, x); }
 
 // _kernels.py:59-80
-PF_DEV void perp_basis(double nx, double ny, double nz, double *e) {
+PF_NOINL void perp_basis(double nx, double ny, double nz, double *e) {
     double ax = fabs(nx), ay = fabs(ny), az = fabs(nz);
     double ux, uy, uz;
     if (ax <= ay && ax <= az) { ux = 1.0; uy = 0.0; uz = 0.0; }
@@ -194,15 +196,19 @@ PF_DEV void perp_basis(double nx, double ny, double nz, double *e) {
 template <class C>
 PF_DEV void load_domain(Poly<C> &A, const CellIn &in) {
     const int L = pfw::lane();
+    #pragma unroll 1
     for (int v = L; v < in.dnv; v += 32) {
         A.x[v] = in.dv[3 * v]; A.y[v] = in.dv[3 * v + 1]; A.z[v] = in.dv[3 * v + 2];
     }
+    #pragma unroll 1
     for (int f = L; f < in.dnf; f += 32) {
         A.nx[f] = in.dp[4 * f]; A.ny[f] = in.dp[4 * f + 1]; A.nz[f] = in.dp[4 * f + 2];
         A.d[f] = in.dp[4 * f + 3];
         A.tag[f] = in.dt[f];
     }
+    #pragma unroll 1
     for (int f = L; f <= in.dnf; f += 32) A.lp[f] = (uint16_t)in.dlp[f];
+    #pragma unroll 1
     for (int k = L; k < in.dnl; k += 32) A.lv[k] = (uint16_t)in.dlv[k];
     if (L == 0) { A.nv = in.dnv; A.nf = in.dnf; A.nl = in.dnl; }
     pfw::sync();
@@ -212,6 +218,7 @@ PF_DEV void load_domain(Poly<C> &A, const CellIn &in) {
 template <class C>
 PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
     double m = 0.0;
+    #pragma unroll 1
     for (int v = pfw::lane(); v < A.nv; v += 32) {
         double d2 = sq(A.x[v] - px) + sq(A.y[v] - py) + sq(A.z[v] - pz);
         if (d2 > m) m = d2;
@@ -223,7 +230,7 @@ PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
 // clip A by n.x <= dd into B (_kernels.py:109-319), warp-cooperative
 // ---------------------------------------------------------------------------
 template <class C>
-PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, double nz,
+PF_NOINL int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, double nz,
                 double dd, int tag, double tol) {
     BuildScratch<C> &S = ws->u.b;
     const int L = pfw::lane();
@@ -233,6 +240,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
 
     // 1. classify vertices (_kernels.py:121-134)
     int n_out = 0;
+    #pragma unroll 1
     for (int v0 = 0; v0 < nv; v0 += 32) {
         int v = v0 + L;
         bool out = false;
@@ -249,6 +257,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
 
     // 2. keep inside vertices in order (_kernels.py:137-147)
     int K = 0;
+    #pragma unroll 1
     for (int v0 = 0; v0 < nv; v0 += 32) {
         int v = v0 + L;
         bool keep = v < nv && S.sd[v] <= tol;
@@ -264,9 +273,11 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     }
 
     // 3a. per facet: emitted loop length and crossing-edge count (_kernels.py:160-228)
+    #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         int start = A.lp[f], m = A.lp[f + 1] - start;
         int k = 0, c = 0;
+        #pragma unroll 1
         for (int e = 0; e < m; e++) {
             int a = A.lv[start + e];
             int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
@@ -286,6 +297,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     // 3b. prefix sums in facet order: crossing bases, kept-facet loop bases
     int NE = 0, NFk = 0, NLk = 0;
     bool small_facet = false;  // a dropped facet that still emitted 1-2 entries
+    #pragma unroll 1
     for (int f0 = 0; f0 < nf; f0 += 32) {
         int f = f0 + L;
         int c = 0, kk = 0, keep = 0;
@@ -309,9 +321,11 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     if (NE > C::CE) { if (L == 0) ws->oflow = 1; pfw::sync(); return CLIP_OVERFLOW; }
     pfw::sync();
     // 3c. crossing entries in walk order
+    #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         int start = A.lp[f], m = A.lp[f + 1] - start;
         int pos = S.fcb[f];
+        #pragma unroll 1
         for (int e = 0; e < m; e++) {
             int a = A.lv[start + e];
             int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
@@ -324,6 +338,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     pfw::sync();
     // 3d. first encounter of each edge creates the crossing vertex (_kernels.py:178-200)
     int NFirst = 0;
+    #pragma unroll 1
     for (int q0 = 0; q0 < NE; q0 += 32) {
         int q = q0 + L;
         bool first = false;
@@ -331,6 +346,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
         if (q < NE) {
             int a = S.ea[q], b = S.eb[q];
             int lo = a < b ? a : b, hi = a < b ? b : a;
+            #pragma unroll 1
             for (int r = 0; r < q; r++) {
                 int ra = S.ea[r], rb = S.eb[r];
                 int rlo = ra < rb ? ra : rb, rhi = ra < rb ? rb : ra;
@@ -362,12 +378,14 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
         return CLIP_OVERFLOW;
     }
     pfw::sync();
+    #pragma unroll 1
     for (int q = L; q < NE; q += 32) {
         int mt = S.emt[q];
         if (mt != q) S.eid[q] = S.eid[mt];
     }
     pfw::sync();
     // 3e. emit kept facets (_kernels.py:229-241)
+    #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         int lb = S.flb[f];
         if (lb == 0xffff) continue;
@@ -378,6 +396,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
         B.lp[o + 1] = (uint16_t)(lb + S.fk[f]);
         int start = A.lp[f], m = A.lp[f + 1] - start;
         int pos = S.fcb[f], w = lb;
+        #pragma unroll 1
         for (int e = 0; e < m; e++) {
             int a = A.lv[start + e];
             int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
@@ -392,6 +411,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     // (sa >= -tol when emitted, i.e. every kept vertex with sd >= -tol) and
     // all crossing vertices, in B index order.
     int ncp = 0;
+    #pragma unroll 1
     for (int v0 = 0; v0 < nv; v0 += 32) {
         int v = v0 + L;
         bool on = v < nv && S.sd[v] <= tol && S.sd[v] >= -tol;
@@ -399,6 +419,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
         if (on) S.onl[ncp + pfw::popc(m & lt)] = S.vmap[v];
         ncp += pfw::popc(m);
     }
+    #pragma unroll 1
     for (int q = L; q < NFirst; q += 32) S.onl[ncp + q] = (uint16_t)(K + q);
     ncp += NFirst;
     if (ncp < 3) { pfw::sync(); return CLIP_DEGENERATE; }
@@ -410,6 +431,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     pfw::sync();
     // centroid: sequential sum in index order, computed redundantly by every lane
     double ccx = 0.0, ccy = 0.0, ccz = 0.0;
+    #pragma unroll 1
     for (int q = 0; q < ncp; q++) {
         int v = S.onl[q];
         ccx += B.x[v]; ccy += B.y[v]; ccz += B.z[v];
@@ -417,17 +439,20 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
     ccx /= (double)ncp; ccy /= (double)ncp; ccz /= (double)ncp;
     double e[6];
     perp_basis(nx, ny, nz, e);
+    #pragma unroll 1
     for (int q = L; q < ncp; q += 32) {
         int v = S.onl[q];
         double rx = B.x[v] - ccx, ry = B.y[v] - ccy, rz = B.z[v] - ccz;
-        S.sd[q] = atan2(rx * e[3] + ry * e[4] + rz * e[5], rx * e[0] + ry * e[1] + rz * e[2]);
+        S.sd[q] = atan2_ool(rx * e[3] + ry * e[4] + rz * e[5], rx * e[0] + ry * e[1] + rz * e[2]);
     }
     pfw::sync();
     // rank sort by (angle, index): the reference's insertion sort is stable on a total order
+    #pragma unroll 1
     for (int q = L; q < ncp; q += 32) {
         double aq = S.sd[q];
         int vq = S.onl[q];
         int r = 0;
+        #pragma unroll 1
         for (int u = 0; u < ncp; u++) {
             double au = S.sd[u];
             int vu = S.onl[u];
@@ -453,17 +478,21 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
         pfw::sync();
         return CLIP_CUT;
     }
+    #pragma unroll 1
     for (int v = L; v < NVB; v += 32) S.vmap[v] = 0;
     pfw::sync();
+    #pragma unroll 1
     for (int k = L; k < NL2; k += 32) S.vmap[B.lv[k]] = 1;
     pfw::sync();
     int nref = 0;
+    #pragma unroll 1
     for (int v0 = 0; v0 < NVB; v0 += 32) {
         int v = v0 + L;
         nref += pfw::popc(pfw::ballot(v < NVB && S.vmap[v] == 1));
     }
     if (nref != NVB) {
         int base = 0;
+        #pragma unroll 1
         for (int v0 = 0; v0 < NVB; v0 += 32) {
             int v = v0 + L;
             bool r = v < NVB && S.vmap[v] == 1;
@@ -476,6 +505,7 @@ PF_DEV int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, d
             base += pfw::popc(m);
             pfw::sync();
         }
+        #pragma unroll 1
         for (int k = L; k < NL2; k += 32) B.lv[k] = (uint16_t)(S.vmap[B.lv[k]] - 2);
         nref = base;
     }
@@ -504,7 +534,7 @@ PF_DEV int bucket_coord(double x, double lo, double ih, int gn) {
 // returns the number of candidates (may exceed CC: overflow); *all_sites set
 // when the bucket range spans the whole grid
 template <class C>
-PF_DEV int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, double py, double pz,
+PF_NOINL int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, double py, double pz,
                         double t_lo, double t_hi, bool *all_sites) {
     BuildScratch<C> &S = ws->u.b;
     const GridView &g = in.g;
@@ -523,6 +553,7 @@ PF_DEV int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, double
     if (L == 0) S.ncand = 0;
     pfw::sync();
     bool beyond = false;
+    #pragma unroll 1
     for (int r0 = 0; r0 < nruns; r0 += 32) {
         int rr = r0 + L;
         int st = 0, len = 0;
@@ -539,6 +570,7 @@ PF_DEV int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, double
         S.run_off[L] = off;
         pfw::sync();
         int nr = nruns - r0 < 32 ? nruns - r0 : 32;
+        #pragma unroll 1
         for (int q0 = 0; q0 < tot; q0 += 32) {
             int q = q0 + L;
             if (q < tot) {
@@ -568,7 +600,7 @@ PF_DEV int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, double
 
 // sort the shell's candidates by (d2, j) in place (rank sort through registers)
 template <class C>
-PF_DEV void sort_candidates(WS<C> *ws, int nc) {
+PF_NOINL void sort_candidates(WS<C> *ws, int nc) {
     BuildScratch<C> &S = ws->u.b;
     const int L = pfw::lane();
     constexpr int PER = (C::CC + 31) / 32;
@@ -582,6 +614,7 @@ PF_DEV void sort_candidates(WS<C> *ws, int nc) {
             kd[t] = S.cd2[q];
             kj[t] = S.cj[q];
             int r = 0;
+            #pragma unroll 1
             for (int u = 0; u < nc; u++) {
                 double du = S.cd2[u];
                 int ju = S.cj[u];
@@ -603,7 +636,7 @@ PF_DEV void sort_candidates(WS<C> *ws, int nc) {
 // returns 0 ok / 1 empty / 3 overflow; *which = buffer holding the cell
 // ---------------------------------------------------------------------------
 template <class C>
-PF_DEV int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int *nclips) {
+PF_NOINL int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int *nclips) {
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const double psii = in.psi[i];
     const double tol = in.tol, dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
@@ -619,6 +652,7 @@ PF_DEV int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int *n
     double t_lo = -1.0;
     double t_hi = in.ball_aware ? br * br * (1.0 + 1e-14) : in.t_init;
     if (!(t_hi > 0.0)) t_hi = 1e-300;
+    #pragma unroll 1
     for (;;) {
         bool all_sites = false;
         int nc = gather_shell(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites);
@@ -637,6 +671,7 @@ PF_DEV int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int *n
             continue;
         }
         sort_candidates(ws, nc);
+        #pragma unroll 1
         for (int c = 0; c < nc; c++) {
             double stop_r = rfar + sqrt(rfar * rfar + dpsi);
             if (in.ball_aware && br < stop_r) stop_r = br;
@@ -684,7 +719,7 @@ enum { PF_ONSPH = 1, PF_CONN = 2, PF_DEL = 4 };
 // (_kernels.py:411-675).  Executed by one lane.  Returns the kind, -1 on
 // MAX_P overflow, -2 on pool overflow.
 template <class C>
-PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double py, double pz,
+PF_NOINL int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double py, double pz,
                           double psi, double tol, double *s_out, double *rc_out, int *head_out,
                           int *np_out) {
     EvalScratch<C> &E = ws->u.e;
@@ -700,6 +735,7 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
     const double qx = px + s * nx, qy = py + s * ny, qz = pz + s * nz;
     const int start = P.lp[f], m = P.lp[f + 1] - start;
     int n_in = 0;
+    #pragma unroll 1
     for (int e = 0; e < m; e++) n_in += E.vin[P.lv[start + e]];
 
     int head = -1, prev = -1, npts = 0;
@@ -716,6 +752,7 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
     } while (0)
 
     if (n_in == m) {
+        #pragma unroll 1
         for (int e = 0; e < m; e++) {
             int v = P.lv[start + e];
             PF_EMIT(P.x[v], P.y[v], P.z[v], 0);
@@ -726,6 +763,7 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
     }
     bool first_entry = false;
     bool cur_inside = E.vin[P.lv[start]] != 0;
+    #pragma unroll 1
     for (int e = 0; e < m; e++) {
         const int a = P.lv[start + e];
         const int bb = P.lv[start + (e + 1 == m ? 0 : e + 1)];
@@ -742,15 +780,18 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
         int g = -1;
         const int dg = E.vdeg[bb];
         if (dg <= 4) {
+            #pragma unroll 1
             for (int t = 0; t < dg; t++) {
                 const int k2 = E.vinc[bb * 4 + t];
                 const int g2 = E.efac[k2];
                 if (E.esv[k2] == a && g2 != f && (g < 0 || g2 < g)) g = g2;
             }
         } else {
+            #pragma unroll 1
             for (int gg = 0; gg < nf && g < 0; gg++) {
                 if (gg == f) continue;
                 int s0 = P.lp[gg], mg = P.lp[gg + 1] - s0;
+                #pragma unroll 1
                 for (int ee = 0; ee < mg; ee++) {
                     if (P.lv[s0 + ee] == bb && P.lv[s0 + (ee + 1 == mg ? 0 : ee + 1)] == a) { g = gg; break; }
                 }
@@ -799,6 +840,7 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
         double tb = ux * (P.x[bb] - x0x) + uy * (P.y[bb] - x0y) + uz * (P.z[bb] - x0z);
         double tlo = ta < tb ? ta : tb;
         double thi = ta < tb ? tb : ta;
+        #pragma unroll 1
         for (int which = 0; which < 2; which++) {
             double t;
             if (ta <= tb) t = which == 0 ? t1 : t2;
@@ -831,6 +873,7 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
         double eb[6];
         perp_basis(nx, ny, nz, eb);
         bool cin = true;
+        #pragma unroll 1
         for (int e = 0; e < m; e++) {
             int a = P.lv[start + e];
             int bb = P.lv[start + (e + 1 == m ? 0 : e + 1)];
@@ -848,6 +891,7 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
     {
         int i = head;
         int kept = 0;
+        #pragma unroll 1
         for (int t = 0; t < npts; t++) {
             int j = E.pnext[i];
             bool jdel = (E.pfl[j] & PF_DEL) != 0;  // only the wrap to a merged head
@@ -865,6 +909,7 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
         if (kept < npts) {
             int nh = -1, lastk = -1;
             i = head;
+            #pragma unroll 1
             for (int t = 0; t < npts; t++) {
                 int j = E.pnext[i];
                 if (!(E.pfl[i] & PF_DEL)) {
@@ -897,12 +942,13 @@ PF_DEV int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double 
 // (see tests/test_degenerate_arcs.py: Monte-Carlo volumes of such cells).
 #define PF_ARC_CHORD 100.0
 template <class C>
-PF_DEV bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
+PF_NOINL bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
                                 double dx, double dy, double dz, double rc, double tol) {
     double dn = sqrt(dx * dx + dy * dy + dz * dz);
     if (!(dn > 0.0)) return false;
     double k = rc / dn;
     double mx = qx - k * dx, my = qy - k * dy, mz = qz - k * dz;
+    #pragma unroll 1
     for (int g = 0; g < P.nf; g++) {
         if (g == f) continue;
         if (P.nx[g] * mx + P.ny[g] * my + P.nz[g] * mz - P.d[g] > tol) return true;
@@ -916,7 +962,7 @@ PF_DEV bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, d
 // identities) and its sweep from one atan2 of (cross, dot), instead of
 // 2 atan2 + 8 sin/cos per arc.  Agrees with the reference to rounding.
 template <class C>
-PF_DEV void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
+PF_NOINL void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
                           double nx, double ny, double nz, double qx, double qy, double qz,
                           double rc, double *out) {
     EvalScratch<C> &E = ws->u.e;
@@ -928,6 +974,7 @@ PF_DEV void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int he
     double x0 = (E.ppx[i] - qx) * e[0] + (E.ppy[i] - qy) * e[1] + (E.ppz[i] - qz) * e[2];
     double y0 = (E.ppx[i] - qx) * e[3] + (E.ppy[i] - qy) * e[4] + (E.ppz[i] - qz) * e[5];
     const double x00 = x0, y00 = y0;
+    #pragma unroll 1
     for (int t = 0; t < npts; t++) {
         const int j = E.pnext[i];
         double x1, y1;
@@ -951,7 +998,7 @@ PF_DEV void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int he
             double r0 = sqrt(x0 * x0 + y0 * y0), r1 = sqrt(x1 * x1 + y1 * y1);
             double c0 = r0 > 0.0 ? x0 / r0 : 1.0, s0 = r0 > 0.0 ? y0 / r0 : 0.0;
             double c1 = r1 > 0.0 ? x1 / r1 : 1.0, s1 = r1 > 0.0 ? y1 / r1 : 0.0;
-            double dth = atan2(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
+            double dth = atan2_ool(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
             if (dth <= 0.0) {
                 dth += 2.0 * PF_PI;
                 double ch2 = (x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0);
@@ -992,7 +1039,7 @@ PF_DEV void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int he
 }
 
 // _kernels.py:819-835
-PF_DEV void project_from(double cx, double cy, double cz, double yx, double yy, double yz,
+PF_NOINL void project_from(double cx, double cy, double cz, double yx, double yy, double yz,
                          double px, double py, double pz, double psi, double *o) {
     double dx = yx - cx, dy = yy - cy, dz = yz - cz;
     double a = dx * dx + dy * dy + dz * dz;
@@ -1015,7 +1062,7 @@ PF_DEV double dot3(const double *a, const double *b) { return fma(a[0], b[0], fm
 PF_DEV double ccw_angle(const double *a, const double *b, const double *m) {
     double c[3];
     cross3(a, b, c);
-    double t = atan2(dot3(c, m), dot3(a, b));
+    double t = atan2_ool(dot3(c, m), dot3(a, b));
     return t < 0.0 ? t + 2.0 * PF_PI : t;
 }
 PF_DEV void unit3(double *v) {
@@ -1032,7 +1079,7 @@ PF_DEV void unit3(double *v) {
 // (cross, dot) -- the reference's two frame angles phP, phQ -- and the
 // segment orientation test keeps the reference's projected-midpoint rule.
 template <class C>
-PF_DEV double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
+PF_NOINL double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
                          double nx, double ny, double nz, double s, double px, double py,
                          double pz, double psi, double cx, double cy, double cz,
                          bool *unstable_out) {
@@ -1047,6 +1094,7 @@ PF_DEV double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int hea
     double tin_i[3] = {0.0, 0.0, 0.0};
     double tout0[3] = {0.0, 0.0, 0.0};
     int i = head;
+    #pragma unroll 1
     for (int t = 0; t < npts; t++) {
         const int j = E.pnext[i];
         if (t + 1 == npts) { prj[0] = pr0[0]; prj[1] = pr0[1]; prj[2] = pr0[2]; }
@@ -1074,6 +1122,7 @@ PF_DEV double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int hea
             }
         }
         if (!skip) {
+            #pragma unroll 1
             for (int attempt = 0; attempt < 2; attempt++) {
                 const double q[3] = {px + ee * m[0], py + ee * m[1], pz + ee * m[2]};
                 if (psi - ee * ee <= 0.0) { unstable = true; break; }
@@ -1113,7 +1162,7 @@ PF_DEV double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int hea
             double cr[3];
             cross3(tin_i, tout, cr);
             const double nv[3] = {(pri[0] - px) * iR, (pri[1] - py) * iR, (pri[2] - pz) * iR};
-            double th = atan2(dot3(cr, nv), dot3(tin_i, tout));
+            double th = atan2_ool(dot3(cr, nv), dot3(tin_i, tout));
             if (fabs(th) > PF_PI - 1e-7) unstable = true;
             th_sum += th;
         }
@@ -1125,7 +1174,7 @@ PF_DEV double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int hea
         double cr[3];
         cross3(tin_i, tout0, cr);
         const double nv[3] = {(pr0[0] - px) * iR, (pr0[1] - py) * iR, (pr0[2] - pz) * iR};
-        double th = atan2(dot3(cr, nv), dot3(tin_i, tout0));
+        double th = atan2_ool(dot3(cr, nv), dot3(tin_i, tout0));
         if (fabs(th) > PF_PI - 1e-7) unstable = true;
         th_sum += th;
     }
@@ -1147,7 +1196,7 @@ struct CellRes {
 // _kernels.py:1008-1170.  Returns with res filled in every lane.  On pool
 // overflow sets ws->oflow (fast instantiation) and returns.
 template <class C>
-PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, double pz,
+PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, double pz,
                           double psi, double tol, int want_m2, CellRes *res) {
     EvalScratch<C> &E = ws->u.e;
     const int L = pfw::lane();
@@ -1158,6 +1207,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     if (psi <= 0.0) return;
     const double R = sqrt(psi);
     const double ball_tol = tol * (2.0 * R + tol);
+    #pragma unroll 1
     for (int v = L; v < P.nv; v += 32) {
         double wx = P.x[v] - px, wy = P.y[v] - py, wz = P.z[v] - pz;
         double q = wx * wx + wy * wy + wz * wz - psi;
@@ -1166,14 +1216,17 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     }
     if (L == 0) E.npool = 0;
     // loop-entry facet and successor vertex, for the twin-facet table
+    #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         const int s0 = P.lp[f], m = P.lp[f + 1] - s0;
+        #pragma unroll 1
         for (int e = 0; e < m; e++) {
             E.efac[s0 + e] = (uint8_t)f;
             E.esv[s0 + e] = P.lv[s0 + (e + 1 == m ? 0 : e + 1)];
         }
     }
     pfw::sync();
+    #pragma unroll 1
     for (int k = L; k < P.nl; k += 32) {
         const int a = P.lv[k];
         const int slot = pfw::atom_add_u8(&E.vdeg[a]);
@@ -1182,6 +1235,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     pfw::sync();
     // restrict + integrate, lane per facet (_kernels.py:1027-1071)
     bool ovf = false, pool_ovf = false;
+    #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         double s, rc;
         int head, npts;
@@ -1219,11 +1273,13 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     }
     if (ws->cen_on) {
         int cross = 0, seg = 0, arc = 0, bp = 0, proj = 0, fc = 0;
+        #pragma unroll 1
         for (int f = L; f < nf; f += 32) {
             int k = E.fkind[f];
             if (k == RF_FULLCIRCLE) fc++;
             if ((k == RF_GENPOLY || k == RF_UNTOUCHED) && E.fnp[f] > 0) {
                 int i = E.fhead[f];
+                #pragma unroll 1
                 for (int t = 0; t < E.fnp[f]; t++) {
                     bp++;
                     if (E.pfl[i] & PF_ONSPH) cross++; else proj++;
@@ -1246,6 +1302,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     }
     pfw::sync();
     bool any_area = false;
+    #pragma unroll 1
     for (int f0 = 0; f0 < nf; f0 += 32) {
         int f = f0 + L;
         any_area |= pfw::any(f < nf && E.fkind[f] != RF_OUTSIDE && E.farea[f] > 0.0);
@@ -1256,6 +1313,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     // which the full-ball/empty branch below treats identically.
     if (!any_area) {
         bool inside = true;
+        #pragma unroll 1
         for (int f0 = 0; f0 < nf; f0 += 32) {
             int f = f0 + L;
             inside &= !pfw::any(f < nf && E.fh[f] < -tol);
@@ -1269,6 +1327,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         return;
     }
     // interior point (_kernels.py:723-816): ray per restricted facet, lane per facet
+    #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         E.fseg[f] = 0;
         if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
@@ -1282,6 +1341,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         double t_hi = -bh + sqrt(disc);
         double t_lo = 0.0;
         bool ok = true;
+        #pragma unroll 1
         for (int g = 0; g < nf; g++) {
             if (g == f) continue;
             double den = P.nx[g] * dx + P.ny[g] * dy + P.nz[g] * dz;
@@ -1301,6 +1361,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         double tm = 0.5 * (t_lo + t_hi);
         double mx = ox + tm * dx, my = oy + tm * dy, mz = oz + tm * dz;
         double mg = sqrt(psi) - sqrt(sq(mx - px) + sq(my - py) + sq(mz - pz));
+        #pragma unroll 1
         for (int g = 0; g < nf; g++) {
             double d2 = P.d[g] - (P.nx[g] * mx + P.ny[g] * my + P.nz[g] * mz);
             if (d2 < mg) mg = d2;
@@ -1314,6 +1375,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         // average of the ray midpoints and the deepest one (first on ties)
         double sx = 0.0, sy = 0.0, sz = 0.0, bm = -1.0;
         int nseg = 0, bf = -1;
+        #pragma unroll 1
         for (int f = L; f < nf; f += 32) {
             if (!E.fseg[f]) continue;
             sx += E.smx[f]; sy += E.smy[f]; sz += E.smz[f];
@@ -1323,6 +1385,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         sx = pfw::sum_d(sx); sy = pfw::sum_d(sy); sz = pfw::sum_d(sz);
         nseg = pfw::sum_i(nseg);
         // argmax margin, lowest facet index among equal margins
+        #pragma unroll 1
         for (int m = 16; m > 0; m >>= 1) {
             double om = pfw::shfl_xor(bm, m);
             int of = pfw::shfl_xor(bf, m);
@@ -1335,6 +1398,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
             double inv = 1.0 / (double)nseg;
             double cx = sx * inv, cy = sy * inv, cz = sz * inv;
             double mg = sqrt(psi) - sqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
+            #pragma unroll 1
             for (int g = L; g < nf; g += 32) {
                 double d2 = P.d[g] - (P.nx[g] * cx + P.ny[g] * cy + P.nz[g] * cz);
                 if (d2 < mg) mg = d2;
@@ -1353,7 +1417,9 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     }
     // occluded areas with perturb-and-retry (_kernels.py:1100-1128)
     double kbar = 0.0;
+    #pragma unroll 1
     for (int attempt = 0; attempt < 4; attempt++) {
+        #pragma unroll 1
         for (int f = L; f < nf; f += 32) {
             E.funs[f] = 0;
             if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0 || E.fkind[f] == RF_FULLCIRCLE) continue;
@@ -1365,6 +1431,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         pfw::sync();
         // first unstable facet in facet order (the reference stops there)
         int first_bad = nf;
+        #pragma unroll 1
         for (int f0 = 0; f0 < nf; f0 += 32) {
             int f = f0 + L;
             unsigned mb = pfw::ballot(f < nf && E.funs[f] && !(E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0));
@@ -1372,6 +1439,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
         }
         const bool bad = first_bad < nf;
         double kb = 0.0;
+        #pragma unroll 1
         for (int f = L; f < first_bad; f += 32) {
             if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
             if (E.fkind[f] == RF_FULLCIRCLE) kb += 2.0 * PF_PI * R * (R - E.fh[f]);
@@ -1391,6 +1459,7 @@ PF_DEV void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, dou
     if (K > PF_FOUR_PI * psi) K = PF_FOUR_PI * psi;
     double vol = 0.0;
     double mx = 0.0, my = 0.0, mz = 0.0, nsx = 0.0, nsy = 0.0, nsz = 0.0, m2 = 0.0;
+    #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
         double fa = E.farea[f], fh = E.fh[f];
@@ -1430,6 +1499,7 @@ PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i)
     if (L == 0) {
         ws->oflow = 0;
         ws->cen_on = out.census16 != nullptr;
+        #pragma unroll 1
         for (int k = 0; k < 16; k++) ws->cen[k] = 0;
     }
     pfw::sync();
@@ -1492,6 +1562,7 @@ PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i)
         const EvalScratch<C> &E = ws->u.e;
         const unsigned lt = pfw::lanemask_lt();
         const int smf = out.smf;
+        #pragma unroll 1
         for (int f0 = 0; f0 < P.nf; f0 += 32) {
             int f = f0 + L;
             bool keep = f < P.nf && !(E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0);
@@ -1526,6 +1597,7 @@ PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
     int r = run_cell_impl(ws, in, out, i);
     if (!(r & FLAG_RETRY) && pfw::lane() == 0) {
         if (out.census16)
+            #pragma unroll 1
             for (int k = 0; k < 16; k++) out.census16[(size_t)i * 16 + k] = k < CEN_N ? ws->cen[k] : 0;
         if (out.flags) out.flags[i] = r;
     }

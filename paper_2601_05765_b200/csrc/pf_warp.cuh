@@ -10,6 +10,9 @@
 #if defined(__CUDACC__) && !defined(PF_EMU)
 #define PF_DEV __device__ __forceinline__
 #define PF_DEVNI __device__ __noinline__
+// out-of-line device function: one copy of the code however many call sites
+// (the cell kernel is instruction-cache bound)
+#define PF_NOINL __device__ __noinline__
 #define PF_FULL 0xffffffffu
 namespace pfw {
 PF_DEV int lane() { return threadIdx.x & 31; }
@@ -41,18 +44,18 @@ PF_DEV int __builtin_ctz_pf(unsigned m) { return __ffs(m) - 1; }
 
 namespace pfw {
 // exact (order-independent) warp reductions
-PF_DEV double max_d(double v) {
+PF_NOINL double max_d(double v) {
     for (int m = 16; m > 0; m >>= 1) {
         double o = shfl_xor(v, m);
         v = o > v ? o : v;
     }
     return v;
 }
-PF_DEV double sum_d(double v) {
+PF_NOINL double sum_d(double v) {
     for (int m = 16; m > 0; m >>= 1) v += shfl_xor(v, m);
     return v;
 }
-PF_DEV int sum_i(int v) {
+PF_NOINL int sum_i(int v) {
     for (int m = 16; m > 0; m >>= 1) v += shfl_xor(v, m);
     return v;
 }
@@ -64,7 +67,7 @@ PF_DEV int max_i(int v) {
     return v;
 }
 // exclusive prefix over lanes of an int
-PF_DEV int excl_scan_i(int v, int *total) {
+PF_NOINL int excl_scan_i(int v, int *total) {
     int x = v;
     for (int o = 1; o < 32; o <<= 1) {
         int y = shfl(x, (lane() - o) & 31);

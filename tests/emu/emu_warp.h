@@ -17,6 +17,7 @@
 
 #define PF_DEV static inline
 #define PF_DEVNI static
+#define PF_NOINL static
 static inline int __builtin_ctz_pf(unsigned m) { return __builtin_ctz(m); }
 
 extern "C" void emu_swap(void **from_sp, void *to_sp);

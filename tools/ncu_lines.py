@@ -12,8 +12,10 @@ tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, check=True,
                capture_output=True)
 cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")]
-sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub[0])], capture_output=True,
-                      text=True).stdout.splitlines()
+sass = []
+for cf in cub:
+    sass += subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cf)], capture_output=True,
+                           text=True).stdout.splitlines()
 addr2line = {}
 infn = False
 cur = None
