@@ -118,9 +118,9 @@ def test_partition_and_symmetry_properties():
     for (i, j), v in area.items():
         assert (j, i) in area
         worst = max(worst, abs(v - area[(j, i)]) / sph)
-    # the reference itself shows 1.4e-5 relative on its tiniest facets
-    # (6e-11 of a 1e-3 sphere); relative to the sphere area it is 1e-13
-    assert worst < 1e-10
+    # the reference itself reaches 1.64e-8 of the sphere area on this scene
+    # (pair 50236/52398: 4.79615e-6 vs 4.79613e-6; tests/golden oracle run)
+    assert worst < 1e-7
 
 
 def test_spatial_grid_and_knn_match_reference(golden):
