@@ -174,6 +174,10 @@ struct CellOut {
 PF_DEV double sq(double x) { return x * x; }
 // one out-of-line copy of the (long) double-precision atan2
 PF_NOINL double atan2_ool(double y, double x) { return atan2(y, x); }
+// out-of-line IEEE division / square root: same bits as the inline operators,
+// one copy of the code (the evaluation kernel is instruction-cache bound)
+PF_NOINL double ddiv(double a, double b) { return a / b; }
+PF_NOINL double dsqrt(double x) { return sqrt(x); }
 
 // _kernels.py:59-80
 PF_NOINL void perp_basis(double nx, double ny, double nz, double *e) {
@@ -727,10 +731,10 @@ PF_NOINL int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, doubl
     const double nx = P.nx[f], ny = P.ny[f], nz = P.nz[f], dd = P.d[f];
     const double s = dd - (nx * px + ny * py + nz * pz);
     const double rc2 = psi - s * s;
-    const double R = sqrt(psi);
+    const double R = dsqrt(psi);
     *s_out = s; *rc_out = 0.0; *head_out = -1; *np_out = 0;
     if (rc2 <= tol * (2.0 * R + tol)) return RF_OUTSIDE;
-    const double rc = sqrt(rc2);
+    const double rc = dsqrt(rc2);
     *rc_out = rc;
     const double qx = px + s * nx, qy = py + s * ny, qz = pz + s * nz;
     const int start = P.lp[f], m = P.lp[f + 1] - start;
@@ -811,9 +815,9 @@ PF_NOINL int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, doubl
             uz = P.z[bb] - P.z[a];
             det = 1.0; c12 = 0.0; gd = 0.0; gx = 0.0; gy = 0.0; gz = 0.0;
         }
-        double un = sqrt(ux * ux + uy * uy + uz * uz);
+        double un = dsqrt(ux * ux + uy * uy + uz * uz);
         if (un < 1e-300 || det <= 1e-300) { cur_inside = inb; continue; }
-        ux /= un; uy /= un; uz /= un;
+        ux = ddiv(ux, un); uy = ddiv(uy, un); uz = ddiv(uz, un);
         if (ux < 0.0 || (ux == 0.0 && (uy < 0.0 || (uy == 0.0 && uz < 0.0)))) {
             ux = -ux; uy = -uy; uz = -uz;
         }
@@ -821,8 +825,8 @@ PF_NOINL int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, doubl
         if (g >= 0) {
             double r1 = dd - (nx * px + ny * py + nz * pz);
             double r2 = gd - (gx * px + gy * py + gz * pz);
-            double al = (r1 - c12 * r2) / det;
-            double be = (r2 - c12 * r1) / det;
+            double al = ddiv(r1 - c12 * r2, det);
+            double be = ddiv(r2 - c12 * r1, det);
             x0x = px + al * nx + be * gx;
             x0y = py + al * ny + be * gy;
             x0z = pz + al * nz + be * gz;
@@ -834,7 +838,7 @@ PF_NOINL int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, doubl
         double cc = w0x * w0x + w0y * w0y + w0z * w0z - psi;
         double disc = bh * bh - cc;
         if (disc <= tol * tol) { cur_inside = inb; continue; }
-        double sqd = sqrt(disc);
+        double sqd = dsqrt(disc);
         double t1 = -bh - sqd, t2 = -bh + sqd;
         double ta = ux * (P.x[a] - x0x) + uy * (P.y[a] - x0y) + uz * (P.z[a] - x0z);
         double tb = ux * (P.x[bb] - x0x) + uy * (P.y[bb] - x0y) + uz * (P.z[bb] - x0z);
@@ -944,9 +948,9 @@ PF_NOINL int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, doubl
 template <class C>
 PF_NOINL bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
                                 double dx, double dy, double dz, double rc, double tol) {
-    double dn = sqrt(dx * dx + dy * dy + dz * dz);
+    double dn = dsqrt(dx * dx + dy * dy + dz * dz);
     if (!(dn > 0.0)) return false;
-    double k = rc / dn;
+    double k = ddiv(rc, dn);
     double mx = qx - k * dx, my = qy - k * dy, mz = qz - k * dz;
     #pragma unroll 1
     for (int g = 0; g < P.nf; g++) {
@@ -995,9 +999,10 @@ PF_NOINL void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int 
             double sy3 = (y0 + y1) * (y0 * y0 + y1 * y1);
             Ip = fma(fma(dy, sx3, -dx * sy3), 1.0 / 12.0, Ip);
         } else {
-            double r0 = sqrt(x0 * x0 + y0 * y0), r1 = sqrt(x1 * x1 + y1 * y1);
-            double c0 = r0 > 0.0 ? x0 / r0 : 1.0, s0 = r0 > 0.0 ? y0 / r0 : 0.0;
-            double c1 = r1 > 0.0 ? x1 / r1 : 1.0, s1 = r1 > 0.0 ? y1 / r1 : 0.0;
+            double r0 = dsqrt(x0 * x0 + y0 * y0), r1 = dsqrt(x1 * x1 + y1 * y1);
+            double ir0 = r0 > 0.0 ? ddiv(1.0, r0) : 0.0, ir1 = r1 > 0.0 ? ddiv(1.0, r1) : 0.0;
+            double c0 = r0 > 0.0 ? x0 * ir0 : 1.0, s0 = y0 * ir0;
+            double c1 = r1 > 0.0 ? x1 * ir1 : 1.0, s1 = y1 * ir1;
             double dth = atan2_ool(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
             if (dth <= 0.0) {
                 dth += 2.0 * PF_PI;
@@ -1011,15 +1016,15 @@ PF_NOINL void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int 
             double s21 = 2.0 * s1 * c1, c21 = fma(c1, c1, -s1 * s1);
             double s40 = 2.0 * s20 * c20, s41 = 2.0 * s21 * c21;
             const double r = rc;
-            double ic3 = (s1 - s1 * s1 * s1 / 3.0) - (s0 - s0 * s0 * s0 / 3.0);
-            double is3 = (-c1 + c1 * c1 * c1 / 3.0) - (-c0 + c0 * c0 * c0 / 3.0);
+            double ic3 = (s1 - s1 * s1 * s1 * (1.0 / 3.0)) - (s0 - s0 * s0 * s0 * (1.0 / 3.0));
+            double is3 = (-c1 + c1 * c1 * c1 * (1.0 / 3.0)) - (-c0 + c0 * c0 * c0 * (1.0 / 3.0));
             double ic4 = 0.375 * dth + 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
             double is4 = 0.375 * dth - 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
             double r2 = r * r;
             A = fma(0.5 * r2, dth, A);
             Mx = fma(0.5 * r * r2, ic3, Mx);
             My = fma(0.5 * r * r2, is3, My);
-            Ip = fma((r / 3.0) * r2 * r, ic4 + is4, Ip);
+            Ip = fma(r * (1.0 / 3.0) * r2 * r, ic4 + is4, Ip);
         }
         x0 = x1;
         y0 = y1;
@@ -1027,7 +1032,7 @@ PF_NOINL void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int 
     }
     double cx, cy, cz;
     if (A > 0.0) {
-        double ia = 1.0 / A;
+        double ia = ddiv(1.0, A);
         double u = Mx * ia, v = My * ia;
         cx = qx + u * e[0] + v * e[3];
         cy = qy + u * e[1] + v * e[4];
@@ -1048,7 +1053,7 @@ PF_NOINL void project_from(double cx, double cy, double cz, double yx, double yy
     double c0 = wx * wx + wy * wy + wz * wz - psi;
     double disc = b * b - a * c0;
     if (disc < 0.0) disc = 0.0;
-    double t = (-b + sqrt(disc)) / a;
+    double t = ddiv(-b + dsqrt(disc), a);
     o[0] = cx + t * dx; o[1] = cy + t * dy; o[2] = cz + t * dz;
 }
 
@@ -1068,7 +1073,7 @@ PF_DEV double ccw_angle(const double *a, const double *b, const double *m) {
 PF_DEV void unit3(double *v) {
     double n2 = dot3(v, v);
     if (n2 > 0.0) {
-        double inv = 1.0 / sqrt(n2);
+        double inv = ddiv(1.0, dsqrt(n2));
         v[0] *= inv; v[1] *= inv; v[2] *= inv;
     }
 }
@@ -1084,7 +1089,7 @@ PF_NOINL double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int h
                          double pz, double psi, double cx, double cy, double cz,
                          bool *unstable_out) {
     EvalScratch<C> &E = ws->u.e;
-    const double R = sqrt(psi), iR = 1.0 / R;
+    const double R = dsqrt(psi), iR = ddiv(1.0, R);
     bool unstable = false;
     double kg_sum = 0.0, th_sum = 0.0;
     double pr0[3], pri[3], prj[3];
@@ -1110,13 +1115,13 @@ PF_NOINL double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int h
             double a3[3] = {E.ppx[i] - cx, E.ppy[i] - cy, E.ppz[i] - cz};
             double b3[3] = {E.ppx[j] - cx, E.ppy[j] - cy, E.ppz[j] - cz};
             cross3(a3, b3, m);
-            double mn = sqrt(dot3(m, m));
+            double mn = dsqrt(dot3(m, m));
             if (mn < 1e-300) {
                 unstable = true;
                 skip = true;
                 ee = 0.0;
             } else {
-                double im = 1.0 / mn;
+                double im = ddiv(1.0, mn);
                 m[0] *= im; m[1] *= im; m[2] *= im;
                 ee = m[0] * (cx - px) + m[1] * (cy - py) + m[2] * (cz - pz);
             }
@@ -1133,7 +1138,7 @@ PF_NOINL double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int h
                     const double d0 = rp[0] - rq[0], d1 = rp[1] - rq[1], d2 = rp[2] - rq[2];
                     if (d0 * d0 + d1 * d1 + d2 * d2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
                         long_arc_impossible(P, f, q[0], q[1], q[2], rp[0], rp[1], rp[2],
-                                            sqrt(psi - ee * ee), tol))
+                                            dsqrt(psi - ee * ee), tol))
                         dPQ -= 2.0 * PF_PI;
                 }
                 if (!arc) {
@@ -1205,7 +1210,7 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
     res->status = CELL_EMPTY; res->vol = 0.0; res->K = 0.0;
     res->cx = px; res->cy = py; res->cz = pz; res->ix = px; res->iy = py; res->iz = pz; res->m2 = 0.0;
     if (psi <= 0.0) return;
-    const double R = sqrt(psi);
+    const double R = dsqrt(psi);
     const double ball_tol = tol * (2.0 * R + tol);
     #pragma unroll 1
     for (int v = L; v < P.nv; v += 32) {
@@ -1338,7 +1343,7 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         double cc = wx * wx + wy * wy + wz * wz - psi;
         double disc = bh * bh - cc;
         if (disc <= 0.0) continue;
-        double t_hi = -bh + sqrt(disc);
+        double t_hi = -bh + dsqrt(disc);
         double t_lo = 0.0;
         bool ok = true;
         #pragma unroll 1
@@ -1347,10 +1352,10 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
             double den = P.nx[g] * dx + P.ny[g] * dy + P.nz[g] * dz;
             double num = P.d[g] - (P.nx[g] * ox + P.ny[g] * oy + P.nz[g] * oz);
             if (den > tol) {
-                double tc = num / den;
+                double tc = ddiv(num, den);
                 if (tc < t_hi) t_hi = tc;
             } else if (den < -tol) {
-                double tc = num / den;
+                double tc = ddiv(num, den);
                 if (tc > t_lo) t_lo = tc;
             } else if (num < -tol) {
                 ok = false;
@@ -1360,7 +1365,7 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         if (!ok || t_hi - t_lo <= tol) continue;
         double tm = 0.5 * (t_lo + t_hi);
         double mx = ox + tm * dx, my = oy + tm * dy, mz = oz + tm * dz;
-        double mg = sqrt(psi) - sqrt(sq(mx - px) + sq(my - py) + sq(mz - pz));
+        double mg = dsqrt(psi) - dsqrt(sq(mx - px) + sq(my - py) + sq(mz - pz));
         #pragma unroll 1
         for (int g = 0; g < nf; g++) {
             double d2 = P.d[g] - (P.nx[g] * mx + P.ny[g] * my + P.nz[g] * mz);
@@ -1395,9 +1400,9 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         if (bf >= 0 && best_margin > -1.0) { bx = E.smx[bf]; by = E.smy[bf]; bz = E.smz[bf]; }
         bool ok = nseg > 0;
         if (ok) {
-            double inv = 1.0 / (double)nseg;
+            double inv = ddiv(1.0, (double)nseg);
             double cx = sx * inv, cy = sy * inv, cz = sz * inv;
-            double mg = sqrt(psi) - sqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
+            double mg = dsqrt(psi) - dsqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
             #pragma unroll 1
             for (int g = L; g < nf; g += 32) {
                 double d2 = P.d[g] - (P.nx[g] * cx + P.ny[g] * cy + P.nz[g] * cz);
@@ -1463,7 +1468,7 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
     for (int f = L; f < nf; f += 32) {
         if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
         double fa = E.farea[f], fh = E.fh[f];
-        double pv = fh * fa / 3.0;
+        double pv = fh * fa * (1.0 / 3.0);
         vol += pv;
         mx += pv * 0.75 * (E.fcx[f] - px);
         my += pv * 0.75 * (E.fcy[f] - py);
@@ -1471,17 +1476,17 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         nsx += P.nx[f] * fa;
         nsy += P.ny[f] * fa;
         nsz += P.nz[f] * fa;
-        if (want_m2) m2 += (fh / 5.0) * (E.fip[f] + fh * fh * fa);
+        if (want_m2) m2 += (fh * 0.2) * (E.fip[f] + fh * fh * fa);
     }
-    vol = R * K / 3.0 + pfw::sum_d(vol);
+    vol = R * K * (1.0 / 3.0) + pfw::sum_d(vol);
     mx = pfw::sum_d(mx); my = pfw::sum_d(my); mz = pfw::sum_d(mz);
     nsx = pfw::sum_d(nsx); nsy = pfw::sum_d(nsy); nsz = pfw::sum_d(nsz);
-    m2 = want_m2 ? R * R * R * K / 5.0 + pfw::sum_d(m2) : 0.0;
+    m2 = want_m2 ? R * R * R * K * 0.2 + pfw::sum_d(m2) : 0.0;
     mx += 0.25 * psi * (-nsx);
     my += 0.25 * psi * (-nsy);
     mz += 0.25 * psi * (-nsz);
     double ccx, ccy, ccz;
-    if (vol > 0.0) { ccx = px + mx / vol; ccy = py + my / vol; ccz = pz + mz / vol; }
+    if (vol > 0.0) { double iv = ddiv(1.0, vol); ccx = px + mx * iv; ccy = py + my * iv; ccz = pz + mz * iv; }
     else { vol = 0.0; ccx = px; ccy = py; ccz = pz; }
     res->status = CELL_CLIPPED;
     res->vol = vol; res->K = K; res->cx = ccx; res->cy = ccy; res->cz = ccz;
@@ -1493,18 +1498,21 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
 // FLAG_RETRY means nothing was written and the cell must be re-run on the
 // reference-capacity instantiation.
 // ---------------------------------------------------------------------------
+// Phase A of one cell: build.  Returns -1 when the cell needs evaluation
+// (polytope in ws->P[*which]), else the cell's final flag word with its
+// outputs already written (empty / overflow), or FLAG_RETRY.
 template <class C>
-PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+PF_DEV int cell_phase_build(WS<C> *ws, const CellIn &in, const CellOut &out, int i, int *which) {
     const int L = pfw::lane();
     if (L == 0) {
         ws->oflow = 0;
         ws->cen_on = out.census16 != nullptr;
-        #pragma unroll 1
+#pragma unroll 1
         for (int k = 0; k < 16; k++) ws->cen[k] = 0;
     }
     pfw::sync();
-    int which, nclips;
-    int st = build_cell(ws, in, i, &which, &nclips);
+    int nclips;
+    int st = build_cell(ws, in, i, which, &nclips);
     if (ws->oflow) {
         pfw::sync();
         if (!C::EXACT) return FLAG_RETRY;
@@ -1532,10 +1540,17 @@ PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i)
             if (out.m2) out.m2[i] = 0.0;
             if (out.fcount) out.fcount[i] = 0;
             if (out.fcount32) out.fcount32[i] = 0;
-            if (out.flags) out.flags[i] = 0;
         }
         return 0;
     }
+    return -1;
+}
+
+// Phase B: evaluate the polytope in ws->P[which] and write the outputs.
+template <class C>
+PF_DEV int cell_phase_eval(WS<C> *ws, const CellIn &in, const CellOut &out, int i, int which) {
+    const int L = pfw::lane();
+    const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const Poly<C> &P = ws->P[which];
     CellRes r;
     evaluate_cell(ws, P, px, py, pz, in.psi[i], in.tol, in.want_m2, &r);
@@ -1593,15 +1608,63 @@ PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i)
 }
 
 template <class C>
-PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
-    int r = run_cell_impl(ws, in, out, i);
+PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+    int which = 0;
+    int r = cell_phase_build(ws, in, out, i, &which);
+    if (r >= 0) return r;
+    return cell_phase_eval(ws, in, out, i, which);
+}
+
+// polytope hand-off between the split build / evaluate kernels (global memory)
+template <class C>
+PF_DEV void poly_store(const Poly<C> &A, Poly<C> *g) {
+    const int L = pfw::lane();
+#pragma unroll 1
+    for (int v = L; v < A.nv; v += 32) { g->x[v] = A.x[v]; g->y[v] = A.y[v]; g->z[v] = A.z[v]; }
+#pragma unroll 1
+    for (int f = L; f < A.nf; f += 32) {
+        g->nx[f] = A.nx[f]; g->ny[f] = A.ny[f]; g->nz[f] = A.nz[f]; g->d[f] = A.d[f]; g->tag[f] = A.tag[f];
+    }
+#pragma unroll 1
+    for (int f = L; f <= A.nf; f += 32) g->lp[f] = A.lp[f];
+#pragma unroll 1
+    for (int k = L; k < A.nl; k += 32) g->lv[k] = A.lv[k];
+    if (L == 0) { g->nv = A.nv; g->nf = A.nf; g->nl = A.nl; }
+}
+template <class C>
+PF_DEV void poly_load(const Poly<C> *g, Poly<C> &A) {
+    const int L = pfw::lane();
+    const int nv = g->nv, nf = g->nf, nl = g->nl;
+#pragma unroll 1
+    for (int v = L; v < nv; v += 32) { A.x[v] = g->x[v]; A.y[v] = g->y[v]; A.z[v] = g->z[v]; }
+#pragma unroll 1
+    for (int f = L; f < nf; f += 32) {
+        A.nx[f] = g->nx[f]; A.ny[f] = g->ny[f]; A.nz[f] = g->nz[f]; A.d[f] = g->d[f]; A.tag[f] = g->tag[f];
+    }
+#pragma unroll 1
+    for (int f = L; f <= nf; f += 32) A.lp[f] = g->lp[f];
+#pragma unroll 1
+    for (int k = L; k < nl; k += 32) A.lv[k] = g->lv[k];
+    if (L == 0) { A.nv = nv; A.nf = nf; A.nl = nl; }
+    pfw::sync();
+}
+
+// per-cell epilogue shared by the fused and the split kernels
+template <class C>
+PF_DEV void cell_finish(WS<C> *ws, const CellOut &out, int i, int r) {
     if (!(r & FLAG_RETRY) && pfw::lane() == 0) {
         if (out.census16)
-            #pragma unroll 1
+#pragma unroll 1
             for (int k = 0; k < 16; k++) out.census16[(size_t)i * 16 + k] = k < CEN_N ? ws->cen[k] : 0;
         if (out.flags) out.flags[i] = r;
     }
     pfw::sync();
+}
+
+template <class C>
+PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+    int r = run_cell_impl(ws, in, out, i);
+    cell_finish(ws, out, i, r);
     return r;
 }
 

@@ -6,6 +6,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -88,6 +90,11 @@ struct pf_ctx {
     size_t census_cap = 0;
     WS<ExactCaps> *exact_ws = nullptr;
     int exact_warps = 0;
+    Poly<FastCaps> *gpoly = nullptr;
+    size_t gpoly_cap = 0;
+    uint8_t *stage = nullptr;
+    size_t stage_cap = 0;
+    int split = 1;  // split build/evaluate kernels (PF_FUSED=1 selects the fused kernel)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool ev_valid = false;
     int fast_blocks = 0;
@@ -272,6 +279,75 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
+// Split pipeline (fast tier).  One fused kernel touches ~130 KB of SASS per
+// cell and stalls on instruction fetch; building in one kernel and
+// evaluating in another halves the hot code each SM cycles through.  The
+// finished polytope travels through global memory (Poly<FastCaps>, ~3 KB).
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+    k_cells_build(CellIn in, CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
+                  uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
+                  unsigned long long *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WS<FastCaps> *ws = (WS<FastCaps> *)(smem + (size_t)wid * sizeof(WS<FastCaps>));
+    const int nw = gridDim.x * FAST_WARPS;
+    int fl = 0;
+    for (int t = blockIdx.x * FAST_WARPS + wid; t < count; t += nw) {
+        const int i = in.cells ? in.cells[t] : in.g.sid[t];
+        int which = 0;
+        int r = cell_phase_build<FastCaps>(ws, in, out, i, &which);
+        if (r < 0) {
+            poly_store(ws->P[which], gpoly + i);
+            if (lane == 0) {
+                stage[i] = 1;
+                if (out.census16)
+                    for (int k = 0; k < 16; k++) out.census16[(size_t)i * 16 + k] = ws->cen[k];
+            }
+        } else {
+            if (lane == 0) stage[i] = 0;
+            if (r & FLAG_RETRY) {
+                if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
+            } else {
+                cell_finish(ws, out, i, r);
+                fl |= r & 7;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
+}
+
+__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+    k_cells_eval(CellIn in, CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
+                 const uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
+                 unsigned long long *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WS<FastCaps> *ws = (WS<FastCaps> *)(smem + (size_t)wid * sizeof(WS<FastCaps>));
+    const int nw = gridDim.x * FAST_WARPS;
+    int fl = 0;
+    for (int t = blockIdx.x * FAST_WARPS + wid; t < count; t += nw) {
+        const int i = in.cells ? in.cells[t] : in.g.sid[t];
+        if (stage[i] != 1) continue;
+        poly_load(gpoly + i, ws->P[0]);
+        if (lane == 0) {
+            ws->oflow = 0;
+            ws->cen_on = out.census16 != nullptr;
+            for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
+        }
+        __syncwarp();
+        int r = cell_phase_eval<FastCaps>(ws, in, out, i, 0);
+        if (r & FLAG_RETRY) {
+            if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
+        } else {
+            cell_finish(ws, out, i, r);
+            fl |= r & 7;
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
+}
+
 // cells that overflowed the fast tier, with the reference's capacities
 __global__ void __launch_bounds__(EXACT_WARPS * 32)
     k_cells_exact(CellIn in, CellOut out, const int *__restrict__ list, const int *__restrict__ counters,
@@ -350,6 +426,12 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        for (const void *kf : {(const void *)k_cells_build, (const void *)k_cells_eval}) {
+            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
+            CK(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
+        c->split = getenv("PF_FUSED") ? 0 : 1;
         int nb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cells_fast, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(WS<FastCaps>)));
@@ -370,10 +452,23 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         CK(cudaEventCreate(&c->ev[1]));
     }
     CK(cudaEventRecord(c->ev[0], st));
-    g_launches++;
-    k_cells_fast<<<(int)blocks, FAST_WARPS * 32, FAST_WARPS * sizeof(WS<FastCaps>), st>>>(
-        in, out, (int)count, c->retry_list, c->counters, c->err);
-    CK(cudaGetLastError());
+    if (c->split && count > 0) {
+        if (ensure(&c->gpoly, &c->gpoly_cap, (size_t)n) || ensure(&c->stage, &c->stage_cap, (size_t)n))
+            return -1;
+        g_launches++;
+        k_cells_build<<<(int)blocks, FAST_WARPS * 32, FAST_WARPS * sizeof(WS<FastCaps>), st>>>(
+            in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
+        CK(cudaGetLastError());
+        g_launches++;
+        k_cells_eval<<<(int)blocks, FAST_WARPS * 32, FAST_WARPS * sizeof(WS<FastCaps>), st>>>(
+            in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
+        CK(cudaGetLastError());
+    } else {
+        g_launches++;
+        k_cells_fast<<<(int)blocks, FAST_WARPS * 32, FAST_WARPS * sizeof(WS<FastCaps>), st>>>(
+            in, out, (int)count, c->retry_list, c->counters, c->err);
+        CK(cudaGetLastError());
+    }
     g_launches++;
     k_cells_exact<<<c->exact_warps / EXACT_WARPS, EXACT_WARPS * 32, 0, st>>>(
         in, out, c->retry_list, c->counters, c->exact_ws, c->err);
@@ -547,7 +642,7 @@ int pf_ctx_destroy(pf_ctx *c) {
     if (!c) return 0;
     void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
                     c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
-                    c->err, c->census, c->exact_ws};
+                    c->err, c->census, c->exact_ws, c->gpoly, c->stage};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete c;
