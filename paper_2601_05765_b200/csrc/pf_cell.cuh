@@ -84,6 +84,8 @@ struct BuildScratch {
     uint16_t fout[C::CF];      // output facet index
     uint16_t ea[C::CE], eb[C::CE], eid[C::CE];  // crossing entries (walk order)
     uint16_t emt[C::CE];       // first-occurrence entry of the same edge
+    uint8_t ecls[C::CL];       // per loop entry of A: bit0 tail inside, bit1 crossing edge
+    double sy[C::CV];          // new-facet vertex ordinates (abscissae in sd)
     double cd2[C::CC];         // candidates (d^2, j)
     int cj[C::CC];
     int ncand;
@@ -218,6 +220,18 @@ PF_DEV void load_domain(Poly<C> &A, const CellIn &in) {
     pfw::sync();
 }
 
+// angle order of atan2(y, x) on (-pi, pi] without evaluating it: lower
+// half-plane (including -pi = atan2(-0, x<0)) first, then orientation
+PF_DEV int half_of(double x, double y) { return (y < 0.0 || (y == 0.0 && x < 0.0 && signbit(y))) ? 0 : 1; }
+PF_DEV bool ang_lt(double xu, double yu, double xv, double yv) {
+    const int hu = half_of(xu, yu), hv = half_of(xv, yv);
+    if (hu != hv) return hu < hv;
+    const double cr = xu * yv - yu * xv;
+    if (cr != 0.0) return cr > 0.0;
+    if (xu * xv + yu * yv >= 0.0) return false;  // same direction: equal angles
+    return xu > 0.0;  // 0 before pi in the upper half
+}
+
 // max_v |v - p| (the running "rfar" of _kernels.py:1230-1237, 1341-1354)
 template <class C>
 PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
@@ -287,12 +301,10 @@ PF_NOINL int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny,
             int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
             double sa = S.sd[a], sb = S.sd[b];
             bool ina = sa <= tol, inb = sb <= tol;
-            if (ina) {
-                k++;
-                if (!inb && sa < -tol) c++;
-            } else if (inb && sb < -tol) {
-                c++;
-            }
+            bool cr = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
+            k += ina;
+            c += cr;
+            S.ecls[start + e] = (uint8_t)((ina ? 1 : 0) | (cr ? 2 : 0));
         }
         S.fk[f] = (uint16_t)(k + c);
         S.fcb[f] = (uint16_t)c;
@@ -331,12 +343,11 @@ PF_NOINL int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny,
         int pos = S.fcb[f];
         #pragma unroll 1
         for (int e = 0; e < m; e++) {
-            int a = A.lv[start + e];
-            int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
-            double sa = S.sd[a], sb = S.sd[b];
-            bool ina = sa <= tol, inb = sb <= tol;
-            bool cr = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
-            if (cr) { S.ea[pos] = (uint16_t)a; S.eb[pos] = (uint16_t)b; pos++; }
+            if (S.ecls[start + e] & 2) {
+                S.ea[pos] = A.lv[start + e];
+                S.eb[pos] = A.lv[start + (e + 1 == m ? 0 : e + 1)];
+                pos++;
+            }
         }
     }
     pfw::sync();
@@ -402,13 +413,9 @@ PF_NOINL int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny,
         int pos = S.fcb[f], w = lb;
         #pragma unroll 1
         for (int e = 0; e < m; e++) {
-            int a = A.lv[start + e];
-            int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
-            double sa = S.sd[a], sb = S.sd[b];
-            bool ina = sa <= tol, inb = sb <= tol;
-            if (ina) B.lv[w++] = S.vmap[a];
-            bool cr = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
-            if (cr) B.lv[w++] = S.eid[pos++];
+            const int cl = S.ecls[start + e];
+            if (cl & 1) B.lv[w++] = S.vmap[A.lv[start + e]];
+            if (cl & 2) B.lv[w++] = S.eid[pos++];
         }
     }
     // 4. new facet (_kernels.py:243-295).  on_new = kept on-plane vertices
@@ -447,20 +454,25 @@ PF_NOINL int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny,
     for (int q = L; q < ncp; q += 32) {
         int v = S.onl[q];
         double rx = B.x[v] - ccx, ry = B.y[v] - ccy, rz = B.z[v] - ccz;
-        S.sd[q] = atan2_ool(rx * e[3] + ry * e[4] + rz * e[5], rx * e[0] + ry * e[1] + rz * e[2]);
+        S.sy[q] = rx * e[3] + ry * e[4] + rz * e[5];
+        S.sd[q] = rx * e[0] + ry * e[1] + rz * e[2];
     }
     pfw::sync();
-    // rank sort by (angle, index): the reference's insertion sort is stable on a total order
+    // rank sort by (atan2 angle, index) -- the reference's insertion sort is
+    // stable on that total order (_kernels.py:269-283); the angle order is
+    // decided by half-plane and orientation instead of evaluating atan2
     #pragma unroll 1
     for (int q = L; q < ncp; q += 32) {
-        double aq = S.sd[q];
-        int vq = S.onl[q];
+        const double xq = S.sd[q], yq = S.sy[q];
+        const int vq = S.onl[q];
         int r = 0;
         #pragma unroll 1
         for (int u = 0; u < ncp; u++) {
-            double au = S.sd[u];
-            int vu = S.onl[u];
-            r += (au < aq || (au == aq && vu < vq)) ? 1 : 0;
+            const double xu = S.sd[u], yu = S.sy[u];
+            const int vu = S.onl[u];
+            const bool lt = ang_lt(xu, yu, xq, yq);
+            const bool eq = !lt && !ang_lt(xq, yq, xu, yu);
+            r += (lt || (eq && vu < vq)) ? 1 : 0;
         }
         B.lv[NLk + r] = (uint16_t)vq;
     }
@@ -1070,12 +1082,33 @@ PF_DEV double ccw_angle(const double *a, const double *b, const double *m) {
     double t = atan2_ool(dot3(c, m), dot3(a, b));
     return t < 0.0 ? t + 2.0 * PF_PI : t;
 }
+// value-only normalisation (tangents): hardware rsqrt + one Newton step
+PF_DEV double rsqrt_nr(double x) {
+    double r = rsqrt(x);
+    return r * fma(-0.5 * x * r, r, 1.5);
+}
 PF_DEV void unit3(double *v) {
     double n2 = dot3(v, v);
     if (n2 > 0.0) {
-        double inv = ddiv(1.0, dsqrt(n2));
+        double inv = rsqrt_nr(n2);
         v[0] *= inv; v[1] *= inv; v[2] *= inv;
     }
+}
+// the CCW angle from a to b about m is <= the one from a to c (+1e-12 slack
+// of the reference's phase comparison, _kernels.py:935-938), without atan2:
+// compare half-turns, then the orientation of (b, c)
+PF_DEV bool ccw_le(const double *a, const double *b, const double *c, const double *m) {
+    double t[3];
+    cross3(a, b, t);
+    const double sb = dot3(t, m), cb = dot3(a, b);
+    cross3(a, c, t);
+    const double sc = dot3(t, m), cc = dot3(a, c);
+    // half-plane index: 0 for angles in [0, pi), 1 for [pi, 2 pi)
+    const int hb = (sb > 0.0 || (sb == 0.0 && cb > 0.0)) ? 0 : 1;
+    const int hc = (sc > 0.0 || (sc == 0.0 && cc > 0.0)) ? 0 : 1;
+    if (hb != hc) return hb < hc;
+    cross3(b, c, t);
+    return dot3(t, m) >= 0.0;
 }
 
 // _kernels.py:838-1001, streamed over the facet's boundary ring by one lane.
@@ -1115,13 +1148,13 @@ PF_NOINL double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int h
             double a3[3] = {E.ppx[i] - cx, E.ppy[i] - cy, E.ppz[i] - cz};
             double b3[3] = {E.ppx[j] - cx, E.ppy[j] - cy, E.ppz[j] - cz};
             cross3(a3, b3, m);
-            double mn = dsqrt(dot3(m, m));
-            if (mn < 1e-300) {
+            double mn2 = dot3(m, m);
+            if (!(mn2 > 0.0)) {  // |m| < 1e-300 (reference) <=> |m|^2 underflows to 0
                 unstable = true;
                 skip = true;
                 ee = 0.0;
             } else {
-                double im = ddiv(1.0, mn);
+                double im = rsqrt_nr(mn2);
                 m[0] *= im; m[1] *= im; m[2] *= im;
                 ee = m[0] * (cx - px) + m[1] * (cy - py) + m[2] * (cz - pz);
             }
@@ -1146,7 +1179,7 @@ PF_NOINL double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int h
                     project_from(cx, cy, cz, 0.5 * (E.ppx[i] + E.ppx[j]), 0.5 * (E.ppy[i] + E.ppy[j]),
                                  0.5 * (E.ppz[i] + E.ppz[j]), px, py, pz, psi, h);
                     const double rm[3] = {h[0] - q[0], h[1] - q[1], h[2] - q[2]};
-                    if (!(ccw_angle(rp, rm, m) <= dPQ + 1e-12)) {
+                    if (!ccw_le(rp, rm, rq, m)) {
                         // traversal is clockwise around m: flip the circle normal
                         m[0] = -m[0]; m[1] = -m[1]; m[2] = -m[2]; ee = -ee;
                         continue;

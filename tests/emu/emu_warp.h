@@ -19,6 +19,7 @@
 #define PF_DEVNI static
 #define PF_NOINL static
 static inline int __builtin_ctz_pf(unsigned m) { return __builtin_ctz(m); }
+static inline double rsqrt(double x) { return 1.0 / std::sqrt(x); }  // device: MUFU-based rsqrt
 
 extern "C" void emu_swap(void **from_sp, void *to_sp);
 
