@@ -129,19 +129,6 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def slab_partition(pts, psi, dpsi, ws, rank):
-    """Owned cells of rank r (x-slab) + ghost sites within the largest search radius."""
-    x = pts[:, 0]
-    lo, hi = rank / ws, (rank + 1) / ws
-    own = (x >= lo) & ((x < hi) if rank < ws - 1 else (x <= 1.0 + 1e-12))
-    br = np.sqrt(np.maximum(psi, 0)) + np.sqrt(np.maximum(psi, 0) + dpsi)
-    W = float(br[own].max()) * (1 + 1e-9) if own.any() else 0.0
-    keep = (x >= lo - W) & (x <= hi + W)
-    idx = np.nonzero(keep)[0]  # global order preserved (ties break on index)
-    owned_local = np.nonzero(own[idx])[0].astype(np.int32)
-    return idx, owned_local
-
-
 def converged_psi(sc, dom):
     import torch
 
@@ -242,10 +229,13 @@ def main():
                   "status": nst["status_name"], "start": "cold (kappa (3 nu/4 pi)^(2/3))",
                   "eps_vol": 0.01, "n": sc.n}
     psi_h = psi_g.cpu().numpy()
-    dpsi = float(max(psi_h.max() - psi_h.min(), 0.0))
+    from paper_2601_05765_b200 import partition
+
+    dpsi = partition.global_dpsi(psi_h) if ws > 1 else float(max(psi_h.max() - psi_h.min(), 0.0))
 
     if ws > 1:
-        idx, owned = slab_partition(sc.pts, psi_h, dpsi, ws, rank)
+        slab = partition.slab_partition(sc.pts, psi_h, dpsi, ws, rank)
+        idx, owned = slab.local_to_global, slab.owned_local
     else:
         idx, owned = np.arange(sc.n), None
     pts_l = torch.as_tensor(np.ascontiguousarray(sc.pts[idx]), device="cuda")
@@ -353,7 +343,7 @@ def main():
             traffic = None
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value if peak.value > 0 else None, "traffic": traffic,
-                "kernel": "k_cells_fast+k_cells_exact",
+                "kernel": "k_cells_build+k_cells_eval (+k_cells_exact retries)",
                 "kernel_ms": t_cells, "kernel_share_of_step": t_cells / t_step,
                 "algorithmic": f"census S_cell (SURVEY.md §8(d)) = {s_cell_total / sc.n:.0f} DP slots/cell,"
                                f" x2 flop/slot; mean processed candidates {mean_clips:.1f}/cell",

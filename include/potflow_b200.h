@@ -151,6 +151,18 @@ int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const double *nu,
 int pf_newton_last_state(double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
                          int64_t n, int smf, void *stream);
 
+/* same, plus the centroids of the final evaluation (cent f64[n,3]) */
+int pf_newton_last_state_ex(double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
+                            double *cent, int64_t n, int smf, void *stream);
+
+/* ---- fluid step --------------------------------------- */
+/* x += dt v, reflected into the box [lo+tau, hi-tau] (velocity component flipped) */
+int pf_fluid_advect(int64_t n, double *x, double *v, double dt, const double *lo_host,
+                    const double *hi_host, double tau, void *stream);
+/* v += dt/m ((c - x)/eps^2 + m g), m = rho nu (spring pressure + gravity) */
+int pf_fluid_forces(int64_t n, const double *x, const double *cent, const double *nu, const double *rho,
+                    double *v, double dt, double eps, const double *g_host, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

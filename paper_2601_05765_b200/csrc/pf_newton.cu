@@ -288,6 +288,8 @@ struct NewtonWS {
     double *psi_t = nullptr, *vol_t = nullptr, *ksur_t = nullptr, *farea_t = nullptr;
     int *hcnt = nullptr, *hcol = nullptr, *fcount = nullptr, *ftag = nullptr;
     int *fcount_t = nullptr, *ftag_t = nullptr;
+    double *cent = nullptr, *cent_t = nullptr;
+    size_t ccap[2] = {0, 0};
     double *part = nullptr, *sc = nullptr, *red = nullptr;
     int *ic = nullptr;
     int64_t *flags = nullptr;
@@ -309,6 +311,7 @@ int ws_alloc(int64_t n, int smf) {
     rc |= dalloc(&w.fcount_t, &w.c[19], N); rc |= dalloc(&w.ftag_t, &w.c[20], E);
     rc |= dalloc(&w.part, &w.c[21], 3 * NPART); rc |= dalloc(&w.sc, &w.c[22], 16);
     rc |= dalloc(&w.red, &w.c[23], 16);
+    rc |= dalloc(&w.cent, &w.ccap[0], 3 * N); rc |= dalloc(&w.cent_t, &w.ccap[1], 3 * N);
     if (!w.ic) NCK(cudaMalloc(&w.ic, 4 * sizeof(int)));
     if (!w.flags) NCK(cudaMalloc(&w.flags, sizeof(int64_t)));
     return rc;
@@ -398,9 +401,9 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
     NewtonWS &w = g_ws;
     if (pf_grid_build(ctx, n, pts, cold_start ? nullptr : psi, 0.0, stream)) return -1;
     auto evaluate = [&](const double *ps, double *vol, double *ksur, int *fcount, int *ftag,
-                        double *farea) -> int {
+                        double *farea, double *cent) -> int {
         S.evaluations++;
-        return pf_evaluate_lean(ctx, n, pts, ps, ball_aware, smf, vol, ksur, fcount, ftag, farea, nullptr,
+        return pf_evaluate_lean(ctx, n, pts, ps, ball_aware, smf, vol, ksur, fcount, ftag, farea, cent,
                                 w.flags, stream);
     };
     double stats3[3];
@@ -410,7 +413,7 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
         for (;;) {
             pf_internal_launches_add(1);
             k_cold_psi<<<nblocks(n), RB, 0, st>>>(n, nu, kappa, psi);
-            if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea)) return -1;
+            if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea, w.cent)) return -1;
             if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
             if (stats3[1] > 0.0) break;
             kappa *= 2.0;
@@ -418,7 +421,7 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
             if (kappa > 1024.0) { S.status = 3; if (stats) *stats = S; return 0; }  // InitFailure
         }
     } else {
-        if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea)) return -1;
+        if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea, w.cent)) return -1;
         if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
     }
     const double floor_v = 0.5 * std::min(stats3[2], stats3[1]);
@@ -444,7 +447,7 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
         while (alpha >= 0x1p-20) {
             pf_internal_launches_add(1);
             k_axpy_to<<<nblocks(n), RB, 0, st>>>(n, psi, alpha, w.x, w.psi_t);
-            if (evaluate(w.psi_t, w.vol_t, w.ksur_t, w.fcount_t, w.ftag_t, w.farea_t)) return -1;
+            if (evaluate(w.psi_t, w.vol_t, w.ksur_t, w.fcount_t, w.ftag_t, w.farea_t, w.cent_t)) return -1;
             if (grad_stats(n, nu, w.vol_t, w.g, stats3, st)) return -1;
             if (stats3[1] >= floor_v) { accepted = true; break; }
             alpha *= 0.5;
@@ -457,6 +460,8 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
         std::swap(w.fcount, w.fcount_t);
         std::swap(w.ftag, w.ftag_t);
         std::swap(w.farea, w.farea_t);
+        std::swap(w.cent, w.cent_t);
+        std::swap(w.ccap[0], w.ccap[1]);
         std::swap(w.c[9], w.c[12]);
         std::swap(w.c[10], w.c[13]);
         std::swap(w.c[17], w.c[19]);
@@ -481,12 +486,74 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
 
 extern "C" int pf_newton_last_state(double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
                                     int64_t n, int smf, void *stream) {
+    return pf_newton_last_state_ex(vol, ksur, fcount, ftag, farea, nullptr, n, smf, stream);
+}
+
+extern "C" int pf_newton_last_state_ex(double *vol, double *ksur, int32_t *fcount, int32_t *ftag,
+                                       double *farea, double *cent, int64_t n, int smf, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     NewtonWS &w = g_ws;
+    if (cent) NCK(cudaMemcpyAsync(cent, w.cent, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     if (vol) NCK(cudaMemcpyAsync(vol, w.vol, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     if (ksur) NCK(cudaMemcpyAsync(ksur, w.ksur, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     if (fcount) NCK(cudaMemcpyAsync(fcount, w.fcount, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     if (ftag) NCK(cudaMemcpyAsync(ftag, w.ftag, (size_t)n * smf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     if (farea) NCK(cudaMemcpyAsync(farea, w.farea, (size_t)n * smf * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// fluid step pieces
+// ---------------------------------------------------------------------------
+namespace {
+// x += dt v, then reflect into the box [lo+tau, hi-tau]
+__global__ void __launch_bounds__(RB) k_advect(int64_t n, double *__restrict__ x, double *__restrict__ v,
+                                              double dt, double lo0, double lo1, double lo2, double hi0,
+                                              double hi1, double hi2, double tau) {
+    const double lo[3] = {lo0 + tau, lo1 + tau, lo2 + tau}, hi[3] = {hi0 - tau, hi1 - tau, hi2 - tau};
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            double p = x[3 * i + a] + dt * v[3 * i + a];
+            if (p < lo[a]) { p = lo[a] + (lo[a] - p); v[3 * i + a] = -v[3 * i + a]; }
+            if (p > hi[a]) { p = hi[a] - (p - hi[a]); v[3 * i + a] = -v[3 * i + a]; }
+            p = p < lo[a] ? lo[a] : (p > hi[a] ? hi[a] : p);
+            x[3 * i + a] = p;
+        }
+    }
+}
+// spring pressure F_p = (c - x)/eps^2, gravity m g, v += dt/m (F_p + F_g), m = rho nu
+__global__ void __launch_bounds__(RB) k_forces(int64_t n, const double *__restrict__ x,
+                                              const double *__restrict__ c, const double *__restrict__ nu,
+                                              const double *__restrict__ rho, double *__restrict__ v,
+                                              double dt, double inv_eps2, double g0, double g1, double g2) {
+    const double g[3] = {g0, g1, g2};
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        const double m = rho[i] * nu[i];
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            double f = (c[3 * i + a] - x[3 * i + a]) * inv_eps2 + m * g[a];
+            v[3 * i + a] += dt * f / m;
+        }
+    }
+}
+}  // namespace
+
+extern "C" int pf_fluid_advect(int64_t n, double *x, double *v, double dt, const double *lo_host,
+                               const double *hi_host, double tau, void *stream) {
+    pf_internal_launches_add(1);
+    k_advect<<<nblocks(n), RB, 0, (cudaStream_t)stream>>>(n, x, v, dt, lo_host[0], lo_host[1], lo_host[2],
+                                                          hi_host[0], hi_host[1], hi_host[2], tau);
+    NCK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int pf_fluid_forces(int64_t n, const double *x, const double *cent, const double *nu,
+                               const double *rho, double *v, double dt, double eps, const double *g_host,
+                               void *stream) {
+    pf_internal_launches_add(1);
+    k_forces<<<nblocks(n), RB, 0, (cudaStream_t)stream>>>(n, x, cent, nu, rho, v, dt, 1.0 / (eps * eps),
+                                                          g_host[0], g_host[1], g_host[2]);
+    NCK(cudaGetLastError());
     return 0;
 }

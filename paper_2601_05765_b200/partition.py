@@ -1,0 +1,75 @@
+"""Spatial decomposition of the cell evaluation across ranks.
+
+Rank r owns the sites of an x-slab and holds, as ghosts, every site within the
+largest ball-aware search radius of its owned cells,
+
+    W_r = max_{i owned} sqrt(psi_i) + sqrt(psi_i + dpsi),   dpsi = global max - min
+
+(the reference's stop radius, _kernels.py:1239-1248), so each owned cell sees
+exactly the candidates it sees on one GPU.  The local site array keeps the
+global index order (owned and ghosts merged, sorted), so the (d^2, j)
+tie-break order is unchanged and per-cell outputs are bit-identical to the
+single-GPU run: the evaluation needs no collective beyond the scalar dpsi
+all-reduce.  Facet tags come back as local indices; `to_global` maps them.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class Slab:
+    rank: int
+    world: int
+    lo: float
+    hi: float
+    local_to_global: np.ndarray  # int64 [n_local], increasing
+    owned_local: np.ndarray      # int32 [n_owned] local indices of owned sites
+    ghost_margin: float
+
+    @property
+    def n_local(self) -> int:
+        return len(self.local_to_global)
+
+
+def global_dpsi(psi_local: np.ndarray, group=None) -> float:
+    """max(psi) - min(psi) over all ranks (one all-reduce of two scalars)."""
+    import torch
+    import torch.distributed as dist
+
+    lo = float(psi_local.min()) if len(psi_local) else np.inf
+    hi = float(psi_local.max()) if len(psi_local) else -np.inf
+    if dist.is_available() and dist.is_initialized():
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor([-lo, hi], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        lo, hi = -float(t[0]), float(t[1])
+    return max(hi - lo, 0.0) if np.isfinite(hi) else 0.0
+
+
+def slab_partition(pts: np.ndarray, psi: np.ndarray, dpsi: float, world: int, rank: int,
+                   lo: float = 0.0, hi: float = 1.0) -> Slab:
+    """x-slab r of [lo, hi] with its ghost sites (pts / psi are the global arrays)."""
+    x = pts[:, 0]
+    w = (hi - lo) / world
+    a, b = lo + rank * w, lo + (rank + 1) * w
+    own = (x >= a) & (x < b) if rank < world - 1 else (x >= a)
+    if rank == 0:
+        own |= x < lo
+    br = np.sqrt(np.maximum(psi, 0.0)) + np.sqrt(np.maximum(psi, 0.0) + dpsi)
+    margin = float(br[own].max()) * (1.0 + 1e-9) if own.any() else 0.0
+    keep = own | ((x >= a - margin) & (x <= b + margin))
+    idx = np.nonzero(keep)[0].astype(np.int64)
+    owned_local = np.nonzero(own[idx])[0].astype(np.int32)
+    return Slab(rank, world, a, b, idx, owned_local, margin)
+
+
+def to_global(slab: Slab, ftag_local: np.ndarray, fcount: np.ndarray) -> np.ndarray:
+    """Map the used site tags (>= 0, slot < fcount) to global indices."""
+    out = np.array(ftag_local, copy=True)
+    used = np.arange(out.shape[1])[None, :] < np.asarray(fcount)[:, None]
+    m = used & (out >= 0)
+    out[m] = slab.local_to_global[out[m]]
+    return out

@@ -47,6 +47,8 @@ def _bind():
         L.pf_newton_solve.argtypes = [vp, i64, vp, vp, vp, i, d, i, i, d, i, C.POINTER(NewtonStats), vp]
         L.pf_newton_solve.restype = i
         L.pf_newton_last_state.argtypes = [vp, vp, vp, vp, vp, i64, i, vp]
+        L.pf_newton_last_state_ex.argtypes = [vp, vp, vp, vp, vp, vp, i64, i, vp]
+        L.pf_newton_last_state_ex.restype = i
         L.pf_newton_last_state.restype = i
         L.pf_newton_hessian.argtypes = [i64, i, vp, vp, vp, vp, vp, vp, d, vp, vp, vp, vp, vp]
         L.pf_newton_hessian.restype = i
