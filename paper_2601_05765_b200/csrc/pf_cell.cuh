@@ -94,34 +94,44 @@ struct BuildScratch {
 
 template <class C>
 struct EvalScratch {
+    // per facet
     double fh[C::CF], frc[C::CF], farea[C::CF], fcx[C::CF], fcy[C::CF], fcz[C::CF], fip[C::CF];
-    double fpa[C::CF];                 // projected (occluded) patch area
-    double smx[C::CF], smy[C::CF], smz[C::CF], smg[C::CF];  // interior-point ray midpoints
-    int16_t fhead[C::CF], fnp[C::CF];
-    uint8_t fkind[C::CF], fseg[C::CF], funs[C::CF];
+    double fpa[C::CF];       // Gauss-Bonnet sum, then the projected (occluded) patch area
+    double fe[6][C::CF];     // facet-circle frame (perp_basis); later the interior-point rays
+    int16_t fhead[C::CF + 1], fnp[C::CF];  // boundary ring = pool[fhead, fhead + fnp)
+    uint8_t fkind[C::CF], fseg[C::CF], funs[C::CF], fmrg[C::CF];
     uint8_t vin[C::CV];
     // twin-facet lookup (replaces the reference's O(nf m) _edge_other_facet scan)
     uint8_t vdeg[C::CV];            // outgoing loop entries per vertex
     uint16_t vinc[C::CV * 4];       // their entry indices (first 4)
     uint8_t efac[C::CL];            // facet of each loop entry
     uint16_t esv[C::CL];            // successor vertex of each loop entry
+    // point pool: the facets' boundary rings, contiguous per facet, walk order
     double ppx[C::CP], ppy[C::CP], ppz[C::CP];
-    int16_t pnext[C::CP];
-    uint8_t pfl[C::CP];  // bit0 on_sph, bit1 conn (arc to next), bit2 deleted
+    double prx[C::CP], pry[C::CP], prz[C::CP];  // central projections from the interior point
+    uint8_t pfl[C::CP];   // PF_ONSPH / PF_CONN (arc to next) / PF_DEL / PF_ENTRY
+    uint8_t pfac[C::CP];  // facet of the point (PF_DEAD: freed by a merge)
     int npool;
 };
 
-template <class C>
-struct WS {
-    Poly<C> P[2];
-    union {
-        BuildScratch<C> b;
-        EvalScratch<C> e;
-    } u;
-    int oflow;  // capacity overflow seen by any lane
+// per-warp workspaces.  WS: both phases (fused and reference-capacity
+// kernels); BWS / EWS: what the split build / evaluate kernels need.
+template <class C_, int NP, class U>
+struct WSX {
+    using Cap = C_;
+    Poly<C_> P[NP];
+    U u;
+    int oflow;    // capacity overflow seen by any lane
     int cen_on;   // census requested for this cell
     int cen[16];  // algorithmic-work census (SURVEY.md §8(d) S_cell terms)
 };
+template <class C> union BEU { BuildScratch<C> b; EvalScratch<C> e; };
+template <class C> struct BU { BuildScratch<C> b; };
+template <class C> struct EU { EvalScratch<C> e; };
+template <class C> using WS = WSX<C, 2, BEU<C>>;
+template <class C> using BWS = WSX<C, 2, BU<C>>;
+template <class C> using EWS = WSX<C, 1, EU<C>>;
+
 
 // census slots:
 enum {
@@ -247,9 +257,10 @@ PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
 // ---------------------------------------------------------------------------
 // clip A by n.x <= dd into B (_kernels.py:109-319), warp-cooperative
 // ---------------------------------------------------------------------------
-template <class C>
-PF_NOINL int clip(WS<C> *ws, const Poly<C> &A, Poly<C> &B, double nx, double ny, double nz,
+template <class W>
+PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B, double nx, double ny, double nz,
                 double dd, int tag, double tol) {
+    using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
     const int L = pfw::lane();
     const unsigned lt = pfw::lanemask_lt();
@@ -549,9 +560,10 @@ PF_DEV int bucket_coord(double x, double lo, double ih, int gn) {
 
 // returns the number of candidates (may exceed CC: overflow); *all_sites set
 // when the bucket range spans the whole grid
-template <class C>
-PF_NOINL int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, double py, double pz,
+template <class W>
+PF_NOINL int gather_shell(W *ws, const CellIn &in, int self, double px, double py, double pz,
                         double t_lo, double t_hi, bool *all_sites) {
+    using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
     const GridView &g = in.g;
     const int L = pfw::lane();
@@ -615,8 +627,9 @@ PF_NOINL int gather_shell(WS<C> *ws, const CellIn &in, int self, double px, doub
 }
 
 // sort the shell's candidates by (d2, j) in place (rank sort through registers)
-template <class C>
-PF_NOINL void sort_candidates(WS<C> *ws, int nc) {
+template <class W>
+PF_NOINL void sort_candidates(W *ws, int nc) {
+    using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
     const int L = pfw::lane();
     constexpr int PER = (C::CC + 31) / 32;
@@ -651,8 +664,9 @@ PF_NOINL void sort_candidates(WS<C> *ws, int nc) {
 // build the Laguerre cell of site i (_kernels.py:1197-1355)
 // returns 0 ok / 1 empty / 3 overflow; *which = buffer holding the cell
 // ---------------------------------------------------------------------------
-template <class C>
-PF_NOINL int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int *nclips) {
+template <class W>
+PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
+    using C = typename W::Cap;
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const double psii = in.psi[i];
     const double tol = in.tol, dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
@@ -728,223 +742,280 @@ PF_NOINL int build_cell(WS<C> *ws, const CellIn &in, int i, int *which_out, int 
 
 // ---------------------------------------------------------------------------
 // evaluation (_kernels.py:411-1170)
+//
+// Lane-parallel over loop entries and boundary points instead of facets: the
+// restriction emits every loop entry's points with one warp scan, so each
+// facet's boundary ring is a contiguous run of the point pool, in the
+// reference's walk order; the generalized-polygon integrals and the
+// Gauss-Bonnet patch terms are then computed lane per boundary point and
+// summed per facet with a segmented warp reduction (fixed shuffle tree:
+// deterministic).  A facet walk done by one lane (the reference's loop)
+// leaves 2/3 of the warp idle on the paper's scenes.
 // ---------------------------------------------------------------------------
-enum { PF_ONSPH = 1, PF_CONN = 2, PF_DEL = 4 };
+enum { PF_ONSPH = 1, PF_CONN = 2, PF_DEL = 4, PF_ENTRY = 8 };
+enum { PF_DEAD = 0xff };  // pfac of a pool slot freed by the zero-length merge
 
-// Restrict facet f to the ball and emit its boundary sequence into the pool
-// (_kernels.py:411-675).  Executed by one lane.  Returns the kind, -1 on
-// MAX_P overflow, -2 on pool overflow.
+// _edge_other_facet (_kernels.py:397-408): lowest facet != f holding the
+// directed edge (bb -> a), through the per-cell vertex incidence table
 template <class C>
-PF_NOINL int restrict_facet(WS<C> *ws, const Poly<C> &P, int f, double px, double py, double pz,
-                          double psi, double tol, double *s_out, double *rc_out, int *head_out,
-                          int *np_out) {
-    EvalScratch<C> &E = ws->u.e;
-    const int nf = P.nf;
-    const double nx = P.nx[f], ny = P.ny[f], nz = P.nz[f], dd = P.d[f];
-    const double s = dd - (nx * px + ny * py + nz * pz);
-    const double rc2 = psi - s * s;
-    const double R = dsqrt(psi);
-    *s_out = s; *rc_out = 0.0; *head_out = -1; *np_out = 0;
-    if (rc2 <= tol * (2.0 * R + tol)) return RF_OUTSIDE;
-    const double rc = dsqrt(rc2);
-    *rc_out = rc;
-    const double qx = px + s * nx, qy = py + s * ny, qz = pz + s * nz;
-    const int start = P.lp[f], m = P.lp[f + 1] - start;
-    int n_in = 0;
-    #pragma unroll 1
-    for (int e = 0; e < m; e++) n_in += E.vin[P.lv[start + e]];
-
-    int head = -1, prev = -1, npts = 0;
-#define PF_EMIT(X, Y, Z, FL)                                        \
-    do {                                                            \
-        int _id = pfw::atom_add(&E.npool, 1);                       \
-        if (_id >= C::CP) return -2;                                \
-        E.ppx[_id] = (X); E.ppy[_id] = (Y); E.ppz[_id] = (Z);       \
-        E.pfl[_id] = (uint8_t)(FL);                                 \
-        E.pnext[_id] = -1;                                          \
-        if (prev >= 0) E.pnext[prev] = (int16_t)_id; else head = _id; \
-        prev = _id;                                                 \
-        npts++;                                                     \
-    } while (0)
-
-    if (n_in == m) {
+PF_DEV int twin_facet(const EvalScratch<C> &E, const Poly<C> &P, int f, int a, int bb) {
+    int g = -1;
+    const int dg = E.vdeg[bb];
+    if (dg <= 4) {
         #pragma unroll 1
-        for (int e = 0; e < m; e++) {
-            int v = P.lv[start + e];
-            PF_EMIT(P.x[v], P.y[v], P.z[v], 0);
+        for (int t = 0; t < dg; t++) {
+            const int k2 = E.vinc[bb * 4 + t];
+            const int g2 = E.efac[k2];
+            if (E.esv[k2] == a && g2 != f && (g < 0 || g2 < g)) g = g2;
         }
-        E.pnext[prev] = (int16_t)head;
-        *head_out = head; *np_out = npts;
-        return RF_UNTOUCHED;
-    }
-    bool first_entry = false;
-    bool cur_inside = E.vin[P.lv[start]] != 0;
-    #pragma unroll 1
-    for (int e = 0; e < m; e++) {
-        const int a = P.lv[start + e];
-        const int bb = P.lv[start + (e + 1 == m ? 0 : e + 1)];
-        const bool ina = E.vin[a] != 0;
-        const bool inb = E.vin[bb] != 0;
-        if (ina) {
-            if (npts >= REF_MAX_P) return -1;
-            PF_EMIT(P.x[a], P.y[a], P.z[a], 0);
-            cur_inside = true;
-        }
-        if (ina && inb) continue;
-        // _edge_other_facet (_kernels.py:397-408): lowest facet != f holding
-        // the directed edge (bb -> a), through the vertex incidence table
-        int g = -1;
-        const int dg = E.vdeg[bb];
-        if (dg <= 4) {
+    } else {
+        #pragma unroll 1
+        for (int gg = 0; gg < P.nf && g < 0; gg++) {
+            if (gg == f) continue;
+            int s0 = P.lp[gg], mg = P.lp[gg + 1] - s0;
             #pragma unroll 1
-            for (int t = 0; t < dg; t++) {
-                const int k2 = E.vinc[bb * 4 + t];
-                const int g2 = E.efac[k2];
-                if (E.esv[k2] == a && g2 != f && (g < 0 || g2 < g)) g = g2;
+            for (int ee = 0; ee < mg; ee++) {
+                if (P.lv[s0 + ee] == bb && P.lv[s0 + (ee + 1 == mg ? 0 : ee + 1)] == a) { g = gg; break; }
             }
-        } else {
+        }
+    }
+    return g;
+}
+
+// Restrict every facet to the ball (_kernels.py:411-675) into the point pool.
+// Returns 0, 1 on a facet with more than MAX_P boundary points (the
+// reference's kind -1), 2 on pool overflow.
+template <class W>
+PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                          double psi, double R, double tol) {
+    using C = typename W::Cap;
+    EvalScratch<C> &E = ws->u.e;
+    const int L = pfw::lane();
+    const int nf = P.nf, nl = P.nl;
+    const double ball_tol = tol * (2.0 * R + tol);
+    // A. per facet: signed height, circle radius; OUTSIDE / UNTOUCHED / GENPOLY (_kernels.py:432-468)
+    #pragma unroll 1
+    for (int f = L; f < nf; f += 32) {
+        const double s = P.d[f] - (P.nx[f] * px + P.ny[f] * py + P.nz[f] * pz);
+        const double rc2 = psi - s * s;
+        int kind = RF_OUTSIDE;
+        double rc = 0.0;
+        if (!(rc2 <= ball_tol)) {
+            rc = dsqrt(rc2);
+            const int s0 = P.lp[f], m = P.lp[f + 1] - s0;
+            int n_in = 0;
             #pragma unroll 1
-            for (int gg = 0; gg < nf && g < 0; gg++) {
-                if (gg == f) continue;
-                int s0 = P.lp[gg], mg = P.lp[gg + 1] - s0;
-                #pragma unroll 1
-                for (int ee = 0; ee < mg; ee++) {
-                    if (P.lv[s0 + ee] == bb && P.lv[s0 + (ee + 1 == mg ? 0 : ee + 1)] == a) { g = gg; break; }
+            for (int e = 0; e < m; e++) n_in += E.vin[P.lv[s0 + e]];
+            kind = n_in == m ? RF_UNTOUCHED : RF_GENPOLY;
+        }
+        E.fh[f] = s; E.frc[f] = rc; E.fkind[f] = (uint8_t)kind; E.fmrg[f] = 0;
+    }
+    pfw::sync();
+    // B. lane per loop entry (edge a -> bb of facet f): the points it adds to
+    // the facet's ring (_kernels.py:470-587) -- a when inside the ball, then
+    // the edge's sphere crossings in walk order, computed from the line of f
+    // and its twin facet as the reference does.  The walk state before an
+    // edge's crossings is always "inside" == (a inside), so every entry is
+    // independent; the pool position comes from one warp scan.
+    int base = 0;
+    #pragma unroll 1
+    for (int k0 = 0; k0 < nl; k0 += 32) {
+        const int k = k0 + L;
+        int cnt = 0, f = 0, fl0 = 0, fl1 = 0;
+        double x0 = 0.0, y0 = 0.0, z0 = 0.0, x1 = 0.0, y1 = 0.0, z1 = 0.0;
+        if (k < nl) {
+            f = E.efac[k];
+            if (E.fkind[f] != RF_OUTSIDE) {
+                const int a = P.lv[k], bb = E.esv[k];
+                const bool ina = E.vin[a] != 0, inb = E.vin[bb] != 0;
+                if (ina) { x0 = P.x[a]; y0 = P.y[a]; z0 = P.z[a]; cnt = 1; }
+                if (!(ina && inb)) {
+                    const double nx = P.nx[f], ny = P.ny[f], nz = P.nz[f], dd = P.d[f];
+                    const int g = twin_facet(E, P, f, a, bb);
+                    double gx, gy, gz, gd, c12, det, ux, uy, uz;
+                    if (g >= 0) {
+                        gx = P.nx[g]; gy = P.ny[g]; gz = P.nz[g]; gd = P.d[g];
+                        c12 = nx * gx + ny * gy + nz * gz;
+                        det = 1.0 - c12 * c12;
+                        ux = ny * gz - nz * gy;
+                        uy = nz * gx - nx * gz;
+                        uz = nx * gy - ny * gx;
+                    } else {
+                        ux = P.x[bb] - P.x[a];
+                        uy = P.y[bb] - P.y[a];
+                        uz = P.z[bb] - P.z[a];
+                        det = 1.0; c12 = 0.0; gd = 0.0; gx = 0.0; gy = 0.0; gz = 0.0;
+                    }
+                    const double un = dsqrt(ux * ux + uy * uy + uz * uz);
+                    if (!(un < 1e-300 || det <= 1e-300)) {
+                        ux = ddiv(ux, un); uy = ddiv(uy, un); uz = ddiv(uz, un);
+                        if (ux < 0.0 || (ux == 0.0 && (uy < 0.0 || (uy == 0.0 && uz < 0.0)))) {
+                            ux = -ux; uy = -uy; uz = -uz;
+                        }
+                        double ox, oy, oz;
+                        if (g >= 0) {
+                            const double r1 = dd - (nx * px + ny * py + nz * pz);
+                            const double r2 = gd - (gx * px + gy * py + gz * pz);
+                            const double al = ddiv(r1 - c12 * r2, det);
+                            const double be = ddiv(r2 - c12 * r1, det);
+                            ox = px + al * nx + be * gx;
+                            oy = py + al * ny + be * gy;
+                            oz = pz + al * nz + be * gz;
+                        } else {
+                            ox = P.x[a]; oy = P.y[a]; oz = P.z[a];
+                        }
+                        const double w0x = ox - px, w0y = oy - py, w0z = oz - pz;
+                        const double bh = ux * w0x + uy * w0y + uz * w0z;
+                        const double cc = w0x * w0x + w0y * w0y + w0z * w0z - psi;
+                        const double disc = bh * bh - cc;
+                        if (!(disc <= tol * tol)) {
+                            const double sqd = dsqrt(disc);
+                            const double t1 = -bh - sqd, t2 = -bh + sqd;
+                            const double ta = ux * (P.x[a] - ox) + uy * (P.y[a] - oy) + uz * (P.z[a] - oz);
+                            const double tb = ux * (P.x[bb] - ox) + uy * (P.y[bb] - oy) + uz * (P.z[bb] - oz);
+                            const double tlo = ta < tb ? ta : tb;
+                            const double thi = ta < tb ? tb : ta;
+                            bool cur = ina;
+                            #pragma unroll 1
+                            for (int which = 0; which < 2; which++) {
+                                const double t = (ta <= tb) == (which == 0) ? t1 : t2;
+                                if (t <= tlo + tol || t >= thi - tol) continue;
+                                // The first root in walk order is where the edge
+                                // enters the ball.  After a vertex classified inside
+                                // it can only pass the range test if that vertex lies
+                                // outside the sphere by less than the tolerance; the
+                                // reference then labels the entry an exit and closes
+                                // the facet with a spurious arc (a whole circular
+                                // segment too much).  It coincides with the vertex to
+                                // ~tol: drop it.  Never fires on consistent geometry.
+                                if (which == 0 && cur) continue;
+                                const double cxx = ox + t * ux, cxy = oy + t * uy, cxz = oz + t * uz;
+                                const int fl = cur ? (PF_ONSPH | PF_CONN) : (PF_ONSPH | PF_ENTRY);
+                                cur = !cur;
+                                if (cnt == 0) { x0 = cxx; y0 = cxy; z0 = cxz; fl0 = fl; }
+                                else { x1 = cxx; y1 = cxy; z1 = cxz; fl1 = fl; }
+                                cnt++;
+                            }
+                        }
+                    }
                 }
             }
         }
-        double gx, gy, gz, gd, c12, det, ux, uy, uz;
-        if (g >= 0) {
-            gx = P.nx[g]; gy = P.ny[g]; gz = P.nz[g]; gd = P.d[g];
-            c12 = nx * gx + ny * gy + nz * gz;
-            det = 1.0 - c12 * c12;
-            ux = ny * gz - nz * gy;
-            uy = nz * gx - nx * gz;
-            uz = nx * gy - ny * gx;
-        } else {
-            ux = P.x[bb] - P.x[a];
-            uy = P.y[bb] - P.y[a];
-            uz = P.z[bb] - P.z[a];
-            det = 1.0; c12 = 0.0; gd = 0.0; gx = 0.0; gy = 0.0; gz = 0.0;
+        int tot;
+        const int pos = base + pfw::excl_scan_i(cnt, &tot);
+        if (k < nl && k == P.lp[f]) E.fhead[f] = (int16_t)pos;  // ring of f starts here
+        if (pos + cnt <= C::CP) {
+            if (cnt > 0) { E.ppx[pos] = x0; E.ppy[pos] = y0; E.ppz[pos] = z0; E.pfl[pos] = (uint8_t)fl0; E.pfac[pos] = (uint8_t)f; }
+            if (cnt > 1) { E.ppx[pos + 1] = x1; E.ppy[pos + 1] = y1; E.ppz[pos + 1] = z1; E.pfl[pos + 1] = (uint8_t)fl1; E.pfac[pos + 1] = (uint8_t)f; }
         }
-        double un = dsqrt(ux * ux + uy * uy + uz * uz);
-        if (un < 1e-300 || det <= 1e-300) { cur_inside = inb; continue; }
-        ux = ddiv(ux, un); uy = ddiv(uy, un); uz = ddiv(uz, un);
-        if (ux < 0.0 || (ux == 0.0 && (uy < 0.0 || (uy == 0.0 && uz < 0.0)))) {
-            ux = -ux; uy = -uy; uz = -uz;
-        }
-        double x0x, x0y, x0z;
-        if (g >= 0) {
-            double r1 = dd - (nx * px + ny * py + nz * pz);
-            double r2 = gd - (gx * px + gy * py + gz * pz);
-            double al = ddiv(r1 - c12 * r2, det);
-            double be = ddiv(r2 - c12 * r1, det);
-            x0x = px + al * nx + be * gx;
-            x0y = py + al * ny + be * gy;
-            x0z = pz + al * nz + be * gz;
-        } else {
-            x0x = P.x[a]; x0y = P.y[a]; x0z = P.z[a];
-        }
-        double w0x = x0x - px, w0y = x0y - py, w0z = x0z - pz;
-        double bh = ux * w0x + uy * w0y + uz * w0z;
-        double cc = w0x * w0x + w0y * w0y + w0z * w0z - psi;
-        double disc = bh * bh - cc;
-        if (disc <= tol * tol) { cur_inside = inb; continue; }
-        double sqd = dsqrt(disc);
-        double t1 = -bh - sqd, t2 = -bh + sqd;
-        double ta = ux * (P.x[a] - x0x) + uy * (P.y[a] - x0y) + uz * (P.z[a] - x0z);
-        double tb = ux * (P.x[bb] - x0x) + uy * (P.y[bb] - x0y) + uz * (P.z[bb] - x0z);
-        double tlo = ta < tb ? ta : tb;
-        double thi = ta < tb ? tb : ta;
-        #pragma unroll 1
-        for (int which = 0; which < 2; which++) {
-            double t;
-            if (ta <= tb) t = which == 0 ? t1 : t2;
-            else t = which == 0 ? t2 : t1;
-            if (t <= tlo + tol || t >= thi - tol) continue;
-            // The first root in walk order is where the edge enters the ball.
-            // After a vertex classified inside (cur_inside == ina here) it can
-            // only pass the range test if that vertex lies outside the sphere
-            // by less than the tolerance; the reference then labels the entry
-            // an exit and closes the facet with a spurious arc (a whole
-            // circular segment too much).  It coincides with the vertex to
-            // ~tol: drop it.  Never fires on consistent geometry.
-            if (which == 0 && cur_inside) continue;
-            if (npts >= REF_MAX_P) return -1;
-            double cxx = x0x + t * ux, cxy = x0y + t * uy, cxz = x0z + t * uz;
-            if (cur_inside) {
-                PF_EMIT(cxx, cxy, cxz, PF_ONSPH | PF_CONN);
-                cur_inside = false;
-            } else {
-                if (prev >= 0) E.pfl[prev] |= PF_CONN;
-                else first_entry = true;
-                PF_EMIT(cxx, cxy, cxz, PF_ONSPH);
-                cur_inside = true;
-            }
-        }
-        cur_inside = inb;
+        base += tot;
     }
-#undef PF_EMIT
-    if (npts == 0) {
+    if (base > C::CP) { pfw::sync(); return 2; }
+    if (L == 0) { E.fhead[nf] = (int16_t)base; E.npool = base; }
+    pfw::sync();
+    // C. per facet: ring range; no point -> full circle or outside
+    // (_kernels.py:590-607); fewer than 2 -> outside; the facet frame
+    bool ovf = false;
+    #pragma unroll 1
+    for (int f = L; f < nf; f += 32) {
+        int kind = E.fkind[f];
+        const int np = E.fhead[f + 1] - E.fhead[f];
+        E.fnp[f] = (int16_t)np;
+        if (kind == RF_OUTSIDE) continue;
+        const double nx = P.nx[f], ny = P.ny[f], nz = P.nz[f];
         double eb[6];
         perp_basis(nx, ny, nz, eb);
-        bool cin = true;
-        #pragma unroll 1
-        for (int e = 0; e < m; e++) {
-            int a = P.lv[start + e];
-            int bb = P.lv[start + (e + 1 == m ? 0 : e + 1)];
-            double p0u = (P.x[a] - qx) * eb[0] + (P.y[a] - qy) * eb[1] + (P.z[a] - qz) * eb[2];
-            double p0v = (P.x[a] - qx) * eb[3] + (P.y[a] - qy) * eb[4] + (P.z[a] - qz) * eb[5];
-            double p1u = (P.x[bb] - qx) * eb[0] + (P.y[bb] - qy) * eb[1] + (P.z[bb] - qz) * eb[2];
-            double p1v = (P.x[bb] - qx) * eb[3] + (P.y[bb] - qy) * eb[4] + (P.z[bb] - qz) * eb[5];
-            if ((p1u - p0u) * (-p0v) - (p1v - p0v) * (-p0u) < 0.0) { cin = false; break; }
-        }
-        return cin ? RF_FULLCIRCLE : RF_OUTSIDE;
-    }
-    E.pnext[prev] = (int16_t)head;  // close the ring
-    if (first_entry) E.pfl[prev] |= PF_CONN;
-    // drop zero-length connectors (_kernels.py:612-636)
-    {
-        int i = head;
-        int kept = 0;
-        #pragma unroll 1
-        for (int t = 0; t < npts; t++) {
-            int j = E.pnext[i];
-            bool jdel = (E.pfl[j] & PF_DEL) != 0;  // only the wrap to a merged head
-            double dxp = E.ppx[i] - E.ppx[j];
-            double dyp = E.ppy[i] - E.ppy[j];
-            double dzp = E.ppz[i] - E.ppz[j];
-            if (!(E.pfl[i] & PF_CONN) && !jdel && dxp * dxp + dyp * dyp + dzp * dzp <= tol * tol) {
-                if (E.pfl[i] & PF_ONSPH) E.pfl[j] |= PF_ONSPH;
-                E.pfl[i] |= PF_DEL;
-            } else {
-                kept++;
-            }
-            i = j;
-        }
-        if (kept < npts) {
-            int nh = -1, lastk = -1;
-            i = head;
-            #pragma unroll 1
-            for (int t = 0; t < npts; t++) {
-                int j = E.pnext[i];
-                if (!(E.pfl[i] & PF_DEL)) {
-                    if (lastk >= 0) E.pnext[lastk] = (int16_t)i; else nh = i;
-                    lastk = i;
+        if (kind == RF_GENPOLY) {
+            if (np > REF_MAX_P) ovf = true;
+            if (np == 0) {
+                const double s = E.fh[f];
+                const double qx = px + s * nx, qy = py + s * ny, qz = pz + s * nz;
+                const int start = P.lp[f], m = P.lp[f + 1] - start;
+                bool cin = true;
+                #pragma unroll 1
+                for (int e = 0; e < m; e++) {
+                    int a = P.lv[start + e];
+                    int bb = P.lv[start + (e + 1 == m ? 0 : e + 1)];
+                    double p0u = (P.x[a] - qx) * eb[0] + (P.y[a] - qy) * eb[1] + (P.z[a] - qz) * eb[2];
+                    double p0v = (P.x[a] - qx) * eb[3] + (P.y[a] - qy) * eb[4] + (P.z[a] - qz) * eb[5];
+                    double p1u = (P.x[bb] - qx) * eb[0] + (P.y[bb] - qy) * eb[1] + (P.z[bb] - qz) * eb[2];
+                    double p1v = (P.x[bb] - qx) * eb[3] + (P.y[bb] - qy) * eb[4] + (P.z[bb] - qz) * eb[5];
+                    if ((p1u - p0u) * (-p0v) - (p1v - p0v) * (-p0u) < 0.0) { cin = false; break; }
                 }
-                i = j;
+                kind = cin ? RF_FULLCIRCLE : RF_OUTSIDE;
+            } else if (np < 2) {
+                kind = RF_OUTSIDE;
             }
-            if (lastk >= 0) E.pnext[lastk] = (int16_t)nh;
-            head = nh;
-            npts = kept;
+            E.fkind[f] = (uint8_t)kind;
         }
+        #pragma unroll
+        for (int t = 0; t < 6; t++) E.fe[t][f] = eb[t];
     }
-    if (npts < 2) return RF_OUTSIDE;
-    // The reference rotates the ring to start at the arc with the smallest
-    // start angle (_kernels.py:640-674); that only fixes a summation order,
-    // and this path's sums are reductions anyway, so the ring keeps its start.
-    *head_out = head; *np_out = npts;
-    return RF_GENPOLY;
+    if (pfw::any(ovf)) return 1;
+    pfw::sync();
+    // D. a point is followed by an arc iff it exits the ball or the next point
+    // enters it (_kernels.py:575-587, incl. the ring-closing first entry);
+    // zero-length segment connectors are merge candidates (_kernels.py:612-636)
+    const int npool = base;
+    bool any_cand = false;
+    #pragma unroll 1
+    for (int q0 = 0; q0 < npool; q0 += 32) {
+        const int q = q0 + L;
+        int nfl = -1;
+        if (q < npool) {
+            const int f = E.pfac[q];
+            if (E.fkind[f] == RF_GENPOLY) {
+                const int head = E.fhead[f], np = E.fnp[f];
+                const int j = q + 1 < head + np ? q + 1 : head;
+                nfl = E.pfl[q];
+                if (E.pfl[j] & PF_ENTRY) nfl |= PF_CONN;
+                if (!(nfl & PF_CONN)) {
+                    const double dxp = E.ppx[q] - E.ppx[j], dyp = E.ppy[q] - E.ppy[j], dzp = E.ppz[q] - E.ppz[j];
+                    if (dxp * dxp + dyp * dyp + dzp * dzp <= tol * tol) { any_cand = true; E.fmrg[f] = 1; }
+                }
+            }
+        }
+        pfw::sync();
+        if (nfl >= 0) E.pfl[q] = (uint8_t)nfl;
+        pfw::sync();
+    }
+    if (pfw::any(any_cand)) {
+        // sequential merge of the facets that have a candidate (rare)
+        #pragma unroll 1
+        for (int f = L; f < nf; f += 32) {
+            if (!E.fmrg[f] || E.fkind[f] != RF_GENPOLY) continue;
+            const int head = E.fhead[f], np = E.fnp[f];
+            int kept = 0;
+            #pragma unroll 1
+            for (int t = 0; t < np; t++) {
+                const int i = head + t, j = t + 1 < np ? i + 1 : head;
+                const bool jdel = (E.pfl[j] & PF_DEL) != 0;  // only the wrap to a merged head
+                const double dxp = E.ppx[i] - E.ppx[j], dyp = E.ppy[i] - E.ppy[j], dzp = E.ppz[i] - E.ppz[j];
+                if (!(E.pfl[i] & PF_CONN) && !jdel && dxp * dxp + dyp * dyp + dzp * dzp <= tol * tol) {
+                    if (E.pfl[i] & PF_ONSPH) E.pfl[j] |= PF_ONSPH;
+                    E.pfl[i] |= PF_DEL;
+                } else {
+                    kept++;
+                }
+            }
+            if (kept < np) {
+                int w = head;
+                #pragma unroll 1
+                for (int t = 0; t < np; t++) {
+                    const int i = head + t;
+                    if (E.pfl[i] & PF_DEL) continue;
+                    E.ppx[w] = E.ppx[i]; E.ppy[w] = E.ppy[i]; E.ppz[w] = E.ppz[i]; E.pfl[w] = E.pfl[i];
+                    w++;
+                }
+                #pragma unroll 1
+                for (; w < head + np; w++) E.pfac[w] = PF_DEAD;
+                E.fnp[f] = (int16_t)kept;
+                if (kept < 2) E.fkind[f] = RF_OUTSIDE;
+            }
+        }
+        pfw::sync();
+    }
+    return 0;
 }
 
 // Degenerate arcs.  When a loop vertex sits within tolerance of the sphere,
@@ -972,87 +1043,112 @@ PF_NOINL bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy,
     return false;
 }
 
-// _kernels.py:678-716 + 331-390: area, centroid, polar moment of a restricted
-// facet.  Same Green forms as the reference; an arc's trigonometric values come
-// from its end-point coordinates (cos a = x/r, sin a = y/r, double-angle
-// identities) and its sweep from one atan2 of (cross, dot), instead of
-// 2 atan2 + 8 sin/cos per arc.  Agrees with the reference to rounding.
+// boundary point q of a live ring: its facet, else -1
 template <class C>
-PF_NOINL void seq_integrals(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
-                          double nx, double ny, double nz, double qx, double qy, double qz,
-                          double rc, double *out) {
+PF_DEV int ring_facet(const EvalScratch<C> &E, int q, bool need_area) {
+    if (q >= E.npool) return -1;
+    const int f = E.pfac[q];
+    if (f == PF_DEAD) return -1;
+    const int k = E.fkind[f];
+    if (k != RF_GENPOLY && k != RF_UNTOUCHED) return -1;
+    if (need_area && !(E.farea[f] > 0.0)) return -1;
+    return f;
+}
+
+// first lane of this lane's run of equal keys / whether it is the run's last
+// lane (runs of equal keys are contiguous in lane order)
+PF_DEV int seg_first(int key) {
+    const int prev = pfw::shfl(key, (pfw::lane() - 1) & 31);
+    const unsigned heads = pfw::ballot(pfw::lane() == 0 || prev != key);
+    return pfw::msb(heads & (0xffffffffu >> (31 - pfw::lane())));
+}
+PF_DEV bool seg_last(int key) {
+    const int next = pfw::shfl(key, (pfw::lane() + 1) & 31);
+    return pfw::lane() == 31 || next != key;
+}
+
+// _kernels.py:678-716 + 331-390: area, first moments and polar moment of the
+// restricted facets, lane per boundary connector (point -> ring successor),
+// summed per facet.  Same Green forms as the reference; an arc's
+// trigonometric values come from its end-point coordinates (cos a = x/r,
+// sin a = y/r, double-angle identities) and its sweep from one atan2 of
+// (cross, dot), instead of 2 atan2 + 8 sin/cos per arc.  Agrees with the
+// reference to rounding.
+template <class W>
+PF_NOINL void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                             double tol) {
+    using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
-    double e[6];
-    perp_basis(nx, ny, nz, e);
-    double A = 0.0, Mx = 0.0, My = 0.0, Ip = 0.0;
-    int i = head;
-    // local frame coordinates of the current point
-    double x0 = (E.ppx[i] - qx) * e[0] + (E.ppy[i] - qy) * e[1] + (E.ppz[i] - qz) * e[2];
-    double y0 = (E.ppx[i] - qx) * e[3] + (E.ppy[i] - qy) * e[4] + (E.ppz[i] - qz) * e[5];
-    const double x00 = x0, y00 = y0;
+    const int L = pfw::lane();
     #pragma unroll 1
-    for (int t = 0; t < npts; t++) {
-        const int j = E.pnext[i];
-        double x1, y1;
-        if (t + 1 == npts) { x1 = x00; y1 = y00; }
-        else {
-            x1 = (E.ppx[j] - qx) * e[0] + (E.ppy[j] - qy) * e[1] + (E.ppz[j] - qz) * e[2];
-            y1 = (E.ppx[j] - qx) * e[3] + (E.ppy[j] - qy) * e[4] + (E.ppz[j] - qz) * e[5];
-        }
-        if (!(E.pfl[i] & PF_CONN)) {
-            double cr = fma(x0, y1, -x1 * y0);
-            A += 0.5 * cr;
-            double dx = x1 - x0, dy = y1 - y0;
-            double xx = fma(x0, x0, fma(x0, x1, x1 * x1));
-            double yy = fma(y0, y0, fma(y0, y1, y1 * y1));
-            Mx = fma(dy * xx, 1.0 / 6.0, Mx);
-            My = fma(-dx * yy, 1.0 / 6.0, My);
-            double sx3 = (x0 + x1) * (x0 * x0 + x1 * x1);
-            double sy3 = (y0 + y1) * (y0 * y0 + y1 * y1);
-            Ip = fma(fma(dy, sx3, -dx * sy3), 1.0 / 12.0, Ip);
-        } else {
-            double r0 = dsqrt(x0 * x0 + y0 * y0), r1 = dsqrt(x1 * x1 + y1 * y1);
-            double ir0 = r0 > 0.0 ? ddiv(1.0, r0) : 0.0, ir1 = r1 > 0.0 ? ddiv(1.0, r1) : 0.0;
-            double c0 = r0 > 0.0 ? x0 * ir0 : 1.0, s0 = y0 * ir0;
-            double c1 = r1 > 0.0 ? x1 * ir1 : 1.0, s1 = y1 * ir1;
-            double dth = atan2_ool(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
-            if (dth <= 0.0) {
-                dth += 2.0 * PF_PI;
-                double ch2 = (x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0);
-                if (ch2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
-                    long_arc_impossible(P, f, qx, qy, qz, x0 * e[0] + y0 * e[3], x0 * e[1] + y0 * e[4],
-                                        x0 * e[2] + y0 * e[5], rc, tol))
-                    dth -= 2.0 * PF_PI;
+    for (int f = L; f < P.nf; f += 32) { E.farea[f] = 0.0; E.fcx[f] = 0.0; E.fcy[f] = 0.0; E.fip[f] = 0.0; }
+    pfw::sync();
+    const int npool = E.npool;
+    #pragma unroll 1
+    for (int q0 = 0; q0 < npool; q0 += 32) {
+        const int q = q0 + L;
+        const int f = ring_facet(E, q, false);
+        double A = 0.0, Mx = 0.0, My = 0.0, Ip = 0.0;
+        if (f >= 0) {
+            const int head = E.fhead[f], np = E.fnp[f];
+            const int j = q + 1 < head + np ? q + 1 : head;
+            const double e0 = E.fe[0][f], e1 = E.fe[1][f], e2 = E.fe[2][f];
+            const double e3 = E.fe[3][f], e4 = E.fe[4][f], e5 = E.fe[5][f];
+            const double s = E.fh[f];
+            const double qx = px + s * P.nx[f], qy = py + s * P.ny[f], qz = pz + s * P.nz[f];
+            const double ax = E.ppx[q] - qx, ay = E.ppy[q] - qy, az = E.ppz[q] - qz;
+            const double bx = E.ppx[j] - qx, by = E.ppy[j] - qy, bz = E.ppz[j] - qz;
+            const double x0 = ax * e0 + ay * e1 + az * e2, y0 = ax * e3 + ay * e4 + az * e5;
+            const double x1 = bx * e0 + by * e1 + bz * e2, y1 = bx * e3 + by * e4 + bz * e5;
+            if (!(E.pfl[q] & PF_CONN)) {
+                const double cr = fma(x0, y1, -x1 * y0);
+                A = 0.5 * cr;
+                const double dx = x1 - x0, dy = y1 - y0;
+                const double xx = fma(x0, x0, fma(x0, x1, x1 * x1));
+                const double yy = fma(y0, y0, fma(y0, y1, y1 * y1));
+                Mx = dy * xx * (1.0 / 6.0);
+                My = -dx * yy * (1.0 / 6.0);
+                const double sx3 = (x0 + x1) * (x0 * x0 + x1 * x1);
+                const double sy3 = (y0 + y1) * (y0 * y0 + y1 * y1);
+                Ip = fma(dy, sx3, -dx * sy3) * (1.0 / 12.0);
+            } else {
+                const double r = E.frc[f];
+                const double r0 = dsqrt(x0 * x0 + y0 * y0), r1 = dsqrt(x1 * x1 + y1 * y1);
+                const double ir0 = r0 > 0.0 ? ddiv(1.0, r0) : 0.0, ir1 = r1 > 0.0 ? ddiv(1.0, r1) : 0.0;
+                const double c0 = r0 > 0.0 ? x0 * ir0 : 1.0, s0 = y0 * ir0;
+                const double c1 = r1 > 0.0 ? x1 * ir1 : 1.0, s1 = y1 * ir1;
+                double dth = atan2_ool(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
+                if (dth <= 0.0) {
+                    dth += 2.0 * PF_PI;
+                    const double ch2 = (x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0);
+                    if (ch2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
+                        long_arc_impossible(P, f, qx, qy, qz, x0 * e0 + y0 * e3, x0 * e1 + y0 * e4,
+                                            x0 * e2 + y0 * e5, r, tol))
+                        dth -= 2.0 * PF_PI;
+                }
+                const double s20 = 2.0 * s0 * c0, c20 = fma(c0, c0, -s0 * s0);
+                const double s21 = 2.0 * s1 * c1, c21 = fma(c1, c1, -s1 * s1);
+                const double s40 = 2.0 * s20 * c20, s41 = 2.0 * s21 * c21;
+                const double ic3 = (s1 - s1 * s1 * s1 * (1.0 / 3.0)) - (s0 - s0 * s0 * s0 * (1.0 / 3.0));
+                const double is3 = (-c1 + c1 * c1 * c1 * (1.0 / 3.0)) - (-c0 + c0 * c0 * c0 * (1.0 / 3.0));
+                const double ic4 = 0.375 * dth + 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
+                const double is4 = 0.375 * dth - 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
+                const double r2 = r * r;
+                A = 0.5 * r2 * dth;
+                Mx = 0.5 * r * r2 * ic3;
+                My = 0.5 * r * r2 * is3;
+                Ip = r * (1.0 / 3.0) * r2 * r * (ic4 + is4);
             }
-            double s20 = 2.0 * s0 * c0, c20 = fma(c0, c0, -s0 * s0);
-            double s21 = 2.0 * s1 * c1, c21 = fma(c1, c1, -s1 * s1);
-            double s40 = 2.0 * s20 * c20, s41 = 2.0 * s21 * c21;
-            const double r = rc;
-            double ic3 = (s1 - s1 * s1 * s1 * (1.0 / 3.0)) - (s0 - s0 * s0 * s0 * (1.0 / 3.0));
-            double is3 = (-c1 + c1 * c1 * c1 * (1.0 / 3.0)) - (-c0 + c0 * c0 * c0 * (1.0 / 3.0));
-            double ic4 = 0.375 * dth + 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
-            double is4 = 0.375 * dth - 0.25 * (s21 - s20) + (s41 - s40) / 32.0;
-            double r2 = r * r;
-            A = fma(0.5 * r2, dth, A);
-            Mx = fma(0.5 * r * r2, ic3, Mx);
-            My = fma(0.5 * r * r2, is3, My);
-            Ip = fma(r * (1.0 / 3.0) * r2 * r, ic4 + is4, Ip);
         }
-        x0 = x1;
-        y0 = y1;
-        i = j;
+        const int rs = seg_first(f);
+        const bool last = seg_last(f);
+        A = pfw::seg_sum_d(A, rs);
+        Mx = pfw::seg_sum_d(Mx, rs);
+        My = pfw::seg_sum_d(My, rs);
+        Ip = pfw::seg_sum_d(Ip, rs);
+        if (f >= 0 && last) { E.farea[f] += A; E.fcx[f] += Mx; E.fcy[f] += My; E.fip[f] += Ip; }
+        pfw::sync();
     }
-    double cx, cy, cz;
-    if (A > 0.0) {
-        double ia = ddiv(1.0, A);
-        double u = Mx * ia, v = My * ia;
-        cx = qx + u * e[0] + v * e[3];
-        cy = qy + u * e[1] + v * e[4];
-        cz = qz + u * e[2] + v * e[5];
-    } else {
-        cx = qx; cy = qy; cz = qz;
-    }
-    out[0] = A; out[1] = cx; out[2] = cy; out[3] = cz; out[4] = Ip;
 }
 
 // _kernels.py:819-835
@@ -1111,117 +1207,145 @@ PF_DEV bool ccw_le(const double *a, const double *b, const double *c, const doub
     return dot3(t, m) >= 0.0;
 }
 
-// _kernels.py:838-1001, streamed over the facet's boundary ring by one lane.
-// Gauss-Bonnet: area = psi (2 pi - sum_arcs (e/R) sweep - sum_vertices theta).
-// Sweeps are CCW angles about the connector circle's axis from one atan2 of
-// (cross, dot) -- the reference's two frame angles phP, phQ -- and the
-// segment orientation test keeps the reference's projected-midpoint rule.
+// Circle carrying connector i -> j of facet f on the sphere, seen from the
+// interior point c (_kernels.py:870-946): an arc lies on the facet circle
+// (axis n_f, offset s_f); a segment projects onto the circle of the plane
+// through c, i and j, oriented so that the projection runs counter-clockwise.
+// Returns whether the connector contributes; *uns is set when it is unstable.
+// The reference decides the segment orientation with the projected midpoint;
+// the rays from c (inside the circle) to the segment sweep less than a half
+// turn counter-clockwise about m = (i - c) x (j - c), and central projection
+// keeps that order, so the test can only fail when the sweep is within
+// rounding of 0 or pi: it is evaluated when sin^2 of the sweep is < 1e-6.
 template <class C>
-PF_NOINL double patch_area(WS<C> *ws, const Poly<C> &P, int f, double tol, int head, int npts,
-                         double nx, double ny, double nz, double s, double px, double py,
-                         double pz, double psi, double cx, double cy, double cz,
-                         bool *unstable_out) {
-    EvalScratch<C> &E = ws->u.e;
-    const double R = dsqrt(psi), iR = ddiv(1.0, R);
-    bool unstable = false;
-    double kg_sum = 0.0, th_sum = 0.0;
-    double pr0[3], pri[3], prj[3];
-    if (E.pfl[head] & PF_ONSPH) { pr0[0] = E.ppx[head]; pr0[1] = E.ppy[head]; pr0[2] = E.ppz[head]; }
-    else project_from(cx, cy, cz, E.ppx[head], E.ppy[head], E.ppz[head], px, py, pz, psi, pr0);
-    pri[0] = pr0[0]; pri[1] = pr0[1]; pri[2] = pr0[2];
-    double tin_i[3] = {0.0, 0.0, 0.0};
-    double tout0[3] = {0.0, 0.0, 0.0};
-    int i = head;
-    #pragma unroll 1
-    for (int t = 0; t < npts; t++) {
-        const int j = E.pnext[i];
-        if (t + 1 == npts) { prj[0] = pr0[0]; prj[1] = pr0[1]; prj[2] = pr0[2]; }
-        else if (E.pfl[j] & PF_ONSPH) { prj[0] = E.ppx[j]; prj[1] = E.ppy[j]; prj[2] = E.ppz[j]; }
-        else project_from(cx, cy, cz, E.ppx[j], E.ppy[j], E.ppz[j], px, py, pz, psi, prj);
-        double tout[3] = {0.0, 0.0, 0.0}, tin_j[3] = {0.0, 0.0, 0.0};
-        const bool arc = (E.pfl[i] & PF_CONN) != 0;
-        double m[3], ee;
-        bool skip = false;
-        if (arc) {
-            m[0] = nx; m[1] = ny; m[2] = nz; ee = s;
-        } else {
-            double a3[3] = {E.ppx[i] - cx, E.ppy[i] - cy, E.ppz[i] - cz};
-            double b3[3] = {E.ppx[j] - cx, E.ppy[j] - cy, E.ppz[j] - cz};
-            cross3(a3, b3, m);
-            double mn2 = dot3(m, m);
-            if (!(mn2 > 0.0)) {  // |m| < 1e-300 (reference) <=> |m|^2 underflows to 0
-                unstable = true;
-                skip = true;
-                ee = 0.0;
-            } else {
-                double im = rsqrt_nr(mn2);
-                m[0] *= im; m[1] *= im; m[2] *= im;
-                ee = m[0] * (cx - px) + m[1] * (cy - py) + m[2] * (cz - pz);
-            }
+PF_NOINL int conn_circle(const EvalScratch<C> &E, int i, int j, bool arc, double nfx, double nfy,
+                         double nfz, double sf, double cx, double cy, double cz, double px,
+                         double py, double pz, double psi, double *m, double *ee, bool *uns) {
+    if (arc) {
+        m[0] = nfx; m[1] = nfy; m[2] = nfz; *ee = sf;
+        if (psi - sf * sf <= 0.0) { *uns = true; return 0; }
+        return 1;
+    }
+    const double a3[3] = {E.ppx[i] - cx, E.ppy[i] - cy, E.ppz[i] - cz};
+    const double b3[3] = {E.ppx[j] - cx, E.ppy[j] - cy, E.ppz[j] - cz};
+    cross3(a3, b3, m);
+    const double mn2 = dot3(m, m);
+    if (!(mn2 > 0.0)) { *uns = true; return 0; }  // |m| < 1e-300 (reference) <=> |m|^2 underflows to 0
+    const double im = rsqrt_nr(mn2);
+    m[0] *= im; m[1] *= im; m[2] *= im;
+    double e = m[0] * (cx - px) + m[1] * (cy - py) + m[2] * (cz - pz);
+    *ee = e;
+    if (psi - e * e <= 0.0) { *uns = true; return 0; }
+    if (mn2 <= 1e-6 * dot3(a3, a3) * dot3(b3, b3)) {
+        const double q[3] = {px + e * m[0], py + e * m[1], pz + e * m[2]};
+        const double rp[3] = {E.prx[i] - q[0], E.pry[i] - q[1], E.prz[i] - q[2]};
+        const double rq[3] = {E.prx[j] - q[0], E.pry[j] - q[1], E.prz[j] - q[2]};
+        double h[3];
+        project_from(cx, cy, cz, 0.5 * (E.ppx[i] + E.ppx[j]), 0.5 * (E.ppy[i] + E.ppy[j]),
+                     0.5 * (E.ppz[i] + E.ppz[j]), px, py, pz, psi, h);
+        const double rm[3] = {h[0] - q[0], h[1] - q[1], h[2] - q[2]};
+        if (!ccw_le(rp, rm, rq, m)) {
+            // traversal is clockwise around m: flip the circle normal, retry once
+            m[0] = -m[0]; m[1] = -m[1]; m[2] = -m[2]; *ee = -e;
+            if (!ccw_le(rp, rm, rq, m)) return 0;
         }
-        if (!skip) {
-            #pragma unroll 1
-            for (int attempt = 0; attempt < 2; attempt++) {
-                const double q[3] = {px + ee * m[0], py + ee * m[1], pz + ee * m[2]};
-                if (psi - ee * ee <= 0.0) { unstable = true; break; }
-                const double rp[3] = {pri[0] - q[0], pri[1] - q[1], pri[2] - q[2]};
-                const double rq[3] = {prj[0] - q[0], prj[1] - q[1], prj[2] - q[2]};
+    }
+    return 1;
+}
+
+// _kernels.py:838-1001, lane per boundary point.  Gauss-Bonnet:
+// area = psi (2 pi - sum_arcs (e/R) sweep - sum_vertices theta).  Lane q owns
+// the connector q -> succ(q) (its sweep, a CCW angle about the connector
+// circle's axis from one atan2 of (cross, dot)) and the turning angle at q
+// (from the end tangent of pred(q) -> q and the start tangent of its own
+// connector).  Per facet: E.fpa = the clamped patch area, E.funs = unstable.
+template <class W>
+PF_NOINL void ring_patches(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                           double psi, double R, double tol, double cx, double cy, double cz) {
+    using C = typename W::Cap;
+    EvalScratch<C> &E = ws->u.e;
+    const int L = pfw::lane();
+    const double iR = ddiv(1.0, R);
+    const int npool = E.npool;
+    // central projections of the boundary points from c (_kernels.py:880-898)
+    #pragma unroll 1
+    for (int q = L; q < npool; q += 32) {
+        if (ring_facet(E, q, true) < 0) continue;
+        if (E.pfl[q] & PF_ONSPH) { E.prx[q] = E.ppx[q]; E.pry[q] = E.ppy[q]; E.prz[q] = E.ppz[q]; }
+        else {
+            double o[3];
+            project_from(cx, cy, cz, E.ppx[q], E.ppy[q], E.ppz[q], px, py, pz, psi, o);
+            E.prx[q] = o[0]; E.pry[q] = o[1]; E.prz[q] = o[2];
+        }
+    }
+    #pragma unroll 1
+    for (int f = L; f < P.nf; f += 32) { E.fpa[f] = 0.0; E.funs[f] = 0; }
+    pfw::sync();
+    #pragma unroll 1
+    for (int q0 = 0; q0 < npool; q0 += 32) {
+        const int q = q0 + L;
+        const int f = ring_facet(E, q, true);
+        double term = 0.0, unst = 0.0;
+        if (f >= 0) {
+            const int head = E.fhead[f], np = E.fnp[f];
+            const int j = q + 1 < head + np ? q + 1 : head;
+            const int pq = q > head ? q - 1 : head + np - 1;
+            const double nfx = P.nx[f], nfy = P.ny[f], nfz = P.nz[f], sf = E.fh[f];
+            const double prq[3] = {E.prx[q], E.pry[q], E.prz[q]};
+            bool uns = false;
+            double m[3], ee;
+            double tout[3] = {0.0, 0.0, 0.0}, tin[3] = {0.0, 0.0, 0.0};
+            const bool arc = (E.pfl[q] & PF_CONN) != 0;
+            if (conn_circle(E, q, j, arc, nfx, nfy, nfz, sf, cx, cy, cz, px, py, pz, psi, m, &ee, &uns)) {
+                const double qc[3] = {px + ee * m[0], py + ee * m[1], pz + ee * m[2]};
+                const double rp[3] = {prq[0] - qc[0], prq[1] - qc[1], prq[2] - qc[2]};
+                const double rq[3] = {E.prx[j] - qc[0], E.pry[j] - qc[1], E.prz[j] - qc[2]};
                 double dPQ = ccw_angle(rp, rq, m);
                 if (arc && dPQ > PF_PI) {
                     const double d0 = rp[0] - rq[0], d1 = rp[1] - rq[1], d2 = rp[2] - rq[2];
                     if (d0 * d0 + d1 * d1 + d2 * d2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
-                        long_arc_impossible(P, f, q[0], q[1], q[2], rp[0], rp[1], rp[2],
+                        long_arc_impossible(P, f, qc[0], qc[1], qc[2], rp[0], rp[1], rp[2],
                                             dsqrt(psi - ee * ee), tol))
                         dPQ -= 2.0 * PF_PI;
                 }
-                if (!arc) {
-                    double h[3];
-                    project_from(cx, cy, cz, 0.5 * (E.ppx[i] + E.ppx[j]), 0.5 * (E.ppy[i] + E.ppy[j]),
-                                 0.5 * (E.ppz[i] + E.ppz[j]), px, py, pz, psi, h);
-                    const double rm[3] = {h[0] - q[0], h[1] - q[1], h[2] - q[2]};
-                    if (!ccw_le(rp, rm, rq, m)) {
-                        // traversal is clockwise around m: flip the circle normal
-                        m[0] = -m[0]; m[1] = -m[1]; m[2] = -m[2]; ee = -ee;
-                        continue;
-                    }
-                }
-                kg_sum = fma(ee * iR, dPQ, kg_sum);
+                term = ee * iR * dPQ;
                 cross3(m, rp, tout);
                 unit3(tout);
-                cross3(m, rq, tin_j);
-                unit3(tin_j);
-                break;
             }
-        }
-        if (t == 0) {
-            tout0[0] = tout[0]; tout0[1] = tout[1]; tout0[2] = tout[2];
-        } else {
-            // turning angle at point i: tin from connector i-1, tout from connector i
+            const bool parc = (E.pfl[pq] & PF_CONN) != 0;
+            if (conn_circle(E, pq, q, parc, nfx, nfy, nfz, sf, cx, cy, cz, px, py, pz, psi, m, &ee, &uns)) {
+                const double rq[3] = {prq[0] - (px + ee * m[0]), prq[1] - (py + ee * m[1]),
+                                      prq[2] - (pz + ee * m[2])};
+                cross3(m, rq, tin);
+                unit3(tin);
+            }
+            // turning angle at q
             double cr[3];
-            cross3(tin_i, tout, cr);
-            const double nv[3] = {(pri[0] - px) * iR, (pri[1] - py) * iR, (pri[2] - pz) * iR};
-            double th = atan2_ool(dot3(cr, nv), dot3(tin_i, tout));
-            if (fabs(th) > PF_PI - 1e-7) unstable = true;
-            th_sum += th;
+            cross3(tin, tout, cr);
+            const double nv[3] = {(prq[0] - px) * iR, (prq[1] - py) * iR, (prq[2] - pz) * iR};
+            const double th = atan2_ool(dot3(cr, nv), dot3(tin, tout));
+            if (fabs(th) > PF_PI - 1e-7) uns = true;
+            term += th;
+            unst = uns ? 1.0 : 0.0;
         }
-        tin_i[0] = tin_j[0]; tin_i[1] = tin_j[1]; tin_i[2] = tin_j[2];
-        pri[0] = prj[0]; pri[1] = prj[1]; pri[2] = prj[2];
-        i = j;
+        const int rs = seg_first(f);
+        const bool last = seg_last(f);
+        term = pfw::seg_sum_d(term, rs);
+        unst = pfw::seg_sum_d(unst, rs);
+        if (f >= 0 && last) { E.fpa[f] += term; if (unst > 0.0) E.funs[f] = 1; }
+        pfw::sync();
     }
-    {
-        double cr[3];
-        cross3(tin_i, tout0, cr);
-        const double nv[3] = {(pr0[0] - px) * iR, (pr0[1] - py) * iR, (pr0[2] - pz) * iR};
-        double th = atan2_ool(dot3(cr, nv), dot3(tin_i, tout0));
-        if (fabs(th) > PF_PI - 1e-7) unstable = true;
-        th_sum += th;
+    #pragma unroll 1
+    for (int f = L; f < P.nf; f += 32) {
+        const int k = E.fkind[f];
+        if (!((k == RF_GENPOLY || k == RF_UNTOUCHED) && E.farea[f] > 0.0)) continue;
+        double area = psi * (2.0 * PF_PI - E.fpa[f]);
+        if (area < -1e-9 * PF_FOUR_PI * psi || area > PF_FOUR_PI * psi * (1.0 + 1e-9)) E.funs[f] = 1;
+        if (area < 0.0) area = 0.0;
+        if (area > PF_FOUR_PI * psi) area = PF_FOUR_PI * psi;
+        E.fpa[f] = area;
     }
-    double area = psi * (2.0 * PF_PI - kg_sum - th_sum);
-    if (area < -1e-9 * PF_FOUR_PI * psi || area > PF_FOUR_PI * psi * (1.0 + 1e-9)) unstable = true;
-    if (area < 0.0) area = 0.0;
-    if (area > PF_FOUR_PI * psi) area = PF_FOUR_PI * psi;
-    *unstable_out = unstable;
-    return area;
+    pfw::sync();
 }
 
 // result of one cell evaluation (uniform across the warp)
@@ -1233,9 +1357,10 @@ struct CellRes {
 
 // _kernels.py:1008-1170.  Returns with res filled in every lane.  On pool
 // overflow sets ws->oflow (fast instantiation) and returns.
-template <class C>
-PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, double pz,
+template <class W>
+PF_NOINL void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                           double psi, double tol, int want_m2, CellRes *res) {
+    using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
     const int L = pfw::lane();
     const int nf = P.nf;
@@ -1252,7 +1377,6 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         E.vin[v] = q <= ball_tol ? 1 : 0;
         E.vdeg[v] = 0;
     }
-    if (L == 0) E.npool = 0;
     // loop-entry facet and successor vertex, for the twin-facet table
     #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
@@ -1271,60 +1395,51 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         if (slot < 4) E.vinc[a * 4 + slot] = (uint16_t)k;
     }
     pfw::sync();
-    // restrict + integrate, lane per facet (_kernels.py:1027-1071)
-    bool ovf = false, pool_ovf = false;
-    #pragma unroll 1
-    for (int f = L; f < nf; f += 32) {
-        double s, rc;
-        int head, npts;
-        int kind = restrict_facet(ws, P, f, px, py, pz, psi, tol, &s, &rc, &head, &npts);
-        if (kind == -1) { ovf = true; kind = RF_OUTSIDE; }
-        if (kind == -2) { pool_ovf = true; kind = RF_OUTSIDE; }
-        E.fkind[f] = (uint8_t)kind; E.fh[f] = s; E.frc[f] = rc; E.fhead[f] = (int16_t)head;
-        E.fnp[f] = (int16_t)npts;
-        if (kind == RF_OUTSIDE) {
-            E.farea[f] = 0.0; E.fcx[f] = px; E.fcy[f] = py; E.fcz[f] = pz; E.fip[f] = 0.0;
-            continue;
-        }
-        double qx = px + s * P.nx[f], qy = py + s * P.ny[f], qz = pz + s * P.nz[f];
-        if (kind == RF_FULLCIRCLE) {
-            E.farea[f] = PF_PI * rc * rc;
-            E.fcx[f] = qx; E.fcy[f] = qy; E.fcz[f] = qz;
-            double rc2 = rc * rc;
-            E.fip[f] = 0.5 * PF_PI * (rc2 * rc2);
-        } else {
-            double o[5];
-            seq_integrals(ws, P, f, tol, head, npts, P.nx[f], P.ny[f], P.nz[f], qx, qy, qz, rc, o);
-            if (o[0] <= 0.0) {
-                E.fkind[f] = RF_OUTSIDE;
-                E.farea[f] = 0.0; E.fcx[f] = px; E.fcy[f] = py; E.fcz[f] = pz; E.fip[f] = 0.0;
-                continue;
-            }
-            E.farea[f] = o[0]; E.fcx[f] = o[1]; E.fcy[f] = o[2]; E.fcz[f] = o[3]; E.fip[f] = o[4];
-        }
-    }
-    if (pfw::any(pool_ovf)) {
+    // restrict + integrate (_kernels.py:1027-1071)
+    const int rst = restrict_all(ws, P, px, py, pz, psi, R, tol);
+    if (rst == 2) {
         if (L == 0) ws->oflow = 1;
         pfw::sync();
         res->flags = FLAG_RETRY;
         return;
     }
+    if (rst == 1) {  // reference: first facet with kind < 0 aborts the cell
+        res->flags = FLAG_OVERFLOW;
+        return;
+    }
+    ring_integrals(ws, P, px, py, pz, tol);
+    #pragma unroll 1
+    for (int f = L; f < nf; f += 32) {
+        const int kind = E.fkind[f];
+        const double s = E.fh[f];
+        const double qx = px + s * P.nx[f], qy = py + s * P.ny[f], qz = pz + s * P.nz[f];
+        if (kind == RF_FULLCIRCLE) {
+            const double rc = E.frc[f], rc2 = rc * rc;
+            E.farea[f] = PF_PI * rc2;
+            E.fcx[f] = qx; E.fcy[f] = qy; E.fcz[f] = qz;
+            E.fip[f] = 0.5 * PF_PI * (rc2 * rc2);
+        } else if (kind != RF_OUTSIDE && E.farea[f] > 0.0) {
+            const double ia = ddiv(1.0, E.farea[f]);
+            const double u = E.fcx[f] * ia, v = E.fcy[f] * ia;
+            E.fcx[f] = qx + u * E.fe[0][f] + v * E.fe[3][f];
+            E.fcy[f] = qy + u * E.fe[1][f] + v * E.fe[4][f];
+            E.fcz[f] = qz + u * E.fe[2][f] + v * E.fe[5][f];
+        } else {
+            E.fkind[f] = RF_OUTSIDE;
+            E.farea[f] = 0.0; E.fcx[f] = px; E.fcy[f] = py; E.fcz[f] = pz; E.fip[f] = 0.0;
+        }
+    }
+    pfw::sync();
     if (ws->cen_on) {
         int cross = 0, seg = 0, arc = 0, bp = 0, proj = 0, fc = 0;
         #pragma unroll 1
-        for (int f = L; f < nf; f += 32) {
-            int k = E.fkind[f];
-            if (k == RF_FULLCIRCLE) fc++;
-            if ((k == RF_GENPOLY || k == RF_UNTOUCHED) && E.fnp[f] > 0) {
-                int i = E.fhead[f];
-                #pragma unroll 1
-                for (int t = 0; t < E.fnp[f]; t++) {
-                    bp++;
-                    if (E.pfl[i] & PF_ONSPH) cross++; else proj++;
-                    if (E.pfl[i] & PF_CONN) arc++; else seg++;
-                    i = E.pnext[i];
-                }
-            }
+        for (int f = L; f < nf; f += 32) fc += E.fkind[f] == RF_FULLCIRCLE;
+        #pragma unroll 1
+        for (int q = L; q < E.npool; q += 32) {
+            if (ring_facet(E, q, false) < 0) continue;
+            bp++;
+            if (E.pfl[q] & PF_ONSPH) cross++; else proj++;
+            if (E.pfl[q] & PF_CONN) arc++; else seg++;
         }
         cross = pfw::sum_i(cross); seg = pfw::sum_i(seg); arc = pfw::sum_i(arc);
         bp = pfw::sum_i(bp); proj = pfw::sum_i(proj); fc = pfw::sum_i(fc);
@@ -1333,12 +1448,8 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
             ws->cen[CEN_ARC] += arc; ws->cen[CEN_BPTS] += bp; ws->cen[CEN_PROJ] += proj;
             ws->cen[CEN_FULLC] += fc;
         }
+        pfw::sync();
     }
-    if (pfw::any(ovf)) {  // reference: first facet with kind < 0 aborts the cell
-        res->flags = FLAG_OVERFLOW;
-        return;
-    }
-    pfw::sync();
     bool any_area = false;
     #pragma unroll 1
     for (int f0 = 0; f0 < nf; f0 += 32) {
@@ -1364,7 +1475,9 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         }
         return;
     }
-    // interior point (_kernels.py:723-816): ray per restricted facet, lane per facet
+    // interior point (_kernels.py:723-816): ray per restricted facet, lane per
+    // facet; the ray midpoints and margins reuse the facet-frame slots
+    double *smx = E.fe[0], *smy = E.fe[1], *smz = E.fe[2], *smg = E.fe[3];
     #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         E.fseg[f] = 0;
@@ -1405,7 +1518,7 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
             if (d2 < mg) mg = d2;
         }
         E.fseg[f] = 1;
-        E.smx[f] = mx; E.smy[f] = my; E.smz[f] = mz; E.smg[f] = mg;
+        smx[f] = mx; smy[f] = my; smz[f] = mz; smg[f] = mg;
     }
     pfw::sync();
     double ix, iy, iz, bx = px, by = py, bz = pz;
@@ -1416,9 +1529,9 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
         #pragma unroll 1
         for (int f = L; f < nf; f += 32) {
             if (!E.fseg[f]) continue;
-            sx += E.smx[f]; sy += E.smy[f]; sz += E.smz[f];
+            sx += smx[f]; sy += smy[f]; sz += smz[f];
             nseg++;
-            if (E.smg[f] > bm) { bm = E.smg[f]; bf = f; }
+            if (smg[f] > bm) { bm = smg[f]; bf = f; }
         }
         sx = pfw::sum_d(sx); sy = pfw::sum_d(sy); sz = pfw::sum_d(sz);
         nseg = pfw::sum_i(nseg);
@@ -1430,7 +1543,7 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
             if (om > bm || (om == bm && of >= 0 && (bf < 0 || of < bf))) { bm = om; bf = of; }
         }
         const double best_margin = bm;
-        if (bf >= 0 && best_margin > -1.0) { bx = E.smx[bf]; by = E.smy[bf]; bz = E.smz[bf]; }
+        if (bf >= 0 && best_margin > -1.0) { bx = smx[bf]; by = smy[bf]; bz = smz[bf]; }
         bool ok = nseg > 0;
         if (ok) {
             double inv = ddiv(1.0, (double)nseg);
@@ -1457,22 +1570,15 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
     double kbar = 0.0;
     #pragma unroll 1
     for (int attempt = 0; attempt < 4; attempt++) {
-        #pragma unroll 1
-        for (int f = L; f < nf; f += 32) {
-            E.funs[f] = 0;
-            if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0 || E.fkind[f] == RF_FULLCIRCLE) continue;
-            bool uns;
-            E.fpa[f] = patch_area(ws, P, f, tol, E.fhead[f], E.fnp[f], P.nx[f], P.ny[f], P.nz[f], E.fh[f],
-                                  px, py, pz, psi, ix, iy, iz, &uns);
-            E.funs[f] = uns ? 1 : 0;
-        }
-        pfw::sync();
+        ring_patches(ws, P, px, py, pz, psi, R, tol, ix, iy, iz);
         // first unstable facet in facet order (the reference stops there)
         int first_bad = nf;
         #pragma unroll 1
         for (int f0 = 0; f0 < nf; f0 += 32) {
             int f = f0 + L;
-            unsigned mb = pfw::ballot(f < nf && E.funs[f] && !(E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0));
+            unsigned mb = pfw::ballot(f < nf && E.funs[f] &&
+                                      !(E.fkind[f] == RF_OUTSIDE || E.fkind[f] == RF_FULLCIRCLE ||
+                                        E.farea[f] <= 0.0));
             if (mb && first_bad == nf) first_bad = f0 + __builtin_ctz_pf(mb);
         }
         const bool bad = first_bad < nf;
@@ -1526,6 +1632,7 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
     res->ix = ix; res->iy = iy; res->iz = iz; res->m2 = m2;
 }
 
+
 // ---------------------------------------------------------------------------
 // one cell end to end (_kernels.py:1374-1474).  Returns the cell's flags;
 // FLAG_RETRY means nothing was written and the cell must be re-run on the
@@ -1534,8 +1641,8 @@ PF_NOINL void evaluate_cell(WS<C> *ws, const Poly<C> &P, double px, double py, d
 // Phase A of one cell: build.  Returns -1 when the cell needs evaluation
 // (polytope in ws->P[*which]), else the cell's final flag word with its
 // outputs already written (empty / overflow), or FLAG_RETRY.
-template <class C>
-PF_DEV int cell_phase_build(WS<C> *ws, const CellIn &in, const CellOut &out, int i, int *which) {
+template <class W>
+PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, int *which) {
     const int L = pfw::lane();
     if (L == 0) {
         ws->oflow = 0;
@@ -1548,7 +1655,7 @@ PF_DEV int cell_phase_build(WS<C> *ws, const CellIn &in, const CellOut &out, int
     int st = build_cell(ws, in, i, which, &nclips);
     if (ws->oflow) {
         pfw::sync();
-        if (!C::EXACT) return FLAG_RETRY;
+        if (!W::Cap::EXACT) return FLAG_RETRY;
         st = 3;
     }
     if (out.census && L == 0) out.census[i] = nclips;
@@ -1580,16 +1687,16 @@ PF_DEV int cell_phase_build(WS<C> *ws, const CellIn &in, const CellOut &out, int
 }
 
 // Phase B: evaluate the polytope in ws->P[which] and write the outputs.
-template <class C>
-PF_DEV int cell_phase_eval(WS<C> *ws, const CellIn &in, const CellOut &out, int i, int which) {
+template <class W>
+PF_DEV int cell_phase_eval(W *ws, const CellIn &in, const CellOut &out, int i, int which) {
     const int L = pfw::lane();
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
-    const Poly<C> &P = ws->P[which];
+    const Poly<typename W::Cap> &P = ws->P[which];
     CellRes r;
     evaluate_cell(ws, P, px, py, pz, in.psi[i], in.tol, in.want_m2, &r);
     if (ws->oflow) {
         pfw::sync();
-        if (!C::EXACT) return FLAG_RETRY;
+        if (!W::Cap::EXACT) return FLAG_RETRY;
         // beyond even the reference-capacity pool: report as overflow
         r.flags = FLAG_OVERFLOW;
         r.status = CELL_EMPTY; r.vol = 0.0; r.K = 0.0;
@@ -1607,7 +1714,7 @@ PF_DEV int cell_phase_eval(WS<C> *ws, const CellIn &in, const CellOut &out, int 
     // restricted facet summaries in facet order, zero-area facets dropped (_kernels.py:1456-1474)
     int nk = 0;
     if (r.status == CELL_CLIPPED) {
-        const EvalScratch<C> &E = ws->u.e;
+        const EvalScratch<typename W::Cap> &E = ws->u.e;
         const unsigned lt = pfw::lanemask_lt();
         const int smf = out.smf;
         #pragma unroll 1
@@ -1640,8 +1747,8 @@ PF_DEV int cell_phase_eval(WS<C> *ws, const CellIn &in, const CellOut &out, int 
     return flags;
 }
 
-template <class C>
-PF_DEV int run_cell_impl(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+template <class W>
+PF_DEV int run_cell_impl(W *ws, const CellIn &in, const CellOut &out, int i) {
     int which = 0;
     int r = cell_phase_build(ws, in, out, i, &which);
     if (r >= 0) return r;
@@ -1683,8 +1790,8 @@ PF_DEV void poly_load(const Poly<C> *g, Poly<C> &A) {
 }
 
 // per-cell epilogue shared by the fused and the split kernels
-template <class C>
-PF_DEV void cell_finish(WS<C> *ws, const CellOut &out, int i, int r) {
+template <class W>
+PF_DEV void cell_finish(W *ws, const CellOut &out, int i, int r) {
     if (!(r & FLAG_RETRY) && pfw::lane() == 0) {
         if (out.census16)
 #pragma unroll 1
@@ -1694,8 +1801,8 @@ PF_DEV void cell_finish(WS<C> *ws, const CellOut &out, int i, int r) {
     pfw::sync();
 }
 
-template <class C>
-PF_DEV int run_cell(WS<C> *ws, const CellIn &in, const CellOut &out, int i) {
+template <class W>
+PF_DEV int run_cell(W *ws, const CellIn &in, const CellOut &out, int i) {
     int r = run_cell_impl(ws, in, out, i);
     cell_finish(ws, out, i, r);
     return r;

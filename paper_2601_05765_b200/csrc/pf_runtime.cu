@@ -97,7 +97,7 @@ struct pf_ctx {
     int split = 1;  // split build/evaluate kernels (PF_FUSED=1 selects the fused kernel)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool ev_valid = false;
-    int fast_blocks = 0;
+    int fast_blocks = 0, build_blocks = 0, eval_blocks = 0;
     bool attr_set = false;
 };
 
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     int fl = 0;
     for (int t = blockIdx.x * FAST_WARPS + wid; t < count; t += nw) {
         const int i = in.cells ? in.cells[t] : in.g.sid[t];
-        int r = run_cell<FastCaps>(ws, in, out, i);
+        int r = run_cell(ws, in, out, i);
         if (r & FLAG_RETRY) {
             if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
         } else {
@@ -289,13 +289,13 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
                   unsigned long long *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WS<FastCaps> *ws = (WS<FastCaps> *)(smem + (size_t)wid * sizeof(WS<FastCaps>));
+    BWS<FastCaps> *ws = (BWS<FastCaps> *)(smem + (size_t)wid * sizeof(BWS<FastCaps>));
     const int nw = gridDim.x * FAST_WARPS;
     int fl = 0;
     for (int t = blockIdx.x * FAST_WARPS + wid; t < count; t += nw) {
         const int i = in.cells ? in.cells[t] : in.g.sid[t];
         int which = 0;
-        int r = cell_phase_build<FastCaps>(ws, in, out, i, &which);
+        int r = cell_phase_build(ws, in, out, i, &which);
         if (r < 0) {
             poly_store(ws->P[which], gpoly + i);
             if (lane == 0) {
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
                  unsigned long long *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WS<FastCaps> *ws = (WS<FastCaps> *)(smem + (size_t)wid * sizeof(WS<FastCaps>));
+    EWS<FastCaps> *ws = (EWS<FastCaps> *)(smem + (size_t)wid * sizeof(EWS<FastCaps>));
     const int nw = gridDim.x * FAST_WARPS;
     int fl = 0;
     for (int t = blockIdx.x * FAST_WARPS + wid; t < count; t += nw) {
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
             for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
         }
         __syncwarp();
-        int r = cell_phase_eval<FastCaps>(ws, in, out, i, 0);
+        int r = cell_phase_eval(ws, in, out, i, 0);
         if (r & FLAG_RETRY) {
             if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
         } else {
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(EXACT_WARPS * 32)
     const int nw = gridDim.x * EXACT_WARPS;
     int fl = 0;
     for (int t = blockIdx.x * EXACT_WARPS + wid; t < count; t += nw) {
-        int r = run_cell<ExactCaps>(ws, in, out, list[t]);
+        int r = run_cell(ws, in, out, list[t]);
         fl |= r & 7;
     }
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
@@ -426,17 +426,24 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        for (const void *kf : {(const void *)k_cells_build, (const void *)k_cells_eval}) {
-            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
+        CK(cudaFuncSetAttribute(k_cells_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(FAST_WARPS * sizeof(BWS<FastCaps>))));
+        CK(cudaFuncSetAttribute(k_cells_eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(FAST_WARPS * sizeof(EWS<FastCaps>))));
+        for (const void *kf : {(const void *)k_cells_build, (const void *)k_cells_eval})
             CK(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        }
         c->split = getenv("PF_FUSED") ? 0 : 1;
-        int nb = 0;
+        int nb = 0, nbb = 0, nbe = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cells_fast, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(WS<FastCaps>)));
-        if (nb < 1) return set_err("fast cell kernel cannot be resident");
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, k_cells_build, FAST_WARPS * 32,
+                                                         FAST_WARPS * sizeof(BWS<FastCaps>)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbe, k_cells_eval, FAST_WARPS * 32,
+                                                         FAST_WARPS * sizeof(EWS<FastCaps>)));
+        if (nb < 1 || nbb < 1 || nbe < 1) return set_err("fast cell kernels cannot be resident");
         c->fast_blocks = nb * c->nsm;
+        c->build_blocks = nbb * c->nsm;
+        c->eval_blocks = nbe * c->nsm;
         c->exact_warps = c->nsm * EXACT_WARPS;
         CK(cudaMalloc(&c->exact_ws, (size_t)c->exact_warps * sizeof(WS<ExactCaps>)));
         c->attr_set = true;
@@ -445,8 +452,10 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
     CK(cudaMemsetAsync(c->counters, 0, 4 * sizeof(int), st));
     CK(cudaMemsetAsync(c->err, 0, sizeof(unsigned long long), st));
     const int64_t count = in.cells ? in.ncells : n;
-    int64_t blocks = std::min<int64_t>(c->fast_blocks, (count + FAST_WARPS - 1) / FAST_WARPS);
-    if (blocks < 1) blocks = 1;
+    const int64_t want = std::max<int64_t>(1, (count + FAST_WARPS - 1) / FAST_WARPS);
+    const int64_t blocks = std::min<int64_t>(c->fast_blocks, want);
+    const int64_t bblocks = std::min<int64_t>(c->build_blocks, want);
+    const int64_t eblocks = std::min<int64_t>(c->eval_blocks, want);
     if (!c->ev[0]) {
         CK(cudaEventCreate(&c->ev[0]));
         CK(cudaEventCreate(&c->ev[1]));
@@ -456,11 +465,11 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         if (ensure(&c->gpoly, &c->gpoly_cap, (size_t)n) || ensure(&c->stage, &c->stage_cap, (size_t)n))
             return -1;
         g_launches++;
-        k_cells_build<<<(int)blocks, FAST_WARPS * 32, FAST_WARPS * sizeof(WS<FastCaps>), st>>>(
+        k_cells_build<<<(int)bblocks, FAST_WARPS * 32, FAST_WARPS * sizeof(BWS<FastCaps>), st>>>(
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
         CK(cudaGetLastError());
         g_launches++;
-        k_cells_eval<<<(int)blocks, FAST_WARPS * 32, FAST_WARPS * sizeof(WS<FastCaps>), st>>>(
+        k_cells_eval<<<(int)eblocks, FAST_WARPS * 32, FAST_WARPS * sizeof(EWS<FastCaps>), st>>>(
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
         CK(cudaGetLastError());
     } else {

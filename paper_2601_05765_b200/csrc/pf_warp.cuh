@@ -33,6 +33,7 @@ PF_DEV int atom_add_u8(uint8_t *p) {
     return (old >> sh) & 0xff;
 }
 PF_DEV unsigned lanemask_lt() { return (1u << lane()) - 1u; }
+PF_DEV int msb(unsigned m) { return 31 - __clz(m); }
 }  // namespace pfw
 PF_DEV int __builtin_ctz_pf(unsigned m) { return __ffs(m) - 1; }
 #else
@@ -63,6 +64,15 @@ PF_DEV int max_i(int v) {
     for (int m = 16; m > 0; m >>= 1) {
         int o = shfl_xor(v, m);
         v = o > v ? o : v;
+    }
+    return v;
+}
+// inclusive sum over lanes [first, lane] (first = start of this lane's run of
+// a segmented reduction); fixed shuffle tree, so the result is deterministic
+PF_NOINL double seg_sum_d(double v, int first) {
+    for (int o = 1; o < 32; o <<= 1) {
+        double y = shfl(v, (lane() - o) & 31);
+        if (lane() - o >= first) v += y;
     }
     return v;
 }

@@ -139,7 +139,7 @@ struct Job {
 template <class C>
 void lane_fn(void *ctx, int lane) {
     Job<C> *j = (Job<C> *)ctx;
-    int r = pf::run_cell<C>(j->ws, *j->in, *j->out, j->cell);
+    int r = pf::run_cell(j->ws, *j->in, *j->out, j->cell);
     if (lane == 0) j->result = r;
 }
 

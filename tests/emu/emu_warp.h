@@ -93,6 +93,7 @@ static inline int atom_add(int *p, int v) {
     return o;
 }
 static inline unsigned lanemask_lt() { return (1u << g_lane) - 1u; }
+static inline int msb(unsigned m) { return 31 - __builtin_clz(m); }
 static inline int atom_add_u8(uint8_t *p) { return (*p)++; }
 
 // run fn(ctx, lane) on 32 fibers to completion; returns 0 or an error code

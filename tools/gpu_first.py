@@ -62,4 +62,4 @@ s1m = scenes.c1_random(n=1_000_000)
 compare("C1 1M cold", s1m.pts, s1m.psi_cold(), oracle=True)
 s4 = scenes.c4_droplet()
 h4 = s4.meta["h"]
-compare("C4 2M (0.85h)^2", s4.pts, np.full(s4.n, (0.85 * h4) ** 2), oracle=False)
+compare("C4 2M (0.85h)^2", s4.pts, np.full(s4.n, (0.85 * h4) ** 2), oracle=True)
