@@ -10,7 +10,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpotflow_b200.so")
+# PF_LIB_PATH: load a variant build (development experiments only)
+LIB_PATH = os.environ.get("PF_LIB_PATH") or os.path.join(_HERE, "libpotflow_b200.so")
 
 _lib = None
 _lock = threading.Lock()

@@ -78,16 +78,23 @@ struct BuildScratch {
     double sd[C::CV];          // signed distances, reused for new-facet angles
     uint16_t vmap[C::CV];      // kept index / referenced map
     uint16_t onl[C::CV];       // new-facet vertex list (B indices, increasing)
-    uint16_t fk[C::CF];        // emitted loop length per facet
-    uint16_t fcb[C::CF];       // crossing-entry base per facet
+    int fk[C::CF];             // emitted loop length per facet
+    uint16_t fscan0[C::CF];    // emitted-entry scan value at the facet's first entry
     uint16_t flb[C::CF];       // output loop base per facet (0xffff = dropped)
     uint16_t fout[C::CF];      // output facet index
     uint16_t ea[C::CE], eb[C::CE], eid[C::CE];  // crossing entries (walk order)
     uint16_t emt[C::CE];       // first-occurrence entry of the same edge
     uint8_t ecls[C::CL];       // per loop entry of A: bit0 tail inside, bit1 crossing edge
+    uint16_t epos[C::CL];      // per loop entry of A: emitted entries before it (all facets)
+    uint16_t cpos[C::CL];      // per loop entry of A: its crossing entry's walk-order index
+    uint8_t lf[2][C::CL];      // facet of each loop entry, per polytope buffer
+    double csd[C::CC];         // sqrt(d^2) of the sorted candidates
     double sy[C::CV];          // new-facet vertex ordinates (abscissae in sd)
-    double cd2[C::CC];         // candidates (d^2, j)
+    uint8_t half[C::CV];       // their half-plane (angle order, see ang_lt)
+    double cd2[C::CC];         // candidates (d^2, j), sorted
     int cj[C::CC];
+    uint16_t cord[C::CC];      // sorted rank -> gather slot of the candidate data below
+    double cx[C::CC], cy[C::CC], cz[C::CC], cw[C::CC];  // position and weight, by gather slot
     int ncand;
     int run_start[32], run_off[32];
 };
@@ -258,10 +265,12 @@ PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
 // clip A by n.x <= dd into B (_kernels.py:109-319), warp-cooperative
 // ---------------------------------------------------------------------------
 template <class W>
-PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B, double nx, double ny, double nz,
-                double dd, int tag, double tol) {
+PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B, int wa, double nx,
+                  double ny, double nz, double dd, int tag, double tol) {
     using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
+    const uint8_t *lfa = S.lf[wa];
+    uint8_t *lfb = S.lf[1 - wa];
     const int L = pfw::lane();
     const unsigned lt = pfw::lanemask_lt();
     const int nv = A.nv, nf = A.nf;
@@ -301,66 +310,66 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
         K += pfw::popc(m);
     }
 
-    // 3a. per facet: emitted loop length and crossing-edge count (_kernels.py:160-228)
+    // 3a. lane per loop entry (edge a -> b of facet f): classification,
+    // crossing entries in walk order (= entry order) and the facet's emitted
+    // loop length (_kernels.py:160-228); one scan of both counts
+    const int nl = A.nl;
     #pragma unroll 1
-    for (int f = L; f < nf; f += 32) {
-        int start = A.lp[f], m = A.lp[f + 1] - start;
-        int k = 0, c = 0;
-        #pragma unroll 1
-        for (int e = 0; e < m; e++) {
-            int a = A.lv[start + e];
-            int b = A.lv[start + (e + 1 == m ? 0 : e + 1)];
-            double sa = S.sd[a], sb = S.sd[b];
-            bool ina = sa <= tol, inb = sb <= tol;
-            bool cr = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
-            k += ina;
-            c += cr;
-            S.ecls[start + e] = (uint8_t)((ina ? 1 : 0) | (cr ? 2 : 0));
+    for (int f = L; f < nf; f += 32) S.fk[f] = 0;
+    pfw::sync();
+    int NE = 0, NEm = 0;
+    #pragma unroll 1
+    for (int k0 = 0; k0 < nl; k0 += 32) {
+        const int k = k0 + L;
+        int cr = 0, em = 0, f = 0, a = 0, b = 0;
+        if (k < nl) {
+            f = lfa[k];
+            const int kn = k + 1 == A.lp[f + 1] ? A.lp[f] : k + 1;
+            a = A.lv[k];
+            b = A.lv[kn];
+            const double sa = S.sd[a], sb = S.sd[b];
+            const bool ina = sa <= tol, inb = sb <= tol;
+            const bool c = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
+            S.ecls[k] = (uint8_t)((ina ? 1 : 0) | (c ? 2 : 0));
+            cr = c ? 1 : 0;
+            em = (ina ? 1 : 0) + cr;
         }
-        S.fk[f] = (uint16_t)(k + c);
-        S.fcb[f] = (uint16_t)c;
+        int tot;
+        const int pk = pfw::excl_scan_i((em << 16) | cr, &tot);
+        if (k < nl) {
+            const int pcr = NE + (pk & 0xffff), pem = NEm + (pk >> 16);
+            if (cr && pcr < C::CE) { S.ea[pcr] = (uint16_t)a; S.eb[pcr] = (uint16_t)b; }
+            S.epos[k] = (uint16_t)pem;
+            S.cpos[k] = (uint16_t)pcr;
+            if (k == A.lp[f]) S.fscan0[f] = (uint16_t)pem;
+            if (em) pfw::atom_add(&S.fk[f], em);
+        }
+        NE += tot & 0xffff;
+        NEm += tot >> 16;
     }
     pfw::sync();
-    // 3b. prefix sums in facet order: crossing bases, kept-facet loop bases
-    int NE = 0, NFk = 0, NLk = 0;
+    // 3b. prefix sums in facet order: kept-facet indices and loop bases
+    int NFk = 0, NLk = 0;
     bool small_facet = false;  // a dropped facet that still emitted 1-2 entries
     #pragma unroll 1
     for (int f0 = 0; f0 < nf; f0 += 32) {
         int f = f0 + L;
-        int c = 0, kk = 0, keep = 0;
+        int kk = 0, keep = 0;
         if (f < nf) {
-            c = S.fcb[f];
             kk = S.fk[f];
             keep = kk >= 3;
         }
         small_facet |= pfw::any(kk >= 1 && kk <= 2);
-        int tc, tk, tl;
-        int oc = pfw::excl_scan_i(c, &tc);
-        int ok = pfw::excl_scan_i(keep, &tk);
-        int ol = pfw::excl_scan_i(keep ? kk : 0, &tl);
+        int tot;
+        const int pk = pfw::excl_scan_i((keep << 16) | (keep ? kk : 0), &tot);
         if (f < nf) {
-            S.fcb[f] = (uint16_t)(NE + oc);
-            S.fout[f] = (uint16_t)(NFk + ok);
-            S.flb[f] = keep ? (uint16_t)(NLk + ol) : (uint16_t)0xffff;
+            S.fout[f] = (uint16_t)(NFk + (pk >> 16));
+            S.flb[f] = keep ? (uint16_t)(NLk + (pk & 0xffff)) : (uint16_t)0xffff;
         }
-        NE += tc; NFk += tk; NLk += tl;
+        NFk += tot >> 16;
+        NLk += tot & 0xffff;
     }
     if (NE > C::CE) { if (L == 0) ws->oflow = 1; pfw::sync(); return CLIP_OVERFLOW; }
-    pfw::sync();
-    // 3c. crossing entries in walk order
-    #pragma unroll 1
-    for (int f = L; f < nf; f += 32) {
-        int start = A.lp[f], m = A.lp[f + 1] - start;
-        int pos = S.fcb[f];
-        #pragma unroll 1
-        for (int e = 0; e < m; e++) {
-            if (S.ecls[start + e] & 2) {
-                S.ea[pos] = A.lv[start + e];
-                S.eb[pos] = A.lv[start + (e + 1 == m ? 0 : e + 1)];
-                pos++;
-            }
-        }
-    }
     pfw::sync();
     // 3d. first encounter of each edge creates the crossing vertex (_kernels.py:178-200)
     int NFirst = 0;
@@ -369,15 +378,22 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
         int q = q0 + L;
         bool first = false;
         int mt = q;
-        if (q < NE) {
-            int a = S.ea[q], b = S.eb[q];
-            int lo = a < b ? a : b, hi = a < b ? b : a;
+        int a = 0, b = 0;
+        if (q < NE) { a = S.ea[q]; b = S.eb[q]; }
+        const int lo = a < b ? a : b, hi = a < b ? b : a;
+        if (NE <= 32) {
+            // one chunk: the entries of the same edge are the lanes with the same key
+            const unsigned mm = pfw::match_any(q < NE ? (lo << 16) | hi : -1 - L);
+            mt = __builtin_ctz_pf(mm);
+        } else if (q < NE) {
             #pragma unroll 1
             for (int r = 0; r < q; r++) {
                 int ra = S.ea[r], rb = S.eb[r];
                 int rlo = ra < rb ? ra : rb, rhi = ra < rb ? rb : ra;
                 if (rlo == lo && rhi == hi) { mt = r; break; }
             }
+        }
+        if (q < NE) {
             first = mt == q;
             S.emt[q] = (uint16_t)mt;
         }
@@ -386,7 +402,6 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
             int id = K + NFirst + pfw::popc(m & lt);
             S.eid[q] = (uint16_t)id;
             if (id < C::CV) {
-                int a = S.ea[q], b = S.eb[q];
                 double sa = S.sd[a], sb = S.sd[b];
                 double t = sa / (sa - sb);
                 B.x[id] = A.x[a] + t * (A.x[b] - A.x[a]);
@@ -410,7 +425,19 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
         if (mt != q) S.eid[q] = S.eid[mt];
     }
     pfw::sync();
-    // 3e. emit kept facets (_kernels.py:229-241)
+    // 3e. emit kept facets (_kernels.py:229-241): lane per loop entry, then
+    // lane per facet for the planes
+    #pragma unroll 1
+    for (int k = L; k < nl; k += 32) {
+        const int f = lfa[k];
+        const int lb = S.flb[f];
+        if (lb == 0xffff) continue;
+        const int o = S.fout[f];
+        const int cl = S.ecls[k];
+        int w = lb + S.epos[k] - S.fscan0[f];
+        if (cl & 1) { B.lv[w] = S.vmap[A.lv[k]]; lfb[w] = (uint8_t)o; w++; }
+        if (cl & 2) { B.lv[w] = S.eid[S.cpos[k]]; lfb[w] = (uint8_t)o; }
+    }
     #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
         int lb = S.flb[f];
@@ -420,14 +447,6 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
         B.tag[o] = A.tag[f];
         B.lp[o] = (uint16_t)lb;
         B.lp[o + 1] = (uint16_t)(lb + S.fk[f]);
-        int start = A.lp[f], m = A.lp[f + 1] - start;
-        int pos = S.fcb[f], w = lb;
-        #pragma unroll 1
-        for (int e = 0; e < m; e++) {
-            const int cl = S.ecls[start + e];
-            if (cl & 1) B.lv[w++] = S.vmap[A.lv[start + e]];
-            if (cl & 2) B.lv[w++] = S.eid[pos++];
-        }
     }
     // 4. new facet (_kernels.py:243-295).  on_new = kept on-plane vertices
     // (sa >= -tol when emitted, i.e. every kept vertex with sd >= -tol) and
@@ -465,27 +484,51 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
     for (int q = L; q < ncp; q += 32) {
         int v = S.onl[q];
         double rx = B.x[v] - ccx, ry = B.y[v] - ccy, rz = B.z[v] - ccz;
-        S.sy[q] = rx * e[3] + ry * e[4] + rz * e[5];
-        S.sd[q] = rx * e[0] + ry * e[1] + rz * e[2];
+        const double yq = rx * e[3] + ry * e[4] + rz * e[5];
+        const double xq = rx * e[0] + ry * e[1] + rz * e[2];
+        S.sy[q] = yq;
+        S.sd[q] = xq;
+        S.half[q] = (uint8_t)half_of(xq, yq);
     }
     pfw::sync();
     // rank sort by (atan2 angle, index) -- the reference's insertion sort is
     // stable on that total order (_kernels.py:269-283); the angle order is
-    // decided by half-plane and orientation instead of evaluating atan2
-    #pragma unroll 1
-    for (int q = L; q < ncp; q += 32) {
-        const double xq = S.sd[q], yq = S.sy[q];
-        const int vq = S.onl[q];
-        int r = 0;
+    // decided by half-plane and orientation instead of evaluating atan2.
+    // Lanes take (u, q) pairs: q = lane mod W, W the smallest power of two
+    // >= ncp (new facets are small: 32 / W comparisons per pass).
+    {
+        const int Wd = ncp <= 8 ? 8 : (ncp <= 16 ? 16 : 32);
+        const int step = 32 / Wd;
         #pragma unroll 1
-        for (int u = 0; u < ncp; u++) {
-            const double xu = S.sd[u], yu = S.sy[u];
-            const int vu = S.onl[u];
-            const bool lt = ang_lt(xu, yu, xq, yq);
-            const bool eq = !lt && !ang_lt(xq, yq, xu, yu);
-            r += (lt || (eq && vu < vq)) ? 1 : 0;
+        for (int q0 = 0; q0 < ncp; q0 += Wd) {
+            const int q = q0 + (L & (Wd - 1));
+            int r = 0;
+            int vq = 0;
+            if (q < ncp) {
+                const double xq = S.sd[q], yq = S.sy[q];
+                const int hq = S.half[q];
+                vq = S.onl[q];
+                #pragma unroll 1
+                for (int u = L / Wd; u < ncp; u += step) {
+                    const double xu = S.sd[u], yu = S.sy[u];
+                    const int hu = S.half[u];
+                    bool lt, eq;
+                    if (hu != hq) { lt = hu < hq; eq = false; }
+                    else {
+                        // ang_lt(u, q) and ang_lt(q, u) from one cross product
+                        // (xq yu - yq xu == -(xu yq - yu xq) exactly)
+                        const double cr = xu * yq - yu * xq;
+                        if (cr != 0.0) { lt = cr > 0.0; eq = false; }
+                        else if (xu * xq + yu * yq >= 0.0) { lt = false; eq = true; }
+                        else { lt = xu > 0.0; eq = !(xu > 0.0) && !(xq > 0.0); }
+                    }
+                    r += (lt || (eq && S.onl[u] < vq)) ? 1 : 0;
+                }
+            }
+            #pragma unroll 1
+            for (int m = Wd; m < 32; m <<= 1) r += pfw::shfl_xor(r, m);
+            if (L < Wd && q < ncp) { B.lv[NLk + r] = (uint16_t)vq; lfb[NLk + r] = (uint8_t)NFk; }
         }
-        B.lv[NLk + r] = (uint16_t)vq;
     }
     if (L == 0) {
         B.nx[NFk] = nx; B.ny[NFk] = ny; B.nz[NFk] = nz; B.d[NFk] = dd;
@@ -614,7 +657,11 @@ PF_NOINL int gather_shell(W *ws, const CellIn &in, int self, double px, double p
                 if (j != self && !(d2 < t_hi)) beyond = true;
                 if (j != self && d2 >= t_lo && d2 < t_hi) {
                     int pos = pfw::atom_add(&S.ncand, 1);
-                    if (pos < C::CC) { S.cd2[pos] = d2; S.cj[pos] = j; }
+                    if (pos < C::CC) {
+                        S.cd2[pos] = d2; S.cj[pos] = j;
+                        S.cx[pos] = g.sx[s]; S.cy[pos] = g.sy[s]; S.cz[pos] = g.sz[s];
+                        S.cw[pos] = in.psi ? in.psi[j] : 0.0;
+                    }
                 }
             }
         }
@@ -655,7 +702,7 @@ PF_NOINL void sort_candidates(W *ws, int nc) {
     pfw::sync();
 #pragma unroll
     for (int t = 0; t < PER; t++) {
-        if (kr[t] >= 0) { S.cd2[kr[t]] = kd[t]; S.cj[kr[t]] = kj[t]; }
+        if (kr[t] >= 0) { S.cd2[kr[t]] = kd[t]; S.cj[kr[t]] = kj[t]; S.cord[kr[t]] = (uint16_t)(t * 32 + L); }
     }
     pfw::sync();
 }
@@ -671,6 +718,11 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     const double psii = in.psi[i];
     const double tol = in.tol, dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
     load_domain(ws->P[0], in);
+    #pragma unroll 1
+    for (int f = pfw::lane(); f < in.dnf; f += 32)
+        #pragma unroll 1
+        for (int k = in.dlp[f]; k < in.dlp[f + 1]; k++) ws->u.b.lf[0][k] = (uint8_t)f;
+    pfw::sync();
     int which = 0;
     *nclips = 0;
     double rfar = poly_rfar(ws->P[0], px, py, pz);
@@ -701,37 +753,51 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
             continue;
         }
         sort_candidates(ws, nc);
+        BuildScratch<C> &S = ws->u.b;
+        // bisector planes of the shell's candidates, lane per candidate, with
+        // the reference's operations (_kernels.py:1325-1330); a coincident
+        // site keeps its weight for the tie rule (_kernels.py:1320-1324)
+        #pragma unroll 1
+        for (int c = pfw::lane(); c < nc; c += 32) {
+            const double D2 = S.cd2[c];
+            const double D = sqrt(D2);
+            S.csd[c] = D;
+            if (D2 <= tol * tol) continue;
+            const int sl = S.cord[c];
+            const double psij = S.cw[sl];
+            const double nxp = (S.cx[sl] - px) / D;
+            const double nyp = (S.cy[sl] - py) / D;
+            const double nzp = (S.cz[sl] - pz) / D;
+            const double hij = 0.5 * (D2 + psii - psij) / D;
+            S.cx[sl] = nxp; S.cy[sl] = nyp; S.cz[sl] = nzp;
+            S.cw[sl] = (nxp * px + nyp * py + nzp * pz) + hij;
+        }
+        pfw::sync();
+        double stop_r = rfar + sqrt(rfar * rfar + dpsi);
+        if (in.ball_aware && br < stop_r) stop_r = br;
         #pragma unroll 1
         for (int c = 0; c < nc; c++) {
-            double stop_r = rfar + sqrt(rfar * rfar + dpsi);
-            if (in.ball_aware && br < stop_r) stop_r = br;
-            const double D2 = ws->u.b.cd2[c];
-            const int j = ws->u.b.cj[c];
-            if (sqrt(D2) >= stop_r) { *which_out = which; return 0; }
-            const double pjx = in.pts[3 * j], pjy = in.pts[3 * j + 1], pjz = in.pts[3 * j + 2];
-            const double psij = in.psi[j];
-            if (D2 <= tol * tol) {
+            if (S.csd[c] >= stop_r) { *which_out = which; return 0; }
+            const int j = S.cj[c];
+            const int sl = S.cord[c];
+            if (S.cd2[c] <= tol * tol) {
+                const double psij = S.cw[sl];
                 if (psij > psii || (psij == psii && j < i)) { *which_out = which; return 1; }
                 continue;
             }
             (*nclips)++;
-            const double D = sqrt(D2);
-            const double nxp = (pjx - px) / D;
-            const double nyp = (pjy - py) / D;
-            const double nzp = (pjz - pz) / D;
-            const double hij = 0.5 * (D2 + psii - psij) / D;
-            const double dd = (nxp * px + nyp * py + nzp * pz) + hij;
-            int st = clip(ws, ws->P[which], ws->P[1 - which], nxp, nyp, nzp, dd, j, tol);
+            int st = clip(ws, ws->P[which], ws->P[1 - which], which, S.cx[sl], S.cy[sl], S.cz[sl], S.cw[sl],
+                          j, tol);
             if (st == CLIP_EMPTY) { *which_out = which; return 1; }
             if (st == CLIP_OVERFLOW) { *which_out = which; return 3; }
             if (st == CLIP_CUT) {
                 which = 1 - which;
                 rfar = poly_rfar(ws->P[which], px, py, pz);
+                stop_r = rfar + sqrt(rfar * rfar + dpsi);
+                if (in.ball_aware && br < stop_r) stop_r = br;
             }
         }
         if (all_sites) break;
-        double stop_r = rfar + sqrt(rfar * rfar + dpsi);
-        if (in.ball_aware && br < stop_r) stop_r = br;
         if (sqrt(t_hi) >= stop_r) break;
         t_lo = t_hi;
         t_hi = t_hi * 4.0;

@@ -283,7 +283,10 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
 // cell and stalls on instruction fetch; building in one kernel and
 // evaluating in another halves the hot code each SM cycles through.  The
 // finished polytope travels through global memory (Poly<FastCaps>, ~3 KB).
-__global__ void __launch_bounds__(FAST_WARPS * 32, 4)
+#ifndef PF_BUILD_MINB
+#define PF_BUILD_MINB 4
+#endif
+__global__ void __launch_bounds__(FAST_WARPS * 32, PF_BUILD_MINB)
     k_cells_build(CellIn in, CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
                   uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
                   unsigned long long *__restrict__ err) {

@@ -12,6 +12,6 @@
 
 namespace pf {
 //                 CV   CF   CL   CC    CE    CP   EXACT
-using FastCaps = Caps<64, 32, 192, 96, 64, 120, false>;
+using FastCaps = Caps<64, 32, 192, 64, 64, 120, false>;
 using ExactCaps = Caps<REF_MAX_V, REF_MAX_F, REF_MAX_L, 1024, REF_MAX_L, 4096, true>;
 }  // namespace pf

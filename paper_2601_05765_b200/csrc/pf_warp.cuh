@@ -34,6 +34,7 @@ PF_DEV int atom_add_u8(uint8_t *p) {
 }
 PF_DEV unsigned lanemask_lt() { return (1u << lane()) - 1u; }
 PF_DEV int msb(unsigned m) { return 31 - __clz(m); }
+PF_DEV unsigned match_any(int key) { return __match_any_sync(PF_FULL, key); }
 }  // namespace pfw
 PF_DEV int __builtin_ctz_pf(unsigned m) { return __ffs(m) - 1; }
 #else

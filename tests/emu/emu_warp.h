@@ -94,6 +94,13 @@ static inline int atom_add(int *p, int v) {
 }
 static inline unsigned lanemask_lt() { return (1u << g_lane) - 1u; }
 static inline int msb(unsigned m) { return 31 - __builtin_clz(m); }
+static inline unsigned match_any(int key) {
+    long e = (long)deposit_and_wait(K_SHFL, (uint64_t)(int64_t)key);
+    unsigned m = 0;
+    for (int l = 0; l < 32; l++)
+        if ((int)(int64_t)g_w->slot[e & 1][l] == key) m |= 1u << l;
+    return m;
+}
 static inline int atom_add_u8(uint8_t *p) { return (*p)++; }
 
 // run fn(ctx, lane) on 32 fibers to completion; returns 0 or an error code
