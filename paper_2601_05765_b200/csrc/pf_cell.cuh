@@ -1421,11 +1421,22 @@ struct CellRes {
     int flags;
 };
 
-// _kernels.py:1008-1170.  Returns with res filled in every lane.  On pool
-// overflow sets ws->oflow (fast instantiation) and returns.
+// Evaluation state of one cell between the phases below (uniform across the
+// warp).  The phases are separate functions so that a kernel can run them
+// block-synchronously: all warps of a block then execute the same phase and
+// share its instructions (the whole evaluation does not fit the instruction
+// cache; warps in different phases thrash it).
+struct EvalState {
+    double R, kbar;
+    double ix, iy, iz, bx, by, bz;
+    int done;     // res is final
+    int attempt;  // next projection attempt (4: finished)
+};
+
+// _kernels.py:1008-1026: defaults, vertex-in-ball flags, twin-facet table
 template <class W>
-PF_NOINL void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
-                          double psi, double tol, int want_m2, CellRes *res) {
+PF_NOINL void eval_setup(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                         double psi, double tol, CellRes *res, EvalState *st) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
     const int L = pfw::lane();
@@ -1433,8 +1444,10 @@ PF_NOINL void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, do
     res->flags = 0;
     res->status = CELL_EMPTY; res->vol = 0.0; res->K = 0.0;
     res->cx = px; res->cy = py; res->cz = pz; res->ix = px; res->iy = py; res->iz = pz; res->m2 = 0.0;
-    if (psi <= 0.0) return;
+    st->done = 0; st->attempt = 0; st->kbar = 0.0;
+    if (psi <= 0.0) { st->done = 1; return; }
     const double R = dsqrt(psi);
+    st->R = R;
     const double ball_tol = tol * (2.0 * R + tol);
     #pragma unroll 1
     for (int v = L; v < P.nv; v += 32) {
@@ -1461,18 +1474,32 @@ PF_NOINL void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, do
         if (slot < 4) E.vinc[a * 4 + slot] = (uint16_t)k;
     }
     pfw::sync();
-    // restrict + integrate (_kernels.py:1027-1071)
-    const int rst = restrict_all(ws, P, px, py, pz, psi, R, tol);
+}
+
+// restriction of every facet (_kernels.py:1027-1040)
+template <class W>
+PF_NOINL void eval_restrict(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                            double psi, double tol, CellRes *res, EvalState *st) {
+    const int rst = restrict_all(ws, P, px, py, pz, psi, st->R, tol);
     if (rst == 2) {
-        if (L == 0) ws->oflow = 1;
+        if (pfw::lane() == 0) ws->oflow = 1;
         pfw::sync();
         res->flags = FLAG_RETRY;
-        return;
-    }
-    if (rst == 1) {  // reference: first facet with kind < 0 aborts the cell
+        st->done = 1;
+    } else if (rst == 1) {  // reference: first facet with kind < 0 aborts the cell
         res->flags = FLAG_OVERFLOW;
-        return;
+        st->done = 1;
     }
+}
+
+// facet integrals, full-ball / empty decision (_kernels.py:1041-1092)
+template <class W>
+PF_NOINL void eval_integrals(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                             double psi, double tol, int want_m2, CellRes *res, EvalState *st) {
+    using C = typename W::Cap;
+    EvalScratch<C> &E = ws->u.e;
+    const int L = pfw::lane();
+    const int nf = P.nf;
     ring_integrals(ws, P, px, py, pz, tol);
     #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
@@ -1534,15 +1561,25 @@ PF_NOINL void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, do
             inside &= !pfw::any(f < nf && E.fh[f] < -tol);
         }
         if ((inside && nf > 0) || nf == 0) {
+            const double R = st->R;
             res->status = CELL_FULLBALL;
             res->vol = PF_FOUR_PI / 3.0 * psi * R;
             res->K = PF_FOUR_PI * psi;
             res->m2 = want_m2 ? PF_FOUR_PI * psi * R * R * R / 5.0 : 0.0;
         }
-        return;
+        st->done = 1;
     }
-    // interior point (_kernels.py:723-816): ray per restricted facet, lane per
-    // facet; the ray midpoints and margins reuse the facet-frame slots
+}
+
+// interior point (_kernels.py:723-816): ray per restricted facet, lane per
+// facet; the ray midpoints and margins reuse the facet-frame slots
+template <class W>
+PF_NOINL void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                            double psi, double tol, CellRes *res, EvalState *st) {
+    using C = typename W::Cap;
+    EvalScratch<C> &E = ws->u.e;
+    const int L = pfw::lane();
+    const int nf = P.nf;
     double *smx = E.fe[0], *smy = E.fe[1], *smz = E.fe[2], *smg = E.fe[3];
     #pragma unroll 1
     for (int f = L; f < nf; f += 32) {
@@ -1587,84 +1624,101 @@ PF_NOINL void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, do
         smx[f] = mx; smy[f] = my; smz[f] = mz; smg[f] = mg;
     }
     pfw::sync();
-    double ix, iy, iz, bx = px, by = py, bz = pz;
-    {
-        // average of the ray midpoints and the deepest one (first on ties)
-        double sx = 0.0, sy = 0.0, sz = 0.0, bm = -1.0;
-        int nseg = 0, bf = -1;
-        #pragma unroll 1
-        for (int f = L; f < nf; f += 32) {
-            if (!E.fseg[f]) continue;
-            sx += smx[f]; sy += smy[f]; sz += smz[f];
-            nseg++;
-            if (smg[f] > bm) { bm = smg[f]; bf = f; }
-        }
-        sx = pfw::sum_d(sx); sy = pfw::sum_d(sy); sz = pfw::sum_d(sz);
-        nseg = pfw::sum_i(nseg);
-        // argmax margin, lowest facet index among equal margins
-        #pragma unroll 1
-        for (int m = 16; m > 0; m >>= 1) {
-            double om = pfw::shfl_xor(bm, m);
-            int of = pfw::shfl_xor(bf, m);
-            if (om > bm || (om == bm && of >= 0 && (bf < 0 || of < bf))) { bm = om; bf = of; }
-        }
-        const double best_margin = bm;
-        if (bf >= 0 && best_margin > -1.0) { bx = smx[bf]; by = smy[bf]; bz = smz[bf]; }
-        bool ok = nseg > 0;
-        if (ok) {
-            double inv = ddiv(1.0, (double)nseg);
-            double cx = sx * inv, cy = sy * inv, cz = sz * inv;
-            double mg = dsqrt(psi) - dsqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
-            #pragma unroll 1
-            for (int g = L; g < nf; g += 32) {
-                double d2 = P.d[g] - (P.nx[g] * cx + P.ny[g] * cy + P.nz[g] * cz);
-                if (d2 < mg) mg = d2;
-            }
-            mg = -pfw::max_d(-mg);
-            if (mg <= 0.0) {
-                if (best_margin > 0.0) { cx = bx; cy = by; cz = bz; }
-                else ok = false;
-            }
-            ix = cx; iy = cy; iz = cz;
-        }
-        if (!ok) {
-            res->flags = FLAG_DEGENERATE_INTERIOR;
-            return;
-        }
-    }
-    // occluded areas with perturb-and-retry (_kernels.py:1100-1128)
-    double kbar = 0.0;
+    // average of the ray midpoints and the deepest one (first on ties)
+    double sx = 0.0, sy = 0.0, sz = 0.0, bm = -1.0;
+    int nseg = 0, bf = -1;
     #pragma unroll 1
-    for (int attempt = 0; attempt < 4; attempt++) {
-        ring_patches(ws, P, px, py, pz, psi, R, tol, ix, iy, iz);
-        // first unstable facet in facet order (the reference stops there)
-        int first_bad = nf;
-        #pragma unroll 1
-        for (int f0 = 0; f0 < nf; f0 += 32) {
-            int f = f0 + L;
-            unsigned mb = pfw::ballot(f < nf && E.funs[f] &&
-                                      !(E.fkind[f] == RF_OUTSIDE || E.fkind[f] == RF_FULLCIRCLE ||
-                                        E.farea[f] <= 0.0));
-            if (mb && first_bad == nf) first_bad = f0 + __builtin_ctz_pf(mb);
-        }
-        const bool bad = first_bad < nf;
-        double kb = 0.0;
-        #pragma unroll 1
-        for (int f = L; f < first_bad; f += 32) {
-            if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
-            if (E.fkind[f] == RF_FULLCIRCLE) kb += 2.0 * PF_PI * R * (R - E.fh[f]);
-            else kb += E.fpa[f];
-        }
-        kbar = pfw::sum_d(kb);
-        pfw::sync();
-        if (!bad) break;
-        if (attempt == 3) { res->flags |= FLAG_UNSTABLE_PROJECTION; break; }
-        double w = 0.35 * (double)(attempt + 1);
-        ix = ix + w * (bx - ix);
-        iy = iy + w * (by - iy);
-        iz = iz + w * (bz - iz);
+    for (int f = L; f < nf; f += 32) {
+        if (!E.fseg[f]) continue;
+        sx += smx[f]; sy += smy[f]; sz += smz[f];
+        nseg++;
+        if (smg[f] > bm) { bm = smg[f]; bf = f; }
     }
-    double K = PF_FOUR_PI * psi - kbar;
+    sx = pfw::sum_d(sx); sy = pfw::sum_d(sy); sz = pfw::sum_d(sz);
+    nseg = pfw::sum_i(nseg);
+    // argmax margin, lowest facet index among equal margins
+    #pragma unroll 1
+    for (int m = 16; m > 0; m >>= 1) {
+        double om = pfw::shfl_xor(bm, m);
+        int of = pfw::shfl_xor(bf, m);
+        if (om > bm || (om == bm && of >= 0 && (bf < 0 || of < bf))) { bm = om; bf = of; }
+    }
+    const double best_margin = bm;
+    st->bx = px; st->by = py; st->bz = pz;
+    if (bf >= 0 && best_margin > -1.0) { st->bx = smx[bf]; st->by = smy[bf]; st->bz = smz[bf]; }
+    bool ok = nseg > 0;
+    if (ok) {
+        double inv = ddiv(1.0, (double)nseg);
+        double cx = sx * inv, cy = sy * inv, cz = sz * inv;
+        double mg = dsqrt(psi) - dsqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
+        #pragma unroll 1
+        for (int g = L; g < nf; g += 32) {
+            double d2 = P.d[g] - (P.nx[g] * cx + P.ny[g] * cy + P.nz[g] * cz);
+            if (d2 < mg) mg = d2;
+        }
+        mg = -pfw::max_d(-mg);
+        if (mg <= 0.0) {
+            if (best_margin > 0.0) { cx = st->bx; cy = st->by; cz = st->bz; }
+            else ok = false;
+        }
+        st->ix = cx; st->iy = cy; st->iz = cz;
+    }
+    if (!ok) {
+        res->flags = FLAG_DEGENERATE_INTERIOR;
+        st->done = 1;
+    }
+}
+
+// one attempt of the occluded areas with perturb-and-retry (_kernels.py:1100-1128)
+template <class W>
+PF_NOINL void eval_patch_attempt(W *ws, const Poly<typename W::Cap> &P, double px, double py,
+                                 double pz, double psi, double tol, CellRes *res, EvalState *st) {
+    using C = typename W::Cap;
+    EvalScratch<C> &E = ws->u.e;
+    const int L = pfw::lane();
+    const int nf = P.nf;
+    const double R = st->R;
+    ring_patches(ws, P, px, py, pz, psi, R, tol, st->ix, st->iy, st->iz);
+    // first unstable facet in facet order (the reference stops there)
+    int first_bad = nf;
+    #pragma unroll 1
+    for (int f0 = 0; f0 < nf; f0 += 32) {
+        int f = f0 + L;
+        unsigned mb = pfw::ballot(f < nf && E.funs[f] &&
+                                  !(E.fkind[f] == RF_OUTSIDE || E.fkind[f] == RF_FULLCIRCLE ||
+                                    E.farea[f] <= 0.0));
+        if (mb && first_bad == nf) first_bad = f0 + __builtin_ctz_pf(mb);
+    }
+    const bool bad = first_bad < nf;
+    double kb = 0.0;
+    #pragma unroll 1
+    for (int f = L; f < first_bad; f += 32) {
+        if (E.fkind[f] == RF_OUTSIDE || E.farea[f] <= 0.0) continue;
+        if (E.fkind[f] == RF_FULLCIRCLE) kb += 2.0 * PF_PI * R * (R - E.fh[f]);
+        else kb += E.fpa[f];
+    }
+    st->kbar = pfw::sum_d(kb);
+    pfw::sync();
+    const int attempt = st->attempt;
+    if (!bad) { st->attempt = 4; return; }
+    if (attempt == 3) { res->flags |= FLAG_UNSTABLE_PROJECTION; st->attempt = 4; return; }
+    double w = 0.35 * (double)(attempt + 1);
+    st->ix = st->ix + w * (st->bx - st->ix);
+    st->iy = st->iy + w * (st->by - st->iy);
+    st->iz = st->iz + w * (st->bz - st->iz);
+    st->attempt = attempt + 1;
+}
+
+// K, volume, centroid, second moment (_kernels.py:1130-1170)
+template <class W>
+PF_NOINL void eval_final(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                         double psi, int want_m2, CellRes *res, EvalState *st) {
+    using C = typename W::Cap;
+    EvalScratch<C> &E = ws->u.e;
+    const int L = pfw::lane();
+    const int nf = P.nf;
+    const double R = st->R;
+    double K = PF_FOUR_PI * psi - st->kbar;
     if (K < 0.0) K = 0.0;
     if (K > PF_FOUR_PI * psi) K = PF_FOUR_PI * psi;
     double vol = 0.0;
@@ -1695,9 +1749,24 @@ PF_NOINL void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, do
     else { vol = 0.0; ccx = px; ccy = py; ccz = pz; }
     res->status = CELL_CLIPPED;
     res->vol = vol; res->K = K; res->cx = ccx; res->cy = ccy; res->cz = ccz;
-    res->ix = ix; res->iy = iy; res->iz = iz; res->m2 = m2;
+    res->ix = st->ix; res->iy = st->iy; res->iz = st->iz; res->m2 = m2;
+    st->done = 1;
 }
 
+// _kernels.py:1008-1170, all phases in sequence.  Returns with res filled in
+// every lane.  On pool overflow sets ws->oflow (fast instantiation).
+template <class W>
+PF_DEV void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+                          double psi, double tol, int want_m2, CellRes *res) {
+    EvalState st;
+    eval_setup(ws, P, px, py, pz, psi, tol, res, &st);
+    if (!st.done) eval_restrict(ws, P, px, py, pz, psi, tol, res, &st);
+    if (!st.done) eval_integrals(ws, P, px, py, pz, psi, tol, want_m2, res, &st);
+    if (!st.done) eval_interior(ws, P, px, py, pz, psi, tol, res, &st);
+    #pragma unroll 1
+    while (!st.done && st.attempt < 4) eval_patch_attempt(ws, P, px, py, pz, psi, tol, res, &st);
+    if (!st.done) eval_final(ws, P, px, py, pz, psi, want_m2, res, &st);
+}
 
 // ---------------------------------------------------------------------------
 // one cell end to end (_kernels.py:1374-1474).  Returns the cell's flags;
@@ -1754,12 +1823,20 @@ PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, 
 
 // Phase B: evaluate the polytope in ws->P[which] and write the outputs.
 template <class W>
+PF_NOINL int eval_write(W *ws, const CellIn &in, const CellOut &out, int i, int which, CellRes r);
+template <class W>
 PF_DEV int cell_phase_eval(W *ws, const CellIn &in, const CellOut &out, int i, int which) {
+    const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
+    CellRes r;
+    evaluate_cell(ws, ws->P[which], px, py, pz, in.psi[i], in.tol, in.want_m2, &r);
+    return eval_write(ws, in, out, i, which, r);
+}
+// write one evaluated cell's outputs (_kernels.py:1441-1474); returns its flags
+template <class W>
+PF_NOINL int eval_write(W *ws, const CellIn &in, const CellOut &out, int i, int which, CellRes r) {
     const int L = pfw::lane();
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const Poly<typename W::Cap> &P = ws->P[which];
-    CellRes r;
-    evaluate_cell(ws, P, px, py, pz, in.psi[i], in.tol, in.want_m2, &r);
     if (ws->oflow) {
         pfw::sync();
         if (!W::Cap::EXACT) return FLAG_RETRY;

@@ -97,7 +97,7 @@ struct pf_ctx {
     int split = 1;  // split build/evaluate kernels (PF_FUSED=1 selects the fused kernel)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool ev_valid = false;
-    int fast_blocks = 0, build_blocks = 0, eval_blocks = 0;
+    int fast_blocks = 0, build_blocks = 0, eval_blocks = 0, eval_sync = 1;
     bool attr_set = false;
 };
 
@@ -351,6 +351,72 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
+// Block-synchronous evaluation: one block of SYNC_WARPS warps per SM, one
+// cell per warp per round; the warps run each phase of the evaluation
+// together (__syncthreads between phases), so the SM's instruction caches
+// hold one phase at a time instead of the whole ~90 KB of evaluation code
+// (measured: the unsynchronised kernel spends half its stall samples on
+// instruction fetch).
+constexpr int SYNC_WARPS = 16;
+__global__ void __launch_bounds__(SYNC_WARPS * 32, 1)
+    k_cells_eval_sync(CellIn in, CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
+                      const uint8_t *__restrict__ stage, int *__restrict__ retry_list,
+                      int *__restrict__ counters, unsigned long long *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    EWS<FastCaps> *ws = (EWS<FastCaps> *)(smem + (size_t)wid * sizeof(EWS<FastCaps>));
+    int fl = 0;
+    for (int base = blockIdx.x * SYNC_WARPS; base < count; base += gridDim.x * SYNC_WARPS) {
+        const int t = base + wid;
+        int i = -1;
+        if (t < count) {
+            i = in.cells ? in.cells[t] : in.g.sid[t];
+            if (stage[i] != 1) i = -1;
+        }
+        const bool act = i >= 0;
+        double px = 0.0, py = 0.0, pz = 0.0, psi = 0.0;
+        CellRes res;
+        EvalState st;
+        st.done = 1;
+        if (act) {
+            poly_load(gpoly + i, ws->P[0]);
+            if (lane == 0) {
+                ws->oflow = 0;
+                ws->cen_on = out.census16 != nullptr;
+                for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
+            }
+            __syncwarp();
+            px = in.pts[3 * i]; py = in.pts[3 * i + 1]; pz = in.pts[3 * i + 2];
+            psi = in.psi[i];
+            eval_setup(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
+        }
+        __syncthreads();
+        if (!st.done) eval_restrict(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
+        __syncthreads();
+        if (!st.done) eval_integrals(ws, ws->P[0], px, py, pz, psi, in.tol, in.want_m2, &res, &st);
+        __syncthreads();
+        if (!st.done) eval_interior(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
+        for (int a = 0; a < 4; a++) {
+            const bool need = !st.done && st.attempt < 4;
+            if (!__syncthreads_or(need)) break;
+            if (need) eval_patch_attempt(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
+        }
+        __syncthreads();
+        if (!st.done) eval_final(ws, ws->P[0], px, py, pz, psi, in.want_m2, &res, &st);
+        if (act) {
+            const int r = eval_write(ws, in, out, i, 0, res);
+            if (r & FLAG_RETRY) {
+                if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
+            } else {
+                cell_finish(ws, out, i, r);
+                fl |= r & 7;
+            }
+        }
+        __syncthreads();
+    }
+    if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
+}
+
 // cells that overflowed the fast tier, with the reference's capacities
 __global__ void __launch_bounds__(EXACT_WARPS * 32)
     k_cells_exact(CellIn in, CellOut out, const int *__restrict__ list, const int *__restrict__ counters,
@@ -433,6 +499,13 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
                                 (int)(FAST_WARPS * sizeof(BWS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(EWS<FastCaps>))));
+        CK(cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(SYNC_WARPS * sizeof(EWS<FastCaps>))));
+        CK(cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        {
+            const char *e = getenv("PF_EVAL_SYNC");
+            c->eval_sync = !(e && e[0] == '0');
+        }
         for (const void *kf : {(const void *)k_cells_build, (const void *)k_cells_eval})
             CK(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         c->split = getenv("PF_FUSED") ? 0 : 1;
@@ -458,7 +531,9 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
     const int64_t want = std::max<int64_t>(1, (count + FAST_WARPS - 1) / FAST_WARPS);
     const int64_t blocks = std::min<int64_t>(c->fast_blocks, want);
     const int64_t bblocks = std::min<int64_t>(c->build_blocks, want);
-    const int64_t eblocks = std::min<int64_t>(c->eval_blocks, want);
+    int64_t eblocks = std::min<int64_t>(c->eval_blocks, want);
+    if (const char *e = getenv("PF_EVAL_BPSM"))  // development experiment: cap eval blocks per SM
+        eblocks = std::min<int64_t>(eblocks, (int64_t)atoi(e) * c->nsm);
     if (!c->ev[0]) {
         CK(cudaEventCreate(&c->ev[0]));
         CK(cudaEventCreate(&c->ev[1]));
@@ -472,8 +547,14 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
         CK(cudaGetLastError());
         g_launches++;
-        k_cells_eval<<<(int)eblocks, FAST_WARPS * 32, FAST_WARPS * sizeof(EWS<FastCaps>), st>>>(
-            in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
+        if (c->eval_sync) {
+            const int64_t sb = std::min<int64_t>(c->nsm, (count + SYNC_WARPS - 1) / SYNC_WARPS);
+            k_cells_eval_sync<<<(int)sb, SYNC_WARPS * 32, SYNC_WARPS * sizeof(EWS<FastCaps>), st>>>(
+                in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
+        } else {
+            k_cells_eval<<<(int)eblocks, FAST_WARPS * 32, FAST_WARPS * sizeof(EWS<FastCaps>), st>>>(
+                in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
+        }
         CK(cudaGetLastError());
     } else {
         g_launches++;
