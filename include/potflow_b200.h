@@ -155,6 +155,39 @@ int pf_newton_last_state(double *vol, double *ksur, int32_t *fcount, int32_t *ft
 int pf_newton_last_state_ex(double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
                             double *cent, int64_t n, int smf, void *stream);
 
+/* ---- spatially partitioned solve ------------------------
+ * A rank owns the cells of its slab; local arrays hold owned + ghost sites in
+ * global index order and `rows` lists the owned local indices.  Scalars land
+ * in device memory (stats_dev / outN_dev) for the cross-rank all-reduce; the
+ * halo exchange of ghost vector entries is done by the host (dist_solver.py).
+ * Replaces, per rank, the single-device pf_newton_solve pieces above. */
+/* lean evaluation of cells[0:ncells] with the given (global) weight slack */
+int pf_evaluate_lean_cells(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double dpsi,
+                           int ball_aware, int64_t smf, const int32_t *cells, int64_t ncells,
+                           double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
+                           double *cent, int64_t *flags, void *stream);
+/* g = nu - vol on rows; stats_dev[3] = (max rel. error, -min vol, -min nu), MAX-reducible */
+int pf_rows_gradient(int nrows, const int32_t *rows, const double *nu, const double *vol, double *g,
+                     double *stats_dev, void *stream);
+/* Hessian rows (entries as pf_newton_hessian) */
+int pf_rows_hessian(int nrows, const int32_t *rows, int smf, const double *pts, const double *psi,
+                    const int32_t *fcount, const int32_t *ftag, const double *farea, const double *ksur,
+                    double tau_psi, int32_t *hcnt, int32_t *hcol, double *hval, double *diag, void *stream);
+/* Jacobi-PCG pieces: init (out2 = partial r.z, b.b), SpMV (out1 = partial p.Ap),
+ * update with alpha = *rz / *pAp (out2 = partial r.z, r.r), direction p = z + (*rz_new / *rz_old) p */
+int pf_dcg_init(int nrows, const int32_t *rows, const double *b, const double *diag, double *x, double *r,
+                double *z, double *p, double *out2_dev, void *stream);
+int pf_dcg_spmv(int nrows, const int32_t *rows, int smf, const int32_t *hcnt, const int32_t *hcol,
+                const double *hval, const double *diag, const double *p, double *Ap, double *out1_dev,
+                void *stream);
+int pf_dcg_update(int nrows, const int32_t *rows, const double *diag, double *x, double *r, double *z,
+                  const double *p, const double *Ap, const double *rz_dev, const double *pAp_dev,
+                  double *out2_dev, void *stream);
+int pf_dcg_pdir(int nrows, const int32_t *rows, const double *z, double *p, const double *rz_new_dev,
+                const double *rz_old_dev, void *stream);
+/* out = a + s b (n entries) */
+int pf_daxpy(int64_t n, const double *a, double s, const double *b, double *out, void *stream);
+
 /* ---- fluid step --------------------------------------- */
 /* x += dt v, reflected into the box [lo+tau, hi-tau] (velocity component flipped) */
 int pf_fluid_advect(int64_t n, double *x, double *v, double dt, const double *lo_host,

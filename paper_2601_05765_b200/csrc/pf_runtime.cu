@@ -894,6 +894,33 @@ int pf_evaluate_lean(pf_ctx *c, int64_t n, const double *pts, const double *psi,
     return 0;
 }
 
+// lean evaluation of a subset of the cells with a given weight slack dpsi
+// (the partitioned solve: owned cells of a slab, all-reduced dpsi)
+int pf_evaluate_lean_cells(pf_ctx *c, int64_t n, const double *pts, const double *psi, double dpsi,
+                           int ball_aware, int64_t smf, const int32_t *cells, int64_t ncells, double *vol,
+                           double *ksur, int32_t *fcount, int32_t *ftag, double *farea, double *cent,
+                           int64_t *flags, void *stream) {
+    cudaStream_t st = S(stream);
+    if (!c->has_domain) return set_err("pf_evaluate_lean_cells: no domain set");
+    if (!(dpsi >= 0.0)) return set_err("pf_evaluate_lean_cells: dpsi must be >= 0");
+    if (c->grid_n != n || c->grid_pts != pts) {
+        if (grid_build(c, n, pts, psi, 0.0, st)) return -1;
+    }
+    CellIn in;
+    fill_cellin(c, in, n, pts, psi, c->tol, dpsi, ball_aware, 0);
+    in.cells = cells;
+    in.ncells = (int)ncells;
+    CellOut out;
+    memset(&out, 0, sizeof out);
+    out.vol = vol; out.ksur = ksur; out.cent = cent; out.fcount32 = fcount; out.ftag32 = ftag;
+    out.farea = farea; out.smf = (int)smf;
+    if (n > 0 && ncells > 0 && launch_cells(c, in, out, n, st)) return -1;
+    if (flags) {
+        CK(cudaMemcpyAsync(flags, c->err, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
+    return 0;
+}
+
 int pf_last_census(pf_ctx *c, int32_t *census, void *stream) {
     if (!c->census || c->grid_n < 0) return set_err("pf_last_census: nothing evaluated");
     CK(cudaMemcpyAsync(census, c->census, c->grid_n * sizeof(int32_t), cudaMemcpyDeviceToDevice, S(stream)));

@@ -1,0 +1,443 @@
+"""Spatially partitioned damped Newton solve across ranks.
+
+One process per GPU.  Rank r owns the cells of an x-slab and holds as ghosts
+every site within the (slack-widened) ball-aware search radius of its cells
+(`partition.halo_plan`); its local arrays keep the global index order, so its
+cells are bit-identical to the single-GPU ones.  Per Newton iteration
+(the algorithm of `pf_newton_solve`):
+
+* evaluation of the owned cells with the all-reduced weight slack dpsi
+  (`pf_evaluate_lean_cells`), gradient statistics all-reduced (one MAX of
+  three scalars: worst error, -min volume, -min nu);
+* Hessian rows of the owned cells (`pf_rows_hessian`), columns may be ghosts;
+* Jacobi-PCG: per iteration one halo exchange of the search direction
+  (P2P send/recv to the slab neighbours) and two scalar all-reduces
+  (p.Ap, then r.z and r.r together);
+* one halo exchange of the Newton step x, after which every damping trial
+  psi + alpha x is formed locally for owned and ghost sites alike.
+
+The ghost margin is checked before every evaluation (weights grow during a
+solve); when a rank's search radius outgrows it, all ranks re-partition from
+the all-gathered weights.  The device work goes through `CudaOps` (the C ABI
+in pf_dist.cu / pf_runtime.cu); the orchestration is backend-agnostic so the
+CPU tests drive it with a numpy stand-in over gloo.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import partition
+
+STATUS = {0: "converged", 1: "max_newton", 2: "DampingStall", 3: "InitFailure"}
+
+
+# ---------------------------------------------------------------------------
+# communication (torch.distributed; NCCL on GPUs, gloo for CPU tests)
+# ---------------------------------------------------------------------------
+class Comm:
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.on = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.world = dist.get_world_size(group) if self.on else 1
+        self.gloo = self.on and dist.get_backend(group) == "gloo"
+
+    def _staged(self, t):
+        return t.cpu() if (self.gloo and t.is_cuda) else t
+
+    def all_reduce(self, t, op="sum"):
+        """In-place all-reduce of a small tensor (sum or max)."""
+        if not self.on or self.world == 1:
+            return t
+        d = self.dist
+        s = self._staged(t)
+        d.all_reduce(s, op=d.ReduceOp.SUM if op == "sum" else d.ReduceOp.MAX, group=self.group)
+        if s is not t:
+            t.copy_(s)
+        return t
+
+    def exchange(self, vec, plan: partition.HaloPlan, idx_send: dict, idx_recv: dict):
+        """Fill the ghost entries of `vec` (local-length) from their owners."""
+        if not self.on or self.world == 1 or (not plan.send and not plan.recv):
+            return vec
+        import torch
+
+        d = self.dist
+        bufs_s = {q: self._staged(vec.index_select(0, ix)) for q, ix in idx_send.items()}
+        bufs_r = {q: torch.empty(len(ix), dtype=vec.dtype,
+                                 device="cpu" if self.gloo else vec.device) for q, ix in idx_recv.items()}
+        ops = [d.P2POp(d.isend, b, self._peer(q)) for q, b in bufs_s.items()]
+        ops += [d.P2POp(d.irecv, b, self._peer(q)) for q, b in bufs_r.items()]
+        if ops:
+            for r in d.batch_isend_irecv(ops):
+                r.wait()
+        for q, ix in idx_recv.items():
+            vec.index_copy_(0, ix, bufs_r[q].to(vec.device))
+        return vec
+
+    def _peer(self, q):
+        return self.dist.get_global_rank(self.group, q) if self.group is not None else q
+
+    def all_gather_objects(self, obj):
+        if not self.on or self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# device backend (the product path)
+# ---------------------------------------------------------------------------
+def _bind():
+    from . import _lib
+
+    L = _lib.lib()
+    if not getattr(L, "_dist_bound", False):
+        vp, i, i64, d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+        L.pf_evaluate_lean_cells.argtypes = [vp, i64, vp, vp, d, i, i64, vp, i64] + [vp] * 7 + [vp]
+        L.pf_rows_gradient.argtypes = [i, vp, vp, vp, vp, vp, vp]
+        L.pf_rows_hessian.argtypes = [i, vp, i, vp, vp, vp, vp, vp, vp, d, vp, vp, vp, vp, vp]
+        L.pf_dcg_init.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pf_dcg_spmv.argtypes = [i, vp, i, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pf_dcg_update.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pf_dcg_pdir.argtypes = [i, vp, vp, vp, vp, vp, vp]
+        L.pf_daxpy.argtypes = [i64, vp, d, vp, vp, vp]
+        for name in ("pf_evaluate_lean_cells", "pf_rows_gradient", "pf_rows_hessian", "pf_dcg_init",
+                     "pf_dcg_spmv", "pf_dcg_update", "pf_dcg_pdir", "pf_daxpy"):
+            getattr(L, name).restype = i
+        L._dist_bound = True
+    return L
+
+
+class CudaOps:
+    """Per-rank device state of one partition: local sites, owned rows, the
+    evaluation buffers (current + trial), Hessian and CG vectors."""
+
+    def __init__(self, pts_local: np.ndarray, nu_local: np.ndarray, rows: np.ndarray, domain,
+                 smf: int, ball_aware: bool, tau_psi: float):
+        import torch
+
+        from . import _lib
+        from .laguerre import domain_pack, upload_domain
+
+        self.torch = torch
+        self.L = _bind()
+        self._lib = _lib
+        dev = dict(device="cuda")
+        f8, i4 = dict(dtype=torch.float64, **dev), dict(dtype=torch.int32, **dev)
+        self.n = n = len(pts_local)
+        self.smf, self.ball_aware, self.tau = smf, int(ball_aware), float(tau_psi)
+        self.pts = torch.as_tensor(np.ascontiguousarray(pts_local), **f8)
+        self.nu = torch.as_tensor(np.ascontiguousarray(nu_local), **f8)
+        self.rows = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.int32), **i4)
+        self.nrows = len(rows)
+        self.psi = torch.zeros(n, **f8)
+        self.psi_t = torch.zeros(n, **f8)
+        self.slots = [dict(vol=torch.zeros(n, **f8), ksur=torch.zeros(n, **f8),
+                           fcount=torch.zeros(n, **i4), ftag=torch.zeros((n, smf), **i4),
+                           farea=torch.zeros((n, smf), **f8), cent=torch.zeros((n, 3), **f8))
+                      for _ in range(2)]
+        self.v = {k: torch.zeros(n, **f8) for k in ("g", "x", "r", "z", "p", "Ap", "diag")}
+        self.hcnt = torch.zeros(n, **i4)
+        self.hcol = torch.zeros((n, smf), **i4)
+        self.hval = torch.zeros((n, smf), **f8)
+        self.flags = torch.zeros(1, dtype=torch.int64, **dev)
+        self.scal = torch.zeros(16, **f8)
+        dpk = domain_pack(domain)
+        self.ctx = _lib.ctx()
+        upload_domain(self.ctx, *dpk.args(), dpk.tol)
+        _lib.check(_lib.lib().pf_grid_build(self.ctx, n, _lib.ptr(self.pts), None, 0.0, self._s()),
+                   "pf_grid_build")
+
+    def _s(self):
+        return self._lib.stream_ptr()
+
+    def p(self, t):
+        return self._lib.ptr(t)
+
+    def chk(self, rc, what):
+        self._lib.check(rc, what)
+
+    # --- weights ---------------------------------------------------------
+    def set_psi(self, psi_local: np.ndarray):
+        self.psi.copy_(self.torch.as_tensor(psi_local))
+
+    def cold_psi(self, kappa: float):
+        self.psi.copy_(kappa * (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0))
+
+    def psi_host(self, trial=False) -> np.ndarray:
+        return (self.psi_t if trial else self.psi).cpu().numpy()
+
+    def search_radius_max(self, dpsi: float, trial=False) -> float:
+        ps = (self.psi_t if trial else self.psi).index_select(0, self.rows.long()).clamp_min(0.0)
+        if self.nrows == 0:
+            return 0.0
+        return float((ps.sqrt() + (ps + dpsi).sqrt()).max())
+
+    def psi_minmax(self, trial=False):
+        """local (-min, max) of the owned weights as a tensor for a MAX all-reduce"""
+        ps = (self.psi_t if trial else self.psi).index_select(0, self.rows.long())
+        if self.nrows == 0:
+            return self.torch.tensor([-np.inf, -np.inf], dtype=self.torch.float64, device="cuda")
+        return self.torch.stack([-ps.min(), ps.max()])
+
+    def trial(self, alpha: float):
+        self.chk(self.L.pf_daxpy(self.n, self.p(self.psi), float(alpha), self.p(self.v["x"]),
+                                 self.p(self.psi_t), self._s()), "pf_daxpy")
+
+    def accept(self):
+        self.psi.copy_(self.psi_t)
+        self.slots.reverse()
+
+    # --- evaluation and Newton pieces --------------------------------------
+    def evaluate(self, dpsi: float, trial=False):
+        s = self.slots[1 if trial else 0]
+        ps = self.psi_t if trial else self.psi
+        self.chk(self.L.pf_evaluate_lean_cells(
+            self.ctx, self.n, self.p(self.pts), self.p(ps), float(dpsi), self.ball_aware, self.smf,
+            self.p(self.rows), self.nrows, self.p(s["vol"]), self.p(s["ksur"]), self.p(s["fcount"]),
+            self.p(s["ftag"]), self.p(s["farea"]), self.p(s["cent"]), self.p(self.flags), self._s()),
+            "pf_evaluate_lean_cells")
+
+    def grad_stats(self, trial=False):
+        s = self.slots[1 if trial else 0]
+        out = self.scal[8:11]
+        self.chk(self.L.pf_rows_gradient(self.nrows, self.p(self.rows), self.p(self.nu), self.p(s["vol"]),
+                                         self.p(self.v["g"]), self.p(out), self._s()), "pf_rows_gradient")
+        return out.clone()
+
+    def hessian(self):
+        s = self.slots[0]
+        self.chk(self.L.pf_rows_hessian(
+            self.nrows, self.p(self.rows), self.smf, self.p(self.pts), self.p(self.psi), self.p(s["fcount"]),
+            self.p(s["ftag"]), self.p(s["farea"]), self.p(s["ksur"]), self.tau, self.p(self.hcnt),
+            self.p(self.hcol), self.p(self.hval), self.p(self.v["diag"]), self._s()), "pf_rows_hessian")
+
+    def cg_init(self):
+        v = self.v
+        out = self.torch.zeros(2, dtype=self.torch.float64, device="cuda")
+        self.chk(self.L.pf_dcg_init(self.nrows, self.p(self.rows), self.p(v["g"]), self.p(v["diag"]),
+                                    self.p(v["x"]), self.p(v["r"]), self.p(v["z"]), self.p(v["p"]),
+                                    self.p(out), self._s()), "pf_dcg_init")
+        return out
+
+    def cg_spmv(self):
+        v = self.v
+        out = self.torch.zeros(1, dtype=self.torch.float64, device="cuda")
+        self.chk(self.L.pf_dcg_spmv(self.nrows, self.p(self.rows), self.smf, self.p(self.hcnt),
+                                    self.p(self.hcol), self.p(self.hval), self.p(v["diag"]), self.p(v["p"]),
+                                    self.p(v["Ap"]), self.p(out), self._s()), "pf_dcg_spmv")
+        return out
+
+    def cg_update(self, rz, pAp):
+        v = self.v
+        out = self.torch.zeros(2, dtype=self.torch.float64, device="cuda")
+        self.chk(self.L.pf_dcg_update(self.nrows, self.p(self.rows), self.p(v["diag"]), self.p(v["x"]),
+                                      self.p(v["r"]), self.p(v["z"]), self.p(v["p"]), self.p(v["Ap"]),
+                                      self.p(rz), self.p(pAp), self.p(out), self._s()), "pf_dcg_update")
+        return out
+
+    def cg_pdir(self, rz_new, rz_old):
+        v = self.v
+        self.chk(self.L.pf_dcg_pdir(self.nrows, self.p(self.rows), self.p(v["z"]), self.p(v["p"]),
+                                    self.p(rz_new), self.p(rz_old), self._s()), "pf_dcg_pdir")
+
+    def vec(self, name):
+        return self.v[name]
+
+    def index(self, ix: np.ndarray):
+        return self.torch.as_tensor(ix, dtype=self.torch.int64, device="cuda")
+
+    def tensor(self, vals):
+        return self.torch.tensor(vals, dtype=self.torch.float64, device="cuda")
+
+    def scalar(self, t) -> float:
+        return float(t)
+
+    def owned(self, name: str) -> np.ndarray:
+        src = self.psi if name == "psi" else self.v[name]
+        return src.index_select(0, self.rows.long()).cpu().numpy()
+
+    def result(self):
+        s = self.slots[0]
+        r = self.rows.long()
+        return {k: s[k].index_select(0, r) for k in ("vol", "ksur", "fcount", "cent")}
+
+
+# ---------------------------------------------------------------------------
+# the solver
+# ---------------------------------------------------------------------------
+@dataclass
+class DistResult:
+    psi_owned: np.ndarray        # weights of the owned sites (global order)
+    owned_global: np.ndarray     # their global indices
+    stats: dict = field(default_factory=dict)
+
+
+class DistNewton:
+    """Partitioned Newton solve.  `pts` / `nu` are the global arrays (replicated
+    on every rank); ops_factory(pts_local, nu_local, rows) builds the backend."""
+
+    def __init__(self, pts: np.ndarray, nu: np.ndarray, domain, group=None, smf: int = 32,
+                 ball_aware: bool = True, slack: float = 1.5, ops_factory=None, axis_lo=None,
+                 axis_hi=None):
+        self.pts = np.ascontiguousarray(pts, dtype=np.float64)
+        self.nu = np.ascontiguousarray(nu, dtype=np.float64)
+        self.domain = domain
+        self.comm = Comm(group)
+        self.smf, self.ball_aware, self.slack = smf, ball_aware, slack
+        lo, hi = domain.bbox()
+        self.lo = float(lo[0]) if axis_lo is None else axis_lo
+        self.hi = float(hi[0]) if axis_hi is None else axis_hi
+        self.tau = 1e-12 * domain.diagonal() ** 2
+        self.ops_factory = ops_factory or (lambda p, n, r: CudaOps(p, n, r, domain, smf, ball_aware,
+                                                                   self.tau))
+        self.repartitions = 0
+        self.halo_entries = 0
+
+    # --- partition --------------------------------------------------------
+    def _partition(self, psi_global: np.ndarray, dpsi: float):
+        c = self.comm
+        self.slab, self.plan = partition.halo_plan(self.pts, psi_global, dpsi, c.world, c.rank,
+                                                   self.lo, self.hi, self.slack)
+        l2g = self.slab.local_to_global
+        self.ops = self.ops_factory(self.pts[l2g], self.nu[l2g], self.slab.owned_local)
+        self.ops.set_psi(psi_global[l2g])
+        self.idx_send = {q: self.ops.index(ix) for q, ix in self.plan.send.items()}
+        self.idx_recv = {q: self.ops.index(ix) for q, ix in self.plan.recv.items()}
+        self.halo_entries = self.plan.volume()
+
+    def _gather_global(self, local_vals: np.ndarray) -> np.ndarray:
+        """Global array from every rank's owned entries of a local-length array."""
+        own = self.slab.owned_local
+        parts = self.comm.all_gather_objects((self.slab.local_to_global[own], local_vals[own]))
+        out = np.zeros(len(self.pts))
+        for g, v in parts:
+            out[g] = v
+        return out
+
+    def _dpsi(self, trial=False) -> float:
+        t = self.comm.all_reduce(self.ops.psi_minmax(trial), "max")
+        lo, hi = -float(t[0]), float(t[1])
+        return max(hi - lo, 0.0) if np.isfinite(hi) else 0.0
+
+    def _margin_ok(self, dpsi: float, trial=False) -> bool:
+        need = self.ops.search_radius_max(dpsi, trial)
+        bad = self.ops.tensor([1.0 if need > self.slab.ghost_margin else 0.0])
+        return float(self.comm.all_reduce(bad, "max")[0]) == 0.0
+
+    def _evaluate(self, trial=False):
+        """Evaluate the owned cells (current or trial weights); returns the
+        all-reduced (worst, min vol, min nu)."""
+        dpsi = self._dpsi(trial)
+        if not self._margin_ok(dpsi, trial):
+            # weights outgrew the ghost layer: re-partition from the global weights
+            psi_g = self._gather_global(self.ops.psi_host(False))
+            x_g = self._gather_global(self.ops.vec("x").cpu().numpy()) if trial else None
+            self._partition(psi_g, dpsi)
+            self.repartitions += 1
+            if trial:
+                l2g = self.slab.local_to_global
+                self.ops.vec("x").copy_(self.ops.torch.as_tensor(x_g[l2g]))
+                self.ops.trial(self._alpha)
+        self.ops.evaluate(dpsi, trial)
+        st = self.comm.all_reduce(self.ops.grad_stats(trial), "max")
+        st = [float(v) for v in st.cpu()]
+        return st[0], -st[1], -st[2]
+
+    # --- Jacobi-PCG ---------------------------------------------------------
+    def _pcg(self, rtol: float, max_iter: int = 10000) -> int:
+        o, c = self.ops, self.comm
+        t = c.all_reduce(o.cg_init(), "sum")
+        rz, bb = t[0:1].clone(), float(t[1])
+        if not bb > 0.0:
+            return 0
+        it = 0
+        while True:
+            c.exchange(o.vec("p"), self.plan, self.idx_send, self.idx_recv)
+            pAp = c.all_reduce(o.cg_spmv(), "sum")
+            t = c.all_reduce(o.cg_update(rz, pAp), "sum")
+            rz_new, rr = t[0:1].clone(), float(t[1])
+            it += 1
+            if np.sqrt(rr) <= rtol * np.sqrt(bb) or it >= max_iter or not np.isfinite(float(rz_new)):
+                break
+            o.cg_pdir(rz_new, rz)
+            rz = rz_new
+        return it
+
+    # --- Newton (same control flow as pf_newton_solve) -------
+    def solve(self, psi_init: np.ndarray | None = None, eps_vol: float = 0.01,
+              max_newton: int = 100) -> DistResult:
+        S = dict(status=0, iterations=0, evaluations=0, cg_iterations=0, damping_halvings=0,
+                 init_doublings=0, worst_initial=0.0, worst_final=0.0, last_alpha=0.0)
+        cold = psi_init is None
+        psi0 = (np.zeros(len(self.pts)) if cold else np.asarray(psi_init, dtype=np.float64))
+        if cold:
+            psi0 = (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0)
+        lo_, hi_ = float(psi0.min()), float(psi0.max())
+        self._partition(psi0, max(hi_ - lo_, 0.0))
+        self._alpha = 1.0
+        if cold:
+            kappa = 1.0
+            while True:
+                self.ops.cold_psi(kappa)
+                S["evaluations"] += 1
+                worst, vmin, nmin = self._evaluate()
+                if vmin > 0.0:
+                    break
+                kappa *= 2.0
+                S["init_doublings"] += 1
+                if kappa > 1024.0:
+                    S["status"] = 3
+                    return self._result(S)
+        else:
+            S["evaluations"] += 1
+            worst, vmin, nmin = self._evaluate()
+        floor_v = 0.5 * min(nmin, vmin)
+        S["worst_initial"] = worst
+        for _ in range(max_newton):
+            if worst <= eps_vol:
+                break
+            self.ops.hessian()
+            rtol = 1e-4 if worst < 10.0 * eps_vol else 1e-3
+            S["cg_iterations"] += self._pcg(rtol)
+            # the step's ghost entries, then every trial is local
+            self.comm.exchange(self.ops.vec("x"), self.plan, self.idx_send, self.idx_recv)
+            alpha, accepted = 1.0, False
+            while alpha >= 2.0 ** -20:
+                self._alpha = alpha
+                self.ops.trial(alpha)
+                S["evaluations"] += 1
+                w_t, vmin_t, _ = self._evaluate(trial=True)
+                if vmin_t >= floor_v:
+                    accepted = True
+                    break
+                alpha *= 0.5
+                S["damping_halvings"] += 1
+            if not accepted:
+                S["status"] = 2
+                break
+            self.ops.accept()
+            S["iterations"] += 1
+            S["last_alpha"] = alpha
+            worst = w_t
+        S["worst_final"] = worst
+        if S["status"] == 0 and worst > eps_vol:
+            S["status"] = 1
+        return self._result(S)
+
+    def _result(self, S) -> DistResult:
+        S["status_name"] = STATUS.get(S["status"], "?")
+        S["repartitions"] = self.repartitions
+        S["halo_entries"] = self.halo_entries
+        S["world"] = self.comm.world
+        own = self.slab.owned_local
+        return DistResult(psi_owned=self.ops.owned("psi"), owned_global=self.slab.local_to_global[own],
+                          stats=S)

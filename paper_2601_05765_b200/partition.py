@@ -49,17 +49,31 @@ def global_dpsi(psi_local: np.ndarray, group=None) -> float:
     return max(hi - lo, 0.0) if np.isfinite(hi) else 0.0
 
 
+def slab_owner(x: np.ndarray, world: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    """Rank owning each x coordinate (x-slabs of equal width over [lo, hi])."""
+    w = (hi - lo) / world
+    return np.clip(np.floor((np.asarray(x) - lo) / w), 0, world - 1).astype(np.int64)
+
+
+def search_radius(psi: np.ndarray, dpsi: float) -> np.ndarray:
+    """Ball-aware stop radius sqrt(psi) + sqrt(psi + dpsi) (_kernels.py:1239-1248)."""
+    p = np.maximum(np.asarray(psi, dtype=np.float64), 0.0)
+    return np.sqrt(p) + np.sqrt(p + dpsi)
+
+
 def slab_partition(pts: np.ndarray, psi: np.ndarray, dpsi: float, world: int, rank: int,
-                   lo: float = 0.0, hi: float = 1.0) -> Slab:
-    """x-slab r of [lo, hi] with its ghost sites (pts / psi are the global arrays)."""
+                   lo: float = 0.0, hi: float = 1.0, slack: float = 1.0) -> Slab:
+    """x-slab r of [lo, hi] with its ghost sites (pts / psi are the global arrays).
+
+    ``slack`` > 1 widens the ghost margin beyond the current search radius so a
+    Newton solve (whose weights grow) can keep the partition for several
+    iterations; `DistNewton` checks the margin before every evaluation."""
     x = pts[:, 0]
     w = (hi - lo) / world
     a, b = lo + rank * w, lo + (rank + 1) * w
-    own = (x >= a) & (x < b) if rank < world - 1 else (x >= a)
-    if rank == 0:
-        own |= x < lo
-    br = np.sqrt(np.maximum(psi, 0.0)) + np.sqrt(np.maximum(psi, 0.0) + dpsi)
-    margin = float(br[own].max()) * (1.0 + 1e-9) if own.any() else 0.0
+    own = slab_owner(x, world, lo, hi) == rank
+    br = search_radius(psi, dpsi)
+    margin = float(br[own].max()) * (1.0 + 1e-9) * slack if own.any() else 0.0
     keep = own | ((x >= a - margin) & (x <= b + margin))
     idx = np.nonzero(keep)[0].astype(np.int64)
     owned_local = np.nonzero(own[idx])[0].astype(np.int32)
@@ -73,3 +87,37 @@ def to_global(slab: Slab, ftag_local: np.ndarray, fcount: np.ndarray) -> np.ndar
     m = used & (out >= 0)
     out[m] = slab.local_to_global[out[m]]
     return out
+
+
+@dataclass
+class HaloPlan:
+    """Who sends which owned entries to whom.  For every peer q: ``send[q]``
+    are local indices of this rank's owned sites that are ghosts of q, and
+    ``recv[q]`` the local indices of this rank's ghosts owned by q; both are in
+    global index order, so the two sides of a message agree entry by entry."""
+    send: dict
+    recv: dict
+
+    def volume(self) -> int:
+        return int(sum(len(v) for v in self.send.values()))
+
+
+def halo_plan(pts: np.ndarray, psi: np.ndarray, dpsi: float, world: int, rank: int,
+              lo: float = 0.0, hi: float = 1.0, slack: float = 1.0):
+    """(slab of this rank, halo plan).  Every rank derives every other rank's
+    ghost set from the replicated global arrays, so no negotiation is needed."""
+    slabs = [slab_partition(pts, psi, dpsi, world, q, lo, hi, slack) for q in range(world)]
+    me = slabs[rank]
+    owner = slab_owner(pts[:, 0], world, lo, hi)
+    send, recv = {}, {}
+    for q in range(world):
+        if q == rank:
+            continue
+        ghosts_q = slabs[q].local_to_global
+        ghosts_q = ghosts_q[owner[ghosts_q] == rank]           # q's ghosts that I own (sorted)
+        if len(ghosts_q):
+            send[q] = np.searchsorted(me.local_to_global, ghosts_q).astype(np.int64)
+        mine_from_q = me.local_to_global[owner[me.local_to_global] == q]  # my ghosts owned by q
+        if len(mine_from_q):
+            recv[q] = np.searchsorted(me.local_to_global, mine_from_q).astype(np.int64)
+    return me, HaloPlan(send, recv)

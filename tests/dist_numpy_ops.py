@@ -1,0 +1,125 @@
+"""TEST INFRASTRUCTURE ONLY: a numpy stand-in for dist_solver.CudaOps, so the
+partitioned Newton orchestration (halo exchange, all-reduces, re-partition,
+PCG recurrences) can run over gloo on CPU.  Cells are evaluated by the CPU
+oracle; never imported by the product package."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import pyoracle as O
+
+
+class NumpyOps:
+    def __init__(self, pts_local, nu_local, rows, dom_args, tol, smf, tau):
+        self.torch = torch
+        self.pts = np.ascontiguousarray(pts_local, np.float64)
+        self.nu = np.ascontiguousarray(nu_local, np.float64)
+        self.rows = np.asarray(rows, np.int64)
+        self.n = len(self.pts)
+        self.dom_args, self.tol, self.smf, self.tau = dom_args, tol, smf, tau
+        self.grid = O.SpatialGrid(self.pts, [0, 0, 0], [1, 1, 1], 1.0)
+        n = self.n
+        self.psi = np.zeros(n)
+        self.psi_t = np.zeros(n)
+        self.slots = [None, None]
+        # vectors are torch CPU tensors sharing numpy storage (halo exchange works in place)
+        self.v = {k: torch.zeros(n, dtype=torch.float64) for k in ("g", "x", "r", "z", "p", "Ap", "diag")}
+        self.cols = self.vals = None
+
+    def _n(self, k):
+        return self.v[k].numpy()
+
+    # weights
+    def set_psi(self, psi_local):
+        self.psi[:] = psi_local
+
+    def cold_psi(self, kappa):
+        self.psi[:] = kappa * (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0)
+
+    def psi_host(self, trial=False):
+        return (self.psi_t if trial else self.psi).copy()
+
+    def search_radius_max(self, dpsi, trial=False):
+        ps = np.maximum((self.psi_t if trial else self.psi)[self.rows], 0.0)
+        return float((np.sqrt(ps) + np.sqrt(ps + dpsi)).max()) if len(ps) else 0.0
+
+    def psi_minmax(self, trial=False):
+        ps = (self.psi_t if trial else self.psi)[self.rows]
+        return torch.tensor([-ps.min(), ps.max()], dtype=torch.float64)
+
+    def trial(self, alpha):
+        self.psi_t[:] = self.psi + alpha * self._n("x")
+
+    def accept(self):
+        self.psi[:] = self.psi_t
+        self.slots.reverse()
+
+    # evaluation / Newton pieces
+    def evaluate(self, dpsi, trial=False):
+        ps = self.psi_t if trial else self.psi
+        o = O.evaluate(self.pts, ps, self.dom_args, self.tol, self.grid, want_m2=False, smf=self.smf,
+                       dpsi=dpsi, i0=0, i1=len(self.rows), cells=self.rows)
+        self.slots[1 if trial else 0] = o
+
+    def grad_stats(self, trial=False):
+        o = self.slots[1 if trial else 0]
+        r = self.rows
+        v, nu = o["vol"][r], self.nu[r]
+        self._n("g")[r] = nu - v
+        return torch.tensor([np.max(np.abs(v - nu) / nu), -v.min(), -nu.min()], dtype=torch.float64)
+
+    def hessian(self):
+        from oracle.newton_ref import hessian_ell
+
+        o = self.slots[0]
+        cols, vals, diag = hessian_ell(self.pts, self.psi, o, self.tau, self.smf)
+        self.cols, self.vals = cols, vals
+        self._n("diag")[:] = diag
+
+    def cg_init(self):
+        r = self.rows
+        b, d = self._n("g")[r], self._n("diag")[r]
+        z = b / d
+        self._n("x")[:] = 0.0
+        self._n("r")[r] = b
+        self._n("z")[r] = z
+        self._n("p")[r] = z
+        return torch.tensor([float(b @ z), float(b @ b)], dtype=torch.float64)
+
+    def cg_spmv(self):
+        r = self.rows
+        p = self._n("p")
+        c, v = self.cols[r], self.vals[r]
+        ps = np.where(c >= 0, p[np.maximum(c, 0)], 0.0)
+        Ap = self._n("diag")[r] * p[r] + (v * ps).sum(1)
+        self._n("Ap")[r] = Ap
+        return torch.tensor([float(p[r] @ Ap)], dtype=torch.float64)
+
+    def cg_update(self, rz, pAp):
+        r = self.rows
+        alpha = float(rz[0]) / float(pAp[0]) if float(pAp[0]) != 0.0 else 0.0
+        x, rr_, z = self._n("x"), self._n("r"), self._n("z")
+        x[r] += alpha * self._n("p")[r]
+        rr_[r] -= alpha * self._n("Ap")[r]
+        z[r] = rr_[r] / self._n("diag")[r]
+        return torch.tensor([float(rr_[r] @ z[r]), float(rr_[r] @ rr_[r])], dtype=torch.float64)
+
+    def cg_pdir(self, rz_new, rz_old):
+        r = self.rows
+        beta = float(rz_new[0]) / float(rz_old[0]) if float(rz_old[0]) != 0.0 else 0.0
+        p = self._n("p")
+        p[r] = self._n("z")[r] + beta * p[r]
+
+    def vec(self, name):
+        return self.v[name]
+
+    def index(self, ix):
+        return torch.as_tensor(np.asarray(ix, np.int64))
+
+    def tensor(self, vals):
+        return torch.tensor(vals, dtype=torch.float64)
+
+    def owned(self, name):
+        src = self.psi if name == "psi" else self._n(name)
+        return src[self.rows].copy()
