@@ -144,6 +144,49 @@ def converged_psi(sc, dom):
     return res.psi, float(e0.elapsed_time(e1)), res.stats
 
 
+def all_reduce_host(vals, op="sum"):
+    """All-reduce of a few host scalars (through the device for NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    gloo = dist.get_backend() == "gloo"
+    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if gloo else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.cpu()
+
+
+def dist_newton(sc, dom, ws):
+    """Partitioned Newton solve over the ranks (x-slabs, halo exchange per CG
+    iteration, all-reduced dots); device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_05765_b200 import dist_solver
+
+    solver = dist_solver.DistNewton(sc.pts, sc.nu, dom)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = solver.solve()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = all_reduce_host([e0.elapsed_time(e1)], "max")
+    parts = [None] * ws
+    dist.all_gather_object(parts, (res.owned_global, res.psi_owned))
+    psi = np.zeros(sc.n)
+    for g, v in parts:
+        psi[g] = v
+    st = res.stats
+    newton = {"ms_per_solve": float(ms[0]), "iterations": st["iterations"], "evaluations": st["evaluations"],
+              "cg_iterations": st["cg_iterations"], "worst_initial": st["worst_initial"],
+              "worst_final": st["worst_final"], "status": st["status_name"],
+              "start": "cold (kappa (3 nu/4 pi)^(2/3))", "eps_vol": 0.01, "n": sc.n,
+              "partition": f"{ws} x-slabs, halo {st['halo_entries']} entries/rank, "
+                           f"{st['repartitions']} re-partitions"}
+    return torch.as_tensor(psi, device="cuda"), newton
+
+
 def cpu_reference_run(sc, psi, steps, warmup, sample_cells, threads):
     """CPU oracle port of _kernels._batch_evaluate on the host cores."""
     from oracle import pyoracle as O
@@ -207,8 +250,13 @@ def main():
     from paper_2601_05765_b200 import _kernels, _lib, geom, laguerre, restricted
 
     if ws > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # PF_DIST_BACKEND=gloo runs several ranks on one device (testing only)
+        backend = os.environ.get("PF_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.cuda.current_device()
     sc = make_scene(a.config)
     dom = geom.box_domain([0, 0, 0], [1, 1, 1])
@@ -221,6 +269,8 @@ def main():
     newton = None
     if a.no_newton:
         psi_g = torch.as_tensor(sc.psi_cold(), device="cuda")
+    elif ws > 1:
+        psi_g, newton = dist_newton(sc, dom, ws)
     else:
         psi_g, newton_ms, nst = converged_psi(sc, dom)
         newton = {"ms_per_solve": newton_ms, "iterations": nst["iterations"],
@@ -286,18 +336,16 @@ def main():
             import ctypes
 
             ms = ctypes.c_double(0.0)
-            _lib.check(L.pf_last_cells_ms(c, ctypes.byref(ms)), "pf_last_cells_ms")
+            if n_eval > 0:
+                _lib.check(L.pf_last_cells_ms(c, ctypes.byref(ms)), "pf_last_cells_ms")
             cells_ms += ms.value
     launches = int(L.pf_launch_count() - launches0)
     t_step = tot_ms / a.steps
     t_cells = cells_ms / a.steps
     if ws > 1:
-        tt = torch.tensor([t_step, t_cells], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tt = all_reduce_host([t_step, t_cells], "max")
         t_step, t_cells = float(tt[0]), float(tt[1])
-        s_all = torch.tensor([s_cell], dtype=torch.float64, device="cuda")
-        dist.all_reduce(s_all)
-        s_cell_total = float(s_all[0])
+        s_cell_total = float(all_reduce_host([s_cell], "sum")[0])
     else:
         s_cell_total = s_cell
     value = sc.n / (t_step * 1e-3)

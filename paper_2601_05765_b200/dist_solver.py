@@ -293,9 +293,8 @@ class DistNewton:
         self.domain = domain
         self.comm = Comm(group)
         self.smf, self.ball_aware, self.slack = smf, ball_aware, slack
-        lo, hi = domain.bbox()
-        self.lo = float(lo[0]) if axis_lo is None else axis_lo
-        self.hi = float(hi[0]) if axis_hi is None else axis_hi
+        # slab boundaries: x-quantiles of the sites (balanced) unless given
+        self.lo, self.hi = axis_lo, axis_hi
         self.tau = 1e-12 * domain.diagonal() ** 2
         self.ops_factory = ops_factory or (lambda p, n, r: CudaOps(p, n, r, domain, smf, ball_aware,
                                                                    self.tau))

@@ -49,10 +49,22 @@ def global_dpsi(psi_local: np.ndarray, group=None) -> float:
     return max(hi - lo, 0.0) if np.isfinite(hi) else 0.0
 
 
-def slab_owner(x: np.ndarray, world: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
-    """Rank owning each x coordinate (x-slabs of equal width over [lo, hi])."""
-    w = (hi - lo) / world
-    return np.clip(np.floor((np.asarray(x) - lo) / w), 0, world - 1).astype(np.int64)
+def slab_cuts(x: np.ndarray, world: int, lo: float | None = None, hi: float | None = None) -> np.ndarray:
+    """Interior slab boundaries along x: equal-width over [lo, hi] when given,
+    else at the x-quantiles of the sites (equal cell counts per rank)."""
+    if world <= 1:
+        return np.zeros(0)
+    if lo is not None and hi is not None:
+        return lo + (hi - lo) * np.arange(1, world) / world
+    return np.quantile(np.asarray(x, dtype=np.float64), np.arange(1, world) / world)
+
+
+def slab_owner(x: np.ndarray, world: int, lo: float | None = None, hi: float | None = None,
+               cuts: np.ndarray | None = None) -> np.ndarray:
+    """Rank owning each x coordinate (slab k = [cuts[k-1], cuts[k]))."""
+    if cuts is None:
+        cuts = slab_cuts(x, world, lo, hi)
+    return np.searchsorted(cuts, np.asarray(x), side="right").astype(np.int64)
 
 
 def search_radius(psi: np.ndarray, dpsi: float) -> np.ndarray:
@@ -62,16 +74,17 @@ def search_radius(psi: np.ndarray, dpsi: float) -> np.ndarray:
 
 
 def slab_partition(pts: np.ndarray, psi: np.ndarray, dpsi: float, world: int, rank: int,
-                   lo: float = 0.0, hi: float = 1.0, slack: float = 1.0) -> Slab:
+                   lo: float | None = None, hi: float | None = None, slack: float = 1.0) -> Slab:
     """x-slab r of [lo, hi] with its ghost sites (pts / psi are the global arrays).
 
     ``slack`` > 1 widens the ghost margin beyond the current search radius so a
     Newton solve (whose weights grow) can keep the partition for several
     iterations; `DistNewton` checks the margin before every evaluation."""
     x = pts[:, 0]
-    w = (hi - lo) / world
-    a, b = lo + rank * w, lo + (rank + 1) * w
-    own = slab_owner(x, world, lo, hi) == rank
+    cuts = slab_cuts(x, world, lo, hi)
+    a = float(cuts[rank - 1]) if rank > 0 else -np.inf
+    b = float(cuts[rank]) if rank < world - 1 else np.inf
+    own = slab_owner(x, world, cuts=cuts) == rank
     br = search_radius(psi, dpsi)
     margin = float(br[own].max()) * (1.0 + 1e-9) * slack if own.any() else 0.0
     keep = own | ((x >= a - margin) & (x <= b + margin))
@@ -103,7 +116,7 @@ class HaloPlan:
 
 
 def halo_plan(pts: np.ndarray, psi: np.ndarray, dpsi: float, world: int, rank: int,
-              lo: float = 0.0, hi: float = 1.0, slack: float = 1.0):
+              lo: float | None = None, hi: float | None = None, slack: float = 1.0):
     """(slab of this rank, halo plan).  Every rank derives every other rank's
     ghost set from the replicated global arrays, so no negotiation is needed."""
     slabs = [slab_partition(pts, psi, dpsi, world, q, lo, hi, slack) for q in range(world)]
