@@ -104,6 +104,19 @@ int pf_evaluate_lean(pf_ctx *ctx, int64_t n, const double *pts, const double *ps
                      int ball_aware, int64_t smf, double *vol, double *ksur, int32_t *fcount,
                      int32_t *ftag, double *farea, double *cent, int64_t *flags, void *stream);
 
+/* pf_batch_evaluate_ex without host synchronisation: the flag word of this
+ * call is OR-ed into *err_accum (device int64).  Used to pipeline the host
+ * round trip of the drop-in (_kernels._batch_evaluate on host arrays) in
+ * chunks of cells: device->host copies of one chunk overlap the next. */
+int pf_batch_evaluate_async(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double tol,
+                            double dpsi_max, int ball_aware, int want_m2, int64_t smf, int64_t *status,
+                            double *vol, double *ksur, double *cent, double *ipt, double *m2,
+                            int64_t *fcount, int64_t *ftag, double *farea, double *fh, double *fnrm,
+                            double *fcent, const int32_t *cells, int64_t ncells, int32_t *cell_flags,
+                            int64_t *err_accum, int rebuild_grid, void *stream);
+/* bucket-ordered permutation of the sites of the current grid (int32[n]) */
+int pf_grid_order(pf_ctx *ctx, int32_t *order, void *stream);
+
 /* per-cell processed-candidate census of the last evaluation (int32[n]) */
 int pf_last_census(pf_ctx *ctx, int32_t *census, void *stream);
 /* device time (ms) of the cell kernels (both tiers) of the last evaluation */

@@ -67,41 +67,89 @@ def _batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
     on_device = _is_torch(pts)
     c = _lib.ctx()
     upload_domain(c, _host(dv), _host(dc), _host(dp), _host(dt), _host(dlp), _host(dlv), float(tol))
-    if on_device:
-        p = _to_dev(pts, f8)
-        w = _to_dev(psi, f8)
-        outs = [_to_dev(o, t) for o, t in zip(outs_host, dtypes)]
-    else:
-        p = torch.from_numpy(np.ascontiguousarray(pts, np.float64)).to("cuda", non_blocking=True)
-        w = torch.from_numpy(np.ascontiguousarray(psi, np.float64)).to("cuda", non_blocking=True)
-        # fixed-stride slots past fcount come back zero (the reference leaves
-        # them untouched; callers allocate zeros)
-        outs = [torch.zeros(o.shape, dtype=t, device="cuda") if k >= 7 else
-                torch.empty(o.shape, dtype=t, device="cuda")
-                for k, (o, t) in enumerate(zip(outs_host, dtypes))]
+    if not on_device:
+        return _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, outs_host,
+                                    dtypes)
+    p = _to_dev(pts, f8)
+    w = _to_dev(psi, f8)
+    outs = [_to_dev(o, t) for o, t in zip(outs_host, dtypes)]
     n = int(p.shape[0])
-    cflags = torch.empty(n, dtype=torch.int32, device="cuda")
     err = int(_lib.lib().pf_batch_evaluate_ex(
         c, n, _lib.ptr(p), _lib.ptr(w), float(tol), float(dpsi_max), int(bool(ball_aware)),
-        int(bool(want_m2)), int(smf), *[_lib.ptr(o) for o in outs], None, 0, _lib.ptr(cflags),
+        int(bool(want_m2)), int(smf), *[_lib.ptr(o) for o in outs], None, 0, None,
         None, 1, _lib.stream_ptr()))
     _lib.check(err, "pf_batch_evaluate_ex")
-    if not on_device:
-        # the reference leaves cent/ipt/m2 of capacity-overflowed cells
-        # untouched (_kernels.py:1393-1399): keep the caller's values there
-        keep = None
-        if err & FLAG_OVERFLOW:
-            keep = ((cflags & 512) != 0).cpu().numpy()  # FLAG_BUILD_OVERFLOW (pf_cell.cuh)
-        for k, (h, d) in enumerate(zip(outs_host, outs)):
-            if keep is not None and k in (3, 4, 5) and keep.any():
-                src = d.cpu().numpy().reshape(h.shape)
-                src[keep] = h[keep]
-                h[...] = src
-            elif isinstance(h, np.ndarray) and h.flags.c_contiguous and h.flags.writeable:
-                torch.from_numpy(h).copy_(d.view(h.shape))  # straight D2H into the caller's buffer
-            else:
-                h[...] = d.cpu().numpy().reshape(h.shape)
     return err
+
+
+def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, outs_host, dtypes,
+                         chunks: int | None = None):
+    """Host-array drop-in: inputs copied in, every output copied back into the
+    caller's arrays.  The cells are evaluated in `chunks` index ranges (each in
+    bucket order) and the device->host copy of one range runs on a side stream
+    while the next range computes, so the round trip hides behind the kernels
+    (the copies are asynchronous when the caller's arrays are pinned)."""
+    import os
+
+    import torch
+
+    L = _lib.lib()
+    n = int(np.asarray(pts).shape[0])
+    K = chunks or int(os.environ.get("PF_E2E_CHUNKS", "8"))
+    K = max(1, min(K, max(n, 1)))
+
+    def h2d(x, dtype):
+        return torch.from_numpy(np.ascontiguousarray(x, dtype)).to("cuda", non_blocking=True)
+
+    p = h2d(pts, np.float64)
+    w = h2d(psi, np.float64)
+    outs = []
+    for k, (o, t) in enumerate(zip(outs_host, dtypes)):
+        if k in (3, 4, 5):
+            # cent / ipt / m2 start from the caller's values: the reference leaves
+            # them untouched for capacity-overflowed cells (_kernels.py:1393-1399)
+            outs.append(h2d(o, np.float64))
+        elif k >= 7:
+            # fixed-stride slots past fcount come back zero (the reference leaves
+            # them untouched; callers allocate zeros, SURVEY.md §9)
+            outs.append(torch.zeros(o.shape, dtype=t, device="cuda"))
+        else:
+            outs.append(torch.empty(o.shape, dtype=t, device="cuda"))
+    err_acc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    comp = torch.cuda.current_stream()
+    sptr = _lib.stream_ptr()
+    _lib.check(L.pf_grid_build(c, n, _lib.ptr(p), _lib.ptr(w), 0.0, sptr), "pf_grid_build")
+    order = torch.empty(n, dtype=torch.int32, device="cuda")
+    _lib.check(L.pf_grid_order(c, _lib.ptr(order), sptr), "pf_grid_order")
+    copy = torch.cuda.Stream()
+    hosts = [torch.from_numpy(h.reshape(h.shape)) if isinstance(h, np.ndarray) and h.flags.c_contiguous
+             and h.flags.writeable else None for h in outs_host]
+    if K > 1:
+        # cells of each index range in bucket order: one stable sort by range id
+        rid = order.long() * K // n
+        cells_all = order[torch.sort(rid, stable=True).indices]
+        offs = [0] + torch.cumsum(torch.bincount(rid, minlength=K), 0).tolist()
+    for k in range(K):
+        i0, i1 = k * n // K, (k + 1) * n // K
+        cells = cells_all[offs[k]:offs[k + 1]] if K > 1 else None
+        _lib.check(L.pf_batch_evaluate_async(
+            c, n, _lib.ptr(p), _lib.ptr(w), float(tol), float(dpsi_max), int(bool(ball_aware)),
+            int(bool(want_m2)), int(smf), *[_lib.ptr(o) for o in outs], _lib.ptr(cells),
+            0 if cells is None else int(cells.numel()), None, _lib.ptr(err_acc), 0, sptr),
+            "pf_batch_evaluate_async")
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev)
+            for h, t, d in zip(outs_host, hosts, outs):
+                if t is not None:
+                    t[i0:i1].copy_(d[i0:i1].view(t[i0:i1].shape), non_blocking=True)
+    copy.synchronize()
+    comp.synchronize()
+    for h, t, d in zip(outs_host, hosts, outs):
+        if t is None:
+            h[...] = d.cpu().numpy().reshape(h.shape)
+    return int(err_acc.item())
 
 
 def _knn(pts, grid_start, grid_sites, lox, loy, loz, ihx, ihy, ihz,

@@ -58,6 +58,11 @@ def lib():
         L.pf_evaluate_lean.argtypes = [vp, i64, vp, vp, i, i64] + [vp] * 7 + [vp]
         L.pf_last_census.argtypes = [vp, vp, vp]
         L.pf_last_retry_count.argtypes = [vp, vp]
+        L.pf_batch_evaluate_async.restype = i
+        L.pf_batch_evaluate_async.argtypes = ([vp, i64, vp, vp, d, d, i, i, i64] + [vp] * 12
+                                              + [vp, i64, vp, vp, i, vp])
+        L.pf_grid_order.restype = i
+        L.pf_grid_order.argtypes = [vp, vp, vp]
         L.pf_knn.restype = i64
         L.pf_knn.argtypes = [vp, i64, vp, i64, vp, i64, vp, vp]
         for name in ("pf_ctx_create", "pf_ctx_destroy", "pf_set_domain", "pf_grid_build",

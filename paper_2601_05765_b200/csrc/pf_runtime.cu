@@ -921,6 +921,52 @@ int pf_evaluate_lean_cells(pf_ctx *c, int64_t n, const double *pts, const double
     return 0;
 }
 
+__global__ void k_or_flags(unsigned long long *acc, const unsigned long long *err) { *acc |= *err; }
+
+// asynchronous evaluation of a cell subset: the flag word is OR-ed into a
+// device accumulator, no host synchronisation (pipelined host round trips)
+int pf_batch_evaluate_async(pf_ctx *c, int64_t n, const double *pts, const double *psi, double tol,
+                            double dpsi_max, int ball_aware, int want_m2, int64_t smf, int64_t *status,
+                            double *vol, double *ksur, double *cent, double *ipt, double *m2,
+                            int64_t *fcount, int64_t *ftag, double *farea, double *fh, double *fnrm,
+                            double *fcent, const int32_t *cells, int64_t ncells, int32_t *cell_flags,
+                            int64_t *err_accum, int rebuild_grid, void *stream) {
+    cudaStream_t st = S(stream);
+    if (!c->has_domain) return set_err("pf_batch_evaluate_async: no domain set");
+    if (n < 0 || n > 0x7fffffff) return set_err("pf_batch_evaluate_async: bad n");
+    if (rebuild_grid || c->grid_n != n || c->grid_pts != pts) {
+        if (grid_build(c, n, pts, psi, 0.0, st)) return -1;
+    }
+    if (dpsi_max < 0.0 && dpsi_dev(c, n, psi, st)) return -1;
+    if (ensure(&c->census, &c->census_cap, (size_t)n + 1)) return -1;
+    CellIn in;
+    fill_cellin(c, in, n, pts, psi, tol, dpsi_max, ball_aware, want_m2);
+    CellOut out;
+    memset(&out, 0, sizeof out);
+    out.status = status; out.vol = vol; out.ksur = ksur; out.cent = cent; out.ipt = ipt; out.m2 = m2;
+    out.fcount = fcount; out.ftag = ftag; out.farea = farea; out.fh = fh; out.fnrm = fnrm;
+    out.fcent = fcent; out.smf = (int)smf; out.census = c->census;
+    out.flags = cell_flags;
+    in.cells = cells;
+    in.ncells = (int)ncells;
+    if (n > 0 && (!cells || ncells > 0)) {
+        if (launch_cells(c, in, out, n, st)) return -1;
+        if (err_accum) {
+            g_launches++;
+            k_or_flags<<<1, 1, 0, st>>>((unsigned long long *)err_accum, c->err);
+            CK(cudaGetLastError());
+        }
+    }
+    return 0;
+}
+
+// the bucket-ordered site permutation of the current grid (int32[n])
+int pf_grid_order(pf_ctx *c, int32_t *order, void *stream) {
+    if (c->grid_n < 0 || !c->sid) return set_err("pf_grid_order: no grid");
+    CK(cudaMemcpyAsync(order, c->sid, (size_t)c->grid_n * sizeof(int32_t), cudaMemcpyDeviceToDevice, S(stream)));
+    return 0;
+}
+
 int pf_last_census(pf_ctx *c, int32_t *census, void *stream) {
     if (!c->census || c->grid_n < 0) return set_err("pf_last_census: nothing evaluated");
     CK(cudaMemcpyAsync(census, c->census, c->grid_n * sizeof(int32_t), cudaMemcpyDeviceToDevice, S(stream)));
