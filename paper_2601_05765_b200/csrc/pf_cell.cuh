@@ -199,7 +199,7 @@ PF_NOINL double ddiv(double a, double b) { return a / b; }
 PF_NOINL double dsqrt(double x) { return sqrt(x); }
 
 // _kernels.py:59-80
-PF_NOINL void perp_basis(double nx, double ny, double nz, double *e) {
+PF_DEV void perp_basis_inl(double nx, double ny, double nz, double *e) {
     double ax = fabs(nx), ay = fabs(ny), az = fabs(nz);
     double ux, uy, uz;
     if (ax <= ay && ax <= az) { ux = 1.0; uy = 0.0; uz = 0.0; }
@@ -215,6 +215,7 @@ PF_NOINL void perp_basis(double nx, double ny, double nz, double *e) {
     e[4] = nz * e1x - nx * e1z;
     e[5] = nx * e1y - ny * e1x;
 }
+PF_NOINL void perp_basis(double nx, double ny, double nz, double *e) { perp_basis_inl(nx, ny, nz, e); }
 
 template <class C>
 PF_DEV void load_domain(Poly<C> &A, const CellIn &in) {
@@ -276,39 +277,61 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
     const int nv = A.nv, nf = A.nf;
     if (ws->cen_on && L == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += nv; }
 
-    // 1. classify vertices (_kernels.py:121-134)
-    int n_out = 0;
-    #pragma unroll 1
-    for (int v0 = 0; v0 < nv; v0 += 32) {
-        int v = v0 + L;
-        bool out = false;
-        if (v < nv) {
-            double s = nx * A.x[v] + ny * A.y[v] + nz * A.z[v] - dd;
-            S.sd[v] = s;
-            out = s > tol;
-        }
-        n_out += pfw::popc(pfw::ballot(out));
-    }
-    if (n_out == 0) return CLIP_UNTOUCHED;
-    if (nv - n_out == 0) return CLIP_EMPTY;
-    pfw::sync();
-
-    // 2. keep inside vertices in order (_kernels.py:137-147)
+    // 1. classify vertices (_kernels.py:121-134) and 2. keep the inside
+    // ones in order (_kernels.py:137-147); one pass when nv <= 32 (the signed
+    // distance stays in a register for the on-plane test of step 4)
     int K = 0;
-    #pragma unroll 1
-    for (int v0 = 0; v0 < nv; v0 += 32) {
-        int v = v0 + L;
-        bool keep = v < nv && S.sd[v] <= tol;
-        unsigned m = pfw::ballot(keep);
-        if (keep) {
-            int idx = K + pfw::popc(m & lt);
-            S.vmap[v] = (uint16_t)idx;
-            B.x[idx] = A.x[v]; B.y[idx] = A.y[v]; B.z[idx] = A.z[v];
-        } else if (v < nv) {
-            S.vmap[v] = 0xffff;
+    double s_reg = 0.0;
+    int vmap_reg = 0xffff;
+    if (nv <= 32) {
+        const int v = L;
+        if (v < nv) {
+            s_reg = nx * A.x[v] + ny * A.y[v] + nz * A.z[v] - dd;
+            S.sd[v] = s_reg;
         }
-        K += pfw::popc(m);
+        const unsigned m_out = pfw::ballot(v < nv && s_reg > tol);
+        if (m_out == 0) return CLIP_UNTOUCHED;
+        if (pfw::popc(m_out) == nv) return CLIP_EMPTY;
+        const bool keep = v < nv && s_reg <= tol;
+        const unsigned m = pfw::ballot(keep);
+        if (keep) {
+            vmap_reg = pfw::popc(m & lt);
+            B.x[vmap_reg] = A.x[v]; B.y[vmap_reg] = A.y[v]; B.z[vmap_reg] = A.z[v];
+        }
+        if (v < nv) S.vmap[v] = (uint16_t)vmap_reg;
+        K = pfw::popc(m);
+    } else {
+        int n_out = 0;
+        #pragma unroll 1
+        for (int v0 = 0; v0 < nv; v0 += 32) {
+            int v = v0 + L;
+            bool out = false;
+            if (v < nv) {
+                double sv = nx * A.x[v] + ny * A.y[v] + nz * A.z[v] - dd;
+                S.sd[v] = sv;
+                out = sv > tol;
+            }
+            n_out += pfw::popc(pfw::ballot(out));
+        }
+        if (n_out == 0) return CLIP_UNTOUCHED;
+        if (nv - n_out == 0) return CLIP_EMPTY;
+        pfw::sync();
+        #pragma unroll 1
+        for (int v0 = 0; v0 < nv; v0 += 32) {
+            int v = v0 + L;
+            bool keep = v < nv && S.sd[v] <= tol;
+            unsigned m = pfw::ballot(keep);
+            if (keep) {
+                int idx = K + pfw::popc(m & lt);
+                S.vmap[v] = (uint16_t)idx;
+                B.x[idx] = A.x[v]; B.y[idx] = A.y[v]; B.z[idx] = A.z[v];
+            } else if (v < nv) {
+                S.vmap[v] = 0xffff;
+            }
+            K += pfw::popc(m);
+        }
     }
+    pfw::sync();
 
     // 3a. lane per loop entry (edge a -> b of facet f): classification,
     // crossing entries in walk order (= entry order) and the facet's emitted
@@ -452,13 +475,20 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
     // (sa >= -tol when emitted, i.e. every kept vertex with sd >= -tol) and
     // all crossing vertices, in B index order.
     int ncp = 0;
-    #pragma unroll 1
-    for (int v0 = 0; v0 < nv; v0 += 32) {
-        int v = v0 + L;
-        bool on = v < nv && S.sd[v] <= tol && S.sd[v] >= -tol;
-        unsigned m = pfw::ballot(on);
-        if (on) S.onl[ncp + pfw::popc(m & lt)] = S.vmap[v];
-        ncp += pfw::popc(m);
+    if (nv <= 32) {
+        const bool on = L < nv && s_reg <= tol && s_reg >= -tol;
+        const unsigned m = pfw::ballot(on);
+        if (on) S.onl[pfw::popc(m & lt)] = (uint16_t)vmap_reg;
+        ncp = pfw::popc(m);
+    } else {
+        #pragma unroll 1
+        for (int v0 = 0; v0 < nv; v0 += 32) {
+            int v = v0 + L;
+            bool on = v < nv && S.sd[v] <= tol && S.sd[v] >= -tol;
+            unsigned m = pfw::ballot(on);
+            if (on) S.onl[ncp + pfw::popc(m & lt)] = S.vmap[v];
+            ncp += pfw::popc(m);
+        }
     }
     #pragma unroll 1
     for (int q = L; q < NFirst; q += 32) S.onl[ncp + q] = (uint16_t)(K + q);
@@ -471,15 +501,17 @@ PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &
     }
     pfw::sync();
     // centroid: sequential sum in index order, computed redundantly by every lane
-    double ccx = 0.0, ccy = 0.0, ccz = 0.0;
-    #pragma unroll 1
-    for (int q = 0; q < ncp; q++) {
-        int v = S.onl[q];
-        ccx += B.x[v]; ccy += B.y[v]; ccz += B.z[v];
+    // (lane a < 3 sums coordinate a: the same sequential sums and divisions)
+    double cc = 0.0;
+    if (L < 3) {
+        const double *crd = L == 0 ? B.x : (L == 1 ? B.y : B.z);
+        #pragma unroll 1
+        for (int q = 0; q < ncp; q++) cc += crd[S.onl[q]];
+        cc /= (double)ncp;
     }
-    ccx /= (double)ncp; ccy /= (double)ncp; ccz /= (double)ncp;
+    const double ccx = pfw::shfl(cc, 0), ccy = pfw::shfl(cc, 1), ccz = pfw::shfl(cc, 2);
     double e[6];
-    perp_basis(nx, ny, nz, e);
+    perp_basis_inl(nx, ny, nz, e);
     #pragma unroll 1
     for (int q = L; q < ncp; q += 32) {
         int v = S.onl[q];
