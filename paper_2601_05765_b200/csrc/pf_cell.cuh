@@ -1624,8 +1624,11 @@ PF_NOINL void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, do
         double cc = wx * wx + wy * wy + wz * wz - psi;
         double disc = bh * bh - cc;
         if (disc <= 0.0) continue;
-        double t_hi = -bh + dsqrt(disc);
-        double t_lo = 0.0;
+        // ray [t_lo, t_hi] inside every other facet plane; the extreme ratios
+        // num/den are tracked as fractions (positive denominators), one
+        // division each at the end instead of one per plane
+        double hn = -bh + dsqrt(disc), hd = 1.0;  // t_hi = hn / hd
+        double ln = 0.0, ld = 1.0;                // t_lo = ln / ld
         bool ok = true;
         #pragma unroll 1
         for (int g = 0; g < nf; g++) {
@@ -1633,17 +1636,18 @@ PF_NOINL void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, do
             double den = P.nx[g] * dx + P.ny[g] * dy + P.nz[g] * dz;
             double num = P.d[g] - (P.nx[g] * ox + P.ny[g] * oy + P.nz[g] * oz);
             if (den > tol) {
-                double tc = ddiv(num, den);
-                if (tc < t_hi) t_hi = tc;
+                if (num * hd < hn * den) { hn = num; hd = den; }
             } else if (den < -tol) {
-                double tc = ddiv(num, den);
-                if (tc > t_lo) t_lo = tc;
+                if (-num * ld > ln * -den) { ln = -num; ld = -den; }
             } else if (num < -tol) {
                 ok = false;
                 break;
             }
         }
-        if (!ok || t_hi - t_lo <= tol) continue;
+        if (!ok) continue;
+        const double t_hi = hd == 1.0 ? hn : ddiv(hn, hd);
+        const double t_lo = ld == 1.0 ? ln : ddiv(ln, ld);
+        if (t_hi - t_lo <= tol) continue;
         double tm = 0.5 * (t_lo + t_hi);
         double mx = ox + tm * dx, my = oy + tm * dy, mz = oz + tm * dz;
         double mg = dsqrt(psi) - dsqrt(sq(mx - px) + sq(my - py) + sq(mz - pz));

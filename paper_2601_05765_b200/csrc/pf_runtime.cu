@@ -374,6 +374,16 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, 1)
             if (stage[i] != 1) i = -1;
         }
         const bool act = i >= 0;
+        {
+            // next round's polytope into L2 while this round computes
+            const int tn = t + gridDim.x * SYNC_WARPS;
+            if (tn < count) {
+                const int inext = in.cells ? in.cells[tn] : in.g.sid[tn];
+                const char *pp = (const char *)(gpoly + inext);
+                const int nlines = (int)((sizeof(Poly<FastCaps>) + 127) / 128);
+                if (lane < nlines) asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + 128 * lane));
+            }
+        }
         double px = 0.0, py = 0.0, pz = 0.0, psi = 0.0;
         CellRes res;
         EvalState st;
