@@ -266,7 +266,7 @@ PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
 // clip A by n.x <= dd into B (_kernels.py:109-319), warp-cooperative
 // ---------------------------------------------------------------------------
 template <class W>
-PF_NOINL int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B, int wa, double nx,
+PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B, int wa, double nx,
                   double ny, double nz, double dd, int tag, double tol) {
     using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
@@ -636,7 +636,7 @@ PF_DEV int bucket_coord(double x, double lo, double ih, int gn) {
 // returns the number of candidates (may exceed CC: overflow); *all_sites set
 // when the bucket range spans the whole grid
 template <class W>
-PF_NOINL int gather_shell(W *ws, const CellIn &in, int self, double px, double py, double pz,
+PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py, double pz,
                         double t_lo, double t_hi, bool *all_sites) {
     using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
@@ -707,7 +707,7 @@ PF_NOINL int gather_shell(W *ws, const CellIn &in, int self, double px, double p
 
 // sort the shell's candidates by (d2, j) in place (rank sort through registers)
 template <class W>
-PF_NOINL void sort_candidates(W *ws, int nc) {
+PF_DEV void sort_candidates(W *ws, int nc) {
     using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
     const int L = pfw::lane();
@@ -756,6 +756,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         for (int k = in.dlp[f]; k < in.dlp[f + 1]; k++) ws->u.b.lf[0][k] = (uint8_t)f;
     pfw::sync();
     int which = 0;
+    int ncl = 0;
     *nclips = 0;
     double rfar = poly_rfar(ws->P[0], px, py, pz);
     const double sq_ball = (in.ball_aware && psii > 0.0) ? sqrt(psii) : -1.0;
@@ -779,6 +780,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
                 if (pfw::lane() == 0) ws->oflow = 1;
                 pfw::sync();
                 *which_out = which;
+                *nclips = ncl;
                 return 3;
             }
             t_hi = nt;
@@ -809,19 +811,19 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         if (in.ball_aware && br < stop_r) stop_r = br;
         #pragma unroll 1
         for (int c = 0; c < nc; c++) {
-            if (S.csd[c] >= stop_r) { *which_out = which; return 0; }
+            if (S.csd[c] >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
             const int j = S.cj[c];
             const int sl = S.cord[c];
             if (S.cd2[c] <= tol * tol) {
                 const double psij = S.cw[sl];
-                if (psij > psii || (psij == psii && j < i)) { *which_out = which; return 1; }
+                if (psij > psii || (psij == psii && j < i)) { *which_out = which; *nclips = ncl; return 1; }
                 continue;
             }
-            (*nclips)++;
+            ncl++;
             int st = clip(ws, ws->P[which], ws->P[1 - which], which, S.cx[sl], S.cy[sl], S.cz[sl], S.cw[sl],
                           j, tol);
-            if (st == CLIP_EMPTY) { *which_out = which; return 1; }
-            if (st == CLIP_OVERFLOW) { *which_out = which; return 3; }
+            if (st == CLIP_EMPTY) { *which_out = which; *nclips = ncl; return 1; }
+            if (st == CLIP_OVERFLOW) { *which_out = which; *nclips = ncl; return 3; }
             if (st == CLIP_CUT) {
                 which = 1 - which;
                 rfar = poly_rfar(ws->P[which], px, py, pz);
@@ -835,6 +837,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         t_hi = t_hi * 4.0;
     }
     *which_out = which;
+    *nclips = ncl;
     return 0;
 }
 
