@@ -382,15 +382,20 @@ def main():
     peak = ctypes.c_double(0.0)
     _lib.check(L.pf_fp64_peak(ctypes.byref(peak), None), "pf_fp64_peak")
     achieved = 2.0 * s_cell_total / (t_cells * 1e-3) / 1e12  # slot = FMA-equivalent (2 flop)
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(a.config)
+            tr = json.load(open(tp)).get(a.config)
+            if tr:
+                traffic = float(tr["k_cells_build_dram_bytes"] + tr["k_cells_eval_sync_dram_bytes"])
+                traffic_src = tr
         except Exception:
             traffic = None
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value if peak.value > 0 else None, "traffic": traffic,
+                "traffic_unit": "bytes per step (DRAM read+write of the cell kernels, ncu)",
+                "traffic_detail": traffic_src,
                 "kernel": "k_cells_build+k_cells_eval (+k_cells_exact retries)",
                 "kernel_ms": t_cells, "kernel_share_of_step": t_cells / t_step,
                 "algorithmic": f"census S_cell (SURVEY.md §8(d)) = {s_cell_total / sc.n:.0f} DP slots/cell,"
