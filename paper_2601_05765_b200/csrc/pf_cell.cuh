@@ -989,7 +989,9 @@ PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, doub
                                 // the facet with a spurious arc (a whole circular
                                 // segment too much).  It coincides with the vertex to
                                 // ~tol: drop it.  Never fires on consistent geometry.
+#if !defined(PF_REF_STRICT) && !defined(PF_KEEP_SPURIOUS)
                                 if (which == 0 && cur) continue;
+#endif
                                 const double cxx = ox + t * ux, cxy = oy + t * uy, cxz = oz + t * uz;
                                 const int fl = cur ? (PF_ONSPH | PF_CONN) : (PF_ONSPH | PF_ENTRY);
                                 cur = !cur;
@@ -1129,9 +1131,14 @@ PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, doub
 // PF_ARC_CHORD * tol and only flips sweeps the geometry proves impossible
 // (see tests/test_degenerate_arcs.py: Monte-Carlo volumes of such cells).
 #define PF_ARC_CHORD 100.0
+// below this sweep (rad) an arc's wrap is decided with the reference's formula
+#define PF_SWEEP_AMBIG 1e-6
 template <class C>
 PF_NOINL bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
                                 double dx, double dy, double dz, double rc, double tol) {
+#if defined(PF_REF_STRICT) || defined(PF_NO_LONGARC)
+    return false;
+#endif
     double dn = dsqrt(dx * dx + dy * dy + dz * dz);
     if (!(dn > 0.0)) return false;
     double k = ddiv(rc, dn);
@@ -1219,6 +1226,9 @@ PF_NOINL void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, d
                 const double c0 = r0 > 0.0 ? x0 * ir0 : 1.0, s0 = y0 * ir0;
                 const double c1 = r1 > 0.0 ? x1 * ir1 : 1.0, s1 = y1 * ir1;
                 double dth = atan2_ool(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
+                // end points (nearly) coincident: decide the wrap exactly as the
+                // reference does, from the two end-point angles (_kernels.py:696-700)
+                if (fabs(dth) < PF_SWEEP_AMBIG) dth = atan2_ool(y1, x1) - atan2_ool(y0, x0);
                 if (dth <= 0.0) {
                     dth += 2.0 * PF_PI;
                     const double ch2 = (x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0);
@@ -1402,6 +1412,18 @@ PF_NOINL void ring_patches(W *ws, const Poly<typename W::Cap> &P, double px, dou
                 const double rp[3] = {prq[0] - qc[0], prq[1] - qc[1], prq[2] - qc[2]};
                 const double rq[3] = {E.prx[j] - qc[0], E.pry[j] - qc[1], E.prz[j] - qc[2]};
                 double dPQ = ccw_angle(rp, rq, m);
+                if (arc && (dPQ < PF_SWEEP_AMBIG || dPQ > 2.0 * PF_PI - PF_SWEEP_AMBIG)) {
+                    // (nearly) coincident end points: the reference's frame angles
+                    // phQ - phP decide whether the arc wraps (_kernels.py:908-923)
+                    double u[6];
+                    perp_basis(m[0], m[1], m[2], u);
+                    const double phP = atan2_ool(rp[0] * u[3] + rp[1] * u[4] + rp[2] * u[5],
+                                                 rp[0] * u[0] + rp[1] * u[1] + rp[2] * u[2]);
+                    const double phQ = atan2_ool(rq[0] * u[3] + rq[1] * u[4] + rq[2] * u[5],
+                                                 rq[0] * u[0] + rq[1] * u[1] + rq[2] * u[2]);
+                    dPQ = phQ - phP;
+                    if (dPQ < 0.0) dPQ += 2.0 * PF_PI;
+                }
                 if (arc && dPQ > PF_PI) {
                     const double d0 = rp[0] - rq[0], d1 = rp[1] - rq[1], d2 = rp[2] - rq[2];
                     if (d0 * d0 + d1 * d1 + d2 * d2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&

@@ -145,7 +145,15 @@ void lane_fn(void *ctx, int lane) {
 
 }  // namespace
 
+static const int *g_only = nullptr;  // optional cell subset (debugging)
+static int g_nonly = 0;
+
 extern "C" {
+
+void pfemu_set_cells(const int *cells, int ncells) {
+    g_only = cells;
+    g_nonly = ncells;
+}
 
 // Build the bucket-sorted SoA grid exactly as the device grid build does
 // (stable counting sort by bucket id) and run every cell through the fast
@@ -208,9 +216,10 @@ int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
         pfw::EmuWarp *w = pfw::emu_new_warp(1 << 18);
         WS<FastCaps> *wsf = (WS<FastCaps> *)aligned_alloc(64, (sizeof(WS<FastCaps>) + 63) / 64 * 64);
         WS<ExactCaps> *wse = (WS<ExactCaps> *)aligned_alloc(64, (sizeof(WS<ExactCaps>) + 63) / 64 * 64);
+        const int nk = g_only ? g_nonly : n;
 #pragma omp for schedule(dynamic, 4)
-        for (int k = 0; k < n; k++) {
-            int i = sid[k];  // cells processed in bucket order, as on the device
+        for (int k = 0; k < nk; k++) {
+            int i = g_only ? g_only[k] : sid[k];  // cells processed in bucket order, as on the device
             int r = FLAG_RETRY;
             if (tier == 0) {
                 Job<FastCaps> job{wsf, &in, &out, i, 0};
