@@ -97,6 +97,19 @@ def newton_solve(pts, nu, dom_args, tol, domain_diag, psi_init=None, eps_vol=0.0
         psi = np.array(psi_init, np.float64)
         o = _evaluate(pts, psi, dom_args, tol, grid, smf)
         stats["evaluations"] += 1
+        # warm start with per-cell rescue (SPEC.md init_weights): empty cells get
+        # psi_i <- max(psi_i, kappa (3 nu_i / 4 pi)^(2/3)), kappa doubling
+        kappa = 1.0
+        while not o["vol"].min() > 0.0:
+            if kappa > 1024.0:
+                stats["status"] = 3
+                return psi, stats
+            e = ~(o["vol"] > 0.0)
+            psi[e] = np.maximum(psi[e], kappa * (3.0 * nu[e] / (4.0 * np.pi)) ** (2.0 / 3.0))
+            stats["init_doublings"] += 1
+            o = _evaluate(pts, psi, dom_args, tol, grid, smf)
+            stats["evaluations"] += 1
+            kappa *= 2.0
     floor_v = 0.5 * min(nu.min(), o["vol"].min())
     worst = float(np.max(np.abs(o["vol"] - nu) / nu))
     stats["worst_initial"] = worst

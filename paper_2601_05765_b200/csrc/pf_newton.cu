@@ -266,6 +266,17 @@ __global__ void __launch_bounds__(RB) k_axpy_to(int64_t n, const double *__restr
         out[i] = a[i] + s * b[i];
 }
 
+// rescue of the cells a warm start leaves empty (SPEC.md init_weights)
+__global__ void __launch_bounds__(RB) k_rescue(int64_t n, const double *__restrict__ nu,
+                                              const double *__restrict__ vol, double kappa,
+                                              double *__restrict__ psi) {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        if (!(vol[i] > 0.0)) {
+            const double r = kappa * pow(3.0 * nu[i] / (4.0 * 3.141592653589793), 2.0 / 3.0);
+            if (!(psi[i] >= r)) psi[i] = r;
+        }
+}
+
 __global__ void __launch_bounds__(RB) k_cold_psi(int64_t n, const double *__restrict__ nu, double kappa,
                                                 double *__restrict__ psi) {
     for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
@@ -423,6 +434,18 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
     } else {
         if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea, w.cent)) return -1;
         if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
+        // warm start with per-cell rescue (SPEC.md init_weights): an empty cell
+        // gets psi_i <- max(psi_i, kappa (3 nu_i / 4 pi)^(2/3)), kappa doubling
+        double kappa = 1.0;
+        while (!(stats3[1] > 0.0)) {
+            if (kappa > 1024.0) { S.status = 3; if (stats) *stats = S; return 0; }  // InitFailure
+            pf_internal_launches_add(1);
+            k_rescue<<<nblocks(n), RB, 0, st>>>(n, nu, w.vol, kappa, psi);
+            S.init_doublings++;
+            if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea, w.cent)) return -1;
+            if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
+            kappa *= 2.0;
+        }
     }
     const double floor_v = 0.5 * std::min(stats3[2], stats3[1]);
     const bool verbose = getenv("PF_NEWTON_VERBOSE") != nullptr;
@@ -522,7 +545,10 @@ __global__ void __launch_bounds__(RB) k_advect(int64_t n, double *__restrict__ x
         }
     }
 }
-// spring pressure F_p = (c - x)/eps^2, gravity m g, v += dt/m (F_p + F_g), m = rho nu
+// Gallouet-Merigot spring: pressure F_p = m (c - x) / eps^2,
+// gravity F_g = m g; v += dt/m (F_p + F_g) = dt ((c - x)/eps^2 + g), m = rho nu.
+// The spring is mass-proportional as in the scheme the paper follows; it is
+// the form for which SPEC.md's stability guideline dt <= eps holds.
 __global__ void __launch_bounds__(RB) k_forces(int64_t n, const double *__restrict__ x,
                                               const double *__restrict__ c, const double *__restrict__ nu,
                                               const double *__restrict__ rho, double *__restrict__ v,
@@ -532,7 +558,7 @@ __global__ void __launch_bounds__(RB) k_forces(int64_t n, const double *__restri
         const double m = rho[i] * nu[i];
 #pragma unroll
         for (int a = 0; a < 3; a++) {
-            double f = (c[3 * i + a] - x[3 * i + a]) * inv_eps2 + m * g[a];
+            double f = m * (c[3 * i + a] - x[3 * i + a]) * inv_eps2 + m * g[a];
             v[3 * i + a] += dt * f / m;
         }
     }

@@ -351,14 +351,17 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
-// Block-synchronous evaluation: one block of SYNC_WARPS warps per SM, one
+// Block-synchronous evaluation: blocks of SYNC_WARPS warps (2 per SM), one
 // cell per warp per round; the warps run each phase of the evaluation
 // together (__syncthreads between phases), so the SM's instruction caches
 // hold one phase at a time instead of the whole ~90 KB of evaluation code
 // (measured: the unsynchronised kernel spends half its stall samples on
 // instruction fetch).
-constexpr int SYNC_WARPS = 16;
-__global__ void __launch_bounds__(SYNC_WARPS * 32, 1)
+#ifndef PF_SYNC_WARPS
+#define PF_SYNC_WARPS 8
+#endif
+constexpr int SYNC_WARPS = PF_SYNC_WARPS;
+__global__ void __launch_bounds__(SYNC_WARPS * 32, 16 / SYNC_WARPS)
     k_cells_eval_sync(CellIn in, CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
                       const uint8_t *__restrict__ stage, int *__restrict__ retry_list,
                       int *__restrict__ counters, unsigned long long *__restrict__ err) {
@@ -558,7 +561,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         CK(cudaGetLastError());
         g_launches++;
         if (c->eval_sync) {
-            const int64_t sb = std::min<int64_t>(c->nsm, (count + SYNC_WARPS - 1) / SYNC_WARPS);
+            const int64_t sb = std::min<int64_t>(c->nsm * (16 / SYNC_WARPS), (count + SYNC_WARPS - 1) / SYNC_WARPS);
             k_cells_eval_sync<<<(int)sb, SYNC_WARPS * 32, SYNC_WARPS * sizeof(EWS<FastCaps>), st>>>(
                 in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
         } else {

@@ -172,6 +172,15 @@ class CudaOps:
     def cold_psi(self, kappa: float):
         self.psi.copy_(kappa * (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0))
 
+    def rescue(self, kappa: float):
+        """psi_i <- max(psi_i, kappa (3 nu_i/4 pi)^(2/3)) on the owned cells left empty."""
+        s = self.slots[0]
+        r = self.rows.long()
+        emp = ~(s["vol"].index_select(0, r) > 0.0)
+        cand = kappa * (3.0 * self.nu.index_select(0, r) / (4.0 * np.pi)) ** (2.0 / 3.0)
+        cur = self.psi.index_select(0, r)
+        self.psi.index_copy_(0, r, self.torch.where(emp, self.torch.maximum(cur, cand), cur))
+
     def psi_host(self, trial=False) -> np.ndarray:
         return (self.psi_t if trial else self.psi).cpu().numpy()
 
@@ -399,6 +408,16 @@ class DistNewton:
         else:
             S["evaluations"] += 1
             worst, vmin, nmin = self._evaluate()
+            kappa = 1.0  # warm start with per-cell rescue (SPEC.md init_weights)
+            while not vmin > 0.0:
+                if kappa > 1024.0:
+                    S["status"] = 3
+                    return self._result(S)
+                self.ops.rescue(kappa)
+                S["init_doublings"] += 1
+                S["evaluations"] += 1
+                worst, vmin, nmin = self._evaluate()
+                kappa *= 2.0
         floor_v = 0.5 * min(nmin, vmin)
         S["worst_initial"] = worst
         for _ in range(max_newton):

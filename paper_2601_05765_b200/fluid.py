@@ -22,6 +22,16 @@ from . import _lib, solver
 from .geom import ConvexCell
 
 
+class OtNonConvergence(RuntimeError):
+    """The step's Newton solve did not converge (SPEC.md fluid_sim.step errors):
+    the simulation halts with the flagged state attached."""
+
+    def __init__(self, diag: dict, state: "FluidState"):
+        super().__init__(f"step {diag['step']}: Newton {diag['status_name']}")
+        self.diag = diag
+        self.state = state
+
+
 @dataclass
 class FluidState:
     x: "torch.Tensor"       # [n,3] positions (sites)
@@ -43,6 +53,7 @@ class SimParams:
     eps_vol: float = 0.01
     max_newton: int = 100
     smf: int = 32
+    best_effort: bool = False  # continue past a non-converged solve (SPEC.md --best-effort)
 
 
 def _bind():
@@ -96,6 +107,9 @@ def step(state: FluidState, params: SimParams, domain: ConvexCell) -> dict:
     state.step_index += 1
     state.time += params.dt
     diag = {"step": state.step_index, **{k: res.stats[k] for k in
-            ("status_name", "iterations", "evaluations", "cg_iterations", "worst_final")}}
+            ("status_name", "iterations", "evaluations", "cg_iterations", "damping_halvings",
+                 "worst_final")}}
     state.history.append(diag)
+    if res.stats["status"] != 0 and not params.best_effort:
+        raise OtNonConvergence(diag, state)
     return diag

@@ -37,6 +37,13 @@ class NumpyOps:
     def cold_psi(self, kappa):
         self.psi[:] = kappa * (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0)
 
+    def rescue(self, kappa):
+        o = self.slots[0]
+        r = self.rows
+        e = ~(o["vol"][r] > 0.0)
+        rr = r[e]
+        self.psi[rr] = np.maximum(self.psi[rr], kappa * (3.0 * self.nu[rr] / (4.0 * np.pi)) ** (2.0 / 3.0))
+
     def psi_host(self, trial=False):
         return (self.psi_t if trial else self.psi).copy()
 

@@ -38,7 +38,7 @@ def test_dam_break_steps():
                                   _lib.stream_ptr())
         m = (st.rho * st.nu)[:, None]
         g = torch.tensor(prm.gravity, dtype=torch.float64, device="cuda")
-        v_ref = torch.where(inside, v0, -v0) + prm.dt * ((cent - st.x) / prm.eps ** 2 + m * g) / m
+        v_ref = torch.where(inside, v0, -v0) + prm.dt * (m * (cent - st.x) / prm.eps ** 2 + m * g) / m
         assert torch.allclose(st.v, v_ref, rtol=1e-12, atol=1e-12)
     # total volume conserved within n * eps_vol * mean(nu) (SPEC.md fluid invariants)
     vol = solver.last_state(sc.n, prm.smf)[0]
