@@ -99,6 +99,17 @@ def newton_solve(pts, nu, dom_args, tol, domain_diag, psi_init=None, eps_vol=0.0
         stats["evaluations"] += 1
         # warm start with per-cell rescue (SPEC.md init_weights): empty cells get
         # psi_i <- max(psi_i, kappa (3 nu_i / 4 pi)^(2/3)), kappa doubling
+        if not o["vol"].min() > 0.0:
+            # an empty cell first takes the weight of its nearest other site
+            from scipy.spatial import cKDTree
+
+            e = np.nonzero(~(o["vol"] > 0.0))[0]
+            _, nn = cKDTree(pts).query(pts[e], k=2)
+            j = np.where(nn[:, 0] == e, nn[:, 1], nn[:, 0])
+            psi[e] = np.maximum(psi[e], psi[j])
+            stats["init_doublings"] += 1
+            o = _evaluate(pts, psi, dom_args, tol, grid, smf)
+            stats["evaluations"] += 1
         kappa = 1.0
         while not o["vol"].min() > 0.0:
             if kappa > 1024.0:

@@ -266,6 +266,27 @@ __global__ void __launch_bounds__(RB) k_axpy_to(int64_t n, const double *__restr
         out[i] = a[i] + s * b[i];
 }
 
+// list of the empty cells and their positions
+__global__ void __launch_bounds__(RB) k_empty_list(int64_t n, const double *__restrict__ vol,
+                                                  const double *__restrict__ pts, int *__restrict__ list,
+                                                  double *__restrict__ q, int *__restrict__ count) {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        if (!(vol[i] > 0.0)) {
+            const int k = atomicAdd(count, 1);
+            list[k] = (int)i;
+            q[3 * k] = pts[3 * i]; q[3 * k + 1] = pts[3 * i + 1]; q[3 * k + 2] = pts[3 * i + 2];
+        }
+}
+// psi_i <- max(psi_i, psi_j), j the nearest other site of the empty cell i
+__global__ void __launch_bounds__(RB) k_rescue_nn(int m, const int *__restrict__ list,
+                                                 const int64_t *__restrict__ nn, double *__restrict__ psi) {
+    for (int t = blockIdx.x * RB + threadIdx.x; t < m; t += gridDim.x * RB) {
+        const int i = list[t];
+        const int64_t j = nn[2 * t] == i ? nn[2 * t + 1] : nn[2 * t];
+        if (j >= 0 && psi[j] > psi[i]) psi[i] = psi[j];
+    }
+}
+
 // rescue of the cells a warm start leaves empty (SPEC.md init_weights)
 __global__ void __launch_bounds__(RB) k_rescue(int64_t n, const double *__restrict__ nu,
                                               const double *__restrict__ vol, double kappa,
@@ -329,6 +350,35 @@ int ws_alloc(int64_t n, int smf) {
 }
 
 int nblocks(int64_t n) { return (int)std::min<int64_t>(NPART, std::max<int64_t>(1, (n + RB - 1) / RB)); }
+
+int rescue_nearest(pf_ctx *ctx, int64_t n, const double *pts, const double *vol, double *psi, cudaStream_t st) {
+    int *list = nullptr, *cnt = nullptr;
+    double *q = nullptr;
+    int64_t *nn = nullptr;
+    NCK(cudaMallocAsync((void **)&cnt, sizeof(int), st));
+    NCK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+    NCK(cudaMallocAsync((void **)&list, n * sizeof(int), st));
+    NCK(cudaMallocAsync((void **)&q, 3 * n * sizeof(double), st));
+    pf_internal_launches_add(1);
+    k_empty_list<<<nblocks(n), RB, 0, st>>>(n, vol, pts, list, q, cnt);
+    int m = 0;
+    NCK(cudaMemcpyAsync(&m, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NCK(cudaStreamSynchronize(st));
+    int rc = 0;
+    if (m > 0) {
+        NCK(cudaMallocAsync((void **)&nn, 2 * (size_t)m * sizeof(int64_t), st));
+        if (pf_knn(ctx, n, pts, m, q, 2, nn, st) < 0) rc = -1;
+        if (!rc) {
+            pf_internal_launches_add(1);
+            k_rescue_nn<<<nblocks(m), RB, 0, st>>>(m, list, nn, psi);
+        }
+        NCK(cudaFreeAsync(nn, st));
+    }
+    NCK(cudaFreeAsync(q, st));
+    NCK(cudaFreeAsync(list, st));
+    NCK(cudaFreeAsync(cnt, st));
+    return rc;
+}
 
 // (worst, min vol, min nu) of the current evaluation
 int grad_stats(int64_t n, const double *nu, const double *vol, double *g, double *out_host,
@@ -434,8 +484,16 @@ extern "C" int pf_newton_solve(pf_ctx *ctx, int64_t n, const double *pts, const 
     } else {
         if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea, w.cent)) return -1;
         if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
-        // warm start with per-cell rescue (SPEC.md init_weights): an empty cell
-        // gets psi_i <- max(psi_i, kappa (3 nu_i / 4 pi)^(2/3)), kappa doubling
+        // warm start with per-cell rescue (SPEC.md init_weights).  First an
+        // empty cell takes the weight of its nearest site (a near-coincident
+        // pair then splits at its midpoint instead of ping-ponging through the
+        // doubling below), then psi_i <- max(psi_i, kappa (3 nu_i / 4 pi)^(2/3)).
+        if (!(stats3[1] > 0.0)) {
+            if (rescue_nearest(ctx, n, pts, w.vol, psi, st)) return -1;
+            S.init_doublings++;
+            if (evaluate(psi, w.vol, w.ksur, w.fcount, w.ftag, w.farea, w.cent)) return -1;
+            if (grad_stats(n, nu, w.vol, w.g, stats3, st)) return -1;
+        }
         double kappa = 1.0;
         while (!(stats3[1] > 0.0)) {
             if (kappa > 1024.0) { S.status = 3; if (stats) *stats = S; return 0; }  // InitFailure

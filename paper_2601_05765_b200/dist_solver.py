@@ -172,6 +172,25 @@ class CudaOps:
     def cold_psi(self, kappa: float):
         self.psi.copy_(kappa * (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0))
 
+    def vec_psi(self):
+        return self.psi
+
+    def rescue_nearest(self):
+        """An owned empty cell takes the weight of its nearest other site."""
+        torch = self.torch
+        s = self.slots[0]
+        r = self.rows.long()
+        e = r[~(s["vol"].index_select(0, r) > 0.0)]
+        m = int(e.numel())
+        if m == 0:
+            return
+        q = self.pts.index_select(0, e).contiguous()
+        nn = torch.empty((m, 2), dtype=torch.int64, device="cuda")
+        self.chk(self._lib.lib().pf_knn(self.ctx, self.n, self.p(self.pts), m, self.p(q), 2, self.p(nn),
+                                        self._s()), "pf_knn")
+        j = torch.where(nn[:, 0] == e, nn[:, 1], nn[:, 0])
+        self.psi.index_copy_(0, e, torch.maximum(self.psi.index_select(0, e), self.psi.index_select(0, j)))
+
     def rescue(self, kappa: float):
         """psi_i <- max(psi_i, kappa (3 nu_i/4 pi)^(2/3)) on the owned cells left empty."""
         s = self.slots[0]
@@ -408,12 +427,19 @@ class DistNewton:
         else:
             S["evaluations"] += 1
             worst, vmin, nmin = self._evaluate()
-            kappa = 1.0  # warm start with per-cell rescue (SPEC.md init_weights)
+            if not vmin > 0.0:  # warm start with per-cell rescue (SPEC.md init_weights)
+                self.ops.rescue_nearest()
+                self.comm.exchange(self.ops.vec_psi(), self.plan, self.idx_send, self.idx_recv)
+                S["init_doublings"] += 1
+                S["evaluations"] += 1
+                worst, vmin, nmin = self._evaluate()
+            kappa = 1.0
             while not vmin > 0.0:
                 if kappa > 1024.0:
                     S["status"] = 3
                     return self._result(S)
                 self.ops.rescue(kappa)
+                self.comm.exchange(self.ops.vec_psi(), self.plan, self.idx_send, self.idx_recv)
                 S["init_doublings"] += 1
                 S["evaluations"] += 1
                 worst, vmin, nmin = self._evaluate()

@@ -37,6 +37,21 @@ class NumpyOps:
     def cold_psi(self, kappa):
         self.psi[:] = kappa * (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0)
 
+    def vec_psi(self):
+        return torch.from_numpy(self.psi)
+
+    def rescue_nearest(self):
+        from scipy.spatial import cKDTree
+
+        o = self.slots[0]
+        r = self.rows
+        e = r[~(o["vol"][r] > 0.0)]
+        if len(e) == 0:
+            return
+        _, nn = cKDTree(self.pts).query(self.pts[e], k=2)
+        j = np.where(nn[:, 0] == e, nn[:, 1], nn[:, 0])
+        self.psi[e] = np.maximum(self.psi[e], self.psi[j])
+
     def rescue(self, kappa):
         o = self.slots[0]
         r = self.rows

@@ -43,3 +43,23 @@ def test_dam_break_steps():
     # total volume conserved within n * eps_vol * mean(nu) (SPEC.md fluid invariants)
     vol = solver.last_state(sc.n, prm.smf)[0]
     assert abs(float(vol.sum()) - float(sc.nu.sum())) <= sc.n * prm.eps_vol * float(sc.nu.mean())
+
+
+def test_chocs_wall_impact_converges():
+    """C3 (BASELINE configs[2]): 500k particles flying radially at 5 m/s hit the
+    walls around step 50; every step's warm-started Newton solve converges,
+    the KMT line search is exercised, and the nearest-site rescue keeps the
+    warm start valid through the impact."""
+    from paper_2601_05765_b200 import fluid, geom, scenes
+
+    sc = scenes.c3_chocs()
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    st = fluid.make_state(sc.pts, sc.vel, sc.nu, sc.rho)
+    prm = fluid.SimParams(dt=1e-3, eps=5e-3)
+    halvings = 0
+    for _ in range(60):
+        d = fluid.step(st, prm, dom)  # raises OtNonConvergence on failure
+        assert d["worst_final"] <= prm.eps_vol
+        halvings += d["damping_halvings"]
+    assert halvings > 0
+    assert float(st.x.min()) > 0.0 and float(st.x.max()) < 1.0
