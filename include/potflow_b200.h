@@ -209,6 +209,17 @@ int pf_fluid_advect(int64_t n, double *x, double *v, double dt, const double *lo
 int pf_fluid_forces(int64_t n, const double *x, const double *cent, const double *nu, const double *rho,
                     double *v, double dt, double eps, const double *g_host, void *stream);
 
+/* implicit velocity update with viscosity mu (fluid graph Laplacian, P1 weights
+ * |B_ij|/(2|p_j-p_i|)), wall friction mu_b (boundary weights, zero wall velocity) and
+ * surface tension gamma: three Jacobi-PCG solves of (m/dt I + mu L) v = m/dt v + F_p + F_g + F_t
+ * on the final evaluation of the step.  Returns the CG iteration total. */
+int pf_fluid_forces_implicit(int64_t n, int smf, const double *x, const double *cent, const double *vol,
+                             const int32_t *fcount, const int32_t *ftag, const double *farea, const double *nu,
+                             const double *rho, double *v, double dt, double eps, const double *g_host,
+                             double mu, double mu_b, double gamma, double affinity, const double *dplanes,
+                             int ndom, int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
+                             double *sol, double rtol, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

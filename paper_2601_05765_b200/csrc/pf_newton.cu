@@ -621,6 +621,74 @@ __global__ void __launch_bounds__(RB) k_forces(int64_t n, const double *__restri
         }
     }
 }
+// ---- full fluid forces ----
+// P1 Laplacian weights from the restricted facets: w_ij = |B_ij| / (2 |p_j - p_i|)
+// (PAPER Eq. 3); boundary weights w_iOmega = mu_b |B_iOmega| / (2 d(p_i, Omega) |V_i|)
+// (SPEC laplacian_weights, as printed).  One row per cell:
+//   A = m/dt I + mu L (+ boundary weights on the diagonal: zero wall velocity)
+//   rhs_a = m/dt v_a + F_p + F_g + F_t,
+//   F_t = gamma (sum_j w_ij (x_j - x_i) + sum_b affinity w^g_b (g_b - x_i)),
+// g_b = orthogonal projection of x_i on the wall plane, moved |V_i|^(1/3) to the
+// fluid side (SPEC surface_tension_force), w^g_b = |B_b| / (2 |g_b - x_i|).
+__global__ void __launch_bounds__(RB) k_fluid_system(
+    int64_t n, int smf, const double *__restrict__ x, const double *__restrict__ cent,
+    const double *__restrict__ vol, const int *__restrict__ fcount, const int *__restrict__ ftag,
+    const double *__restrict__ farea, const double *__restrict__ nu, const double *__restrict__ rho,
+    const double *__restrict__ v, double dt, double inv_eps2, double g0, double g1, double g2, double mu,
+    double mu_b, double gamma, double affinity, const double *__restrict__ dplanes, int ndom,
+    int *__restrict__ hcnt, int *__restrict__ hcol, double *__restrict__ hval, double *__restrict__ diag,
+    double *__restrict__ rhs) {
+    const double g[3] = {g0, g1, g2};
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        const double m = rho[i] * nu[i];
+        const double px = x[3 * i], py = x[3 * i + 1], pz = x[3 * i + 2];
+        int c = fcount[i];
+        if (c > smf) c = smf;
+        double d = m / dt, ft[3] = {0.0, 0.0, 0.0};
+        int k = 0;
+        const double vi = vol[i] > 0.0 ? vol[i] : nu[i];
+        for (int s = 0; s < c; s++) {
+            const int64_t j = ftag[i * smf + s];
+            const double A = farea[i * smf + s];
+            if (j >= 0) {
+                const double dx = x[3 * j] - px, dy = x[3 * j + 1] - py, dz = x[3 * j + 2] - pz;
+                const double w = 0.5 * A / sqrt(dx * dx + dy * dy + dz * dz);
+                hcol[i * smf + k] = (int)j;
+                hval[i * smf + k] = -mu * w;
+                d += mu * w;
+                k++;
+                ft[0] += w * dx; ft[1] += w * dy; ft[2] += w * dz;
+            } else {
+                const int b = (int)(-j - 1);
+                if (b >= ndom) continue;
+                const double nx = dplanes[4 * b], ny = dplanes[4 * b + 1], nz = dplanes[4 * b + 2];
+                const double dist = dplanes[4 * b + 3] - (nx * px + ny * py + nz * pz);  // >= 0 inside
+                const double dd = dist > 1e-300 ? dist : 1e-300;
+                d += mu_b * 0.5 * A / (dd * vi);
+                // ghost: projection on the wall, |V_i|^(1/3) back toward the fluid
+                const double off = dist - cbrt(vi);
+                const double gx = off * nx, gy = off * ny, gz = off * nz;  // g - x
+                const double gl = sqrt(gx * gx + gy * gy + gz * gz);
+                if (gl > 0.0) {
+                    const double wg = affinity * 0.5 * A / gl;
+                    ft[0] += wg * gx; ft[1] += wg * gy; ft[2] += wg * gz;
+                }
+            }
+        }
+        hcnt[i] = k;
+        diag[i] = d;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const double fp = m * (cent[3 * i + a] - x[3 * i + a]) * inv_eps2;
+            rhs[a * n + i] = m / dt * v[3 * i + a] + fp + m * g[a] + gamma * ft[a];
+        }
+    }
+}
+__global__ void __launch_bounds__(RB) k_scatter_v(int64_t n, const double *__restrict__ sol, int a,
+                                                 double *__restrict__ v) {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        v[3 * i + a] = sol[i];
+}
 }  // namespace
 
 extern "C" int pf_fluid_advect(int64_t n, double *x, double *v, double dt, const double *lo_host,
@@ -640,4 +708,34 @@ extern "C" int pf_fluid_forces(int64_t n, const double *x, const double *cent, c
                                                           g_host[0], g_host[1], g_host[2]);
     NCK(cudaGetLastError());
     return 0;
+}
+
+// implicit velocity update with viscosity, boundary friction and surface
+// tension (SPEC.md fluid_sim assemble_viscosity_system / surface_tension_force):
+// three Jacobi-PCG solves (one per axis) on (m/dt I + mu L); returns the total
+// CG iteration count.  Scratch: hcnt i32[n], hcol i32[n,smf], hval f64[n,smf],
+// diag f64[n], rhs f64[3n], sol f64[n].
+extern "C" int pf_fluid_forces_implicit(int64_t n, int smf, const double *x, const double *cent,
+                                        const double *vol, const int32_t *fcount, const int32_t *ftag,
+                                        const double *farea, const double *nu, const double *rho, double *v,
+                                        double dt, double eps, const double *g_host, double mu, double mu_b,
+                                        double gamma, double affinity, const double *dplanes, int ndom,
+                                        int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
+                                        double *sol, double rtol, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    pf_internal_launches_add(1);
+    k_fluid_system<<<nblocks(n), RB, 0, st>>>(n, smf, x, cent, vol, fcount, ftag, farea, nu, rho, v, dt,
+                                               1.0 / (eps * eps), g_host[0], g_host[1], g_host[2], mu, mu_b,
+                                               gamma, affinity, dplanes, ndom, hcnt, hcol, hval, diag, rhs);
+    NCK(cudaGetLastError());
+    int total = 0;
+    for (int a = 0; a < 3; a++) {
+        int it = pf_pcg(n, smf, hcnt, hcol, hval, diag, rhs + a * n, sol, rtol, 10000, stream);
+        if (it < 0) return -1;
+        total += it;
+        pf_internal_launches_add(1);
+        k_scatter_v<<<nblocks(n), RB, 0, st>>>(n, sol, a, v);
+        NCK(cudaGetLastError());
+    }
+    return total;
 }

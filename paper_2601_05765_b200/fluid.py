@@ -7,9 +7,16 @@ PAPER.md:332-334 and 374-381); this is its in-scope part:
     psi <- newton_solve(x, nu, warm psi)
     F_p = (c_i - x_i) / eps^2,  F_g = m g,  v <- v + dt/m (F_p + F_g)
 
-Viscosity and surface tension are out of scope.
-All state stays in device tensors; the per-particle updates are CUDA kernels
-in libpotflow_b200.so (pf_fluid_advect / pf_fluid_forces).
+With viscosity, wall friction or surface tension (the first
+"next" row of SURVEY §8(f)) the velocity update is implicit:
+
+    (m/dt I + mu L) v <- m/dt v + F_p + F_g + F_t      (Eq. 4)
+
+L the fluid graph Laplacian with the P1 weights |B_ij| / (2 |p_j - p_i|) of the
+step's restricted facets (wall facets: zero wall velocity), F_t = gamma times the
+graph Laplacian of the positions with wall ghosts; three Jacobi-PCG solves
+(pf_fluid_forces_implicit).  All state stays in device tensors; the
+per-particle updates are CUDA kernels in libpotflow_b200.so.
 """
 from __future__ import annotations
 
@@ -54,12 +61,21 @@ class SimParams:
     max_newton: int = 100
     smf: int = 32
     best_effort: bool = False  # continue past a non-converged solve (SPEC.md --best-effort)
+    viscosity: float = 0.0            # mu (fluid-fluid)
+    boundary_viscosity: float = 0.0   # mu_b (fluid-wall friction, zero wall velocity)
+    surface_tension: float = 0.0      # gamma
+    boundary_affinity: float = 1.0    # weight of the wall ghosts in the surface-tension Laplacian
+    implicit: bool | None = None      # None: implicit iff any of the three above is non-zero
+    visc_rtol: float = 1e-10
 
 
 def _bind():
     L = solver._bind()
     if not getattr(L, "_fluid_bound", False):
-        vp, i64, d = C.c_void_p, C.c_int64, C.c_double
+        vp, i64, d, i = C.c_void_p, C.c_int64, C.c_double, C.c_int
+        L.pf_fluid_forces_implicit.argtypes = ([i64, i] + [vp] * 9 + [d, d, vp, d, d, d, d, vp, i]
+                                               + [vp] * 6 + [d, vp])
+        L.pf_fluid_forces_implicit.restype = C.c_int
         L.pf_fluid_advect.argtypes = [i64, vp, vp, d, vp, vp, d, vp]
         L.pf_fluid_advect.restype = C.c_int
         L.pf_fluid_forces.argtypes = [i64, vp, vp, vp, vp, vp, d, d, vp, vp]
@@ -99,17 +115,51 @@ def step(state: FluidState, params: SimParams, domain: ConvexCell) -> dict:
     cent = torch.empty((n, 3), dtype=torch.float64, device="cuda")
     _lib.check(L.pf_newton_last_state_ex(None, None, None, None, None, _lib.ptr(cent), n, params.smf, s),
                "pf_newton_last_state_ex")
-    # (5)-(7) spring pressure + gravity, velocity update
+    # (5)-(7) spring pressure + gravity (+ surface tension, viscosity), velocity update
     g = (C.c_double * 3)(*[float(v) for v in params.gravity])
-    _lib.check(L.pf_fluid_forces(n, _lib.ptr(state.x), _lib.ptr(cent), _lib.ptr(state.nu),
-                                 _lib.ptr(state.rho), _lib.ptr(state.v), float(params.dt),
-                                 float(params.eps), g, s), "pf_fluid_forces")
+    implicit = params.implicit
+    if implicit is None:
+        implicit = bool(params.viscosity or params.boundary_viscosity or params.surface_tension)
+    visc_cg = 0
+    if implicit:
+        visc_cg = implicit_forces(state, params, domain, cent, g)
+    else:
+        _lib.check(L.pf_fluid_forces(n, _lib.ptr(state.x), _lib.ptr(cent), _lib.ptr(state.nu),
+                                     _lib.ptr(state.rho), _lib.ptr(state.v), float(params.dt),
+                                     float(params.eps), g, s), "pf_fluid_forces")
     state.step_index += 1
     state.time += params.dt
     diag = {"step": state.step_index, **{k: res.stats[k] for k in
             ("status_name", "iterations", "evaluations", "cg_iterations", "damping_halvings",
                  "worst_final")}}
+    diag["viscosity_cg_iterations"] = visc_cg
     state.history.append(diag)
     if res.stats["status"] != 0 and not params.best_effort:
         raise OtNonConvergence(diag, state)
     return diag
+
+
+def implicit_forces(state: FluidState, params: SimParams, domain: ConvexCell, cent, g) -> int:
+    """Implicit velocity update on the step's final evaluation (see module doc)."""
+    import torch
+
+    from .laguerre import domain_pack
+
+    L = _bind()
+    n, smf = state.x.shape[0], params.smf
+    vol, _, fcount, ftag, farea = solver.last_state(n, smf)
+    dpk = domain_pack(domain)
+    ndom = int(dpk.args()[1][1])
+    planes = torch.as_tensor(np.ascontiguousarray(dpk.args()[2][:ndom]), dtype=torch.float64, device="cuda")
+    f8, i4 = dict(dtype=torch.float64, device="cuda"), dict(dtype=torch.int32, device="cuda")
+    hcnt, hcol = torch.empty(n, **i4), torch.empty((n, smf), **i4)
+    hval, diag = torch.empty((n, smf), **f8), torch.empty(n, **f8)
+    rhs, sol = torch.empty(3 * n, **f8), torch.empty(n, **f8)
+    P = _lib.ptr
+    it = L.pf_fluid_forces_implicit(
+        n, smf, P(state.x), P(cent), P(vol), P(fcount), P(ftag), P(farea), P(state.nu), P(state.rho),
+        P(state.v), float(params.dt), float(params.eps), g, float(params.viscosity),
+        float(params.boundary_viscosity), float(params.surface_tension), float(params.boundary_affinity),
+        P(planes), ndom, P(hcnt), P(hcol), P(hval), P(diag), P(rhs), P(sol), float(params.visc_rtol),
+        _lib.stream_ptr())
+    return _lib.check(it, "pf_fluid_forces_implicit")
