@@ -114,6 +114,16 @@ int pf_batch_evaluate_async(pf_ctx *ctx, int64_t n, const double *pts, const dou
                             int64_t *fcount, int64_t *ftag, double *farea, double *fh, double *fnrm,
                             double *fcent, const int32_t *cells, int64_t ncells, int32_t *cell_flags,
                             int64_t *err_accum, int rebuild_grid, void *stream);
+/* _kernels._batch_build (_kernels.py:1481-1559): every
+ * unrestricted Laguerre cell into fixed-stride packed arrays in the reference's
+ * layout -- status (0 ok / 1 empty / 3 overflow), counts, verts f64[n,smv,3],
+ * planes f64[n,smf,4], tags/lp/lv int64 -- and the OR of the cell flags.
+ * Used by laguerre.build_diagram_packed (laguerre.py:226-265). */
+int64_t pf_batch_build(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double tol,
+                       double dpsi_max, int ball_aware, int64_t smv, int64_t smf, int64_t sml,
+                       int64_t *status, int64_t *nv, int64_t *nf, int64_t *nl, double *verts, double *planes,
+                       int64_t *tags, int64_t *lp, int64_t *lv, int rebuild_grid, void *stream);
+
 /* bucket-ordered permutation of the sites of the current grid (int32[n]) */
 int pf_grid_order(pf_ctx *ctx, int32_t *order, void *stream);
 

@@ -5,6 +5,7 @@ same returned flag word as /root/reference/pkg/src/potflow/_kernels.py, but
 the work runs on the B200 through libpotflow_b200.so:
 
 * ``_batch_evaluate``  _kernels.py:1362-1478 -> pf_batch_evaluate
+* ``_batch_build``     _kernels.py:1481-1559 -> pf_batch_build
 * ``_knn``             _kernels.py:1562-1620 -> pf_knn
 
 Arrays may be numpy (copied to the device and back, as a drop-in for the numba
@@ -150,6 +151,38 @@ def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, o
         if t is None:
             h[...] = d.cpu().numpy().reshape(h.shape)
     return int(err_acc.item())
+
+
+def _batch_build(pts, psi, dv, dc, dp, dt, dlp, dlv,
+                 grid_start, grid_sites, lox, loy, loz, ihx, ihy, ihz,
+                 gnx, gny, gnz, h_min, tol, dpsi_max, ball_aware,
+                 smv, smf, sml,
+                 out_status, out_nv, out_nf, out_nl,
+                 out_verts, out_planes, out_tags, out_lp, out_lv):
+    """Build every Laguerre cell into fixed-stride packed storage (returns the flag word)."""
+    import torch
+
+    f8, i8 = torch.float64, torch.int64
+    outs_host = [out_status, out_nv, out_nf, out_nl, out_verts, out_planes, out_tags, out_lp, out_lv]
+    dtypes = [i8, i8, i8, i8, f8, f8, i8, i8, i8]
+    c = _lib.ctx()
+    upload_domain(c, _host(dv), _host(dc), _host(dp), _host(dt), _host(dlp), _host(dlv), float(tol))
+    on_device = _is_torch(pts)
+    p, w = _to_dev(pts, f8), _to_dev(psi, f8)
+    if on_device:
+        outs = [_to_dev(o, t) for o, t in zip(outs_host, dtypes)]
+    else:
+        # the reference writes only the used prefix of each row: start from the caller's arrays
+        outs = [torch.from_numpy(np.ascontiguousarray(o)).to("cuda") for o in outs_host]
+    n = int(p.shape[0])
+    err = int(_lib.lib().pf_batch_build(
+        c, n, _lib.ptr(p), _lib.ptr(w), float(tol), float(dpsi_max), int(bool(ball_aware)), int(smv),
+        int(smf), int(sml), *[_lib.ptr(o) for o in outs], 1, _lib.stream_ptr()))
+    _lib.check(err, "pf_batch_build")
+    if not on_device:
+        for h, d in zip(outs_host, outs):
+            h[...] = d.cpu().numpy().reshape(h.shape)
+    return err
 
 
 def _knn(pts, grid_start, grid_sites, lox, loy, loz, ihx, ihy, ihz,

@@ -61,6 +61,8 @@ def lib():
         L.pf_batch_evaluate_async.restype = i
         L.pf_batch_evaluate_async.argtypes = ([vp, i64, vp, vp, d, d, i, i, i64] + [vp] * 12
                                               + [vp, i64, vp, vp, i, vp])
+        L.pf_batch_build.restype = i64
+        L.pf_batch_build.argtypes = [vp, i64, vp, vp, d, d, i, i64, i64, i64] + [vp] * 9 + [i, vp]
         L.pf_grid_order.restype = i
         L.pf_grid_order.argtypes = [vp, vp, vp]
         L.pf_knn.restype = i64

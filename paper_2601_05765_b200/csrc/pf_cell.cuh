@@ -188,6 +188,11 @@ struct CellOut {
     int *flags;     // [n] per-cell flag word (incl. FLAG_RETRY)
     int *census;    // [n] processed candidates (clips attempted)
     int *census16;  // [n, 16] full census (CEN_*), optional
+    // unrestricted packed cells (_batch_build, _kernels.py:1481-1559): when
+    // pk_status is set the build writes these and no evaluation follows
+    int64_t *pk_status, *pk_nv, *pk_nf, *pk_nl, *pk_tags, *pk_lp, *pk_lv;
+    double *pk_verts, *pk_planes;
+    int smv, smfb, sml;
 };
 
 PF_DEV double sq(double x) { return x * x; }
@@ -1837,6 +1842,40 @@ PF_DEV void evaluate_cell(W *ws, const Poly<typename W::Cap> &P, double px, doub
 // Phase A of one cell: build.  Returns -1 when the cell needs evaluation
 // (polytope in ws->P[*which]), else the cell's final flag word with its
 // outputs already written (empty / overflow), or FLAG_RETRY.
+// _batch_build's per-cell output (_kernels.py:1508-1555): status 1 empty
+// (counts 0), 3 overflow (build overflow or beyond the caller's strides), 0 ok
+template <class W>
+PF_NOINL int write_packed(W *ws, const CellOut &out, int i, int st, int which) {
+    const int L = pfw::lane();
+    const Poly<typename W::Cap> &A = ws->P[which];
+    if (st == 1) {
+        if (L == 0) { out.pk_status[i] = 1; out.pk_nv[i] = 0; out.pk_nf[i] = 0; out.pk_nl[i] = 0; }
+        return 0;
+    }
+    if (st == 3 || A.nv > out.smv || A.nf > out.smfb || A.nl > out.sml) {
+        if (L == 0) out.pk_status[i] = 3;
+        return FLAG_OVERFLOW;
+    }
+    const size_t iv = (size_t)i * out.smv, jf = (size_t)i * out.smfb, kl = (size_t)i * out.sml;
+    #pragma unroll 1
+    for (int v = L; v < A.nv; v += 32) {
+        out.pk_verts[3 * (iv + v)] = A.x[v]; out.pk_verts[3 * (iv + v) + 1] = A.y[v];
+        out.pk_verts[3 * (iv + v) + 2] = A.z[v];
+    }
+    #pragma unroll 1
+    for (int f = L; f < A.nf; f += 32) {
+        out.pk_planes[4 * (jf + f)] = A.nx[f]; out.pk_planes[4 * (jf + f) + 1] = A.ny[f];
+        out.pk_planes[4 * (jf + f) + 2] = A.nz[f]; out.pk_planes[4 * (jf + f) + 3] = A.d[f];
+        out.pk_tags[jf + f] = A.tag[f];
+    }
+    #pragma unroll 1
+    for (int f = L; f <= A.nf; f += 32) out.pk_lp[(size_t)i * (out.smfb + 1) + f] = A.lp[f];
+    #pragma unroll 1
+    for (int k = L; k < A.nl; k += 32) out.pk_lv[kl + k] = A.lv[k];
+    if (L == 0) { out.pk_status[i] = 0; out.pk_nv[i] = A.nv; out.pk_nf[i] = A.nf; out.pk_nl[i] = A.nl; }
+    return 0;
+}
+
 template <class W>
 PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, int *which) {
     const int L = pfw::lane();
@@ -1855,6 +1894,7 @@ PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, 
         st = 3;
     }
     if (out.census && L == 0) out.census[i] = nclips;
+    if (out.pk_status) return write_packed(ws, out, i, st, *which);
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     if (st == 3) {
         if (L == 0) {

@@ -907,6 +907,38 @@ int pf_evaluate_lean(pf_ctx *c, int64_t n, const double *pts, const double *psi,
     return 0;
 }
 
+// _kernels._batch_build (_kernels.py:1481-1559): every unrestricted Laguerre
+// cell (ball-aware or full security-radius mode) into the caller's
+// fixed-stride packed arrays; returns the OR of the cells' flags
+int64_t pf_batch_build(pf_ctx *c, int64_t n, const double *pts, const double *psi, double tol,
+                       double dpsi_max, int ball_aware, int64_t smv, int64_t smf, int64_t sml,
+                       int64_t *status, int64_t *nv, int64_t *nf, int64_t *nl, double *verts, double *planes,
+                       int64_t *tags, int64_t *lp, int64_t *lv, int rebuild_grid, void *stream) {
+    cudaStream_t st = S(stream);
+    if (!c->has_domain) return set_err("pf_batch_build: no domain set");
+    if (n < 0 || n > 0x7fffffff) return set_err("pf_batch_build: bad n");
+    if (rebuild_grid || c->grid_n != n || c->grid_pts != pts) {
+        if (grid_build(c, n, pts, psi, 0.0, st)) return -1;
+    }
+    if (dpsi_max < 0.0 && dpsi_dev(c, n, psi, st)) return -1;
+    if (ensure(&c->census, &c->census_cap, (size_t)n + 1)) return -1;
+    CellIn in;
+    fill_cellin(c, in, n, pts, psi, tol, dpsi_max, ball_aware, 0);
+    CellOut out;
+    memset(&out, 0, sizeof out);
+    out.census = c->census;
+    out.pk_status = status; out.pk_nv = nv; out.pk_nf = nf; out.pk_nl = nl;
+    out.pk_verts = verts; out.pk_planes = planes; out.pk_tags = tags; out.pk_lp = lp; out.pk_lv = lv;
+    out.smv = (int)smv; out.smfb = (int)smf; out.sml = (int)sml;
+    if (n > 0 && launch_cells(c, in, out, n, st)) return -1;
+    unsigned long long e = 0;
+    if (n > 0) {
+        CK(cudaMemcpyAsync(&e, c->err, sizeof e, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return (int64_t)e;
+}
+
 // lean evaluation of a subset of the cells with a given weight slack dpsi
 // (the partitioned solve: owned cells of a slab, all-reduced dpsi)
 int pf_evaluate_lean_cells(pf_ctx *c, int64_t n, const double *pts, const double *psi, double dpsi,

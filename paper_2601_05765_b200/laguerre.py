@@ -200,3 +200,77 @@ def knn(grid: SpatialGrid, q, k: int, domain: ConvexCell | None = None) -> np.nd
         domain = box_domain(lo, hi)
     return knn_batch(grid.points, np.asarray(q, dtype=np.float64).reshape(1, 3), k,
                      domain)[0].cpu().numpy()
+
+
+class PackedDiagram:
+    """All unrestricted Laguerre cells in fixed-stride packed storage
+    (laguerre.py:186-222 of the reference; host numpy arrays)."""
+
+    def __init__(self, pts, psi, status, nv, nf, nl, verts, planes, tags, lp, lv, domain: ConvexCell):
+        self.pts, self.psi = pts, psi
+        self.status, self.nv, self.nf, self.nl = status, nv, nf, nl  # status 0 ok, 1 empty
+        self.verts, self.planes, self.tags, self.lp, self.lv = verts, planes, tags, lp, lv
+        self.domain = domain
+
+    def __len__(self):
+        return len(self.status)
+
+    def is_empty(self, i: int) -> bool:
+        return self.status[i] != 0
+
+    def cell(self, i: int):
+        from . import _kernels as _k
+        from .geom import unpack_cell
+
+        if self.status[i] != 0:
+            return None
+        nf = int(self.nf[i])
+        lp = np.empty(_k.MAX_F + 1, dtype=np.int64)
+        lp[:nf + 1] = self.lp[i, :nf + 1]
+        return unpack_cell(self.verts[i], np.array([self.nv[i], nf, self.nl[i]]), self.planes[i],
+                           self.tags[i], lp, self.lv[i])
+
+    def neighbors(self, i: int) -> np.ndarray:
+        """Site indices of the facet neighbours of cell i."""
+        t = self.tags[i, :int(self.nf[i])]
+        return t[t >= 0]
+
+
+def build_diagram_packed(sites, domain: ConvexCell, grid=None, ball_aware: bool = False) -> PackedDiagram:
+    """Every Laguerre cell on the device (pf_batch_build), with the reference's
+    capacity-doubling retry (laguerre.py:226-265).  ``grid`` is accepted for
+    signature compatibility; the device builds its own bucket grid."""
+    from . import _kernels as _k
+
+    if isinstance(sites, (list, tuple)) and len(sites) and isinstance(sites[0], Site):
+        pts, psi, _, _ = sites_to_arrays(sites)
+    else:
+        pts, psi = sites
+        pts = np.asarray(pts, dtype=np.float64).reshape(-1, 3)
+        psi = np.asarray(psi, dtype=np.float64)
+    n = len(pts)
+    dp = domain_pack(domain)
+    gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
+    dpsi = float(max(psi.max() - psi.min(), 0.0)) if n else 0.0
+    smv, smf, sml = 128, 64, 512
+    while True:
+        status = np.zeros(n, dtype=np.int64)
+        nv, nf, nl = (np.zeros(n, dtype=np.int64) for _ in range(3))
+        verts, planes = np.zeros((n, smv, 3)), np.zeros((n, smf, 4))
+        tags, lp, lv = (np.zeros((n, smf), dtype=np.int64), np.zeros((n, smf + 1), dtype=np.int64),
+                        np.zeros((n, sml), dtype=np.int64))
+        err = _k._batch_build(pts, psi, *dp.args(), *gargs, dp.tol, dpsi, ball_aware, smv, smf, sml,
+                              status, nv, nf, nl, verts, planes, tags, lp, lv)
+        if err == 0:
+            break
+        smv, smf, sml = smv * 2, smf * 2, sml * 2
+        if smv > _k.MAX_V or smf > _k.MAX_F * 2 or sml > _k.MAX_L:
+            raise RuntimeError("diagram cell exceeded kernel buffer capacity")
+        smv, smf, sml = min(smv, _k.MAX_V), min(smf, _k.MAX_F), min(sml, _k.MAX_L)
+    return PackedDiagram(pts, psi, status, nv, nf, nl, verts, planes, tags, lp, lv, domain)
+
+
+def build_diagram(sites, domain: ConvexCell, grid=None, ball_aware: bool = False) -> list:
+    """One Laguerre cell per site; empty cells are None (laguerre.py:268-272)."""
+    packed = build_diagram_packed(sites, domain, grid, ball_aware)
+    return [packed.cell(i) for i in range(len(packed))]

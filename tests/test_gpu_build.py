@@ -1,0 +1,45 @@
+"""Unrestricted Laguerre cells on the device: the
+reference's `_kernels._batch_build` drop-in and `laguerre.build_diagram_packed`
+against the reference's own outputs (tests/golden, ball-aware and full
+security-radius mode): every array bit-exact."""
+import numpy as np
+import pytest
+
+from conftest import golden_domain
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("status", "nv", "nf", "nl", "verts", "planes", "tags", "lp", "lv")
+
+
+@pytest.mark.parametrize("mode", ["ba", "full"])
+def test_dropin_batch_build_matches_reference(golden, mode):
+    from paper_2601_05765_b200 import _kernels
+
+    pts, psi = golden["bb_pts"], golden["bb_psi"]
+    n = len(pts)
+    smv, smf, sml = (golden[f"bb_{mode}_verts"].shape[1], golden[f"bb_{mode}_planes"].shape[1],
+                     golden[f"bb_{mode}_lv"].shape[1])
+    arrs = [np.zeros(n, np.int64) for _ in range(4)] + [
+        np.zeros((n, smv, 3)), np.zeros((n, smf, 4)), np.zeros((n, smf), np.int64),
+        np.zeros((n, smf + 1), np.int64), np.zeros((n, sml), np.int64)]
+    gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
+    err = _kernels._batch_build(pts, psi, *golden_domain(golden), *gargs, float(golden["dom_unit_tol"]),
+                                float(psi.max() - psi.min()), mode == "ba", smv, smf, sml, *arrs)
+    assert err == 0
+    for k, a in zip(KEYS, arrs):
+        assert np.array_equal(a, golden[f"bb_{mode}_{k}"]), k
+
+
+@pytest.mark.parametrize("mode", ["ba", "full"])
+def test_build_diagram_packed_matches_reference(golden, mode):
+    from paper_2601_05765_b200 import geom, laguerre
+
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    d = laguerre.build_diagram_packed((golden["bb_pts"], golden["bb_psi"]), dom, ball_aware=(mode == "ba"))
+    for k in KEYS:
+        assert np.array_equal(getattr(d, k), golden[f"bb_{mode}_{k}"]), k
+    if mode == "full":  # full security radius: the cells partition the domain
+        cells = laguerre.build_diagram((golden["bb_pts"], golden["bb_psi"]), dom)
+        vol = sum(geom.cell_volume_convex(c) for c in cells if c is not None)
+        assert abs(vol - 1.0) < 1e-9
