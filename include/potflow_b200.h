@@ -131,6 +131,11 @@ int pf_grid_order(pf_ctx *ctx, int32_t *order, void *stream);
 int pf_last_census(pf_ctx *ctx, int32_t *census, void *stream);
 /* device time (ms) of the cell kernels (both tiers) of the last evaluation */
 int pf_last_cells_ms(pf_ctx *ctx, double *ms_host);
+/* per-stage device timing of every evaluation after pf_stage_timing(ctx, 1) (resets):
+ * total build-kernel ms ("Laguerre") and evaluation-kernel ms ("Evaluation",
+ * incl. the capacity-overflow tier) and the evaluation count (cmd_bench) */
+int pf_stage_timing(pf_ctx *ctx, int enable);
+int pf_stage_times(pf_ctx *ctx, double *build_ms_host, double *eval_ms_host, int64_t *evaluations_host);
 /* number of cells that overflowed the shared-memory tier in the last evaluation */
 int pf_last_retry_count(pf_ctx *ctx, int64_t *count_host);
 

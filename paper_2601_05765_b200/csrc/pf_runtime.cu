@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <array>
+#include <vector>
 
 #include "pf_tiers.cuh"
 #include "../../include/potflow_b200.h"
@@ -97,6 +99,11 @@ struct pf_ctx {
     int split = 1;  // split build/evaluate kernels (PF_FUSED=1 selects the fused kernel)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool ev_valid = false;
+    // per-stage timing (cmd_bench): build / evaluation event triples of every
+    // evaluation since pf_stage_timing(ctx, 1)
+    bool stage_on = false;
+    std::vector<std::array<cudaEvent_t, 3>> stage_ev;
+    size_t stage_n = 0;
     int fast_blocks = 0, build_blocks = 0, eval_blocks = 0, eval_sync = 1;
     bool attr_set = false;
 };
@@ -552,6 +559,16 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         CK(cudaEventCreate(&c->ev[1]));
     }
     CK(cudaEventRecord(c->ev[0], st));
+    cudaEvent_t *sev = nullptr;
+    if (c->stage_on && c->split && count > 0) {
+        if (c->stage_n == c->stage_ev.size()) {
+            std::array<cudaEvent_t, 3> t;
+            for (auto &e : t) CK(cudaEventCreate(&e));
+            c->stage_ev.push_back(t);
+        }
+        sev = c->stage_ev[c->stage_n++].data();
+        CK(cudaEventRecord(sev[0], st));
+    }
     if (c->split && count > 0) {
         if (ensure(&c->gpoly, &c->gpoly_cap, (size_t)n) || ensure(&c->stage, &c->stage_cap, (size_t)n))
             return -1;
@@ -559,6 +576,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         k_cells_build<<<(int)bblocks, FAST_WARPS * 32, FAST_WARPS * sizeof(BWS<FastCaps>), st>>>(
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
         CK(cudaGetLastError());
+        if (sev) CK(cudaEventRecord(sev[1], st));
         g_launches++;
         if (c->eval_sync) {
             const int64_t sb = std::min<int64_t>(c->nsm * (16 / SYNC_WARPS), (count + SYNC_WARPS - 1) / SYNC_WARPS);
@@ -580,6 +598,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         in, out, c->retry_list, c->counters, c->exact_ws, c->err);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[1], st));
+    if (sev) CK(cudaEventRecord(sev[2], st));
     c->ev_valid = true;
     return 0;
 }
@@ -1024,6 +1043,29 @@ int pf_last_cells_ms(pf_ctx *c, double *ms) {
     float f = 0.f;
     CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[1]));
     *ms = f;
+    return 0;
+}
+
+int pf_stage_timing(pf_ctx *c, int enable) {
+    c->stage_on = enable != 0;
+    c->stage_n = 0;
+    return 0;
+}
+
+int pf_stage_times(pf_ctx *c, double *build_ms, double *eval_ms, int64_t *evaluations) {
+    double b = 0.0, e = 0.0;
+    for (size_t k = 0; k < c->stage_n; k++) {
+        auto &t = c->stage_ev[k];
+        CK(cudaEventSynchronize(t[2]));
+        float x = 0.f, y = 0.f;
+        CK(cudaEventElapsedTime(&x, t[0], t[1]));
+        CK(cudaEventElapsedTime(&y, t[1], t[2]));
+        b += x;
+        e += y;
+    }
+    *build_ms = b;
+    *eval_ms = e;
+    *evaluations = (int64_t)c->stage_n;
     return 0;
 }
 
