@@ -96,7 +96,7 @@ def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, o
 
     L = _lib.lib()
     n = int(np.asarray(pts).shape[0])
-    K = chunks or int(os.environ.get("PF_E2E_CHUNKS", "8"))
+    K = chunks or int(os.environ.get("PF_E2E_CHUNKS", "16"))
     K = max(1, min(K, max(n, 1)))
 
     def h2d(x, dtype):

@@ -1156,6 +1156,12 @@ PF_NOINL bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy,
     return false;
 }
 
+// value-only normalisation (tangents): hardware rsqrt + one Newton step
+PF_DEV double rsqrt_nr(double x) {
+    double r = rsqrt(x);
+    return r * fma(-0.5 * x * r, r, 1.5);
+}
+
 // boundary point q of a live ring: its facet, else -1
 template <class C>
 PF_DEV int ring_facet(const EvalScratch<C> &E, int q, bool need_area) {
@@ -1226,10 +1232,11 @@ PF_NOINL void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, d
                 Ip = fma(dy, sx3, -dx * sy3) * (1.0 / 12.0);
             } else {
                 const double r = E.frc[f];
-                const double r0 = dsqrt(x0 * x0 + y0 * y0), r1 = dsqrt(x1 * x1 + y1 * y1);
-                const double ir0 = r0 > 0.0 ? ddiv(1.0, r0) : 0.0, ir1 = r1 > 0.0 ? ddiv(1.0, r1) : 0.0;
-                const double c0 = r0 > 0.0 ? x0 * ir0 : 1.0, s0 = y0 * ir0;
-                const double c1 = r1 > 0.0 ? x1 * ir1 : 1.0, s1 = y1 * ir1;
+                // cos / sin of the end-point angles (values only: rsqrt + one Newton step)
+                const double q0 = x0 * x0 + y0 * y0, q1 = x1 * x1 + y1 * y1;
+                const double ir0 = q0 > 0.0 ? rsqrt_nr(q0) : 0.0, ir1 = q1 > 0.0 ? rsqrt_nr(q1) : 0.0;
+                const double c0 = q0 > 0.0 ? x0 * ir0 : 1.0, s0 = y0 * ir0;
+                const double c1 = q1 > 0.0 ? x1 * ir1 : 1.0, s1 = y1 * ir1;
                 double dth = atan2_ool(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
                 // end points (nearly) coincident: decide the wrap exactly as the
                 // reference does, from the two end-point angles (_kernels.py:696-700)
@@ -1277,7 +1284,8 @@ PF_NOINL void project_from(double cx, double cy, double cz, double yx, double yy
     double c0 = wx * wx + wy * wy + wz * wz - psi;
     double disc = b * b - a * c0;
     if (disc < 0.0) disc = 0.0;
-    double t = ddiv(-b + dsqrt(disc), a);
+    // values only: reciprocal instead of an IEEE division (<= 1 ulp apart)
+    double t = (-b + dsqrt(disc)) * __drcp_rn(a);
     o[0] = cx + t * dx; o[1] = cy + t * dy; o[2] = cz + t * dz;
 }
 
@@ -1293,11 +1301,6 @@ PF_DEV double ccw_angle(const double *a, const double *b, const double *m) {
     cross3(a, b, c);
     double t = atan2_ool(dot3(c, m), dot3(a, b));
     return t < 0.0 ? t + 2.0 * PF_PI : t;
-}
-// value-only normalisation (tangents): hardware rsqrt + one Newton step
-PF_DEV double rsqrt_nr(double x) {
-    double r = rsqrt(x);
-    return r * fma(-0.5 * x * r, r, 1.5);
 }
 PF_DEV void unit3(double *v) {
     double n2 = dot3(v, v);

@@ -20,6 +20,7 @@
 #define PF_NOINL static
 static inline int __builtin_ctz_pf(unsigned m) { return __builtin_ctz(m); }
 static inline double rsqrt(double x) { return 1.0 / std::sqrt(x); }  // device: MUFU-based rsqrt
+static inline double __drcp_rn(double x) { return 1.0 / x; }  // device: correctly rounded reciprocal
 
 extern "C" void emu_swap(void **from_sp, void *to_sp);
 

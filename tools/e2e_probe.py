@@ -15,7 +15,7 @@ print("pinned:", torch.from_numpy(host["ftag"]).is_pinned(), flush=True)
 pts, w = pin(s.pts), pin(psi)
 gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
 dpsi = 0.0
-for K in (1, 2, 4, 8):
+for K in (8, 16, 32):
     os.environ["PF_E2E_CHUNKS"] = str(K)
     ts = []
     for it in range(3):
