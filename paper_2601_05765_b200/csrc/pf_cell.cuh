@@ -264,7 +264,7 @@ PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
         double d2 = sq(A.x[v] - px) + sq(A.y[v] - py) + sq(A.z[v] - pz);
         if (d2 > m) m = d2;
     }
-    return sqrt(pfw::max_d(m));
+    return sqrt(pfw::max_d_inl(m));
 }
 
 // ---------------------------------------------------------------------------
@@ -363,7 +363,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
             em = (ina ? 1 : 0) + cr;
         }
         int tot;
-        const int pk = pfw::excl_scan_i((em << 16) | cr, &tot);
+        const int pk = pfw::excl_scan_inl((em << 16) | cr, L, &tot);
         if (k < nl) {
             const int pcr = NE + (pk & 0xffff), pem = NEm + (pk >> 16);
             if (cr && pcr < C::CE) { S.ea[pcr] = (uint16_t)a; S.eb[pcr] = (uint16_t)b; }
@@ -389,7 +389,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         }
         small_facet |= pfw::any(kk >= 1 && kk <= 2);
         int tot;
-        const int pk = pfw::excl_scan_i((keep << 16) | (keep ? kk : 0), &tot);
+        const int pk = pfw::excl_scan_inl((keep << 16) | (keep ? kk : 0), L, &tot);
         if (f < nf) {
             S.fout[f] = (uint16_t)(NFk + (pk >> 16));
             S.flb[f] = keep ? (uint16_t)(NLk + (pk & 0xffff)) : (uint16_t)0xffff;
@@ -510,8 +510,14 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
     double cc = 0.0;
     if (L < 3) {
         const double *crd = L == 0 ? B.x : (L == 1 ? B.y : B.z);
+        int q = 0;
         #pragma unroll 1
-        for (int q = 0; q < ncp; q++) cc += crd[S.onl[q]];
+        for (; q + 4 <= ncp; q += 4) {  // loads first, then the sequential sum
+            const double a0 = crd[S.onl[q]], a1 = crd[S.onl[q + 1]], a2 = crd[S.onl[q + 2]], a3 = crd[S.onl[q + 3]];
+            cc += a0; cc += a1; cc += a2; cc += a3;
+        }
+        #pragma unroll 1
+        for (; q < ncp; q++) cc += crd[S.onl[q]];
         cc /= (double)ncp;
     }
     const double ccx = pfw::shfl(cc, 0), ccy = pfw::shfl(cc, 1), ccz = pfw::shfl(cc, 2);
@@ -673,7 +679,7 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
             len = g.bstart[lin1 + 1] - st;
         }
         int tot;
-        int off = pfw::excl_scan_i(len, &tot);
+        int off = pfw::excl_scan_inl(len, L, &tot);
         S.run_start[L] = st;
         S.run_off[L] = off;
         pfw::sync();

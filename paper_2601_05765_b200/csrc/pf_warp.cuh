@@ -77,6 +77,24 @@ PF_NOINL double seg_sum_d(double v, int first) {
     }
     return v;
 }
+// exclusive prefix over lanes of an int (inline copy for the clip loop,
+// given the caller's lane index)
+PF_DEV int excl_scan_inl(int v, int L, int *total) {
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = shfl(x, (L - o) & 31);
+        if (L >= o) x += y;
+    }
+    *total = shfl(x, 31);
+    return x - v;
+}
+PF_DEV double max_d_inl(double v) {
+    for (int m = 16; m > 0; m >>= 1) {
+        double o = shfl_xor(v, m);
+        v = o > v ? o : v;
+    }
+    return v;
+}
 // exclusive prefix over lanes of an int
 PF_NOINL int excl_scan_i(int v, int *total) {
     int x = v;
