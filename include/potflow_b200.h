@@ -213,6 +213,19 @@ int pf_dcg_update(int nrows, const int32_t *rows, const double *diag, double *x,
                   double *out2_dev, void *stream);
 int pf_dcg_pdir(int nrows, const int32_t *rows, const double *z, double *p, const double *rz_new_dev,
                 const double *rz_old_dev, void *stream);
+/* single-reduction Jacobi-PCG (Chronopoulos-Gear), one all-reduce per iteration:
+ * init (x = 0, r = b, u = D^-1 b, p = s = 0); spmv_dots: w = A u (u's ghosts exchanged)
+ * and out3 = partial (r.u, w.u, r.r); step: scalars from the all-reduced (r.u, w.u)
+ * into sc_dev[0..2] (gamma, alpha, beta), then p = u + beta p, s = w + beta s,
+ * x += alpha p, r -= alpha s, u = D^-1 r */
+int pf_cg1_init(int nrows, const int32_t *rows, const double *b, const double *diag, double *x, double *r,
+                double *u, double *p, double *s, void *stream);
+int pf_cg1_spmv_dots(int nrows, const int32_t *rows, int smf, const int32_t *hcnt, const int32_t *hcol,
+                     const double *hval, const double *diag, const double *u, const double *r, double *w,
+                     double *out3_dev, void *stream);
+int pf_cg1_step(int nrows, const int32_t *rows, const double *diag, double *x, double *r, double *u,
+                const double *w, double *p, double *s, const double *red_dev, double *sc_dev, int first,
+                void *stream);
 /* out = a + s b (n entries) */
 int pf_daxpy(int64_t n, const double *a, double s, const double *b, double *out, void *stream);
 

@@ -218,6 +218,81 @@ __global__ void __launch_bounds__(DB) k_dcg_pdir(int nrows, const int *__restric
     }
 }
 
+// ---- single-reduction PCG (Chronopoulos & Gear): one all-reduce per iteration ----
+// sc (device, caller-owned, 8 doubles): [0] gamma = r.u, [1] alpha, [2] beta
+// w = A u and partial (r.u, w.u, r.r) -> part, to be all-reduced by the caller
+__global__ void __launch_bounds__(DB) k_cg1_spmv_dots(int nrows, const int *__restrict__ rows, int smf,
+                                                      const int *__restrict__ hcnt, const int *__restrict__ hcol,
+                                                      const double *__restrict__ hval,
+                                                      const double *__restrict__ diag, const double *__restrict__ u,
+                                                      const double *__restrict__ r, double *__restrict__ w,
+                                                      double *__restrict__ part) {
+    double v[3] = {0.0, 0.0, 0.0};
+    const int op[3] = {0, 0, 0};
+    for (int t = blockIdx.x * DB + threadIdx.x; t < nrows; t += DNB * DB) {
+        const int64_t i = rows[t];
+        double s = diag[i] * u[i];
+        const int c = hcnt[i];
+        const int *col = hcol + i * smf;
+        const double *val = hval + i * smf;
+        for (int k = 0; k < c; k++) s += val[k] * u[col[k]];
+        w[i] = s;
+        v[0] += r[i] * u[i];
+        v[1] += s * u[i];
+        v[2] += r[i] * r[i];
+    }
+    block_reduce<3>(v, op);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 3; k++) part[k * DNB + blockIdx.x] = v[k];
+}
+
+// scalars from the reduced (gamma_new, delta): first iteration alpha = gamma/delta,
+// then beta = gamma_new/gamma, alpha = gamma_new / (delta - beta gamma_new / alpha)
+__global__ void k_cg1_scalars(const double *__restrict__ red, double *__restrict__ sc, int first) {
+    const double g = red[0], dl = red[1];
+    double beta = 0.0, alpha;
+    if (first) {
+        alpha = dl != 0.0 ? g / dl : 0.0;
+    } else {
+        beta = sc[0] != 0.0 ? g / sc[0] : 0.0;
+        const double den = dl - (sc[1] != 0.0 ? beta * g / sc[1] : 0.0);
+        alpha = den != 0.0 ? g / den : 0.0;
+    }
+    sc[0] = g; sc[1] = alpha; sc[2] = beta;
+}
+
+// p = u + beta p; s = w + beta s; x += alpha p; r -= alpha s; u = r / diag
+__global__ void __launch_bounds__(DB) k_cg1_update(int nrows, const int *__restrict__ rows,
+                                                   const double *__restrict__ diag, double *__restrict__ x,
+                                                   double *__restrict__ r, double *__restrict__ u,
+                                                   const double *__restrict__ w, double *__restrict__ p,
+                                                   double *__restrict__ s, const double *__restrict__ sc) {
+    const double alpha = sc[1], beta = sc[2];
+    for (int t = blockIdx.x * DB + threadIdx.x; t < nrows; t += DNB * DB) {
+        const int i = rows[t];
+        const double pi = u[i] + beta * p[i];
+        const double si = w[i] + beta * s[i];
+        p[i] = pi;
+        s[i] = si;
+        x[i] += alpha * pi;
+        const double ri = r[i] - alpha * si;
+        r[i] = ri;
+        u[i] = ri / diag[i];
+    }
+}
+
+// x = 0, r = b, u = b / diag, p = s = 0
+__global__ void __launch_bounds__(DB) k_cg1_init(int nrows, const int *__restrict__ rows,
+                                                 const double *__restrict__ b, const double *__restrict__ diag,
+                                                 double *__restrict__ x, double *__restrict__ r,
+                                                 double *__restrict__ u, double *__restrict__ p,
+                                                 double *__restrict__ s) {
+    for (int t = blockIdx.x * DB + threadIdx.x; t < nrows; t += DNB * DB) {
+        const int i = rows[t];
+        x[i] = 0.0; r[i] = b[i]; u[i] = b[i] / diag[i]; p[i] = 0.0; s[i] = 0.0;
+    }
+}
+
 // out = a + s b on all n local entries
 __global__ void __launch_bounds__(DB) k_daxpy(int64_t n, const double *__restrict__ a, double s,
                                               const double *__restrict__ b, double *__restrict__ out) {
@@ -288,6 +363,37 @@ int pf_dcg_pdir(int nrows, const int32_t *rows, const double *z, double *p, cons
                 const double *rz_old_dev, void *stream) {
     pf_internal_launches_add(1);
     k_dcg_pdir<<<DNB, DB, 0, (cudaStream_t)stream>>>(nrows, rows, z, p, rz_new_dev, rz_old_dev);
+    DCK(cudaGetLastError());
+    return 0;
+}
+
+int pf_cg1_init(int nrows, const int32_t *rows, const double *b, const double *diag, double *x, double *r,
+                double *u, double *p, double *s, void *stream) {
+    pf_internal_launches_add(1);
+    k_cg1_init<<<DNB, DB, 0, (cudaStream_t)stream>>>(nrows, rows, b, diag, x, r, u, p, s);
+    DCK(cudaGetLastError());
+    return 0;
+}
+
+int pf_cg1_spmv_dots(int nrows, const int32_t *rows, int smf, const int32_t *hcnt, const int32_t *hcol,
+                     const double *hval, const double *diag, const double *u, const double *r, double *w,
+                     double *out3_dev, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (part_alloc()) return -1;
+    pf_internal_launches_add(2);
+    k_cg1_spmv_dots<<<DNB, DB, 0, st>>>(nrows, rows, smf, hcnt, hcol, hval, diag, u, r, w, g_part);
+    k_finish<3><<<1, DB, 0, st>>>(g_part, out3_dev, 0, 0, 0, 0);
+    DCK(cudaGetLastError());
+    return 0;
+}
+
+int pf_cg1_step(int nrows, const int32_t *rows, const double *diag, double *x, double *r, double *u,
+                const double *w, double *p, double *s, const double *red_dev, double *sc_dev, int first,
+                void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    pf_internal_launches_add(2);
+    k_cg1_scalars<<<1, 1, 0, st>>>(red_dev, sc_dev, first);
+    k_cg1_update<<<DNB, DB, 0, st>>>(nrows, rows, diag, x, r, u, w, p, s, sc_dev);
     DCK(cudaGetLastError());
     return 0;
 }

@@ -10,9 +10,10 @@ cells are bit-identical to the single-GPU ones.  Per Newton iteration
   (`pf_evaluate_lean_cells`), gradient statistics all-reduced (one MAX of
   three scalars: worst error, -min volume, -min nu);
 * Hessian rows of the owned cells (`pf_rows_hessian`), columns may be ghosts;
-* Jacobi-PCG: per iteration one halo exchange of the search direction
-  (P2P send/recv to the slab neighbours) and two scalar all-reduces
-  (p.Ap, then r.z and r.r together);
+* Jacobi-PCG in the single-reduction form (Chronopoulos & Gear): per
+  iteration one halo exchange of the preconditioned residual (P2P send/recv
+  to the slab neighbours) and ONE all-reduce of three scalars (the classic
+  two-reduction form is kept as cg="classic");
 * one halo exchange of the Newton step x, after which every damping trial
   psi + alpha x is formed locally for owned and ghost sites alike.
 
@@ -109,6 +110,11 @@ def _bind():
         L.pf_dcg_update.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.pf_dcg_pdir.argtypes = [i, vp, vp, vp, vp, vp, vp]
         L.pf_daxpy.argtypes = [i64, vp, d, vp, vp, vp]
+        L.pf_cg1_init.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pf_cg1_spmv_dots.argtypes = [i, vp, i, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pf_cg1_step.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, vp]
+        for name in ("pf_cg1_init", "pf_cg1_spmv_dots", "pf_cg1_step"):
+            getattr(L, name).restype = i
         for name in ("pf_evaluate_lean_cells", "pf_rows_gradient", "pf_rows_hessian", "pf_dcg_init",
                      "pf_dcg_spmv", "pf_dcg_update", "pf_dcg_pdir", "pf_daxpy"):
             getattr(L, name).restype = i
@@ -144,7 +150,8 @@ class CudaOps:
                            fcount=torch.zeros(n, **i4), ftag=torch.zeros((n, smf), **i4),
                            farea=torch.zeros((n, smf), **f8), cent=torch.zeros((n, 3), **f8))
                       for _ in range(2)]
-        self.v = {k: torch.zeros(n, **f8) for k in ("g", "x", "r", "z", "p", "Ap", "diag")}
+        self.v = {k: torch.zeros(n, **f8) for k in ("g", "x", "r", "z", "p", "Ap", "diag", "s")}
+        self.cg1_sc = torch.zeros(8, **f8)
         self.hcnt = torch.zeros(n, **i4)
         self.hcol = torch.zeros((n, smf), **i4)
         self.hval = torch.zeros((n, smf), **f8)
@@ -277,6 +284,29 @@ class CudaOps:
         self.chk(self.L.pf_dcg_pdir(self.nrows, self.p(self.rows), self.p(v["z"]), self.p(v["p"]),
                                     self.p(rz_new), self.p(rz_old), self._s()), "pf_dcg_pdir")
 
+    # single-reduction PCG (u = z, w = Ap)
+    def cg1_init(self):
+        v = self.v
+        self.chk(self.L.pf_cg1_init(self.nrows, self.p(self.rows), self.p(v["g"]), self.p(v["diag"]),
+                                    self.p(v["x"]), self.p(v["r"]), self.p(v["z"]), self.p(v["p"]),
+                                    self.p(v["s"]), self._s()), "pf_cg1_init")
+
+    def cg1_spmv_dots(self):
+        v = self.v
+        out = self.torch.zeros(3, dtype=self.torch.float64, device="cuda")
+        self.chk(self.L.pf_cg1_spmv_dots(self.nrows, self.p(self.rows), self.smf, self.p(self.hcnt),
+                                         self.p(self.hcol), self.p(self.hval), self.p(v["diag"]), self.p(v["z"]),
+                                         self.p(v["r"]), self.p(v["Ap"]), self.p(out), self._s()),
+                 "pf_cg1_spmv_dots")
+        return out
+
+    def cg1_step(self, red, first: bool):
+        v = self.v
+        self.chk(self.L.pf_cg1_step(self.nrows, self.p(self.rows), self.p(v["diag"]), self.p(v["x"]),
+                                    self.p(v["r"]), self.p(v["z"]), self.p(v["Ap"]), self.p(v["p"]),
+                                    self.p(v["s"]), self.p(red), self.p(self.cg1_sc), int(first), self._s()),
+                 "pf_cg1_step")
+
     def vec(self, name):
         return self.v[name]
 
@@ -315,12 +345,13 @@ class DistNewton:
 
     def __init__(self, pts: np.ndarray, nu: np.ndarray, domain, group=None, smf: int = 32,
                  ball_aware: bool = True, slack: float = 1.5, ops_factory=None, axis_lo=None,
-                 axis_hi=None):
+                 axis_hi=None, cg: str = "single"):
         self.pts = np.ascontiguousarray(pts, dtype=np.float64)
         self.nu = np.ascontiguousarray(nu, dtype=np.float64)
         self.domain = domain
         self.comm = Comm(group)
         self.smf, self.ball_aware, self.slack = smf, ball_aware, slack
+        self.cg = cg  # "single": one all-reduce per CG iteration; "classic": two
         # slab boundaries: x-quantiles of the sites (balanced) unless given
         self.lo, self.hi = axis_lo, axis_hi
         self.tau = 1e-12 * domain.diagonal() ** 2
@@ -380,6 +411,25 @@ class DistNewton:
         return st[0], -st[1], -st[2]
 
     # --- Jacobi-PCG ---------------------------------------------------------
+    def _pcg1(self, rtol: float, max_iter: int = 10000) -> int:
+        """Single-reduction Jacobi-PCG (Chronopoulos & Gear): per iteration one halo
+        exchange of u = D^-1 r and ONE all-reduce of (r.u, w.u, r.r), w = A u."""
+        o, c = self.ops, self.comm
+        o.cg1_init()
+        bb, it = 0.0, 0
+        while True:
+            c.exchange(o.vec("z"), self.plan, self.idx_send, self.idx_recv)
+            red = c.all_reduce(o.cg1_spmv_dots(), "sum")
+            rr = float(red[2])
+            if it == 0:
+                bb = rr
+                if not bb > 0.0:
+                    return 0
+            elif np.sqrt(rr) <= rtol * np.sqrt(bb) or it >= max_iter or not np.isfinite(rr):
+                return it
+            o.cg1_step(red, it == 0)
+            it += 1
+
     def _pcg(self, rtol: float, max_iter: int = 10000) -> int:
         o, c = self.ops, self.comm
         t = c.all_reduce(o.cg_init(), "sum")
@@ -451,7 +501,7 @@ class DistNewton:
                 break
             self.ops.hessian()
             rtol = 1e-4 if worst < 10.0 * eps_vol else 1e-3
-            S["cg_iterations"] += self._pcg(rtol)
+            S["cg_iterations"] += self._pcg1(rtol) if self.cg == "single" else self._pcg(rtol)
             # the step's ghost entries, then every trial is local
             self.comm.exchange(self.ops.vec("x"), self.plan, self.idx_send, self.idx_recv)
             alpha, accepted = 1.0, False

@@ -24,7 +24,8 @@ class NumpyOps:
         self.psi_t = np.zeros(n)
         self.slots = [None, None]
         # vectors are torch CPU tensors sharing numpy storage (halo exchange works in place)
-        self.v = {k: torch.zeros(n, dtype=torch.float64) for k in ("g", "x", "r", "z", "p", "Ap", "diag")}
+        self.v = {k: torch.zeros(n, dtype=torch.float64) for k in ("g", "x", "r", "z", "p", "Ap", "diag", "s")}
+        self.sc = [0.0, 0.0, 0.0]
         self.cols = self.vals = None
 
     def _n(self, k):
@@ -132,6 +133,42 @@ class NumpyOps:
         beta = float(rz_new[0]) / float(rz_old[0]) if float(rz_old[0]) != 0.0 else 0.0
         p = self._n("p")
         p[r] = self._n("z")[r] + beta * p[r]
+
+    def cg1_init(self):
+        r = self.rows
+        b, d = self._n("g")[r], self._n("diag")[r]
+        self._n("x")[:] = 0.0
+        self._n("r")[r] = b
+        self._n("z")[r] = b / d
+        self._n("p")[r] = 0.0
+        self._n("s")[r] = 0.0
+
+    def cg1_spmv_dots(self):
+        r = self.rows
+        u = self._n("z")
+        c, v = self.cols[r], self.vals[r]
+        us = np.where(c >= 0, u[np.maximum(c, 0)], 0.0)
+        w = self._n("diag")[r] * u[r] + (v * us).sum(1)
+        self._n("Ap")[r] = w
+        rr = self._n("r")[r]
+        return torch.tensor([float(rr @ u[r]), float(w @ u[r]), float(rr @ rr)], dtype=torch.float64)
+
+    def cg1_step(self, red, first):
+        g, dl = float(red[0]), float(red[1])
+        if first:
+            beta, alpha = 0.0, (g / dl if dl != 0.0 else 0.0)
+        else:
+            beta = g / self.sc[0] if self.sc[0] != 0.0 else 0.0
+            den = dl - (beta * g / self.sc[1] if self.sc[1] != 0.0 else 0.0)
+            alpha = g / den if den != 0.0 else 0.0
+        self.sc = [g, alpha, beta]
+        r = self.rows
+        p, s = self._n("p"), self._n("s")
+        p[r] = self._n("z")[r] + beta * p[r]
+        s[r] = self._n("Ap")[r] + beta * s[r]
+        self._n("x")[r] += alpha * p[r]
+        self._n("r")[r] -= alpha * s[r]
+        self._n("z")[r] = self._n("r")[r] / self._n("diag")[r]
 
     def vec(self, name):
         return self.v[name]
