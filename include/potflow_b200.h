@@ -248,6 +248,15 @@ int pf_fluid_forces_implicit(int64_t n, int smf, const double *x, const double *
                              int ndom, int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
                              double *sol, double rtol, void *stream);
 
+/* ---- renderer ----------------------
+ * first hit of one ray per pixel with the fluid (the union of the balls, whose
+ * first point along a ray lies in the entered ball's Laguerre cell): hit_id
+ * int32[h*w] (-1 miss), hit_t f64[h*w].  cam_host[14] = eye[3], forward[3],
+ * right[3], up[3] (unit), tan(fov/2), aspect; rmax = largest ball radius. */
+int pf_render_first_hit(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double rmax,
+                        const double *cam_host, int width, int height, int32_t *hit_id, double *hit_t,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,8 +1,8 @@
-"""Command-line driver (SPEC.md:497-534; SURVEY §8(f) row 3): `simulate` runs
+"""Command-line driver (SPEC.md:497-534; SURVEY §8(f) rows 3-4): `simulate` runs
 the fluid scheme writing POTF frames and a CSV of per-step statistics (warm
 start from a frame), `bench` prints the per-stage timings in the shape of the
 paper's Table 1 (Laguerre / Evaluation / Solve / Complete
-Step, mean over the steps).
+Step, mean over the steps), `render` writes a frame's fluid surface as PPM.
 
     python -m paper_2601_05765_b200.cli bench --sizes 10000,50000 --steps 20
     python -m paper_2601_05765_b200.cli simulate --config C2 --steps 100 --out runs/c2
@@ -110,6 +110,25 @@ def cmd_simulate(a) -> int:
     return 0
 
 
+def cmd_render(a) -> int:
+    """Render a frame's fluid surface (Raw mode) to a binary PPM."""
+    import time
+
+    import torch
+
+    from . import frames, render
+
+    f = frames.read_frame(a.frame)
+    cam = render.Camera(eye=tuple(a.eye), look_at=tuple(a.look_at), fov=a.fov, width=a.width, height=a.height)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    img = render.render_raw(f.x, f.psi, cam)
+    torch.cuda.synchronize()
+    render.write_ppm(a.out, img)
+    print(f"rendered {f.n} particles, {a.width}x{a.height} in {1e3 * (time.perf_counter() - t0):.1f} ms -> {a.out}")
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="potflow_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -124,8 +143,16 @@ def main(argv=None) -> int:
     s.add_argument("--frame-stride", type=int, default=10)
     s.add_argument("--warm-start", default=None, help="POTF frame to resume from")
     s.add_argument("--best-effort", action="store_true")
+    r = sub.add_parser("render", help="render a frame (Raw first-hit shading) to .ppm")
+    r.add_argument("frame")
+    r.add_argument("--out", default="frame.ppm")
+    r.add_argument("--eye", type=float, nargs=3, default=[0.5, -1.2, 0.9])
+    r.add_argument("--look-at", type=float, nargs=3, default=[0.5, 0.5, 0.2])
+    r.add_argument("--fov", type=float, default=0.8)
+    r.add_argument("--width", type=int, default=1280)
+    r.add_argument("--height", type=int, default=720)
     a = ap.parse_args(argv)
-    return {"bench": cmd_bench, "simulate": cmd_simulate}[a.cmd](a)
+    return {"bench": cmd_bench, "simulate": cmd_simulate, "render": cmd_render}[a.cmd](a)
 
 
 if __name__ == "__main__":

@@ -834,6 +834,16 @@ int pf_grid_build_dims(pf_ctx *c, int64_t n, const double *pts, const int *dims_
     return grid_build(c, n, pts, nullptr, 1.0, S(stream), dims_host);
 }
 
+}  // extern "C"
+// device view of the current bucket grid (renderer)
+int pf_internal_grid_view(pf_ctx *c, const double **sx, const double **sy, const double **sz, const int **sid,
+                          const int **bstart, int *gn, double *lo, double *h) {
+    if (c->grid_n < 0 || !c->sid) return set_err("grid view: no grid");
+    *sx = c->sx; *sy = c->sy; *sz = c->sz; *sid = c->sid; *bstart = c->bstart;
+    for (int a = 0; a < 3; a++) { gn[a] = c->gn[a]; lo[a] = c->glo[a]; h[a] = c->gh[a]; }
+    return 0;
+}
+extern "C" {
 int pf_grid_info(pf_ctx *c, int *dims, double *lo, double *h) {
     for (int a = 0; a < 3; a++) {
         if (dims) dims[a] = c->gn[a];
