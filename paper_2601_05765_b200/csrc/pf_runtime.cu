@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
 // evaluating in another halves the hot code each SM cycles through.  The
 // finished polytope travels through global memory (Poly<FastCaps>, ~3 KB).
 #ifndef PF_BUILD_MINB
-#define PF_BUILD_MINB 4
+#define PF_BUILD_MINB 5
 #endif
 __global__ void __launch_bounds__(FAST_WARPS * 32, PF_BUILD_MINB)
     k_cells_build(CellIn in, CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
