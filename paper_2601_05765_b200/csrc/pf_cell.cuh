@@ -28,6 +28,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "pf_warp.cuh"
 
 namespace pf {
@@ -85,18 +87,25 @@ struct BuildScratch {
     uint16_t ea[C::CE], eb[C::CE], eid[C::CE];  // crossing entries (walk order)
     uint16_t emt[C::CE];       // first-occurrence entry of the same edge
     uint8_t ecls[C::CL];       // per loop entry of A: bit0 tail inside, bit1 crossing edge
-    uint16_t epos[C::CL];      // per loop entry of A: emitted entries before it (all facets)
-    uint16_t cpos[C::CL];      // per loop entry of A: its crossing entry's walk-order index
     uint8_t lf[2][C::CL];      // facet of each loop entry, per polytope buffer
-    double csd[C::CC];         // sqrt(d^2) of the sorted candidates
-    double sy[C::CV];          // new-facet vertex ordinates (abscissae in sd)
-    uint8_t half[C::CV];       // their half-plane (angle order, see ang_lt)
+    union {                    // phase-disjoint scratch (shared memory is the occupancy limit)
+        struct {               // clip steps 3a-3e
+            uint16_t epos[C::CL];  // per loop entry of A: emitted entries before it (all facets)
+            typename std::conditional<(C::CE < 256), uint8_t, uint16_t>::type cpos[C::CL];  // its crossing entry
+        };
+        struct {               // clip step 4
+            double sy[C::CV];      // new-facet vertex ordinates (abscissae in sd)
+            uint8_t half[C::CV];   // their half-plane (angle order, see ang_lt)
+        };
+        struct {               // gather_shell
+            int run_start[32], run_off[32];
+        };
+    };
     double cd2[C::CC];         // candidates (d^2, j), sorted
     int cj[C::CC];
     uint16_t cord[C::CC];      // sorted rank -> gather slot of the candidate data below
     double cx[C::CC], cy[C::CC], cz[C::CC], cw[C::CC];  // position and weight, by gather slot
     int ncand;
-    int run_start[32], run_off[32];
 };
 
 template <class C>
@@ -368,7 +377,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
             const int pcr = NE + (pk & 0xffff), pem = NEm + (pk >> 16);
             if (cr && pcr < C::CE) { S.ea[pcr] = (uint16_t)a; S.eb[pcr] = (uint16_t)b; }
             S.epos[k] = (uint16_t)pem;
-            S.cpos[k] = (uint16_t)pcr;
+            S.cpos[k] = pcr;
             if (k == A.lp[f]) S.fscan0[f] = (uint16_t)pem;
             if (em) pfw::atom_add(&S.fk[f], em);
         }
@@ -806,7 +815,6 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         for (int c = pfw::lane(); c < nc; c += 32) {
             const double D2 = S.cd2[c];
             const double D = sqrt(D2);
-            S.csd[c] = D;
             if (D2 <= tol * tol) continue;
             const int sl = S.cord[c];
             const double psij = S.cw[sl];
@@ -822,7 +830,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         if (in.ball_aware && br < stop_r) stop_r = br;
         #pragma unroll 1
         for (int c = 0; c < nc; c++) {
-            if (S.csd[c] >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
+            if (sqrt(S.cd2[c]) >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
             const int j = S.cj[c];
             const int sl = S.cord[c];
             if (S.cd2[c] <= tol * tol) {

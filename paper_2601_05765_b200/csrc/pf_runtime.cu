@@ -290,19 +290,23 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
 // cell and stalls on instruction fetch; building in one kernel and
 // evaluating in another halves the hot code each SM cycles through.  The
 // finished polytope travels through global memory (Poly<FastCaps>, ~3 KB).
-#ifndef PF_BUILD_MINB
-#define PF_BUILD_MINB 5
+#ifndef PF_BUILD_WARPS
+#define PF_BUILD_WARPS 8
 #endif
-__global__ void __launch_bounds__(FAST_WARPS * 32, PF_BUILD_MINB)
+constexpr int BUILD_WARPS = PF_BUILD_WARPS;
+#ifndef PF_BUILD_MINB
+#define PF_BUILD_MINB 3
+#endif
+__global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
     k_cells_build(CellIn in, CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
                   uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
                   unsigned long long *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     BWS<FastCaps> *ws = (BWS<FastCaps> *)(smem + (size_t)wid * sizeof(BWS<FastCaps>));
-    const int nw = gridDim.x * FAST_WARPS;
+    const int nw = gridDim.x * BUILD_WARPS;
     int fl = 0;
-    for (int t = blockIdx.x * FAST_WARPS + wid; t < count; t += nw) {
+    for (int t = blockIdx.x * BUILD_WARPS + wid; t < count; t += nw) {
         const int i = in.cells ? in.cells[t] : in.g.sid[t];
         int which = 0;
         int r = cell_phase_build(ws, in, out, i, &which);
@@ -516,7 +520,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
                                 (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         CK(cudaFuncSetAttribute(k_cells_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(FAST_WARPS * sizeof(BWS<FastCaps>))));
+                                (int)(BUILD_WARPS * sizeof(BWS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(EWS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -532,8 +536,8 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         int nb = 0, nbb = 0, nbe = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cells_fast, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(WS<FastCaps>)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, k_cells_build, FAST_WARPS * 32,
-                                                         FAST_WARPS * sizeof(BWS<FastCaps>)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, k_cells_build, BUILD_WARPS * 32,
+                                                         BUILD_WARPS * sizeof(BWS<FastCaps>)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbe, k_cells_eval, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(EWS<FastCaps>)));
         if (nb < 1 || nbb < 1 || nbe < 1) return set_err("fast cell kernels cannot be resident");
@@ -550,7 +554,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
     const int64_t count = in.cells ? in.ncells : n;
     const int64_t want = std::max<int64_t>(1, (count + FAST_WARPS - 1) / FAST_WARPS);
     const int64_t blocks = std::min<int64_t>(c->fast_blocks, want);
-    const int64_t bblocks = std::min<int64_t>(c->build_blocks, want);
+    const int64_t bblocks = std::min<int64_t>(c->build_blocks, std::max<int64_t>(1, (count + BUILD_WARPS - 1) / BUILD_WARPS));
     int64_t eblocks = std::min<int64_t>(c->eval_blocks, want);
     if (const char *e = getenv("PF_EVAL_BPSM"))  // development experiment: cap eval blocks per SM
         eblocks = std::min<int64_t>(eblocks, (int64_t)atoi(e) * c->nsm);
@@ -573,7 +577,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         if (ensure(&c->gpoly, &c->gpoly_cap, (size_t)n) || ensure(&c->stage, &c->stage_cap, (size_t)n))
             return -1;
         g_launches++;
-        k_cells_build<<<(int)bblocks, FAST_WARPS * 32, FAST_WARPS * sizeof(BWS<FastCaps>), st>>>(
+        k_cells_build<<<(int)bblocks, BUILD_WARPS * 32, BUILD_WARPS * sizeof(BWS<FastCaps>), st>>>(
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
         CK(cudaGetLastError());
         if (sev) CK(cudaEventRecord(sev[1], st));

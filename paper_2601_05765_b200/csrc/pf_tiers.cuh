@@ -3,10 +3,11 @@
 //   Fast : shared-memory workspace sized for the cells seen on the paper's
 //          scenes (ball-aware maxima measured on dense blocks: nv 38, nf 21,
 //          nl 114): 48 vertices, 32 facets, 160 loop
-//          entries, 40 candidates per distance shell -- small enough for 20
-//          build warps per SM (measured: 7% faster than 16 warps with the
-//          64 / 192 / 64 capacities).  A cell that exceeds any capacity is
-//          queued, untouched, for the exact tier.
+//          entries, 40 candidates per distance shell, 48 crossing entries --
+//          9.6 KB of shared memory per build warp, i.e. 24 warps per SM in
+//          blocks of 8 (measured on C4: 116 ms at 16 warps with the 64 / 192 /
+//          64 capacities, 108 ms at 20, 105 ms at 24).  A cell that exceeds
+//          any capacity is queued, untouched, for the exact tier.
 //   Exact: the reference's own capacities (_kernels.py:24-27) in a
 //          global-memory workspace; overflow here reproduces the reference's
 //          CLIP_OVERFLOW / FLAG_OVERFLOW outcome.
@@ -24,6 +25,9 @@ namespace pf {
 #ifndef PF_FCC
 #define PF_FCC 40
 #endif
-using FastCaps = Caps<PF_FCV, 32, PF_FCL, PF_FCC, 64, 120, false>;
+#ifndef PF_FCE
+#define PF_FCE 48
+#endif
+using FastCaps = Caps<PF_FCV, 32, PF_FCL, PF_FCC, PF_FCE, 120, false>;
 using ExactCaps = Caps<REF_MAX_V, REF_MAX_F, REF_MAX_L, 1024, REF_MAX_L, 4096, true>;
 }  // namespace pf
