@@ -371,8 +371,12 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
 #ifndef PF_SYNC_WARPS
 #define PF_SYNC_WARPS 8
 #endif
+#ifndef PF_SYNC_BLOCKS
+#define PF_SYNC_BLOCKS 2
+#endif
 constexpr int SYNC_WARPS = PF_SYNC_WARPS;
-__global__ void __launch_bounds__(SYNC_WARPS * 32, 16 / SYNC_WARPS)
+constexpr int SYNC_BLOCKS = PF_SYNC_BLOCKS;  // blocks per SM
+__global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
     k_cells_eval_sync(CellIn in, CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
                       const uint8_t *__restrict__ stage, int *__restrict__ retry_list,
                       int *__restrict__ counters, unsigned long long *__restrict__ err) {
@@ -583,7 +587,7 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         if (sev) CK(cudaEventRecord(sev[1], st));
         g_launches++;
         if (c->eval_sync) {
-            const int64_t sb = std::min<int64_t>(c->nsm * (16 / SYNC_WARPS), (count + SYNC_WARPS - 1) / SYNC_WARPS);
+            const int64_t sb = std::min<int64_t>(c->nsm * SYNC_BLOCKS, (count + SYNC_WARPS - 1) / SYNC_WARPS);
             k_cells_eval_sync<<<(int)sb, SYNC_WARPS * 32, SYNC_WARPS * sizeof(EWS<FastCaps>), st>>>(
                 in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
         } else {
