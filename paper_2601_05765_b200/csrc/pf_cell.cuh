@@ -830,17 +830,31 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         if (in.ball_aware && br < stop_r) stop_r = br;
         #pragma unroll 1
         for (int c = 0; c < nc; c++) {
-            if (sqrt(S.cd2[c]) >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
+            // candidate c into registers; the warp syncs before any lane acts on
+            // it (a lane that runs ahead must not overwrite the shared scratch
+            // -- next shell's gather, evaluation workspace -- under a slower lane)
+            const double D2 = S.cd2[c];
             const int j = S.cj[c];
             const int sl = S.cord[c];
-            if (S.cd2[c] <= tol * tol) {
-                const double psij = S.cw[sl];
+            const double nxc = S.cx[sl], nyc = S.cy[sl], nzc = S.cz[sl], ddc = S.cw[sl];
+            pfw::sync();
+            if (sqrt(D2) >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
+            if (D2 <= tol * tol) {
+                const double psij = ddc;  // coincident site: the slot kept its weight
                 if (psij > psii || (psij == psii && j < i)) { *which_out = which; *nclips = ncl; return 1; }
                 continue;
             }
             ncl++;
-            int st = clip(ws, ws->P[which], ws->P[1 - which], which, S.cx[sl], S.cy[sl], S.cz[sl], S.cw[sl],
-                          j, tol);
+            // Every vertex lies within rfar of the site, so a bisector plane
+            // farther than rfar (h = dd - n.p) leaves the polytope untouched:
+            // the reference's vertex classification would find no vertex with
+            // s > tol.  Skip it (exact: the margin dwarfs the rounding of s, h
+            // and rfar).  Same census as the classification.
+            if (ddc - (nxc * px + nyc * py + nzc * pz) > rfar * (1.0 + 1e-12) + 1e-12) {
+                if (ws->cen_on && pfw::lane() == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += ws->P[which].nv; }
+                continue;
+            }
+            int st = clip(ws, ws->P[which], ws->P[1 - which], which, nxc, nyc, nzc, ddc, j, tol);
             if (st == CLIP_EMPTY) { *which_out = which; *nclips = ncl; return 1; }
             if (st == CLIP_OVERFLOW) { *which_out = which; *nclips = ncl; return 3; }
             if (st == CLIP_CUT) {
