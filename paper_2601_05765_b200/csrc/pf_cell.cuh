@@ -98,7 +98,8 @@ struct BuildScratch {
             uint8_t half[C::CV];   // their half-plane (angle order, see ang_lt)
         };
         struct {               // gather_shell
-            int run_start[32], run_off[32];
+            int run_start[32], run_off[32];  // per column: first run, offset in the batch
+            int run_la[32], run_stb[32];      // length of the first run, start of the second
         };
     };
     double cd2[C::CC];         // candidates (d^2, j), sorted
@@ -679,18 +680,44 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
     #pragma unroll 1
     for (int r0 = 0; r0 < nruns; r0 += 32) {
         int rr = r0 + L;
-        int st = 0, len = 0;
+        int st = 0, len = 0, la = 0, stb = 0;
         if (rr < nruns) {
-            int ix = i0 + rr / ny, iy = j0 + rr % ny;
-            int lin0 = (ix * g.gn[1] + iy) * g.gn[2] + k0;
-            int lin1 = (ix * g.gn[1] + iy) * g.gn[2] + k1;
-            st = g.bstart[lin0];
-            len = g.bstart[lin1 + 1] - st;
+            // the column's buckets [k0, k1] minus the middle ones lying wholly
+            // inside the previous shells (d^2 < t_lo): two runs of sites.  Edge
+            // buckets (which also hold clamped sites) are never skipped; the
+            // 1e-6-bucket margins dwarf the rounding of the bucket assignment.
+            const int ix = i0 + rr / ny, iy = j0 + rr % ny;
+            const int base = (ix * g.gn[1] + iy) * g.gn[2];
+            int ka1 = k1, kb0 = k1 + 1;
+            if (t_lo > 0.0 && ix > 0 && ix < g.gn[0] - 1 && iy > 0 && iy < g.gn[1] - 1) {
+                const double hx = 1.0 / g.ih[0], hy = 1.0 / g.ih[1];
+                const double xl = g.lo[0] + (ix - 1e-6) * hx, xh = g.lo[0] + (ix + 1 + 1e-6) * hx;
+                const double yl = g.lo[1] + (iy - 1e-6) * hy, yh = g.lo[1] + (iy + 1 + 1e-6) * hy;
+                const double dx = fmax(fabs(xl - px), fabs(xh - px));
+                const double dy = fmax(fabs(yl - py), fabs(yh - py));
+                const double rem = t_lo * (1.0 - 1e-9) - dx * dx - dy * dy;
+                if (rem > 0.0) {
+                    const double sz = sqrt(rem);
+                    int kin0 = (int)ceil((pz - sz - g.lo[2]) * g.ih[2] + 1e-6);
+                    int kin1 = (int)floor((pz + sz - g.lo[2]) * g.ih[2] - 1e-6) - 1;
+                    if (kin0 < k0) kin0 = k0;
+                    if (kin0 < 1) kin0 = 1;
+                    if (kin1 > k1) kin1 = k1;
+                    if (kin1 > g.gn[2] - 2) kin1 = g.gn[2] - 2;
+                    if (kin0 <= kin1) { ka1 = kin0 - 1; kb0 = kin1 + 1; }
+                }
+            }
+            st = g.bstart[base + k0];
+            la = g.bstart[base + ka1 + 1] - st;
+            stb = g.bstart[base + kb0];
+            len = la + (g.bstart[base + k1 + 1] - stb);
         }
         int tot;
         int off = pfw::excl_scan_inl(len, L, &tot);
         S.run_start[L] = st;
         S.run_off[L] = off;
+        S.run_la[L] = la;
+        S.run_stb[L] = stb;
         pfw::sync();
         int nr = nruns - r0 < 32 ? nruns - r0 : 32;
         #pragma unroll 1
@@ -703,7 +730,8 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
                     int mid = (lo + hi + 1) >> 1;
                     if (S.run_off[mid] <= q) lo = mid; else hi = mid - 1;
                 }
-                int s = S.run_start[lo] + (q - S.run_off[lo]);
+                const int e = q - S.run_off[lo], la_ = S.run_la[lo];
+                int s = e < la_ ? S.run_start[lo] + e : S.run_stb[lo] + (e - la_);
                 int j = g.sid[s];
                 double d2 = sq(g.sx[s] - px) + sq(g.sy[s] - py) + sq(g.sz[s] - pz);
                 if (j != self && !(d2 < t_hi)) beyond = true;
@@ -787,6 +815,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     double t_lo = -1.0;
     double t_hi = in.ball_aware ? br * br * (1.0 + 1e-14) : in.t_init;
     if (!(t_hi > 0.0)) t_hi = 1e-300;
+    int ngot = 0;
     #pragma unroll 1
     for (;;) {
         bool all_sites = false;
@@ -794,8 +823,13 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         if (nc > C::CC) {
             // too many candidates in this shell: narrow it (ties at one d^2
             // cannot be split -> overflow)
+            // (aim at 0.7 CC candidates, assuming a uniform density of sites in the shell)
             double base = t_lo > 0.0 ? t_lo : 0.0;
-            double nt = base + (t_hi - base) * 0.25;
+            const double rl3 = base * sqrt(base), rh3 = t_hi * sqrt(t_hi);
+            const double r3 = rl3 + (rh3 - rl3) * (0.7 * C::CC / nc);
+            double nt = cbrt(r3 * r3);
+            const double half = base + (t_hi - base) * 0.5;
+            if (!(nt < half)) nt = half;
             if (!(nt > base) || !(nt < t_hi)) {
                 if (pfw::lane() == 0) ws->oflow = 1;
                 pfw::sync();
@@ -866,8 +900,17 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         }
         if (all_sites) break;
         if (sqrt(t_hi) >= stop_r) break;
+        // next shell: sized for ~0.7 CC candidates from the density seen so far
+        // (volume x 8 at most), and never past the stop radius -- the shells
+        // only batch the (d^2, j)-ordered candidate stream, any cut is exact
+        ngot += nc;
+        double f = ngot > 0 ? 1.0 + 0.7 * C::CC / ngot : 8.0;
+        if (f > 8.0) f = 8.0;
+        const double cf = cbrt(f);
         t_lo = t_hi;
-        t_hi = t_hi * 4.0;
+        t_hi = t_hi * (cf * cf);
+        const double tstop = stop_r * stop_r * (1.0 + 1e-12);
+        if (t_hi > tstop) t_hi = tstop;
     }
     *which_out = which;
     *nclips = ncl;
