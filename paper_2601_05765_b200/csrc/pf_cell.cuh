@@ -656,7 +656,7 @@ PF_DEV int bucket_coord(double x, double lo, double ih, int gn) {
 
 // returns the number of candidates (may exceed CC: overflow); *all_sites set
 // when the bucket range spans the whole grid
-template <class W>
+template <bool SKIP_INNER, class W>
 PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py, double pz,
                         double t_lo, double t_hi, bool *all_sites) {
     using C = typename W::Cap;
@@ -689,7 +689,7 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
             const int ix = i0 + rr / ny, iy = j0 + rr % ny;
             const int base = (ix * g.gn[1] + iy) * g.gn[2];
             int ka1 = k1, kb0 = k1 + 1;
-            if (t_lo > 0.0 && ix > 0 && ix < g.gn[0] - 1 && iy > 0 && iy < g.gn[1] - 1) {
+            if (SKIP_INNER && t_lo > 0.0 && ix > 0 && ix < g.gn[0] - 1 && iy > 0 && iy < g.gn[1] - 1) {
                 const double hx = 1.0 / g.ih[0], hy = 1.0 / g.ih[1];
                 const double xl = g.lo[0] + (ix - 1e-6) * hx, xh = g.lo[0] + (ix + 1 + 1e-6) * hx;
                 const double yl = g.lo[1] + (iy - 1e-6) * hy, yh = g.lo[1] + (iy + 1 + 1e-6) * hy;
@@ -708,9 +708,13 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
                 }
             }
             st = g.bstart[base + k0];
-            la = g.bstart[base + ka1 + 1] - st;
-            stb = g.bstart[base + kb0];
-            len = la + (g.bstart[base + k1 + 1] - stb);
+            if (ka1 == k1) {
+                len = la = g.bstart[base + k1 + 1] - st;
+            } else {
+                la = g.bstart[base + ka1 + 1] - st;
+                stb = g.bstart[base + kb0];
+                len = la + (g.bstart[base + k1 + 1] - stb);
+            }
         }
         int tot;
         int off = pfw::excl_scan_inl(len, L, &tot);
@@ -730,8 +734,12 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
                     int mid = (lo + hi + 1) >> 1;
                     if (S.run_off[mid] <= q) lo = mid; else hi = mid - 1;
                 }
-                const int e = q - S.run_off[lo], la_ = S.run_la[lo];
-                int s = e < la_ ? S.run_start[lo] + e : S.run_stb[lo] + (e - la_);
+                const int e = q - S.run_off[lo];
+                int s = S.run_start[lo] + e;
+                if (SKIP_INNER) {  // only later shells have two runs per column
+                    const int la_ = S.run_la[lo];
+                    if (e >= la_) s = S.run_stb[lo] + (e - la_);
+                }
                 int j = g.sid[s];
                 double d2 = sq(g.sx[s] - px) + sq(g.sy[s] - py) + sq(g.sz[s] - pz);
                 if (j != self && !(d2 < t_hi)) beyond = true;
@@ -787,6 +795,14 @@ PF_DEV void sort_candidates(W *ws, int nc) {
     pfw::sync();
 }
 
+// later shells (t_lo > 0) out of line: the first shell -- the only one of most
+// cells at converged weights -- keeps the lean single-run gather
+template <class W>
+PF_NOINL int gather_later(W *ws, const CellIn &in, int self, double px, double py, double pz, double t_lo,
+                          double t_hi, bool *all_sites) {
+    return gather_shell<true>(ws, in, self, px, py, pz, t_lo, t_hi, all_sites);
+}
+
 // ---------------------------------------------------------------------------
 // build the Laguerre cell of site i (_kernels.py:1197-1355)
 // returns 0 ok / 1 empty / 3 overflow; *which = buffer holding the cell
@@ -819,7 +835,8 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     #pragma unroll 1
     for (;;) {
         bool all_sites = false;
-        int nc = gather_shell(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites);
+        int nc = t_lo > 0.0 ? gather_later(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites)
+                            : gather_shell<false>(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites);
         if (nc > C::CC) {
             // too many candidates in this shell: narrow it (ties at one d^2
             // cannot be split -> overflow)

@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(EXACT_WARPS * 32)
         int got = 0;
         for (;;) {
             bool all = false;
-            int nc = gather_shell(ws, in, -1, qx, qy, qz, tlo, thi, &all);
+            int nc = gather_shell<true>(ws, in, -1, qx, qy, qz, tlo, thi, &all);
             if (nc > ExactCaps::CC) {
                 double base = tlo > 0.0 ? tlo : 0.0;
                 double nt = base + (thi - base) * 0.25;
