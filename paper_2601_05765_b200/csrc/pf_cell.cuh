@@ -153,7 +153,7 @@ template <class C> using EWS = WSX<C, 1, EU<C>>;
 // census slots:
 enum {
     CEN_CLIPS = 0, CEN_TESTS, CEN_NEWV, CEN_NFV, CEN_RFAR, CEN_CUTS, CEN_LOOP, CEN_CROSS,
-    CEN_RFAC, CEN_RFAC_NF, CEN_SEG, CEN_ARC, CEN_BPTS, CEN_PROJ, CEN_FULLC, CEN_N
+    CEN_RFAC, CEN_RFAC_NF, CEN_SEG, CEN_ARC, CEN_BPTS, CEN_PROJ, CEN_FULLC, CEN_GATH, CEN_N
 };
 
 // ---------------------------------------------------------------------------
@@ -165,6 +165,10 @@ struct GridView {
     const int *bstart;           // [ncell + 1]
     double lo[3], ih[3];
     int gn[3];
+    // per super-bucket (sf^3 buckets) maximum weight, or null: bounds the
+    // weights near a site for its security radius (build_cell)
+    const double *smax;
+    int sgn[3], sf;
 };
 
 struct CellIn {
@@ -181,6 +185,7 @@ struct CellIn {
     const double *dpsi_ptr;  // when set, dpsi is read from device memory
     int ball_aware, want_m2;
     double t_init;  // first shell radius^2 when not ball-aware
+    const double *cslack;  // optional: per-cell weight slack (cell_slack), ball-aware only
     const int *cells;  // optional: evaluate only these cells (original indices)
     int ncells;
 };
@@ -795,6 +800,37 @@ PF_DEV void sort_candidates(W *ws, int nc) {
     pfw::sync();
 }
 
+// Weight slack of site i's security radius rfar + sqrt(rfar^2 + slack).  The
+// reference takes the global max - min weight (_kernels.py:1300-1306).  A site
+// j can only cut the cell while |p_j - p_i| < rfar + sqrt(rfar^2 + psi_j -
+// psi_i), so any bound of psi_j - psi_i over the sites the reference processes
+// -- all within the ball-aware radius br of p_i -- is an exact slack: the sites
+// between the two radii leave the polytope untouched (h_ij >= rfar), as the
+// reference's own classification would find.  The bound is the max weight of
+// the super-buckets covering the box p_i +- br.  br itself keeps the global
+// slack (it is the reference's stop, not a property of the polytope).
+// Thread-per-site (pf_runtime.cu k_cell_slack); host-callable for the emulator.
+PF_DEV double cell_slack(const GridView &g, double px, double py, double pz, double psii, double dpsi) {
+    if (!(psii > 0.0)) return dpsi;
+    const double br = (sqrt(psii) + sqrt(psii + dpsi)) * (1.0 + 1e-12);
+    const int f = g.sf;
+    const int a0 = bucket_coord(px - br, g.lo[0], g.ih[0], g.gn[0]) / f;
+    const int a1 = bucket_coord(px + br, g.lo[0], g.ih[0], g.gn[0]) / f;
+    const int b0 = bucket_coord(py - br, g.lo[1], g.ih[1], g.gn[1]) / f;
+    const int b1 = bucket_coord(py + br, g.lo[1], g.ih[1], g.gn[1]) / f;
+    const int c0 = bucket_coord(pz - br, g.lo[2], g.ih[2], g.gn[2]) / f;
+    const int c1 = bucket_coord(pz + br, g.lo[2], g.ih[2], g.gn[2]) / f;
+    double m = -1e300;
+    for (int a = a0; a <= a1; a++)
+        for (int b = b0; b <= b1; b++)
+            for (int c = c0; c <= c1; c++) {
+                const double v = g.smax[(a * g.sgn[1] + b) * g.sgn[2] + c];
+                m = v > m ? v : m;
+            }
+    const double dl = m - psii;
+    return dl > 0.0 ? (dl < dpsi ? dl : dpsi) : 0.0;
+}
+
 // later shells (t_lo > 0) out of line: the first shell -- the only one of most
 // cells at converged weights -- keeps the lean single-run gather
 template <class W>
@@ -828,6 +864,10 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     if (in.ball_aware && psii <= 0.0) { *which_out = 0; return 0; }
     const double br = sq_ball + sq_psi_slack;
 
+    // weight slack of the security radius: the per-cell bound of cell_slack()
+    // when the runtime computed it, else the reference's global one
+    const double dpsi_s = (in.ball_aware && in.cslack) ? in.cslack[i] : dpsi;
+
     double t_lo = -1.0;
     double t_hi = in.ball_aware ? br * br * (1.0 + 1e-14) : in.t_init;
     if (!(t_hi > 0.0)) t_hi = 1e-300;
@@ -835,6 +875,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     #pragma unroll 1
     for (;;) {
         bool all_sites = false;
+        if (ws->cen_on && pfw::lane() == 0) ws->cen[CEN_GATH]++;
         int nc = t_lo > 0.0 ? gather_later(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites)
                             : gather_shell<false>(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites);
         if (nc > C::CC) {
@@ -877,7 +918,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
             S.cw[sl] = (nxp * px + nyp * py + nzp * pz) + hij;
         }
         pfw::sync();
-        double stop_r = rfar + sqrt(rfar * rfar + dpsi);
+        double stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
         if (in.ball_aware && br < stop_r) stop_r = br;
         #pragma unroll 1
         for (int c = 0; c < nc; c++) {
@@ -911,7 +952,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
             if (st == CLIP_CUT) {
                 which = 1 - which;
                 rfar = poly_rfar(ws->P[which], px, py, pz);
-                stop_r = rfar + sqrt(rfar * rfar + dpsi);
+                stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
                 if (in.ball_aware && br < stop_r) stop_r = br;
             }
         }

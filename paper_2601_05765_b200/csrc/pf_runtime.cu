@@ -74,6 +74,10 @@ struct pf_ctx {
     size_t sid_cap = 0, bid_cap = 0;
     int *bcount = nullptr, *bstart = nullptr;
     size_t bcount_cap = 0, bstart_cap = 0;
+    double *smax = nullptr;  // per super-bucket max weight (build_cell's local slack)
+    size_t smax_cap = 0;
+    double *cslack = nullptr;  // per-site weight slack
+    size_t cslack_cap = 0;
     int *scan_tmp = nullptr;
     size_t scan_tmp_cap = 0;
     int64_t grid_n = -1;
@@ -518,7 +522,34 @@ void fill_cellin(pf_ctx *c, CellIn &in, int64_t n, const double *pts, const doub
     in.t_init = (3.0 * h) * (3.0 * h);
 }
 
-int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cudaStream_t st) {
+// max weight per super-bucket (PF_SUPER^3 buckets), thread per super-bucket over
+// its columns' contiguous bucket runs
+enum { PF_SUPER = 4 };
+__global__ void k_super_max(GridView g, const double *__restrict__ psi, double *__restrict__ smax) {
+    const int ns = g.sgn[0] * g.sgn[1] * g.sgn[2];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ns; t += gridDim.x * blockDim.x) {
+        const int a = t / (g.sgn[1] * g.sgn[2]), b = (t / g.sgn[2]) % g.sgn[1], cz = t % g.sgn[2];
+        const int f = g.sf;
+        const int k0 = cz * f, k1 = min(k0 + f, g.gn[2]) - 1;
+        double m = -1e300;
+        for (int ix = a * f; ix < min(a * f + f, g.gn[0]); ix++)
+            for (int iy = b * f; iy < min(b * f + f, g.gn[1]); iy++) {
+                const int base = (ix * g.gn[1] + iy) * g.gn[2];
+                for (int s = g.bstart[base + k0]; s < g.bstart[base + k1 + 1]; s++) m = fmax(m, psi[g.sid[s]]);
+            }
+        smax[t] = m;
+    }
+}
+
+// per-site weight slack (pf_cell.cuh cell_slack), thread per site
+__global__ void k_cell_slack(CellIn in, int64_t n, double *__restrict__ slack) {
+    const double dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        slack[i] = cell_slack(in.g, in.pts[3 * i], in.pts[3 * i + 1], in.pts[3 * i + 2], in.psi[i], dpsi);
+}
+
+int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cudaStream_t st) {
+    CellIn in = in_;
     if (!c->attr_set) {
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
@@ -567,6 +598,22 @@ int launch_cells(pf_ctx *c, const CellIn &in, const CellOut &out, int64_t n, cud
         CK(cudaEventCreate(&c->ev[1]));
     }
     CK(cudaEventRecord(c->ev[0], st));
+    if (in.ball_aware && count > 0 && !getenv("PF_GLOBAL_SLACK")) {
+        in.g.sf = PF_SUPER;
+        if (const char *e = getenv("PF_SUPER_F")) in.g.sf = std::max(1, atoi(e));  // development experiment
+        for (int a = 0; a < 3; a++) in.g.sgn[a] = (in.g.gn[a] + in.g.sf - 1) / in.g.sf;
+        const size_t ns = (size_t)in.g.sgn[0] * in.g.sgn[1] * in.g.sgn[2];
+        if (ensure(&c->smax, &c->smax_cap, ns)) return -1;
+        g_launches++;
+        k_super_max<<<(int)std::min<size_t>((ns + 255) / 256, (size_t)c->nsm * 8), 256, 0, st>>>(in.g, in.psi, c->smax);
+        CK(cudaGetLastError());
+        in.g.smax = c->smax;
+        if (ensure(&c->cslack, &c->cslack_cap, (size_t)n)) return -1;
+        g_launches++;
+        k_cell_slack<<<(int)std::min<int64_t>((n + 255) / 256, (int64_t)c->nsm * 16), 256, 0, st>>>(in, n, c->cslack);
+        CK(cudaGetLastError());
+        in.cslack = c->cslack;
+    }
     cudaEvent_t *sev = nullptr;
     if (c->stage_on && c->split && count > 0) {
         if (c->stage_n == c->stage_ev.size()) {
@@ -775,7 +822,7 @@ int pf_ctx_destroy(pf_ctx *c) {
     if (!c) return 0;
     void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
                     c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
-                    c->err, c->census, c->exact_ws, c->gpoly, c->stage};
+                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete c;

@@ -201,6 +201,25 @@ int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
     in.dnv = dnv; in.dnf = dnf; in.dnl = dnl;
     in.tol = tol; in.dpsi = dpsi; in.ball_aware = ball_aware; in.want_m2 = want_m2;
     in.t_init = t_init;
+    // per super-bucket max weight, as pf_runtime.cu's k_super_max (PF_SUPER = 4)
+    std::vector<double> smax, cslack;
+    if (ball_aware && !getenv("PF_GLOBAL_SLACK")) {
+        const int f = 4, G[3] = {gn0, gn1, gn2};
+        for (int a = 0; a < 3; a++) in.g.sgn[a] = (G[a] + f - 1) / f;
+        in.g.sf = f;
+        smax.assign((size_t)in.g.sgn[0] * in.g.sgn[1] * in.g.sgn[2], -1e300);
+        for (int ix = 0; ix < gn0; ix++)
+            for (int iy = 0; iy < gn1; iy++)
+                for (int iz = 0; iz < gn2; iz++) {
+                    const int b = (ix * gn1 + iy) * gn2 + iz;
+                    double &m = smax[((ix / f) * in.g.sgn[1] + iy / f) * in.g.sgn[2] + iz / f];
+                    for (int s = bstart[b]; s < bstart[b + 1]; s++) m = std::max(m, psi[sid[s]]);
+                }
+        in.g.smax = smax.data();
+        cslack.resize(n);
+        for (int i = 0; i < n; i++) cslack[i] = cell_slack(in.g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], psi[i], dpsi);
+        in.cslack = cslack.data();
+    }
     CellOut out;
     memset(&out, 0, sizeof(out));
     out.status = status; out.vol = vol; out.ksur = ksur; out.cent = cent; out.ipt = ipt; out.m2 = m2;
