@@ -257,6 +257,33 @@ int pf_render_first_hit(pf_ctx *ctx, int64_t n, const double *pts, const double 
                         const double *cam_host, int width, int height, int32_t *hit_id, double *hit_t,
                         void *stream);
 
+/* Depth mode: in-fluid path length of each pixel ray (the union of the ball
+ * chords, clipped to the grid box), f64[h*w]; -1 flags a pixel whose ray met
+ * more than 48 ball entries inside one bucket segment (diagnostic pixel). */
+int pf_render_depth(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double rmax,
+                    const double *cam_host, int width, int height, double *depth, void *stream);
+
+/* Smooth mode: sphere tracing (<= 64 steps, surface eps) of the cubic smooth
+ * union of the sphere distances with blend radius k > 0, started just before
+ * the Raw hit raw_t (f64[h*w], -1 miss, from pf_render_first_hit); hit_t
+ * f64[h*w] (-1 miss), normal f64[h*w*3] (central differences). */
+int pf_render_smooth(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double rmax, double k,
+                     double eps, const double *cam_host, int width, int height, const double *raw_t,
+                     double *hit_t, double *normal, void *stream);
+
+/* smooth_sdf at m device points xq[m*3] -> out[m] (same field as Smooth). */
+int pf_smooth_sdf(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double rmax, double k,
+                  int64_t m, const double *xq, double *out, void *stream);
+
+/* sample_surface: sample q draws uniform points on sphere cell[q] (int64) until
+ * one lies on the free-surface patch K_i -- in the current domain (pf_set_domain)
+ * and strictly inside no other ball -- at most max_tries[q] draws; x[m*3],
+ * outward unit normal[m*3], status[m] (0 ok, 1 tries exhausted).  Counter-based
+ * RNG: the result is a function of (seed, q). */
+int pf_sample_surface(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double rmax, int64_t m,
+                      const int64_t *cell, const int64_t *max_tries, uint64_t seed, double *x, double *normal,
+                      int32_t *status, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,7 +111,8 @@ def cmd_simulate(a) -> int:
 
 
 def cmd_render(a) -> int:
-    """Render a frame's fluid surface (Raw mode) to a binary PPM."""
+    """Render a frame's fluid surface (Raw / Smooth / Depth) to a binary PPM and
+    optionally sample its surface to a point cloud."""
     import time
 
     import torch
@@ -122,10 +123,16 @@ def cmd_render(a) -> int:
     cam = render.Camera(eye=tuple(a.eye), look_at=tuple(a.look_at), fov=a.fov, width=a.width, height=a.height)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    img = render.render_raw(f.x, f.psi, cam)
+    kw = {"k": a.blend} if a.mode == "smooth" else {}
+    img = render.render(f.x, f.psi, cam, a.mode, **kw)
     torch.cuda.synchronize()
     render.write_ppm(a.out, img)
-    print(f"rendered {f.n} particles, {a.width}x{a.height} in {1e3 * (time.perf_counter() - t0):.1f} ms -> {a.out}")
+    print(f"rendered {f.n} particles ({a.mode}), {a.width}x{a.height} in "
+          f"{1e3 * (time.perf_counter() - t0):.1f} ms -> {a.out}")
+    if a.samples > 0:
+        x, nrm, _ = render.sample_surface(f.x, f.psi, a.samples)
+        render.write_point_cloud(a.cloud, x, nrm)
+        print(f"{a.samples} surface samples -> {a.cloud}")
     return 0
 
 
@@ -143,7 +150,7 @@ def main(argv=None) -> int:
     s.add_argument("--frame-stride", type=int, default=10)
     s.add_argument("--warm-start", default=None, help="POTF frame to resume from")
     s.add_argument("--best-effort", action="store_true")
-    r = sub.add_parser("render", help="render a frame (Raw first-hit shading) to .ppm")
+    r = sub.add_parser("render", help="render a frame (raw | smooth | depth) to .ppm, optionally a surface point cloud")
     r.add_argument("frame")
     r.add_argument("--out", default="frame.ppm")
     r.add_argument("--eye", type=float, nargs=3, default=[0.5, -1.2, 0.9])
@@ -151,6 +158,10 @@ def main(argv=None) -> int:
     r.add_argument("--fov", type=float, default=0.8)
     r.add_argument("--width", type=int, default=1280)
     r.add_argument("--height", type=int, default=720)
+    r.add_argument("--mode", default="raw", choices=["raw", "smooth", "depth"])
+    r.add_argument("--blend", type=float, default=None, help="Smooth blend radius k (default 0.5 x mean radius)")
+    r.add_argument("--samples", type=int, default=0, help="also write this many surface samples")
+    r.add_argument("--cloud", default="surface.xyz", help="point cloud path for --samples")
     a = ap.parse_args(argv)
     return {"bench": cmd_bench, "simulate": cmd_simulate, "render": cmd_render}[a.cmd](a)
 

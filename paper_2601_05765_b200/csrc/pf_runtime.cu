@@ -898,6 +898,11 @@ int pf_internal_grid_view(pf_ctx *c, const double **sx, const double **sy, const
     for (int a = 0; a < 3; a++) { gn[a] = c->gn[a]; lo[a] = c->glo[a]; h[a] = c->gh[a]; }
     return 0;
 }
+int pf_internal_domain_view(pf_ctx *c, const double **dp, int *nf, double *tol) {
+    if (!c->has_domain) return set_err("domain view: no domain set");
+    *dp = c->dp; *nf = c->dnf; *tol = c->tol;
+    return 0;
+}
 extern "C" {
 int pf_grid_info(pf_ctx *c, int *dims, double *lo, double *h) {
     for (int a = 0; a < 3; a++) {

@@ -37,3 +37,22 @@ def test_bench_table(capsys):
     assert cli.main(["bench", "--sizes", "8000", "--steps", "3"]) == 0
     txt = capsys.readouterr().out
     assert "Laguerre" in txt and "Evaluation" in txt and "Complete Step" in txt
+
+
+@pytest.mark.parametrize("mode", ["raw", "smooth", "depth"])
+def test_render_frame(tmp_path, mode):
+    from paper_2601_05765_b200 import cli
+
+    out = tmp_path / "run"
+    assert cli.main(["simulate", "--config", "C2", "--steps", "1", "--out", str(out), "--frame-stride", "1"]) == 0
+    img = tmp_path / f"{mode}.ppm"
+    args = ["render", str(out / "frame_000001.potf"), "--out", str(img), "--mode", mode, "--width", "160",
+            "--height", "120"]
+    if mode == "raw":
+        args += ["--samples", "500", "--cloud", str(tmp_path / "s.xyz")]
+    assert cli.main(args) == 0
+    raw = open(img, "rb").read()
+    assert raw.startswith(b"P6\n160 120\n255\n") and len(raw) == len(b"P6\n160 120\n255\n") + 160 * 120 * 3
+    if mode == "raw":
+        pts = np.loadtxt(tmp_path / "s.xyz")
+        assert pts.shape == (500, 6) and np.allclose(np.linalg.norm(pts[:, 3:], axis=1), 1.0)
