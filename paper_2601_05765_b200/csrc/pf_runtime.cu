@@ -90,6 +90,9 @@ struct pf_ctx {
     // evaluation scratch
     int *retry_list = nullptr;
     size_t retry_cap = 0;
+    int *retry_list2 = nullptr;  // the mid tier's overflow
+    size_t retry2_cap = 0;
+    bool mid = true;
     int *counters = nullptr;  // [0] retry count
     unsigned long long *err = nullptr;
     int *census = nullptr;
@@ -119,6 +122,7 @@ namespace {
 
 constexpr int FAST_WARPS = 4;
 constexpr int EXACT_WARPS = 2;
+constexpr int MID_WARPS = 4;
 
 __device__ __forceinline__ unsigned long long ord_bits(double x) {
     unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -449,7 +453,30 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
-// cells that overflowed the fast tier, with the reference's capacities
+// cells that overflowed the fast tier: larger capacities, still in shared memory;
+// their own overflow is queued for the exact tier
+__global__ void __launch_bounds__(MID_WARPS * 32, 1)
+    k_cells_mid(CellIn in, CellOut out, const int *__restrict__ list, int *__restrict__ counters,
+                int *__restrict__ list2, unsigned long long *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WS<MidCaps> *ws = (WS<MidCaps> *)(smem + (size_t)wid * sizeof(WS<MidCaps>));
+    const int count = counters[0];
+    const int nw = gridDim.x * MID_WARPS;
+    int fl = 0;
+    for (int t = blockIdx.x * MID_WARPS + wid; t < count; t += nw) {
+        const int i = list[t];
+        int r = run_cell(ws, in, out, i);
+        if (r & FLAG_RETRY) {
+            if (lane == 0) list2[atomicAdd(&counters[1], 1)] = i;
+        } else {
+            fl |= r & 7;
+        }
+    }
+    if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
+}
+
+// cells that overflowed the mid tier, with the reference's capacities
 __global__ void __launch_bounds__(EXACT_WARPS * 32)
     k_cells_exact(CellIn in, CellOut out, const int *__restrict__ list, const int *__restrict__ counters,
                   WS<ExactCaps> *__restrict__ wsbase, unsigned long long *__restrict__ err) {
@@ -561,6 +588,9 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
         CK(cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(SYNC_WARPS * sizeof(EWS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CK(cudaFuncSetAttribute(k_cells_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(MID_WARPS * sizeof(WS<MidCaps>))));
+        c->mid = !getenv("PF_NO_MID");
         {
             const char *e = getenv("PF_EVAL_SYNC");
             c->eval_sync = !(e && e[0] == '0');
@@ -648,9 +678,17 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
             in, out, (int)count, c->retry_list, c->counters, c->err);
         CK(cudaGetLastError());
     }
+    if (c->mid) {
+        if (ensure(&c->retry_list2, &c->retry2_cap, (size_t)n + 1)) return -1;
+        g_launches++;
+        k_cells_mid<<<c->nsm, MID_WARPS * 32, MID_WARPS * sizeof(WS<MidCaps>), st>>>(
+            in, out, c->retry_list, c->counters, c->retry_list2, c->err);
+        CK(cudaGetLastError());
+    }
     g_launches++;
     k_cells_exact<<<c->exact_warps / EXACT_WARPS, EXACT_WARPS * 32, 0, st>>>(
-        in, out, c->retry_list, c->counters, c->exact_ws, c->err);
+        in, out, c->mid ? c->retry_list2 : c->retry_list, c->mid ? c->counters + 1 : c->counters, c->exact_ws,
+        c->err);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[1], st));
     if (sev) CK(cudaEventRecord(sev[2], st));
@@ -822,7 +860,7 @@ int pf_ctx_destroy(pf_ctx *c) {
     if (!c) return 0;
     void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
                     c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
-                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack};
+                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete c;

@@ -1,4 +1,4 @@
-// pf_tiers.cuh -- the two capacity instantiations of the cell kernel.
+// pf_tiers.cuh -- the three capacity instantiations of the cell kernel.
 //
 //   Fast : shared-memory workspace sized for the cells seen on the paper's
 //          scenes (ball-aware maxima measured on dense blocks: nv 38, nf 21,
@@ -8,6 +8,8 @@
 //          blocks of 8 (measured on C4: 116 ms at 16 warps with the 64 / 192 /
 //          64 capacities, 108 ms at 20, 105 ms at 24).  A cell that exceeds
 //          any capacity is queued, untouched, for the exact tier.
+//   Mid  : 128 V / 64 F / 448 entries / 64 candidates / 512 pool points in
+//          shared memory for the fast tier's overflow; its own overflow goes on.
 //   Exact: the reference's own capacities (_kernels.py:24-27) in a
 //          global-memory workspace; overflow here reproduces the reference's
 //          CLIP_OVERFLOW / FLAG_OVERFLOW outcome.
@@ -29,5 +31,8 @@ namespace pf {
 #define PF_FCE 48
 #endif
 using FastCaps = Caps<PF_FCV, 32, PF_FCL, PF_FCC, PF_FCE, 120, false>;
+// Mid: the fast tier's overflow (mostly the boundary-point pool of cells whose
+// sphere meets many facets) in shared memory, 4 warps (48 KB each) per SM.
+using MidCaps = Caps<128, 64, 448, 64, 128, 512, false>;
 using ExactCaps = Caps<REF_MAX_V, REF_MAX_F, REF_MAX_L, 1024, REF_MAX_L, 4096, true>;
 }  // namespace pf

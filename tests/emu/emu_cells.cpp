@@ -157,7 +157,8 @@ void pfemu_set_cells(const int *cells, int ncells) {
 
 // Build the bucket-sorted SoA grid exactly as the device grid build does
 // (stable counting sort by bucket id) and run every cell through the fast
-// tier, then the exact tier for retries.  tier: 0 = fast->exact, 1 = exact only.
+// tier, then the mid and exact tiers for retries.  tier: 0 = fast->mid->exact,
+// 1 = exact only, 2 = mid->exact.
 int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
                        const double *dv, int dnv, const double *dp, const int *dt, int dnf,
                        const int *dlp, const int *dlv, int dnl,
@@ -235,6 +236,7 @@ int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
         pfw::EmuWarp *w = pfw::emu_new_warp(1 << 18);
         WS<FastCaps> *wsf = (WS<FastCaps> *)aligned_alloc(64, (sizeof(WS<FastCaps>) + 63) / 64 * 64);
         WS<ExactCaps> *wse = (WS<ExactCaps> *)aligned_alloc(64, (sizeof(WS<ExactCaps>) + 63) / 64 * 64);
+        WS<MidCaps> *wsm = (WS<MidCaps> *)aligned_alloc(64, (sizeof(WS<MidCaps>) + 63) / 64 * 64);
         const int nk = g_only ? g_nonly : n;
 #pragma omp for schedule(dynamic, 4)
         for (int k = 0; k < nk; k++) {
@@ -246,8 +248,14 @@ int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
                 if (e > emu_error) emu_error = e;
                 r = job.result;
             }
+            if (tier == 0 && (r & FLAG_RETRY)) retries++;
+            if ((r & FLAG_RETRY) && tier != 1) {
+                Job<MidCaps> job{wsm, &in, &out, i, 0};
+                int e = pfw::emu_run_warp(w, lane_fn<MidCaps>, &job, seed + (uint64_t)i * 31337u);
+                if (e > emu_error) emu_error = e;
+                r = job.result;
+            }
             if (r & FLAG_RETRY) {
-                if (tier == 0) retries++;
                 Job<ExactCaps> job{wse, &in, &out, i, 0};
                 int e = pfw::emu_run_warp(w, lane_fn<ExactCaps>, &job, seed + (uint64_t)i * 104729u);
                 if (e > emu_error) emu_error = e;
@@ -258,6 +266,7 @@ int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
         ncoll += w->n_collectives;
         free(wsf);
         free(wse);
+        free(wsm);
         pfw::emu_free_warp(w);
     }
     if (n_retry) *n_retry = retries;

@@ -27,7 +27,7 @@ def grid_for(pts, psi, dpsi):
 
 
 @pytest.mark.parametrize("name", NAMES)
-@pytest.mark.parametrize("tier", [0, 1])
+@pytest.mark.parametrize("tier", [0, 1, 2])
 def test_emulated_kernel_vs_reference(golden, name, tier):
     s = golden_scene(golden, name)
     lo, ih, gn = grid_for(s["pts"], s["psi"], float(s["dpsi"]))
