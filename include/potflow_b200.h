@@ -248,6 +248,16 @@ int pf_fluid_forces_implicit(int64_t n, int smf, const double *x, const double *
                              int ndom, int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
                              double *sol, double rtol, void *stream);
 
+/* compact per-facet CSR of an evaluation's fixed-stride facet outputs
+ * (SURVEY §8(b)): row_ptr int64[n+1] (row i = the min(fcount[i], smf) facets of
+ * cell i, in the fixed-stride order), then per facet tag / area / h (nnz),
+ * nrm / cent (nnz*3); any output may be null.  *nnz receives the facet count;
+ * more than `cap` facets -> error (call with cap 0 to size the buffers). */
+int pf_facets_csr(pf_ctx *ctx, int64_t n, int64_t smf, const int64_t *fcount, const int64_t *ftag,
+                  const double *farea, const double *fh, const double *fnrm, const double *fcent, int64_t cap,
+                  int64_t *nnz, int64_t *row_ptr, int64_t *tag, double *area, double *h, double *nrm, double *cent,
+                  void *stream);
+
 /* ---- renderer ----------------------
  * first hit of one ray per pixel with the fluid (the union of the balls, whose
  * first point along a ray lies in the entered ball's Laguerre cell): hit_id

@@ -65,6 +65,8 @@ def lib():
         L.pf_batch_build.argtypes = [vp, i64, vp, vp, d, d, i, i64, i64, i64] + [vp] * 9 + [i, vp]
         L.pf_grid_order.restype = i
         L.pf_grid_order.argtypes = [vp, vp, vp]
+        L.pf_facets_csr.restype = i
+        L.pf_facets_csr.argtypes = [vp, i64, i64] + [vp] * 6 + [i64] + [vp] * 7 + [vp]
         L.pf_knn.restype = i64
         L.pf_knn.argtypes = [vp, i64, vp, i64, vp, i64, vp, vp]
         for name in ("pf_ctx_create", "pf_ctx_destroy", "pf_set_domain", "pf_grid_build",

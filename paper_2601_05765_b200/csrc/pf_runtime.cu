@@ -76,6 +76,8 @@ struct pf_ctx {
     size_t bcount_cap = 0, bstart_cap = 0;
     double *smax = nullptr;  // per super-bucket max weight (build_cell's local slack)
     size_t smax_cap = 0;
+    int *csr_cnt = nullptr, *csr_off = nullptr;  // pf_facets_csr scratch
+    size_t csr_cnt_cap = 0, csr_off_cap = 0;
     double *cslack = nullptr;  // per-site weight slack
     size_t cslack_cap = 0;
     int *scan_tmp = nullptr;
@@ -860,7 +862,7 @@ int pf_ctx_destroy(pf_ctx *c) {
     if (!c) return 0;
     void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
                     c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
-                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2};
+                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2, c->csr_cnt, c->csr_off};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete c;
@@ -941,6 +943,37 @@ int pf_internal_domain_view(pf_ctx *c, const double **dp, int *nf, double *tol) 
     *dp = c->dp; *nf = c->dnf; *tol = c->tol;
     return 0;
 }
+// compact per-facet CSR of the fixed-stride outputs:
+// count per cell, two-level exclusive scan, then a thread-per-cell copy
+__global__ void k_facet_count(int64_t n, int64_t smf, const int64_t *__restrict__ fcount, int *__restrict__ cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = i < n ? fcount[i] : 0;
+        cnt[i] = (int)(k < 0 ? 0 : (k > smf ? smf : k));
+    }
+}
+__global__ void k_facet_fill(int64_t n, int64_t smf, const int *__restrict__ off, const int64_t *__restrict__ ftag,
+                             const double *__restrict__ farea, const double *__restrict__ fh,
+                             const double *__restrict__ fnrm, const double *__restrict__ fcent,
+                             int64_t *__restrict__ row_ptr, int64_t *__restrict__ tag_o, double *__restrict__ area_o,
+                             double *__restrict__ h_o, double *__restrict__ nrm_o, double *__restrict__ cent_o) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = off[i];
+        if (row_ptr) row_ptr[i] = o;
+        if (i == n) continue;
+        const int64_t m = off[i + 1] - o;
+        for (int64_t s = 0; s < m; s++) {
+            const int64_t a = i * smf + s, b = o + s;
+            if (tag_o) tag_o[b] = ftag[a];
+            if (area_o) area_o[b] = farea[a];
+            if (h_o) h_o[b] = fh[a];
+            for (int d = 0; d < 3; d++) {
+                if (nrm_o) nrm_o[3 * b + d] = fnrm[3 * a + d];
+                if (cent_o) cent_o[3 * b + d] = fcent[3 * a + d];
+            }
+        }
+    }
+}
+
 extern "C" {
 int pf_grid_info(pf_ctx *c, int *dims, double *lo, double *h) {
     for (int a = 0; a < 3; a++) {
@@ -1211,6 +1244,39 @@ int64_t pf_knn(pf_ctx *c, int64_t n, const double *pts, int64_t nq, const double
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return k;
+}
+
+int pf_facets_csr(pf_ctx *c, int64_t n, int64_t smf, const int64_t *fcount, const int64_t *ftag,
+                  const double *farea, const double *fh, const double *fnrm, const double *fcent, int64_t cap,
+                  int64_t *nnz, int64_t *row_ptr, int64_t *tag, double *area, double *h, double *nrm, double *cent,
+                  void *stream) {
+    cudaStream_t st = S(stream);
+    if (n < 0 || smf <= 0 || !fcount) return set_err("pf_facets_csr: bad arguments");
+    if ((double)n * (double)smf > 2147483647.0) return set_err("pf_facets_csr: n * smf exceeds int32 offsets");
+    const int64_t nblk = (n + 1 + SCAN_B - 1) / SCAN_B;
+    if (nblk > SCAN_B) return set_err("pf_facets_csr: too many cells for the two-level scan");
+    if (ensure(&c->csr_cnt, &c->csr_cnt_cap, (size_t)n + 1) || ensure(&c->csr_off, &c->csr_off_cap, (size_t)n + 1) ||
+        ensure(&c->scan_tmp, &c->scan_tmp_cap, 2 * nblk + 2))
+        return -1;
+    const int gb = (int)std::min<int64_t>(c->nsm * 8, (n + 256) / 256);
+    g_launches += 2;
+    k_facet_count<<<gb, 256, 0, st>>>(n, smf, fcount, c->csr_cnt);
+    k_scan_blocks<<<(int)nblk, SCAN_T, 0, st>>>(c->csr_cnt, c->csr_off, n + 1, c->scan_tmp);
+    if (nblk > 1) {
+        g_launches += 2;
+        k_scan_blocks<<<1, SCAN_T, 0, st>>>(c->scan_tmp, c->scan_tmp + nblk + 1, nblk, nullptr);
+        k_scan_add<<<(int)nblk, 256, 0, st>>>(c->csr_off, n + 1, c->scan_tmp + nblk + 1);
+    }
+    int tot = 0;
+    CK(cudaMemcpyAsync(&tot, c->csr_off + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (nnz) *nnz = tot;
+    if (tot > cap) return set_err("pf_facets_csr: %d facets exceed the capacity %lld", tot, (long long)cap);
+    g_launches++;
+    k_facet_fill<<<gb, 256, 0, st>>>(n, smf, c->csr_off, ftag, farea, fh, fnrm, fcent, row_ptr, tag, area, h, nrm,
+                                      cent);
+    CK(cudaGetLastError());
+    return 0;
 }
 
 }  // extern "C"

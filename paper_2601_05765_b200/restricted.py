@@ -63,6 +63,40 @@ def evaluate(pts, psi, domain: ConvexCell, ball_aware: bool = True, want_m2: boo
     return RestrictedDiagram(*o, flags=err)
 
 
+@dataclass
+class FacetCSR:
+    row_ptr: "torch.Tensor"  # int64 [n+1]
+    tag: "torch.Tensor"      # int64 [nnz] neighbour j >= 0 or domain face -(k+1)
+    area: "torch.Tensor"     # f64 [nnz]
+    h: "torch.Tensor"        # f64 [nnz]
+    nrm: "torch.Tensor"      # f64 [nnz,3]
+    cent: "torch.Tensor"     # f64 [nnz,3]
+
+
+def facets_csr(d: RestrictedDiagram) -> FacetCSR:
+    """Compact per-facet CSR of an evaluation's fixed-stride facet arrays
+    (pf_facets_csr): row i holds the min(fcount[i], smf) facets of
+    cell i in the fixed-stride order."""
+    import ctypes as C
+
+    import torch
+
+    L = _lib.lib()
+    n, smf = d.ftag.shape
+    nnz = C.c_int64(0)
+    args = [_lib.ctx(), n, smf] + [_lib.ptr(t) for t in (d.fcount, d.ftag, d.farea, d.fh, d.fnrm, d.fcent)]
+    # size query (cap 0 fails when there are facets: read nnz from it)
+    L.pf_facets_csr(*args, 0, C.byref(nnz), *([None] * 6), _lib.stream_ptr())
+    m = int(nnz.value)
+    f8, i8 = dict(dtype=torch.float64, device="cuda"), dict(dtype=torch.int64, device="cuda")
+    out = FacetCSR(torch.empty(n + 1, **i8), torch.empty(m, **i8), torch.empty(m, **f8), torch.empty(m, **f8),
+                   torch.empty((m, 3), **f8), torch.empty((m, 3), **f8))
+    _lib.check(L.pf_facets_csr(*args, m, C.byref(nnz), _lib.ptr(out.row_ptr), _lib.ptr(out.tag),
+                               _lib.ptr(out.area), _lib.ptr(out.h), _lib.ptr(out.nrm), _lib.ptr(out.cent),
+                               _lib.stream_ptr()), "pf_facets_csr")
+    return out
+
+
 def census(n: int):
     """Per-cell processed-candidate counts of the last evaluation (int32 [n])."""
     import torch

@@ -153,3 +153,24 @@ def test_dpsi_max_matches():
     psi = rng.random(100_003) * 1e-3 - 2e-4
     assert laguerre._dpsi_max(psi) == float(max(psi.max() - psi.min(), 0.0))
     assert laguerre._dpsi_max(np.array([])) == 0.0
+
+
+def test_facets_csr_matches_the_fixed_stride_arrays():
+    """pf_facets_csr: the compact per-facet CSR holds exactly the
+    first min(fcount, smf) facets of every cell, in order, bit-equal."""
+    import torch
+
+    from paper_2601_05765_b200 import geom, restricted, scenes
+
+    sc = scenes.c2_dam_break(m=14)
+    h = sc.meta["h"]
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    d = restricted.evaluate(torch.as_tensor(sc.pts, device="cuda"),
+                            torch.full((sc.n,), (0.85 * h) ** 2, dtype=torch.float64, device="cuda"), dom, smf=8)
+    c = restricted.facets_csr(d)
+    fc = np.minimum(d.fcount.cpu().numpy(), 8)
+    rp = c.row_ptr.cpu().numpy()
+    assert rp[0] == 0 and np.array_equal(np.diff(rp), fc)
+    mask = np.arange(8)[None, :] < fc[:, None]
+    for a, b in ((c.tag, d.ftag), (c.area, d.farea), (c.h, d.fh), (c.nrm, d.fnrm), (c.cent, d.fcent)):
+        assert np.array_equal(a.cpu().numpy(), b.cpu().numpy()[mask])
