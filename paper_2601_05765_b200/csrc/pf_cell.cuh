@@ -679,6 +679,12 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
                  k1 == g.gn[2] - 1;
     const int ny = j1 - j0 + 1;
     const int nruns = (i1 - i0 + 1) * ny;
+    // the grid arrays into registers: `in` lives in local memory and the
+    // compiler must otherwise reload it after every (generic) shared store
+    const double *__restrict__ gsx = g.sx, *__restrict__ gsy = g.sy, *__restrict__ gsz = g.sz;
+    const int *__restrict__ gsid = g.sid, *__restrict__ gbst = g.bstart;
+    const double *__restrict__ gpsi = in.psi;
+    const int gn1 = g.gn[1], gn2 = g.gn[2];
     if (L == 0) S.ncand = 0;
     pfw::sync();
     bool beyond = false;
@@ -692,7 +698,7 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
             // buckets (which also hold clamped sites) are never skipped; the
             // 1e-6-bucket margins dwarf the rounding of the bucket assignment.
             const int ix = i0 + rr / ny, iy = j0 + rr % ny;
-            const int base = (ix * g.gn[1] + iy) * g.gn[2];
+            const int base = (ix * gn1 + iy) * gn2;
             int ka1 = k1, kb0 = k1 + 1;
             if (SKIP_INNER && t_lo > 0.0 && ix > 0 && ix < g.gn[0] - 1 && iy > 0 && iy < g.gn[1] - 1) {
                 const double hx = 1.0 / g.ih[0], hy = 1.0 / g.ih[1];
@@ -712,13 +718,13 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
                     if (kin0 <= kin1) { ka1 = kin0 - 1; kb0 = kin1 + 1; }
                 }
             }
-            st = g.bstart[base + k0];
+            st = gbst[base + k0];
             if (ka1 == k1) {
-                len = la = g.bstart[base + k1 + 1] - st;
+                len = la = gbst[base + k1 + 1] - st;
             } else {
-                la = g.bstart[base + ka1 + 1] - st;
-                stb = g.bstart[base + kb0];
-                len = la + (g.bstart[base + k1 + 1] - stb);
+                la = gbst[base + ka1 + 1] - st;
+                stb = gbst[base + kb0];
+                len = la + (gbst[base + k1 + 1] - stb);
             }
         }
         int tot;
@@ -745,15 +751,15 @@ PF_DEV int gather_shell(W *ws, const CellIn &in, int self, double px, double py,
                     const int la_ = S.run_la[lo];
                     if (e >= la_) s = S.run_stb[lo] + (e - la_);
                 }
-                int j = g.sid[s];
-                double d2 = sq(g.sx[s] - px) + sq(g.sy[s] - py) + sq(g.sz[s] - pz);
+                int j = gsid[s];
+                double d2 = sq(gsx[s] - px) + sq(gsy[s] - py) + sq(gsz[s] - pz);
                 if (j != self && !(d2 < t_hi)) beyond = true;
                 if (j != self && d2 >= t_lo && d2 < t_hi) {
                     int pos = pfw::atom_add(&S.ncand, 1);
                     if (pos < C::CC) {
                         S.cd2[pos] = d2; S.cj[pos] = j;
-                        S.cx[pos] = g.sx[s]; S.cy[pos] = g.sy[s]; S.cz[pos] = g.sz[s];
-                        S.cw[pos] = in.psi ? in.psi[j] : 0.0;
+                        S.cx[pos] = gsx[s]; S.cy[pos] = gsy[s]; S.cz[pos] = gsz[s];
+                        S.cw[pos] = gpsi ? gpsi[j] : 0.0;
                     }
                 }
             }
@@ -848,6 +854,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     using C = typename W::Cap;
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const double psii = in.psi[i];
+    const bool ball_aware = in.ball_aware != 0;  // hoisted: `in` is in local memory
     const double tol = in.tol, dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
     load_domain(ws->P[0], in);
     #pragma unroll 1
@@ -859,17 +866,17 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     int ncl = 0;
     *nclips = 0;
     double rfar = poly_rfar(ws->P[0], px, py, pz);
-    const double sq_ball = (in.ball_aware && psii > 0.0) ? sqrt(psii) : -1.0;
+    const double sq_ball = (ball_aware && psii > 0.0) ? sqrt(psii) : -1.0;
     const double sq_psi_slack = sqrt((psii > 0.0 ? psii : 0.0) + dpsi);
-    if (in.ball_aware && psii <= 0.0) { *which_out = 0; return 0; }
+    if (ball_aware && psii <= 0.0) { *which_out = 0; return 0; }
     const double br = sq_ball + sq_psi_slack;
 
     // weight slack of the security radius: the per-cell bound of cell_slack()
     // when the runtime computed it, else the reference's global one
-    const double dpsi_s = (in.ball_aware && in.cslack) ? in.cslack[i] : dpsi;
+    const double dpsi_s = (ball_aware && in.cslack) ? in.cslack[i] : dpsi;
 
     double t_lo = -1.0;
-    double t_hi = in.ball_aware ? br * br * (1.0 + 1e-14) : in.t_init;
+    double t_hi = ball_aware ? br * br * (1.0 + 1e-14) : in.t_init;
     if (!(t_hi > 0.0)) t_hi = 1e-300;
     int ngot = 0;
     #pragma unroll 1
@@ -919,7 +926,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         }
         pfw::sync();
         double stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
-        if (in.ball_aware && br < stop_r) stop_r = br;
+        if (ball_aware && br < stop_r) stop_r = br;
         #pragma unroll 1
         for (int c = 0; c < nc; c++) {
             // candidate c into registers; the warp syncs before any lane acts on
@@ -953,7 +960,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
                 which = 1 - which;
                 rfar = poly_rfar(ws->P[which], px, py, pz);
                 stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
-                if (in.ball_aware && br < stop_r) stop_r = br;
+                if (ball_aware && br < stop_r) stop_r = br;
             }
         }
         if (all_sites) break;
