@@ -185,14 +185,29 @@ __global__ void __launch_bounds__(RB) k_spmv(int64_t n, int smf, const int *__re
     if (ic[0]) return;
     __shared__ double sh[32];
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        double s = diag[i] * p[i];
-        const int c = hcnt[i];
-        const int *col = hcol + i * smf;
-        const double *val = hval + i * smf;
-        for (int k = 0; k < c; k++) s += val[k] * p[col[k]];
-        Ap[i] = s;
-        acc += p[i] * s;
+    // 8 lanes per row: a row's ELL slots are read as contiguous 32 / 64-byte
+    // segments and its gathers p[col] are in flight together (thread-per-row
+    // walked them one dependent load at a time)
+    const int sub = threadIdx.x & 7;
+    const int64_t rows_per_pass = (int64_t)gridDim.x * (RB / 8);
+    for (int64_t i = blockIdx.x * (int64_t)(RB / 8) + (threadIdx.x >> 3); i - (threadIdx.x >> 3) < n;
+         i += rows_per_pass) {
+        double s = 0.0;
+        const bool row = i < n;
+        if (row) {
+            const int c = hcnt[i];
+            const int *col = hcol + i * smf;
+            const double *val = hval + i * smf;
+            for (int k = sub; k < c; k += 8) s += val[k] * p[col[k]];
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (row && sub == 0) {
+            s += diag[i] * p[i];
+            Ap[i] = s;
+            acc += p[i] * s;
+        }
     }
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
