@@ -26,6 +26,15 @@ def _scene(kind):
     if kind == "C3":
         sc = scenes.c3_chocs()
         return sc, sc.psi_cold()
+    if kind == "C3c":  # converged weights: large local weight spread (per-cell slack, mid tier)
+        import torch
+
+        from paper_2601_05765_b200 import geom, solver
+
+        sc = scenes.c3_chocs()
+        res = solver.newton_solve(torch.as_tensor(sc.pts, device="cuda"), torch.as_tensor(sc.nu, device="cuda"),
+                                  geom.box_domain([0, 0, 0], [1, 1, 1]))
+        return sc, res.psi.cpu().numpy()
     if kind == "C4":
         sc = scenes.c4_droplet()
         return sc, np.full(sc.n, (0.85 * sc.meta["h"]) ** 2)
@@ -34,7 +43,7 @@ def _scene(kind):
     return sc, np.where(sc.nu > h ** 3 * 1.5, (1.7 * h) ** 2, (0.85 * h) ** 2)
 
 
-@pytest.mark.parametrize("kind", ["C3", "C4", "C5"])
+@pytest.mark.parametrize("kind", ["C3", "C3c", "C4", "C5"])
 def test_full_size_sample_matches_oracle(kind):
     import torch
 
