@@ -388,6 +388,9 @@ def main():
 
     peak = ctypes.c_double(0.0)
     _lib.check(L.pf_fp64_peak(ctypes.byref(peak), None), "pf_fp64_peak")
+    peak_v = peak.value
+    if ws > 1:  # achieved is whole-job (all ranks' cells / max time): compare with the job's peak
+        peak_v = float(all_reduce_host([peak_v], "sum")[0])
     achieved = 2.0 * s_cell_total / (t_cells * 1e-3) / 1e12  # slot = FMA-equivalent (2 flop)
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -399,15 +402,16 @@ def main():
                 traffic_src = tr
         except Exception:
             traffic = None
-    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                "frac": achieved / peak.value if peak.value > 0 else None, "traffic": traffic,
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_v, "unit": "TFLOP/s",
+                "frac": achieved / peak_v if peak_v > 0 else None, "traffic": traffic,
                 "traffic_unit": "bytes per step (DRAM read+write of the cell kernels, ncu)",
                 "traffic_detail": traffic_src,
                 "kernel": "k_cells_build+k_cells_eval (+k_cells_exact retries)",
                 "kernel_ms": t_cells, "kernel_share_of_step": t_cells / t_step,
                 "algorithmic": f"census S_cell (SURVEY.md §8(d)) = {s_cell_total / sc.n:.0f} DP slots/cell,"
                                f" x2 flop/slot; mean processed candidates {mean_clips:.1f}/cell",
-                "peak_source": "measured in-run by pf_fp64_peak (DFMA chains; MEASURED_PEAKS.json has no FP64 entry)"}
+                "peak_source": "measured in-run by pf_fp64_peak (DFMA chains; MEASURED_PEAKS.json has no FP64 entry)"
+                               + (f", summed over the {ws} ranks' GPUs" if ws > 1 else "")}
 
     # ---- CPU baseline: oracle port on the host cores (rank 0, N=1)
     cpu = None
