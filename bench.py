@@ -358,17 +358,21 @@ def main():
     value = sc.n / (t_step * 1e-3)
 
     # ---- end to end through the drop-in numpy API (N=1)
+    # (N > 1: every rank calls the drop-in on its slab's host arrays -- owned
+    # cells plus ghosts, the ghost results discarded -- max time over ranks)
     e2e = None
-    if not a.no_e2e and ws == 1:
+    if not a.no_e2e:
         from oracle import pyoracle as O  # only for the output allocator shapes
 
-        host = O.alloc_outputs(sc.n, smf)
+        host = O.alloc_outputs(n_l, smf)
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
-        pts_p, psi_p = pin(sc.pts), pin(psi_h)
+        pts_p, psi_p = pin(sc.pts[idx]), pin(psi_h[idx])
         host = {k: pin(v) for k, v in host.items()}
         gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
         times = []
         for it in range(2 + a.steps):
+            if ws > 1:
+                dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             _kernels._batch_evaluate(pts_p, psi_p, *dpk.args(), *gargs, dpk.tol, dpsi, True, True, smf,
@@ -377,11 +381,16 @@ def main():
             if it >= 2:
                 times.append(time.perf_counter() - t0)
         t_e2e = sum(times) / len(times)
-        h2d = sc.pts.nbytes + psi_h.nbytes
+        h2d = pts_p.nbytes + psi_p.nbytes
         d2h = sum(host[k].nbytes for k in O.OUT_ORDER)
+        if ws > 1:
+            t_e2e = float(all_reduce_host([t_e2e], "max")[0])
+            tot = all_reduce_host([h2d, d2h], "sum")
+            h2d, d2h = float(tot[0]), float(tot[1])
         e2e = {"value": sc.n / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * t_e2e,
-               "api": "paper_2601_05765_b200._kernels._batch_evaluate (numpy, pinned host buffers)"}
+               "api": "paper_2601_05765_b200._kernels._batch_evaluate (numpy, pinned host buffers)"
+                      + (f"; {ws} ranks, each on its slab (owned + ghost cells), max over ranks" if ws > 1 else "")}
 
     # ---- FP64 roofline of the dominant kernel (k_cells_fast + exact tier)
     import ctypes
