@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-newton", action="store_true")
+    ap.add_argument("--no-hbm", action="store_true")
     return ap.parse_args()
 
 
@@ -185,6 +186,72 @@ def dist_newton(sc, dom, ws):
               "partition": f"{ws} x-slabs, halo {st['halo_entries']} entries/rank, "
                            f"{st['repartitions']} re-partitions"}
     return torch.as_tensor(psi, device="cuda"), newton
+
+
+def hbm_kernels(sc, dom, psi_g, smf, reps=5, cg_iters=50):
+    """Achieved HBM bandwidth of the two memory-bound kernels on this workload
+    (SURVEY §8(d) algorithmic bytes): the grid counting sort (68 B/site) and a
+    Jacobi-PCG iteration on the Newton Hessian of the converged weights
+    (12 nnz + 108 n bytes).  CUDA events on the launching stream."""
+    import ctypes
+
+    import torch
+
+    from paper_2601_05765_b200 import _lib, solver
+
+    L = _lib.lib()
+    c = _lib.ctx()
+    n = sc.n
+    pts = torch.as_tensor(sc.pts, device="cuda")
+    s = _lib.stream_ptr()
+    peak = None
+    pp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pp):
+        peak = json.load(open(pp)).get("hbm_gbs")
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # grid counting sort (bucket size from the weights, as every evaluation does)
+    _lib.check(L.pf_grid_build(c, n, _lib.ptr(pts), _lib.ptr(psi_g), 0.0, s), "pf_grid_build")
+    e0, e1 = ev(), ev()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        _lib.check(L.pf_grid_build(c, n, _lib.ptr(pts), _lib.ptr(psi_g), 0.0, s), "pf_grid_build")
+    e1.record()
+    torch.cuda.synchronize()
+    t_grid = e0.elapsed_time(e1) / reps
+    # PCG iterations on the final Hessian of the last Newton solve
+    solver._bind()
+    _, ksur, fcount, ftag, farea = solver.last_state(n, smf)
+    f8, i4 = dict(dtype=torch.float64, device="cuda"), dict(dtype=torch.int32, device="cuda")
+    hcnt, hcol = torch.empty(n, **i4), torch.empty((n, smf), **i4)
+    hval, diag = torch.empty((n, smf), **f8), torch.empty(n, **f8)
+    tau = 1e-12 * dom.diagonal() ** 2
+    _lib.check(L.pf_newton_hessian(n, smf, _lib.ptr(pts), _lib.ptr(psi_g), _lib.ptr(fcount), _lib.ptr(ftag),
+                                   _lib.ptr(farea), _lib.ptr(ksur), float(tau), _lib.ptr(hcnt), _lib.ptr(hcol),
+                                   _lib.ptr(hval), _lib.ptr(diag), s), "pf_newton_hessian")
+    b = torch.rand(n, generator=torch.Generator(device="cuda").manual_seed(1), **f8)
+    x = torch.empty(n, **f8)
+    L.pf_pcg(n, smf, _lib.ptr(hcnt), _lib.ptr(hcol), _lib.ptr(hval), _lib.ptr(diag), _lib.ptr(b), _lib.ptr(x),
+             0.0, 8, s)
+    torch.cuda.synchronize()
+    e0.record()
+    it = L.pf_pcg(n, smf, _lib.ptr(hcnt), _lib.ptr(hcol), _lib.ptr(hval), _lib.ptr(diag), _lib.ptr(b),
+                  _lib.ptr(x), 0.0, cg_iters, s)
+    e1.record()
+    torch.cuda.synchronize()
+    t_it = e0.elapsed_time(e1) / max(it, 1)
+    nnz = int(hcnt.sum())
+    gb_grid = 68.0 * n / (t_grid * 1e-3) / 1e9
+    gb_cg = (12.0 * nnz + 108.0 * n) / (t_it * 1e-3) / 1e9
+    mk = lambda gbs, ms, by, note: {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",  # noqa: E731
+                                    "frac": gbs / peak if peak else None, "ms": ms, "algorithmic_bytes": by,
+                                    "note": note}
+    return {"grid_counting_sort": mk(gb_grid, t_grid, 68 * n, "68 B/site (SURVEY §8(d)); 6 small kernels + 1 host "
+                                     "read of the bucket-size sum"),
+            "pcg_iteration": mk(gb_cg, t_it, int(12 * nnz + 108 * n),
+                                f"12 nnz + 108 n bytes, nnz={nnz}; 5 kernels per iteration (SpMV 8 lanes/row, "
+                                "2 single-block reductions, 2 vector updates), host check every 8"),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
 
 def cpu_reference_run(sc, psi, steps, warmup, sample_cells, threads):
@@ -422,6 +489,11 @@ def main():
                 "peak_source": "measured in-run by pf_fp64_peak (DFMA chains; MEASURED_PEAKS.json has no FP64 entry)"
                                + (f", summed over the {ws} ranks' GPUs" if ws > 1 else "")}
 
+    # ---- HBM-bound kernels of the path (N=1, converged weights)
+    hbm = None
+    if ws == 1 and newton is not None and not a.no_hbm:
+        hbm = hbm_kernels(sc, dom, psi_g, smf)
+
     # ---- CPU baseline: oracle port on the host cores (rank 0, N=1)
     cpu = None
     if not a.no_cpu and ws == 1 and rank == 0:
@@ -443,7 +515,7 @@ def main():
                            "parallelism": f"x-slab spatial partition over {ws} GPU(s), ghosts by search radius"
                            if ws > 1 else "1 GPU"},
                 "flags": fl, "e2e": e2e, "gpu_launches": launches,
-                "roofline": roofline, "cpu_baseline": cpu, "newton": newton,
+                "roofline": roofline, "roofline_hbm_kernels": hbm, "cpu_baseline": cpu, "newton": newton,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if ws > 1:

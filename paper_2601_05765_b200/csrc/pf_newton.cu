@@ -177,7 +177,8 @@ __global__ void k_sum2(const double *__restrict__ part, int nb, double *out0, do
 }
 
 // Ap = H p and partial p.Ap
-__global__ void __launch_bounds__(RB) k_spmv(int64_t n, int smf, const int *__restrict__ hcnt,
+constexpr int SPMV_T = 1024;  // SpMV block: 128 rows in flight per block (latency-bound gathers)
+__global__ void __launch_bounds__(SPMV_T) k_spmv(int64_t n, int smf, const int *__restrict__ hcnt,
                                             const int *__restrict__ hcol, const double *__restrict__ hval,
                                             const double *__restrict__ diag, const double *__restrict__ p,
                                             double *__restrict__ Ap, double *__restrict__ part,
@@ -189,8 +190,8 @@ __global__ void __launch_bounds__(RB) k_spmv(int64_t n, int smf, const int *__re
     // segments and its gathers p[col] are in flight together (thread-per-row
     // walked them one dependent load at a time)
     const int sub = threadIdx.x & 7;
-    const int64_t rows_per_pass = (int64_t)gridDim.x * (RB / 8);
-    for (int64_t i = blockIdx.x * (int64_t)(RB / 8) + (threadIdx.x >> 3); i - (threadIdx.x >> 3) < n;
+    const int64_t rows_per_pass = (int64_t)gridDim.x * (SPMV_T / 8);
+    for (int64_t i = blockIdx.x * (int64_t)(SPMV_T / 8) + (threadIdx.x >> 3); i - (threadIdx.x >> 3) < n;
          i += rows_per_pass) {
         double s = 0.0;
         const bool row = i < n;
@@ -447,7 +448,7 @@ int pf_pcg(int64_t n, int smf, const int32_t *hcnt, const int32_t *hcol, const d
     while (true) {
         for (int t = 0; t < batch; t++) {
             pf_internal_launches_add(5);
-            k_spmv<<<nb, RB, 0, st>>>(n, smf, hcnt, hcol, hval, diag, w.p, w.Ap, w.part, w.ic);
+            k_spmv<<<nb, SPMV_T, 0, st>>>(n, smf, hcnt, hcol, hval, diag, w.p, w.Ap, w.part, w.ic);
             k_alpha<<<1, 1024, 0, st>>>(w.part, nb, w.sc, w.ic);
             k_update<<<nb, RB, 0, st>>>(n, diag, x, w.r, w.z, w.p, w.Ap, w.sc, w.part, w.ic);
             k_beta<<<1, 1024, 0, st>>>(w.part, nb, w.sc, w.ic, rtol, max_iter);
