@@ -110,7 +110,8 @@ struct BuildScratch {
 };
 
 template <class C>
-struct EvalScratch {
+struct alignas(16) EvalScratch {  // 16-byte multiple: the evaluation workspaces stay TMA-aligned
+    unsigned long long mbar;  // per-warp mbarrier of the polytope's bulk (TMA) load (k_cells_eval_sync)
     // per facet
     double fh[C::CF], frc[C::CF], farea[C::CF], fcx[C::CF], fcy[C::CF], fcz[C::CF], fip[C::CF];
     double fpa[C::CF];       // Gauss-Bonnet sum, then the projected (occluded) patch area
@@ -2154,6 +2155,36 @@ PF_DEV void poly_store(const Poly<C> &A, Poly<C> *g) {
     for (int k = L; k < A.nl; k += 32) g->lv[k] = A.lv[k];
     if (L == 0) { g->nv = A.nv; g->nf = A.nf; g->nl = A.nl; }
 }
+#ifdef __CUDACC__
+// One-lane bulk (TMA) copy of a whole polytope record HBM -> shared memory,
+// completion tracked by a per-warp mbarrier (transaction bytes); the record and
+// the shared layout are the same Poly<C> (16-byte multiple, 16-byte aligned).
+PF_DEV void mbar_init(unsigned long long *mb) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+template <class C>
+PF_DEV void poly_load_tma(const Poly<C> *g, Poly<C> &A, unsigned long long *mb, unsigned &phase) {
+    static_assert(sizeof(Poly<C>) % 16 == 0, "bulk copy size");
+    const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+    pfw::sync();  // every lane is done with the previous cell's polytope
+    if (pfw::lane() == 0) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&A);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a),
+                     "r"((unsigned)sizeof(Poly<C>)) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(g), "r"((unsigned)sizeof(Poly<C>)), "r"(a) : "memory");
+    }
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(phase) : "memory");
+    phase ^= 1u;
+}
+#endif
+
 template <class C>
 PF_DEV void poly_load(const Poly<C> *g, Poly<C> &A) {
     const int L = pfw::lane();

@@ -300,6 +300,9 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
 // cell and stalls on instruction fetch; building in one kernel and
 // evaluating in another halves the hot code each SM cycles through.  The
 // finished polytope travels through global memory (Poly<FastCaps>, ~3 KB).
+#ifndef PF_NO_TMA_LOAD
+#define PF_NO_TMA_LOAD 0  // 1: the evaluation loads the polytope with lane loads instead of a bulk copy
+#endif
 #ifndef PF_BUILD_WARPS
 #define PF_BUILD_WARPS 8
 #endif
@@ -394,6 +397,10 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     EWS<FastCaps> *ws = (EWS<FastCaps> *)(smem + (size_t)wid * sizeof(EWS<FastCaps>));
     int fl = 0;
+    const bool tma = !PF_NO_TMA_LOAD;
+    unsigned phase = 0;
+    if (tma && lane == 0) mbar_init(&ws->u.e.mbar);
+    __syncwarp();
     for (int base = blockIdx.x * SYNC_WARPS; base < count; base += gridDim.x * SYNC_WARPS) {
         const int t = base + wid;
         int i = -1;
@@ -417,7 +424,8 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
         EvalState st;
         st.done = 1;
         if (act) {
-            poly_load(gpoly + i, ws->P[0]);
+            if (tma) poly_load_tma(gpoly + i, ws->P[0], &ws->u.e.mbar, phase);
+            else poly_load(gpoly + i, ws->P[0]);
             if (lane == 0) {
                 ws->oflow = 0;
                 ws->cen_on = out.census16 != nullptr;
