@@ -578,11 +578,14 @@ __global__ void k_super_max(GridView g, const double *__restrict__ psi, double *
     }
 }
 
-// per-site weight slack (pf_cell.cuh cell_slack), thread per site
-__global__ void k_cell_slack(CellIn in, int64_t n, double *__restrict__ slack) {
+// per-site weight slack (pf_cell.cuh cell_slack), thread per evaluated cell
+// (the cells of a subset call only: chunked callers pay it once in total)
+__global__ void k_cell_slack(CellIn in, int64_t count, double *__restrict__ slack) {
     const double dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = in.cells ? in.cells[t] : t;
         slack[i] = cell_slack(in.g, in.pts[3 * i], in.pts[3 * i + 1], in.pts[3 * i + 2], in.psi[i], dpsi);
+    }
 }
 
 int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cudaStream_t st) {
@@ -650,7 +653,8 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
         in.g.smax = c->smax;
         if (ensure(&c->cslack, &c->cslack_cap, (size_t)n)) return -1;
         g_launches++;
-        k_cell_slack<<<(int)std::min<int64_t>((n + 255) / 256, (int64_t)c->nsm * 16), 256, 0, st>>>(in, n, c->cslack);
+        k_cell_slack<<<(int)std::min<int64_t>((count + 255) / 256, (int64_t)c->nsm * 16), 256, 0, st>>>(in, count,
+                                                                                                          c->cslack);
         CK(cudaGetLastError());
         in.cslack = c->cslack;
     }
