@@ -104,25 +104,33 @@ def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, o
 
     p = h2d(pts, np.float64)
     w = h2d(psi, np.float64)
-    outs = []
-    for k, (o, t) in enumerate(zip(outs_host, dtypes)):
-        if k in (3, 4, 5):
-            # cent / ipt / m2 start from the caller's values: the reference leaves
-            # them untouched for capacity-overflowed cells (_kernels.py:1393-1399)
-            outs.append(h2d(o, np.float64))
-        elif k >= 7:
-            # fixed-stride slots past fcount come back zero (the reference leaves
-            # them untouched; callers allocate zeros)
-            outs.append(torch.zeros(o.shape, dtype=t, device="cuda"))
-        else:
-            outs.append(torch.empty(o.shape, dtype=t, device="cuda"))
+    outs = [torch.empty(o.shape, dtype=t, device="cuda") for o, t in zip(outs_host, dtypes)]
     err_acc = torch.zeros(1, dtype=torch.int64, device="cuda")
     comp = torch.cuda.current_stream()
     sptr = _lib.stream_ptr()
+    copy = torch.cuda.Stream()
+    prep_s = torch.cuda.Stream()  # host->device prep: its own stream (the other copy direction)
+    # Per index range, on the prep stream ahead of the range's kernels: cent /
+    # ipt / m2 start from the caller's values (the reference leaves them
+    # untouched for capacity-overflowed cells, _kernels.py:1393-1399) and the
+    # fixed-stride slots past fcount start zero (the reference leaves them
+    # untouched; callers allocate zeros) -- off the critical path.
+    src = [torch.from_numpy(np.ascontiguousarray(outs_host[k], np.float64)) for k in (3, 4, 5)]
+    prep = []
+    prep_s.wait_stream(comp)
+    with torch.cuda.stream(prep_s):
+        for k in range(K):
+            i0, i1 = k * n // K, (k + 1) * n // K
+            for j, sk in zip((3, 4, 5), src):
+                outs[j][i0:i1].copy_(sk[i0:i1].view(outs[j][i0:i1].shape), non_blocking=True)
+            for j in range(7, len(outs)):
+                outs[j][i0:i1].zero_()
+            e = torch.cuda.Event()
+            e.record(prep_s)
+            prep.append(e)
     _lib.check(L.pf_grid_build(c, n, _lib.ptr(p), _lib.ptr(w), 0.0, sptr), "pf_grid_build")
     order = torch.empty(n, dtype=torch.int32, device="cuda")
     _lib.check(L.pf_grid_order(c, _lib.ptr(order), sptr), "pf_grid_order")
-    copy = torch.cuda.Stream()
     hosts = [torch.from_numpy(h.reshape(h.shape)) if isinstance(h, np.ndarray) and h.flags.c_contiguous
              and h.flags.writeable else None for h in outs_host]
     if K > 1:
@@ -133,6 +141,7 @@ def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, o
     for k in range(K):
         i0, i1 = k * n // K, (k + 1) * n // K
         cells = cells_all[offs[k]:offs[k + 1]] if K > 1 else None
+        comp.wait_event(prep[k])
         _lib.check(L.pf_batch_evaluate_async(
             c, n, _lib.ptr(p), _lib.ptr(w), float(tol), float(dpsi_max), int(bool(ball_aware)),
             int(bool(want_m2)), int(smf), *[_lib.ptr(o) for o in outs], _lib.ptr(cells),
@@ -146,6 +155,7 @@ def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, o
                 if t is not None:
                     t[i0:i1].copy_(d[i0:i1].view(t[i0:i1].shape), non_blocking=True)
     copy.synchronize()
+    prep_s.synchronize()
     comp.synchronize()
     for h, t, d in zip(outs_host, hosts, outs):
         if t is None:
