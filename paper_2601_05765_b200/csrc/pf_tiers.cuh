@@ -30,7 +30,10 @@ namespace pf {
 #ifndef PF_FCE
 #define PF_FCE 48
 #endif
-using FastCaps = Caps<PF_FCV, 32, PF_FCL, PF_FCC, PF_FCE, 120, false>;
+#ifndef PF_FCP
+#define PF_FCP 120
+#endif
+using FastCaps = Caps<PF_FCV, 32, PF_FCL, PF_FCC, PF_FCE, PF_FCP, false>;
 // Mid: the fast tier's overflow (mostly the boundary-point pool of cells whose
 // sphere meets many facets) in shared memory, 4 warps (48 KB each) per SM.
 using MidCaps = Caps<128, 64, 448, 64, 128, 512, false>;
