@@ -83,6 +83,18 @@ def _batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
     return err
 
 
+def _chunk_bounds(n: int, K: int) -> np.ndarray:
+    """Index-range boundaries [0 = b_0 <= ... <= b_K = n] of the host drop-in's
+    ranges: equal, except the last three shrink (1/2, 1/4, 1/8 of one) so the
+    device->host copy left after the last kernel is short."""
+    wts = np.ones(K)
+    if K >= 6:
+        wts[-3:] = (0.5, 0.25, 0.125)
+    bnd = np.rint(np.concatenate([[0.0], np.cumsum(wts)]) / wts.sum() * n).astype(np.int64)
+    bnd[0], bnd[-1] = 0, n
+    return bnd
+
+
 def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, outs_host, dtypes,
                          chunks: int | None = None):
     """Host-array drop-in: inputs copied in, every output copied back into the
@@ -102,13 +114,7 @@ def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, o
     def h2d(x, dtype):
         return torch.from_numpy(np.ascontiguousarray(x, dtype)).to("cuda", non_blocking=True)
 
-    # index ranges: equal, except the last three shrink (1/2, 1/4, 1/8 of one) so
-    # the device->host copy left after the last kernel is short
-    wts = np.ones(K)
-    if K >= 6:
-        wts[-3:] = (0.5, 0.25, 0.125)
-    bnd = np.rint(np.concatenate([[0.0], np.cumsum(wts)]) / wts.sum() * n).astype(np.int64)
-    bnd[-1] = n
+    bnd = _chunk_bounds(n, K)
     p = h2d(pts, np.float64)
     w = h2d(psi, np.float64)
     outs = [torch.empty(o.shape, dtype=t, device="cuda") for o, t in zip(outs_host, dtypes)]
