@@ -2183,6 +2183,23 @@ PF_DEV void poly_load_tma(const Poly<C> *g, Poly<C> &A, unsigned long long *mb, 
         "@!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(phase) : "memory");
     phase ^= 1u;
 }
+// bulk (TMA) store of a whole polytope record shared -> HBM (async; the
+// shared buffer may be reused after poly_store_tma_wait)
+template <class C>
+PF_DEV void poly_store_tma(const Poly<C> &A, Poly<C> *g) {
+    pfw::sync();
+    if (pfw::lane() == 0) {
+        const unsigned src = (unsigned)__cvta_generic_to_shared(&A);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(src),
+                     "r"((unsigned)sizeof(Poly<C>)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
+PF_DEV void poly_store_tma_wait() {
+    if (pfw::lane() == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    pfw::sync();
+}
 #endif
 
 template <class C>

@@ -322,9 +322,10 @@ __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
     for (int t = blockIdx.x * BUILD_WARPS + wid; t < count; t += nw) {
         const int i = in.cells ? in.cells[t] : in.g.sid[t];
         int which = 0;
+        poly_store_tma_wait();  // the previous cell's bulk store has read its buffer
         int r = cell_phase_build(ws, in, out, i, &which);
         if (r < 0) {
-            poly_store(ws->P[which], gpoly + i);
+            poly_store_tma(ws->P[which], gpoly + i);
             if (lane == 0) {
                 stage[i] = 1;
                 if (out.census16)
@@ -372,6 +373,8 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
         }
         __syncwarp();
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+    __syncwarp();
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
