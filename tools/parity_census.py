@@ -1,5 +1,5 @@
 """Whole-scene parity census vs the CPU oracle (dev tool): how many cells
-differ beyond 1e-9 and what they look like.  usage: parity_census.py c4|c3|c3c|c5|c2"""
+differ beyond 1e-9 and what they look like.  usage: parity_census.py c4|c3|c3c|c5|c5c|c2|c1c"""
 import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,6 +12,16 @@ elif which == "c2":
     sc = scenes.c2_dam_break(); psi = np.full(sc.n, (0.85 * sc.meta["h"]) ** 2)
 elif which == "c3":
     sc = scenes.c3_chocs(); psi = sc.psi_cold()
+elif which == "c1c":  # C1 10k random at its converged weights
+    from paper_2601_05765_b200 import solver
+    sc = scenes.c1_random()
+    psi = solver.newton_solve(torch.as_tensor(sc.pts, device="cuda"), torch.as_tensor(sc.nu, device="cuda"),
+                              geom.box_domain([0, 0, 0], [1, 1, 1])).psi.cpu().numpy()
+elif which == "c5c":  # C5 two-fluid at its converged weights
+    from paper_2601_05765_b200 import solver
+    sc = scenes.c5_two_fluid()
+    psi = solver.newton_solve(torch.as_tensor(sc.pts, device="cuda"), torch.as_tensor(sc.nu, device="cuda"),
+                              geom.box_domain([0, 0, 0], [1, 1, 1])).psi.cpu().numpy()
 elif which == "c3c":  # C3 at its converged weights (large local weight spread)
     from paper_2601_05765_b200 import solver
     sc = scenes.c3_chocs()
