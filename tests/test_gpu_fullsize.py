@@ -26,12 +26,12 @@ def _scene(kind):
     if kind == "C3":
         sc = scenes.c3_chocs()
         return sc, sc.psi_cold()
-    if kind == "C3c":  # converged weights: large local weight spread (per-cell slack, mid tier)
+    if kind in ("C3c", "C5c"):  # converged weights: large local weight spread (per-cell slack, mid tier)
         import torch
 
         from paper_2601_05765_b200 import geom, solver
 
-        sc = scenes.c3_chocs()
+        sc = scenes.c3_chocs() if kind == "C3c" else scenes.c5_two_fluid()
         res = solver.newton_solve(torch.as_tensor(sc.pts, device="cuda"), torch.as_tensor(sc.nu, device="cuda"),
                                   geom.box_domain([0, 0, 0], [1, 1, 1]))
         return sc, res.psi.cpu().numpy()
@@ -43,7 +43,7 @@ def _scene(kind):
     return sc, np.where(sc.nu > h ** 3 * 1.5, (1.7 * h) ** 2, (0.85 * h) ** 2)
 
 
-@pytest.mark.parametrize("kind", ["C3", "C3c", "C4", "C5"])
+@pytest.mark.parametrize("kind", ["C3", "C3c", "C4", "C5", "C5c"])
 def test_full_size_sample_matches_oracle(kind):
     import torch
 
