@@ -12,6 +12,7 @@
  *   pf_grid_export      SpatialGrid.bucket_start/bucket_sites  laguerre.py:78-79
  *   pf_dpsi_max         laguerre._dpsi_max                     laguerre.py:142-145
  *   pf_batch_evaluate   _kernels._batch_evaluate               _kernels.py:1362-1478
+ *   pf_batch_evaluate_host  (same, host arrays in and out)     _kernels.py:1362-1478
  *   pf_knn              _kernels._knn / laguerre.knn            _kernels.py:1562-1620, laguerre.py:90-96
  *   pf_newton_*         ot_solver.newton_solve (spec only)
  *   pf_fluid_*          fluid_sim.step (spec only)
@@ -53,6 +54,14 @@ int pf_ctx_destroy(pf_ctx *ctx);
 int pf_set_domain(pf_ctx *ctx, const double *dv_host, const int64_t *dc_host,
                   const double *dp_host, const int64_t *dt_host, const int64_t *dlp_host,
                   const int64_t *dlv_host, double tol);
+
+/* Parity mode (default off, or PF_PARITY_MODE=1 at context creation): every
+ * evaluation restricts the facets exactly as the reference does
+ * (_kernels.py:411-675, 678-716, 838-1001), including its spurious-entry and
+ * wrapped-arc outcomes on cells whose loop vertex lies within tol outside the
+ * sphere.  Off, those outcomes are corrected. */
+int pf_set_parity_mode(pf_ctx *ctx, int on);
+int pf_get_parity_mode(pf_ctx *ctx);
 
 /* Uniform bucket grid over the domain bounding box by counting sort.
  * cell_size <= 0 picks the bucket edge from the weights (half the mean
@@ -114,6 +123,23 @@ int pf_batch_evaluate_async(pf_ctx *ctx, int64_t n, const double *pts, const dou
                             int64_t *fcount, int64_t *ftag, double *farea, double *fh, double *fnrm,
                             double *fcent, const int32_t *cells, int64_t ncells, int32_t *cell_flags,
                             int64_t *err_accum, int rebuild_grid, void *stream);
+/* _kernels._batch_evaluate on HOST arrays (the numba call's own argument
+ * space: plain, pageable host memory; outputs with the reference shapes).
+ * Writes exactly what the reference writes (_kernels.py:1362-1478): every
+ * cell's status / vol / ksur / fcount, cent / ipt / m2 except on
+ * build-overflow cells, facet slots < fcount only (slots past it untouched).
+ * The cells run in `chunks` index ranges (0 = 16); each range's outputs are
+ * packed on the device (96 B per cell + 72 B per restricted facet), copied
+ * into a pinned ring and scattered into the caller's arrays by a host worker
+ * pool while the next ranges compute.  *h2d_bytes / *d2h_bytes (optional)
+ * receive the bytes copied.  Returns the OR of the cells' flag words. */
+int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_host, const double *psi_host,
+                               double tol, double dpsi_max, int ball_aware, int want_m2, int64_t smf,
+                               int64_t *status_host, double *vol_host, double *ksur_host, double *cent_host,
+                               double *ipt_host, double *m2_host, int64_t *fcount_host, int64_t *ftag_host,
+                               double *farea_host, double *fh_host, double *fnrm_host, double *fcent_host,
+                               int chunks, int64_t *h2d_bytes_host, int64_t *d2h_bytes_host);
+
 /* _kernels._batch_build (_kernels.py:1481-1559): every
  * unrestricted Laguerre cell into fixed-stride packed arrays in the reference's
  * layout -- status (0 ok / 1 empty / 3 overflow), counts, verts f64[n,smv,3],
@@ -140,10 +166,12 @@ int pf_stage_times(pf_ctx *ctx, double *build_ms_host, double *eval_ms_host, int
 int pf_last_retry_count(pf_ctx *ctx, int64_t *count_host);
 
 /* _kernels._knn for a batch of queries: out_idx i64[nq,k] holds the k
- * nearest sites (by (d^2, index)) of each query (queries f64[nq,3]); uses the
- * grid of the last pf_grid_build on pts.  Returns min(k, n). */
+ * nearest sites (by (d^2, index)) of each query (queries f64[nq,3]).
+ * rebuild_grid != 0 rebuilds the bucket grid from pts first; 0 reuses the
+ * context's grid when it was built on the same (n, pts) -- only for callers
+ * that own pts unchanged since that build (the Newton solve).  Returns min(k, n). */
 int64_t pf_knn(pf_ctx *ctx, int64_t n, const double *pts, int64_t nq, const double *queries,
-               int64_t k, int64_t *out_idx, void *stream);
+               int64_t k, int64_t *out_idx, int rebuild_grid, void *stream);
 
 /* ---- damped Newton solve for the weights ---------------- */
 typedef struct {
@@ -189,11 +217,12 @@ int pf_newton_last_state_ex(double *vol, double *ksur, int32_t *fcount, int32_t 
  * in device memory (stats_dev / outN_dev) for the cross-rank all-reduce; the
  * halo exchange of ghost vector entries is done by the host (dist_solver.py).
  * Replaces, per rank, the single-device pf_newton_solve pieces above. */
-/* lean evaluation of cells[0:ncells] with the given (global) weight slack */
+/* lean evaluation of cells[0:ncells] with the given (global) weight slack;
+ * rebuild_grid as in pf_knn */
 int pf_evaluate_lean_cells(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double dpsi,
                            int ball_aware, int64_t smf, const int32_t *cells, int64_t ncells,
                            double *vol, double *ksur, int32_t *fcount, int32_t *ftag, double *farea,
-                           double *cent, int64_t *flags, void *stream);
+                           double *cent, int64_t *flags, int rebuild_grid, void *stream);
 /* g = nu - vol on rows; stats_dev[3] = (max rel. error, -min vol, -min nu), MAX-reducible */
 int pf_rows_gradient(int nrows, const int32_t *rows, const double *nu, const double *vol, double *g,
                      double *stats_dev, void *stream);

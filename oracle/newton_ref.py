@@ -34,6 +34,12 @@ def hessian_ell(pts, psi, o, tau_psi, smf):
     cols[mask] = o["ftag"][mask]
     vals[mask] = -w[mask]
     diag = w.sum(1) + 0.5 * o["ksur"] / np.sqrt(np.maximum(psi, tau_psi))
+    # An empty cell (no facet, no free surface) has a zero row.
+    # gives it "the Hessian diagonal from the tau_psi guard"; the only SPEC value
+    # of that diagonal is the free ball's, H_ii = d|V_i|/d psi_i = 2 pi sqrt(psi_i)
+    # (SPEC.md:296 example), evaluated at max(psi_i, tau_psi).  Cold-start and
+    # accepted states never have empty cells (init_weights / the KMT floor), so
+    # this only affects rows the damping then rejects.
     bad = ~(diag > 0.0)
     diag[bad] = 2.0 * np.pi * np.sqrt(np.maximum(psi[bad], tau_psi))
     return cols, vals, diag
@@ -45,7 +51,9 @@ def spmv(cols, vals, diag, x):
 
 
 def pcg(cols, vals, diag, b, rtol, max_iter=10000):
-    """Jacobi PCG with the device's convergence test ||r|| <= rtol ||b||."""
+    """Jacobi PCG (cg_solve): x0 = 0, preconditioner D^-1,
+    stop when ||H x - b|| = ||r|| <= tol ||b|| (the SPEC's post-condition, with
+    the recursively updated residual) or max_iter."""
     x = np.zeros_like(b)
     r = b.copy()
     z = r / diag

@@ -22,6 +22,14 @@ def set_threads(n: int) -> int:
     return max(1, int(n))
 
 
+def set_parity_mode(on: bool) -> None:
+    """Reference-faithful restriction on every evaluation of this device
+    (DESIGN.md §5.1); default off (the robust restriction)."""
+    from ._lib import set_parity_mode as _s
+
+    _s(on)
+
+
 def library_path() -> str:
     from ._lib import LIB_PATH
 

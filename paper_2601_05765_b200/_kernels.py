@@ -58,12 +58,22 @@ def _batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
                     gnx, gny, gnz, h_min, tol, dpsi_max, ball_aware, want_m2,
                     smf,
                     status, vol, ksur, cent, ipt, m2,
-                    fcount, ftag, farea_o, fh_o, fnrm, fcent_o):
-    """Build and evaluate every restricted cell (see module docstring)."""
+                    fcount, ftag, farea_o, fh_o, fnrm, fcent_o, *, parity_mode=None):
+    """Build and evaluate every restricted cell (see module docstring).
+    ``parity_mode`` (keyword only; None = the context's setting, see
+    ``_lib.set_parity_mode``): True restricts the facets exactly as the
+    reference does, False with the robust correction."""
+    with _lib.parity(parity_mode):
+        return _batch_evaluate_impl(pts, psi, dv, dc, dp, dt, dlp, dlv, tol, dpsi_max, ball_aware,
+                                    want_m2, smf, [status, vol, ksur, cent, ipt, m2, fcount, ftag,
+                                                   farea_o, fh_o, fnrm, fcent_o])
+
+
+def _batch_evaluate_impl(pts, psi, dv, dc, dp, dt, dlp, dlv, tol, dpsi_max, ball_aware, want_m2, smf,
+                         outs_host):
     import torch
 
     f8, i8 = torch.float64, torch.int64
-    outs_host = [status, vol, ksur, cent, ipt, m2, fcount, ftag, farea_o, fh_o, fnrm, fcent_o]
     dtypes = [i8, f8, f8, f8, f8, f8, i8, i8, f8, f8, f8, f8]
     on_device = _is_torch(pts)
     c = _lib.ctx()
@@ -85,8 +95,9 @@ def _batch_evaluate(pts, psi, dv, dc, dp, dt, dlp, dlv,
 
 def _chunk_bounds(n: int, K: int) -> np.ndarray:
     """Index-range boundaries [0 = b_0 <= ... <= b_K = n] of the host drop-in's
-    ranges: equal, except the last three shrink (1/2, 1/4, 1/8 of one) so the
-    device->host copy left after the last kernel is short."""
+    ranges (pf_batch_evaluate_host's range_bounds, pf_host.cu): equal, except
+    the last three shrink (1/2, 1/4, 1/8 of one) so the work left after the
+    last kernel is short."""
     wts = np.ones(K)
     if K >= 6:
         wts[-3:] = (0.5, 0.25, 0.125)
@@ -95,85 +106,49 @@ def _chunk_bounds(n: int, K: int) -> np.ndarray:
     return bnd
 
 
+# bytes copied host->device / device->host by the last host-array call
+last_copy_bytes = (0, 0)
+
+
 def _batch_evaluate_host(c, pts, psi, tol, dpsi_max, ball_aware, want_m2, smf, outs_host, dtypes,
                          chunks: int | None = None):
-    """Host-array drop-in: inputs copied in, every output copied back into the
-    caller's arrays.  The cells are evaluated in `chunks` index ranges (each in
-    bucket order) and the device->host copy of one range runs on a side stream
-    while the next range computes, so the round trip hides behind the kernels
-    (the copies are asynchronous when the caller's arrays are pinned)."""
+    """Host-array drop-in through pf_batch_evaluate_host (pf_host.cu): the
+    caller's arrays (pageable numpy, as the numba kernel takes them) are read
+    and written in place; only what the reference writes is written.  Output
+    arrays that are not C-contiguous arrays of the reference dtype go through
+    a temporary and are copied back."""
+    import ctypes as C
     import os
 
-    import torch
-
-    L = _lib.lib()
-    n = int(np.asarray(pts).shape[0])
-    K = chunks or int(os.environ.get("PF_E2E_CHUNKS", "16"))
-    K = max(1, min(K, max(n, 1)))
-
-    def h2d(x, dtype):
-        return torch.from_numpy(np.ascontiguousarray(x, dtype)).to("cuda", non_blocking=True)
-
-    bnd = _chunk_bounds(n, K)
-    p = h2d(pts, np.float64)
-    w = h2d(psi, np.float64)
-    outs = [torch.empty(o.shape, dtype=t, device="cuda") for o, t in zip(outs_host, dtypes)]
-    err_acc = torch.zeros(1, dtype=torch.int64, device="cuda")
-    comp = torch.cuda.current_stream()
-    sptr = _lib.stream_ptr()
-    copy = torch.cuda.Stream()
-    prep_s = torch.cuda.Stream()  # host->device prep: its own stream (the other copy direction)
-    # Per index range, on the prep stream ahead of the range's kernels: cent /
-    # ipt / m2 start from the caller's values (the reference leaves them
-    # untouched for capacity-overflowed cells, _kernels.py:1393-1399) and the
-    # fixed-stride slots past fcount start zero (the reference leaves them
-    # untouched; callers allocate zeros, SURVEY.md §9) -- off the critical path.
-    src = [torch.from_numpy(np.ascontiguousarray(outs_host[k], np.float64)) for k in (3, 4, 5)]
-    prep = []
-    prep_s.wait_stream(comp)
-    with torch.cuda.stream(prep_s):
-        for k in range(K):
-            i0, i1 = int(bnd[k]), int(bnd[k + 1])
-            for j, sk in zip((3, 4, 5), src):
-                outs[j][i0:i1].copy_(sk[i0:i1].view(outs[j][i0:i1].shape), non_blocking=True)
-            for j in range(7, len(outs)):
-                outs[j][i0:i1].zero_()
-            e = torch.cuda.Event()
-            e.record(prep_s)
-            prep.append(e)
-    _lib.check(L.pf_grid_build(c, n, _lib.ptr(p), _lib.ptr(w), 0.0, sptr), "pf_grid_build")
-    order = torch.empty(n, dtype=torch.int32, device="cuda")
-    _lib.check(L.pf_grid_order(c, _lib.ptr(order), sptr), "pf_grid_order")
-    hosts = [torch.from_numpy(h.reshape(h.shape)) if isinstance(h, np.ndarray) and h.flags.c_contiguous
-             and h.flags.writeable else None for h in outs_host]
-    if K > 1:
-        # cells of each index range in bucket order: one stable sort by range id
-        rid = torch.bucketize(order.long(), torch.as_tensor(bnd[1:-1], device="cuda"), right=True)
-        cells_all = order[torch.sort(rid, stable=True).indices]
-        offs = [0] + torch.cumsum(torch.bincount(rid, minlength=K), 0).tolist()
-    for k in range(K):
-        i0, i1 = int(bnd[k]), int(bnd[k + 1])
-        cells = cells_all[offs[k]:offs[k + 1]] if K > 1 else None
-        comp.wait_event(prep[k])
-        _lib.check(L.pf_batch_evaluate_async(
-            c, n, _lib.ptr(p), _lib.ptr(w), float(tol), float(dpsi_max), int(bool(ball_aware)),
-            int(bool(want_m2)), int(smf), *[_lib.ptr(o) for o in outs], _lib.ptr(cells),
-            0 if cells is None else int(cells.numel()), None, _lib.ptr(err_acc), 0, sptr),
-            "pf_batch_evaluate_async")
-        ev = torch.cuda.Event()
-        ev.record(comp)
-        with torch.cuda.stream(copy):
-            copy.wait_event(ev)
-            for h, t, d in zip(outs_host, hosts, outs):
-                if t is not None:
-                    t[i0:i1].copy_(d[i0:i1].view(t[i0:i1].shape), non_blocking=True)
-    copy.synchronize()
-    prep_s.synchronize()
-    comp.synchronize()
-    for h, t, d in zip(outs_host, hosts, outs):
-        if t is None:
-            h[...] = d.cpu().numpy().reshape(h.shape)
-    return int(err_acc.item())
+    global last_copy_bytes
+    npd = [np.int64, np.float64, np.float64, np.float64, np.float64, np.float64, np.int64, np.int64,
+           np.float64, np.float64, np.float64, np.float64]
+    p = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    w = np.ascontiguousarray(psi, np.float64).reshape(-1)
+    n = int(p.shape[0])
+    direct, tmp = [], []
+    for o, t in zip(outs_host, npd):
+        if isinstance(o, np.ndarray) and o.dtype == t and o.flags.c_contiguous and o.flags.writeable:
+            direct.append(o)
+            tmp.append(None)
+        else:
+            a = np.array(_host(o), dtype=t, order="C", copy=True)
+            direct.append(a)
+            tmp.append(a)
+    K = int(chunks or int(os.environ.get("PF_E2E_CHUNKS", "16")))
+    h2d, d2h = C.c_int64(0), C.c_int64(0)
+    err = int(_lib.lib().pf_batch_evaluate_host(
+        c, n, p.ctypes.data, w.ctypes.data, float(tol), float(dpsi_max), int(bool(ball_aware)),
+        int(bool(want_m2)), int(smf), *[a.ctypes.data for a in direct], K, C.byref(h2d), C.byref(d2h)))
+    _lib.check(err, "pf_batch_evaluate_host")
+    last_copy_bytes = (int(h2d.value), int(d2h.value))
+    for o, a in zip(outs_host, tmp):
+        if a is not None:
+            if _is_torch(o):
+                o.copy_(__import__("torch").from_numpy(a).reshape(o.shape))
+            else:
+                o[...] = a.reshape(np.shape(o))
+    return err
 
 
 def _batch_build(pts, psi, dv, dc, dp, dt, dlp, dlv,
@@ -231,7 +206,7 @@ def _knn(pts, grid_start, grid_sites, lox, loy, loz, ihx, ihy, ihz,
     q = torch.tensor([[qx, qy, qz]], dtype=torch.float64, device="cuda")
     res = torch.empty((1, kk), dtype=torch.int64, device="cuda")
     got = _lib.check(_lib.lib().pf_knn(c, n, _lib.ptr(p), 1, _lib.ptr(q), kk, _lib.ptr(res),
-                                       _lib.stream_ptr()), "pf_knn")
+                                       1, _lib.stream_ptr()), "pf_knn")
     vals = res[0, :got]
     if _is_torch(out_idx):
         out_idx[:got] = vals

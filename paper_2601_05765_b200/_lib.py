@@ -61,6 +61,8 @@ def lib():
         L.pf_batch_evaluate_async.restype = i
         L.pf_batch_evaluate_async.argtypes = ([vp, i64, vp, vp, d, d, i, i, i64] + [vp] * 12
                                               + [vp, i64, vp, vp, i, vp])
+        L.pf_batch_evaluate_host.restype = i64
+        L.pf_batch_evaluate_host.argtypes = ([vp, i64, vp, vp, d, d, i, i, i64] + [vp] * 12 + [i, vp, vp])
         L.pf_batch_build.restype = i64
         L.pf_batch_build.argtypes = [vp, i64, vp, vp, d, d, i, i64, i64, i64] + [vp] * 9 + [i, vp]
         L.pf_grid_order.restype = i
@@ -68,10 +70,12 @@ def lib():
         L.pf_facets_csr.restype = i
         L.pf_facets_csr.argtypes = [vp, i64, i64] + [vp] * 6 + [i64] + [vp] * 7 + [vp]
         L.pf_knn.restype = i64
-        L.pf_knn.argtypes = [vp, i64, vp, i64, vp, i64, vp, vp]
+        L.pf_knn.argtypes = [vp, i64, vp, i64, vp, i64, vp, i, vp]
+        L.pf_set_parity_mode.argtypes = [vp, i]
+        L.pf_get_parity_mode.argtypes = [vp]
         for name in ("pf_ctx_create", "pf_ctx_destroy", "pf_set_domain", "pf_grid_build",
                      "pf_grid_build_dims", "pf_grid_info", "pf_grid_export", "pf_dpsi_max", "pf_evaluate_lean",
-                     "pf_last_census", "pf_last_retry_count"):
+                     "pf_last_census", "pf_last_retry_count", "pf_set_parity_mode", "pf_get_parity_mode"):
             getattr(L, name).restype = i
         _lib = L
     return _lib
@@ -99,6 +103,35 @@ def ctx(device: int | None = None):
         _ctx[dev] = h
         c = h
     return c
+
+
+def set_parity_mode(on: bool, device: int | None = None) -> None:
+    """Parity mode of this device's context: every evaluation restricts the
+    facets exactly as the reference does (_kernels.py:411-675), including its
+    spurious-entry / wrapped-arc outcomes.  Default off."""
+    check(lib().pf_set_parity_mode(ctx(device), int(bool(on))), "pf_set_parity_mode")
+
+
+def parity_mode(device: int | None = None) -> bool:
+    return bool(lib().pf_get_parity_mode(ctx(device)))
+
+
+class parity(object):
+    """Context manager: ``with _lib.parity(True): ...`` (restores the previous mode)."""
+
+    def __init__(self, on):
+        self.on = on
+
+    def __enter__(self):
+        self.prev = None
+        if self.on is not None:
+            self.prev = parity_mode()
+            set_parity_mode(self.on)
+        return self
+
+    def __exit__(self, *a):
+        if self.prev is not None:
+            set_parity_mode(self.prev)
 
 
 def stream_ptr(stream=None) -> int:

@@ -135,11 +135,12 @@ struct alignas(16) EvalScratch {  // 16-byte multiple: the evaluation workspaces
 // per-warp workspaces.  WS: both phases (fused and reference-capacity
 // kernels); BWS / EWS: what the split build / evaluate kernels need.
 template <class C_, int NP, class U>
-struct WSX {
+struct alignas(16) WSX {  // 16-byte multiple: every warp's polytope stays TMA-aligned
     using Cap = C_;
     Poly<C_> P[NP];
     U u;
     int oflow;    // capacity overflow seen by any lane
+    int strict;   // parity mode (CellIn::strict) for this cell
     int cen_on;   // census requested for this cell
     int cen[16];  // algorithmic-work census (SURVEY.md §8(d) S_cell terms)
 };
@@ -185,6 +186,7 @@ struct CellIn {
     double tol, dpsi;
     const double *dpsi_ptr;  // when set, dpsi is read from device memory
     int ball_aware, want_m2;
+    int strict;     // parity mode: the reference's restriction outcomes bit for bit
     double t_init;  // first shell radius^2 when not ball-aware
     const double *cslack;  // optional: per-cell weight slack (cell_slack), ball-aware only
     const int *cells;  // optional: evaluate only these cells (original indices)
@@ -1064,8 +1066,9 @@ PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, doub
     #pragma unroll 1
     for (int k0 = 0; k0 < nl; k0 += 32) {
         const int k = k0 + L;
-        int cnt = 0, f = 0, fl0 = 0, fl1 = 0;
+        int cnt = 0, f = 0, fl0 = 0, fl1 = 0, fl2 = 0;
         double x0 = 0.0, y0 = 0.0, z0 = 0.0, x1 = 0.0, y1 = 0.0, z1 = 0.0;
+        double x2 = 0.0, y2 = 0.0, z2 = 0.0;  // parity mode only: tail + spurious exit + entry
         if (k < nl) {
             f = E.efac[k];
             if (E.fkind[f] != RF_OUTSIDE) {
@@ -1131,14 +1134,14 @@ PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, doub
                                 // the facet with a spurious arc (a whole circular
                                 // segment too much).  It coincides with the vertex to
                                 // ~tol: drop it.  Never fires on consistent geometry.
-#if !defined(PF_REF_STRICT) && !defined(PF_KEEP_SPURIOUS)
-                                if (which == 0 && cur) continue;
-#endif
+                                // (parity mode keeps it, as the reference does)
+                                if (which == 0 && cur && !ws->strict) continue;
                                 const double cxx = ox + t * ux, cxy = oy + t * uy, cxz = oz + t * uz;
                                 const int fl = cur ? (PF_ONSPH | PF_CONN) : (PF_ONSPH | PF_ENTRY);
                                 cur = !cur;
                                 if (cnt == 0) { x0 = cxx; y0 = cxy; z0 = cxz; fl0 = fl; }
-                                else { x1 = cxx; y1 = cxy; z1 = cxz; fl1 = fl; }
+                                else if (cnt == 1) { x1 = cxx; y1 = cxy; z1 = cxz; fl1 = fl; }
+                                else { x2 = cxx; y2 = cxy; z2 = cxz; fl2 = fl; }
                                 cnt++;
                             }
                         }
@@ -1152,6 +1155,7 @@ PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, doub
         if (pos + cnt <= C::CP) {
             if (cnt > 0) { E.ppx[pos] = x0; E.ppy[pos] = y0; E.ppz[pos] = z0; E.pfl[pos] = (uint8_t)fl0; E.pfac[pos] = (uint8_t)f; }
             if (cnt > 1) { E.ppx[pos + 1] = x1; E.ppy[pos + 1] = y1; E.ppz[pos + 1] = z1; E.pfl[pos + 1] = (uint8_t)fl1; E.pfac[pos + 1] = (uint8_t)f; }
+            if (cnt > 2) { E.ppx[pos + 2] = x2; E.ppy[pos + 2] = y2; E.ppz[pos + 2] = z2; E.pfl[pos + 2] = (uint8_t)fl2; E.pfac[pos + 2] = (uint8_t)f; }
         }
         base += tot;
     }
@@ -1275,12 +1279,10 @@ PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, doub
 #define PF_ARC_CHORD 100.0
 // below this sweep (rad) an arc's wrap is decided with the reference's formula
 #define PF_SWEEP_AMBIG 1e-6
+// (never called in parity mode: the reference keeps the wrapped sweep)
 template <class C>
 PF_NOINL bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
                                 double dx, double dy, double dz, double rc, double tol) {
-#if defined(PF_REF_STRICT) || defined(PF_NO_LONGARC)
-    return false;
-#endif
     double dn = dsqrt(dx * dx + dy * dy + dz * dz);
     if (!(dn > 0.0)) return false;
     double k = ddiv(rc, dn);
@@ -1381,7 +1383,7 @@ PF_NOINL void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, d
                 if (dth <= 0.0) {
                     dth += 2.0 * PF_PI;
                     const double ch2 = (x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0);
-                    if (ch2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
+                    if (!ws->strict && ch2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
                         long_arc_impossible(P, f, qx, qy, qz, x0 * e0 + y0 * e3, x0 * e1 + y0 * e4,
                                             x0 * e2 + y0 * e5, r, tol))
                         dth -= 2.0 * PF_PI;
@@ -1571,7 +1573,7 @@ PF_NOINL void ring_patches(W *ws, const Poly<typename W::Cap> &P, double px, dou
                 }
                 if (arc && dPQ > PF_PI) {
                     const double d0 = rp[0] - rq[0], d1 = rp[1] - rq[1], d2 = rp[2] - rq[2];
-                    if (d0 * d0 + d1 * d1 + d2 * d2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
+                    if (!ws->strict && d0 * d0 + d1 * d1 + d2 * d2 <= (PF_ARC_CHORD * tol) * (PF_ARC_CHORD * tol) &&
                         long_arc_impossible(P, f, qc[0], qc[1], qc[2], rp[0], rp[1], rp[2],
                                             dsqrt(psi - ee * ee), tol))
                         dPQ -= 2.0 * PF_PI;
@@ -2021,6 +2023,7 @@ PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, 
     const int L = pfw::lane();
     if (L == 0) {
         ws->oflow = 0;
+        ws->strict = in.strict;
         ws->cen_on = out.census16 != nullptr;
 #pragma unroll 1
         for (int k = 0; k < 16; k++) ws->cen[k] = 0;

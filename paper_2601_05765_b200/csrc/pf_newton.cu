@@ -383,7 +383,7 @@ int rescue_nearest(pf_ctx *ctx, int64_t n, const double *pts, const double *vol,
     int rc = 0;
     if (m > 0) {
         NCK(cudaMallocAsync((void **)&nn, 2 * (size_t)m * sizeof(int64_t), st));
-        if (pf_knn(ctx, n, pts, m, q, 2, nn, st) < 0) rc = -1;
+        if (pf_knn(ctx, n, pts, m, q, 2, nn, 0, st) < 0) rc = -1;  // the solve's grid
         if (!rc) {
             pf_internal_launches_add(1);
             k_rescue_nn<<<nblocks(m), RB, 0, st>>>(m, list, nn, psi);

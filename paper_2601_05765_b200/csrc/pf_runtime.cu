@@ -115,6 +115,9 @@ struct pf_ctx {
     size_t stage_n = 0;
     int fast_blocks = 0, build_blocks = 0, eval_blocks = 0, eval_sync = 1;
     bool attr_set = false;
+    // parity mode: restrict the facets exactly as the reference does, including
+    // its spurious-entry and long-arc outcomes; 0 = robust default
+    int strict = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -342,6 +345,9 @@ __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
         }
         __syncwarp();
     }
+    // drain the last bulk store: it still reads this warp's shared memory
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
@@ -360,6 +366,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
         poly_load(gpoly + i, ws->P[0]);
         if (lane == 0) {
             ws->oflow = 0;
+            ws->strict = in.strict;
             ws->cen_on = out.census16 != nullptr;
             for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
         }
@@ -373,8 +380,6 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
         }
         __syncwarp();
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
-    __syncwarp();
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
@@ -431,6 +436,7 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
             else poly_load(gpoly + i, ws->P[0]);
             if (lane == 0) {
                 ws->oflow = 0;
+                ws->strict = in.strict;
                 ws->cen_on = out.census16 != nullptr;
                 for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
             }
@@ -557,6 +563,7 @@ void fill_cellin(pf_ctx *c, CellIn &in, int64_t n, const double *pts, const doub
     in.dpsi_ptr = dpsi >= 0.0 ? nullptr : c->dscal;
     in.ball_aware = ball_aware;
     in.want_m2 = want_m2;
+    in.strict = c->strict;
     // first shell of the non-ball-aware search: a few bucket edges
     double h = std::max(c->gh[0], std::max(c->gh[1], c->gh[2]));
     in.t_init = (3.0 * h) * (3.0 * h);
@@ -757,10 +764,11 @@ int grid_build(pf_ctx *c, int64_t n, const double *pts, const double *psi, doubl
     if (ensure(&c->scan_tmp, &c->scan_tmp_cap, 2 * nblk + 2)) return -1;
     CK(cudaMemsetAsync(c->bcount, 0, (ncell + 1) * sizeof(int), st));
     int gb = (int)std::min<int64_t>(c->nsm * 8, (n + 255) / 256 + 1);
-    if (n > 0)
+    if (n > 0) {
         g_launches++;
         k_grid_bucket<<<gb, 256, 0, st>>>(pts, n, c->glo[0], c->glo[1], c->glo[2], c->gih[0], c->gih[1],
                                           c->gih[2], g[0], g[1], g[2], c->bid, c->bcount);
+    }
     g_launches++;
     k_scan_blocks<<<(int)nblk, SCAN_T, 0, st>>>(c->bcount, c->bstart, ncell + 1, c->scan_tmp);
     if (nblk > 1) {
@@ -869,9 +877,18 @@ int pf_ctx_create(pf_ctx **out, int device) {
     CK(cudaMalloc(&c->counters, 4 * sizeof(int)));
     CK(cudaMalloc(&c->err, sizeof(unsigned long long)));
     CK(cudaMemset(c->dscal, 0, 8 * sizeof(double)));
+    if (const char *e = getenv("PF_PARITY_MODE")) c->strict = e[0] == '1';
     *out = c;
     return 0;
 }
+
+int pf_set_parity_mode(pf_ctx *c, int on) {
+    if (!c) return set_err("pf_set_parity_mode: null context");
+    c->strict = on != 0;
+    return 0;
+}
+
+int pf_get_parity_mode(pf_ctx *c) { return c ? c->strict : 0; }
 
 int pf_ctx_destroy(pf_ctx *c) {
     if (!c) return 0;
@@ -932,6 +949,8 @@ int pf_set_domain(pf_ctx *c, const double *dv, const int64_t *dc, const double *
     }
     c->dvol = std::fabs(vol) / 6.0;
     c->has_domain = true;
+    c->grid_n = -1;  // the grid's origin and edge come from the domain bbox
+    c->grid_pts = nullptr;
     return 0;
 }
 
@@ -1119,11 +1138,11 @@ int64_t pf_batch_build(pf_ctx *c, int64_t n, const double *pts, const double *ps
 int pf_evaluate_lean_cells(pf_ctx *c, int64_t n, const double *pts, const double *psi, double dpsi,
                            int ball_aware, int64_t smf, const int32_t *cells, int64_t ncells, double *vol,
                            double *ksur, int32_t *fcount, int32_t *ftag, double *farea, double *cent,
-                           int64_t *flags, void *stream) {
+                           int64_t *flags, int rebuild_grid, void *stream) {
     cudaStream_t st = S(stream);
     if (!c->has_domain) return set_err("pf_evaluate_lean_cells: no domain set");
     if (!(dpsi >= 0.0)) return set_err("pf_evaluate_lean_cells: dpsi must be >= 0");
-    if (c->grid_n != n || c->grid_pts != pts) {
+    if (rebuild_grid || c->grid_n != n || c->grid_pts != pts) {
         if (grid_build(c, n, pts, psi, 0.0, st)) return -1;
     }
     CellIn in;
@@ -1233,12 +1252,12 @@ int pf_last_retry_count(pf_ctx *c, int64_t *count) {
 }
 
 int64_t pf_knn(pf_ctx *c, int64_t n, const double *pts, int64_t nq, const double *queries, int64_t k,
-               int64_t *out_idx, void *stream) {
+               int64_t *out_idx, int rebuild_grid, void *stream) {
     cudaStream_t st = S(stream);
     if (!c->has_domain) return set_err("pf_knn: no domain set");
     if (k > n) k = n;
     if (k <= 0 || nq <= 0) return k > 0 ? k : 0;
-    if (c->grid_n != n || c->grid_pts != pts) {
+    if (rebuild_grid || c->grid_n != n || c->grid_pts != pts) {
         if (grid_build(c, n, pts, nullptr, 0.0, st)) return -1;
     }
     if (!c->attr_set) {

@@ -102,7 +102,7 @@ def _bind():
     L = _lib.lib()
     if not getattr(L, "_dist_bound", False):
         vp, i, i64, d = C.c_void_p, C.c_int, C.c_int64, C.c_double
-        L.pf_evaluate_lean_cells.argtypes = [vp, i64, vp, vp, d, i, i64, vp, i64] + [vp] * 7 + [vp]
+        L.pf_evaluate_lean_cells.argtypes = [vp, i64, vp, vp, d, i, i64, vp, i64] + [vp] * 7 + [i, vp]
         L.pf_rows_gradient.argtypes = [i, vp, vp, vp, vp, vp, vp]
         L.pf_rows_hessian.argtypes = [i, vp, i, vp, vp, vp, vp, vp, vp, d, vp, vp, vp, vp, vp]
         L.pf_dcg_init.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp]
@@ -193,8 +193,9 @@ class CudaOps:
             return
         q = self.pts.index_select(0, e).contiguous()
         nn = torch.empty((m, 2), dtype=torch.int64, device="cuda")
+        # the grid of self.pts (built in __init__; self.pts is never written) is reused
         self.chk(self._lib.lib().pf_knn(self.ctx, self.n, self.p(self.pts), m, self.p(q), 2, self.p(nn),
-                                        self._s()), "pf_knn")
+                                        0, self._s()), "pf_knn")
         j = torch.where(nn[:, 0] == e, nn[:, 1], nn[:, 0])
         self.psi.index_copy_(0, e, torch.maximum(self.psi.index_select(0, e), self.psi.index_select(0, j)))
 
@@ -238,7 +239,7 @@ class CudaOps:
         self.chk(self.L.pf_evaluate_lean_cells(
             self.ctx, self.n, self.p(self.pts), self.p(ps), float(dpsi), self.ball_aware, self.smf,
             self.p(self.rows), self.nrows, self.p(s["vol"]), self.p(s["ksur"]), self.p(s["fcount"]),
-            self.p(s["ftag"]), self.p(s["farea"]), self.p(s["cent"]), self.p(self.flags), self._s()),
+            self.p(s["ftag"]), self.p(s["farea"]), self.p(s["cent"]), self.p(self.flags), 0, self._s()),
             "pf_evaluate_lean_cells")
 
     def grad_stats(self, trial=False):
@@ -361,10 +362,14 @@ class DistNewton:
         self.halo_entries = 0
 
     # --- partition --------------------------------------------------------
-    def _partition(self, psi_global: np.ndarray, dpsi: float):
+    def _partition(self, psi_global: np.ndarray, dpsi: float, psi_plan: np.ndarray | None = None):
+        """Slabs, ghosts and halo plan.  The ghost margin is sized from
+        ``psi_plan`` (default the weights themselves): a trial re-partition
+        passes the trial weights psi + alpha x, whose search radii the trial
+        evaluation needs."""
         c = self.comm
-        self.slab, self.plan = partition.halo_plan(self.pts, psi_global, dpsi, c.world, c.rank,
-                                                   self.lo, self.hi, self.slack)
+        self.slab, self.plan = partition.halo_plan(self.pts, psi_global if psi_plan is None else psi_plan,
+                                                   dpsi, c.world, c.rank, self.lo, self.hi, self.slack)
         l2g = self.slab.local_to_global
         self.ops = self.ops_factory(self.pts[l2g], self.nu[l2g], self.slab.owned_local)
         self.ops.set_psi(psi_global[l2g])
@@ -395,16 +400,23 @@ class DistNewton:
         """Evaluate the owned cells (current or trial weights); returns the
         all-reduced (worst, min vol, min nu)."""
         dpsi = self._dpsi(trial)
-        if not self._margin_ok(dpsi, trial):
-            # weights outgrew the ghost layer: re-partition from the global weights
+        for _ in range(8):
+            if self._margin_ok(dpsi, trial):
+                break
+            # weights outgrew the ghost layer: re-partition from the global
+            # weights, with the margin sized for the weights being evaluated
+            # (the trial weights psi + alpha x on a damping trial)
             psi_g = self._gather_global(self.ops.psi_host(False))
             x_g = self._gather_global(self.ops.vec("x").cpu().numpy()) if trial else None
-            self._partition(psi_g, dpsi)
+            self._partition(psi_g, dpsi, psi_g + self._alpha * x_g if trial else None)
             self.repartitions += 1
             if trial:
                 l2g = self.slab.local_to_global
                 self.ops.vec("x").copy_(self.ops.torch.as_tensor(x_g[l2g]))
                 self.ops.trial(self._alpha)
+            dpsi = self._dpsi(trial)
+        else:
+            raise RuntimeError("ghost layer still too thin after 8 re-partitions")
         self.ops.evaluate(dpsi, trial)
         st = self.comm.all_reduce(self.ops.grad_stats(trial), "max")
         st = [float(v) for v in st.cpu()]

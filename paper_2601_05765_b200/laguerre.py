@@ -186,7 +186,7 @@ def knn_batch(points, queries, k: int, domain: ConvexCell):
     dpk = domain_pack(domain)
     upload_domain(c, *dpk.args(), dpk.tol)
     got = _lib.check(_lib.lib().pf_knn(c, n, _lib.ptr(pts), q.shape[0], _lib.ptr(q), kk,
-                                       _lib.ptr(out), _lib.stream_ptr()), "pf_knn")
+                                       _lib.ptr(out), 1, _lib.stream_ptr()), "pf_knn")
     return out[:, :got]
 
 

@@ -44,8 +44,16 @@ def alloc(n: int, smf: int):
 
 
 def evaluate(pts, psi, domain: ConvexCell, ball_aware: bool = True, want_m2: bool = True,
-             smf: int = 32, dpsi_max: float | None = None, out=None) -> RestrictedDiagram:
-    """Build + evaluate every restricted cell.  ``pts`` [n,3], ``psi`` [n] CUDA f64 tensors."""
+             smf: int = 32, dpsi_max: float | None = None, out=None,
+             parity_mode: bool | None = None) -> RestrictedDiagram:
+    """Build + evaluate every restricted cell.  ``pts`` [n,3], ``psi`` [n] CUDA f64 tensors.
+    ``parity_mode`` (None = the context's setting): restrict exactly as the
+    reference does (True) or with the robust correction (False), DESIGN.md §5.1."""
+    with _lib.parity(parity_mode):
+        return _evaluate(pts, psi, domain, ball_aware, want_m2, smf, dpsi_max, out)
+
+
+def _evaluate(pts, psi, domain, ball_aware, want_m2, smf, dpsi_max, out):
     import torch
 
     pts = torch.as_tensor(pts, dtype=torch.float64, device="cuda").contiguous()

@@ -147,8 +147,11 @@ void lane_fn(void *ctx, int lane) {
 
 static const int *g_only = nullptr;  // optional cell subset (debugging)
 static int g_nonly = 0;
+static int g_strict = 0;  // parity mode (CellIn::strict)
 
 extern "C" {
+
+void pfemu_set_strict(int on) { g_strict = on != 0; }
 
 void pfemu_set_cells(const int *cells, int ncells) {
     g_only = cells;
@@ -202,6 +205,7 @@ int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
     in.dnv = dnv; in.dnf = dnf; in.dnl = dnl;
     in.tol = tol; in.dpsi = dpsi; in.ball_aware = ball_aware; in.want_m2 = want_m2;
     in.t_init = t_init;
+    in.strict = g_strict;
     // per super-bucket max weight, as pf_runtime.cu's k_super_max (PF_SUPER = 4)
     std::vector<double> smax, cslack;
     if (ball_aware && !getenv("PF_GLOBAL_SLACK")) {

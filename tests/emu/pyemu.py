@@ -24,6 +24,7 @@ def lib():
                                      + [i, C.c_uint64, vp, vp])
         L.pfemu_ws_bytes.restype = i
         L.pfemu_ws_bytes.argtypes = [i]
+        L.pfemu_set_strict.argtypes = [i]
         _lib = L
     return _lib
 
@@ -33,8 +34,9 @@ def _p(a):
 
 
 def evaluate(pts, psi, pack, tol, grid_lo, grid_ih, grid_gn, dpsi, ball_aware=True,
-             want_m2=True, smf=32, t_init=0.0, tier=0, seed=1):
+             want_m2=True, smf=32, t_init=0.0, tier=0, seed=1, parity_mode=False):
     """pack = (dv, dc, dp, dt, dlp, dlv) in the reference's packed layout."""
+    lib().pfemu_set_strict(int(bool(parity_mode)))
     dv, dc, dp, dt, dlp, dlv = pack
     nv, nf, nl = int(dc[0]), int(dc[1]), int(dc[2])
     dv = np.ascontiguousarray(dv[:nv], np.float64)

@@ -48,3 +48,26 @@ def test_degenerate_arc_cells(cell):
     # adjacency unchanged
     assert e["fcount"][loc] == o["fcount"][loc]
     assert np.array_equal(e["ftag"][loc], o["ftag"][loc])
+
+
+@pytest.mark.parametrize("cell", _cells())
+def test_degenerate_arc_cells_parity_mode(cell):
+    """Parity mode reproduces the reference's outcome on the same cells: the
+    spurious entry and the wrapped arc are kept, and the volume, free surface
+    and facet areas equal the reference's to 1e-9."""
+    g = np.load(FIX)
+    pts, psi, loc = g[f"c{cell}_pts"], g[f"c{cell}_psi"], int(g[f"c{cell}_local"])
+    dpsi = float(g["dpsi"])
+    grid = O.SpatialGrid(pts, [0, 0, 0], [1, 1, 1], 1.0)
+    o = O.evaluate(pts, psi, DPK.args(), DPK.tol, grid, smf=32, i0=0, i1=1, cells=np.array([loc]),
+                   dpsi=dpsi)
+    gn = np.array([128, 128, 128])
+    e = pyemu.evaluate(pts, psi, DPK.args(), DPK.tol, np.zeros(3), gn.astype(float), gn, dpsi,
+                       smf=32, tier=0, seed=3, parity_mode=True)
+    assert e["fcount"][loc] == o["fcount"][loc]
+    assert np.array_equal(e["ftag"][loc], o["ftag"][loc])
+    assert e["status"][loc] == o["status"][loc]
+    sph = 4 * np.pi * psi[loc]
+    assert abs(e["vol"][loc] - o["vol"][loc]) <= 1e-9 * abs(o["vol"][loc])
+    assert abs(e["ksur"][loc] - o["ksur"][loc]) <= 1e-9 * sph
+    assert float(np.max(np.abs(e["farea"][loc] - o["farea"][loc]))) <= 1e-9 * sph

@@ -1,50 +1,67 @@
-"""Parity at the BASELINE.json sizes (C3 500k chocs, C4 2M droplet, C5 1M
-two-fluid): the device evaluates every cell; the CPU oracle re-evaluates a
-random sample of them (cells are independent, so a sample is an exact check
-of those cells).  Size-independent properties are checked on all cells:
-facet adjacency symmetric (i sees j <=> j sees i), facet areas equal from
-both sides, run-to-run determinism.
+"""Parity at the BASELINE.json sizes (C2 97k dam break, C3 500k chocs, C4 2M
+droplet, C5 1M two-fluid; the 'c' kinds at the config's Newton-converged
+weights, the bench workload -- tests/golden/psi_<C>.npz).
 
-Adjacency (status, fcount, ordered ftag) is bit-exact on every sampled cell.
-Values agree to 1e-9 relative except on the cells of DESIGN.md §5.1 (the
-reference's degenerate-arc / spurious-entry cases, where the device follows
-the geometry and the oracle keeps the reference's wrong values): at most
-0.05% of the sample."""
+* Parity mode (the reference's restriction bit for bit):
+  the device evaluates every cell; the CPU oracle re-evaluates a random
+  sample (cells are independent, so the sample is an exact check of those
+  cells).  Adjacency (status, fcount, ordered ftag) is bit-exact and volume,
+  free surface and facet areas agree to 1e-9 relative on EVERY sampled cell.
+  (profiles/r02_parity_census.txt holds the whole-scene census.)
+* Robust mode (the default): on the whole scene, adjacency equals parity
+  mode's, and values differ from it only on the few cells whose restriction
+  the correction changes -- at most the whole-scene counts observed
+  (C3 7, C4 161, C5 44, C5c 7 cells, +20% headroom, others 0).
+Size-independent properties on all cells: facet adjacency symmetric, facet
+areas equal from both sides, run-to-run determinism."""
+import os
+
 import numpy as np
 import pytest
 
-from conftest import OUT_KEYS
+from conftest import OUT_KEYS, ROOT
 
 pytestmark = pytest.mark.gpu
 
 REL = 1e-9
+# robust vs parity: differing cells in the whole-scene census (r01h / r02)
+ROBUST_MAX = {"C2c": 0, "C3": 9, "C3c": 0, "C4": 194, "C4c": 38, "C5": 53, "C5c": 9}
 
 
 def _scene(kind):
     from paper_2601_05765_b200 import scenes
 
-    if kind == "C3":
-        sc = scenes.c3_chocs()
-        return sc, sc.psi_cold()
-    if kind in ("C3c", "C5c"):  # converged weights: large local weight spread (per-cell slack, mid tier)
+    cfg = kind[:2]
+    sc = scenes.make(cfg)
+    if kind.endswith("c"):
+        fx = os.path.join(ROOT, "tests", "golden", f"psi_{cfg}.npz")
+        if os.path.exists(fx):
+            return sc, np.load(fx)["psi"].astype(np.float64)
         import torch
 
         from paper_2601_05765_b200 import geom, solver
 
-        sc = scenes.c3_chocs() if kind == "C3c" else scenes.c5_two_fluid()
         res = solver.newton_solve(torch.as_tensor(sc.pts, device="cuda"), torch.as_tensor(sc.nu, device="cuda"),
                                   geom.box_domain([0, 0, 0], [1, 1, 1]))
         return sc, res.psi.cpu().numpy()
+    if kind == "C3":
+        return sc, sc.psi_cold()
     if kind == "C4":
-        sc = scenes.c4_droplet()
         return sc, np.full(sc.n, (0.85 * sc.meta["h"]) ** 2)
-    sc = scenes.c5_two_fluid()
     h = sc.meta["h"]
     return sc, np.where(sc.nu > h ** 3 * 1.5, (1.7 * h) ** 2, (0.85 * h) ** 2)
 
 
-@pytest.mark.parametrize("kind", ["C3", "C3c", "C4", "C5", "C5c"])
-def test_full_size_sample_matches_oracle(kind):
+def _values_bad(o, r, psi, cells):
+    sph = 4 * np.pi * psi[cells]
+    dv = np.abs(o["vol"][cells] - r["vol"][cells]) / np.maximum(np.abs(r["vol"][cells]), sph ** 1.5 * 1e-6)
+    dk = np.abs(o["ksur"][cells] - r["ksur"][cells]) / sph
+    da = np.max(np.abs(o["farea"][cells] - r["farea"][cells]), axis=1) / sph
+    return (dv > REL) | (dk > REL) | (da > REL)
+
+
+@pytest.mark.parametrize("kind", ["C2c", "C3", "C3c", "C4", "C4c", "C5", "C5c"])
+def test_full_size_parity_mode_and_robust_mode(kind):
     import torch
 
     from oracle import pyoracle as O
@@ -53,25 +70,29 @@ def test_full_size_sample_matches_oracle(kind):
     sc, psi = _scene(kind)
     dom = geom.box_domain([0, 0, 0], [1, 1, 1])
     dpk = laguerre.domain_pack(dom)
-    d = restricted.evaluate(torch.as_tensor(sc.pts, device="cuda"), torch.as_tensor(psi, device="cuda"),
-                            dom, smf=32)
-    o = {k: getattr(d, k).cpu().numpy() for k in OUT_KEYS}
+    tp, tw = torch.as_tensor(sc.pts, device="cuda"), torch.as_tensor(psi, device="cuda")
+    dp = restricted.evaluate(tp, tw, dom, smf=32, parity_mode=True)
+    p = {k: getattr(dp, k).cpu().numpy() for k in OUT_KEYS}
+    del dp
     rng = np.random.default_rng(1)
-    cells = np.sort(rng.choice(sc.n, size=20_000, replace=False)).astype(np.int64)
+    cells = np.sort(rng.choice(sc.n, size=min(sc.n, 20_000), replace=False)).astype(np.int64)
     g = O.SpatialGrid(sc.pts, [0, 0, 0], [1, 1, 1], 1.0)
     r = O.evaluate(sc.pts, psi, dpk.args(), dpk.tol, g, smf=32, i0=0, i1=len(cells), cells=cells)
     for k in ("status", "fcount", "ftag"):
-        assert np.array_equal(o[k][cells], r[k][cells]), k
-    sph = 4 * np.pi * float(psi.max())
-    dv = np.abs(o["vol"][cells] - r["vol"][cells]) / np.maximum(np.abs(r["vol"][cells]), sph ** 1.5 * 1e-6)
-    da = np.max(np.abs(o["farea"][cells] - r["farea"][cells]) / sph, axis=1)
-    bad = (dv > REL) | (da > REL)
-    assert bad.sum() <= max(1, int(5e-4 * len(cells))), (kind, int(bad.sum()), float(dv.max()))
-    ok = ~bad
-    assert float(np.max(np.abs(o["ksur"][cells][ok] - r["ksur"][cells][ok]) / sph)) <= REL
+        assert np.array_equal(p[k][cells], r[k][cells]), k
+    bad = _values_bad(p, r, psi, cells)
+    assert int(bad.sum()) == 0, (kind, int(bad.sum()))
+    # robust mode, whole scene, against parity mode
+    dr = restricted.evaluate(tp, tw, dom, smf=32, parity_mode=False)
+    q = {k: getattr(dr, k).cpu().numpy() for k in OUT_KEYS}
+    for k in ("status", "fcount", "ftag"):
+        assert np.array_equal(q[k], p[k]), k
+    allc = np.arange(sc.n)
+    nb = int(_values_bad(q, p, psi, allc).sum())
+    assert nb <= ROBUST_MAX[kind], (kind, nb)
 
 
-@pytest.mark.parametrize("kind", ["C4"])
+@pytest.mark.parametrize("kind", ["C4c"])
 def test_full_size_symmetry_and_determinism(kind):
     import torch
 
@@ -105,8 +126,7 @@ def test_full_size_symmetry_and_determinism(kind):
         (int((~found).sum()), float(lone.max()) if lone.size else 0.0)
     twin = A[o1[pos]][found]
     # two-sided areas agree to < 1e-7 of the sphere area except on tolerance-level
-    # slivers, where the reference is itself asymmetric (C4, oracle: pair
-    # 1557572/1563799 has 3.678e-9 vs 3.096e-9, 5e-6 of the sphere area)
+    # slivers, where the reference is itself asymmetric
     dif = np.abs(A[found] - twin) / sph
     assert int((dif > 1e-7).sum()) <= 1e-6 * len(dif) and float(np.max(dif)) < 1e-4, \
         (float(np.max(dif)), int((dif > 1e-7).sum()))
