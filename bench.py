@@ -5,26 +5,32 @@
 
 Metric (BASELINE.json): "generalized Laguerre cells/sec (vol+areas) and ms per
 Newton solve at 2M cells".  Workload at N=1: C4, the 2M-cell droplet scene
-(paper teaser scale), weights psi at convergence of the
-config's first (cold-start) Newton solve, which is computed in the untimed
-set-up and itself timed once as ``newton.ms_per_solve``.
+(paper teaser scale), at the weights psi of the config's
+first (cold-start) Newton solve -- the committed fixture
+tests/golden/psi_C4.npz (tools/make_psi_fixtures.py), read by BOTH arms so
+they time bit-identical inputs.  The cold Newton solve itself is timed once
+(median of three) as ``newton.ms_per_solve``.
 
 One step = one full evaluation of the restricted Laguerre cells (bucket grid
 counting sort + dpsi reduction + candidate gather + clip + restriction +
-volumes / free-surface / facet areas / centroids), fp64, ball-aware, outputs
-in the reference's fixed-stride layout (smf=32) resident in HBM.  L2 is
-flushed (a 256 MiB write) before every timed step.  `e2e` repeats the step
-through the reference-facing drop-in (`_kernels._batch_evaluate` on host numpy
-arrays): host->device copy of (pts, psi) and device->host copy of all twelve
-outputs inside the timed region.
+volumes / free-surface / facet areas / centroids), fp64, ball-aware, in
+parity mode (the reference's restriction bit for bit; the
+robust default's time is reported beside it), outputs in the reference's
+fixed-stride layout (smf=32) resident in HBM.  L2 is flushed (a 256 MiB
+write) before every timed step.  `e2e` repeats the step through the
+reference-facing drop-in (`_kernels._batch_evaluate` on pageable numpy
+arrays, allocated once like a caller's, -> pf_batch_evaluate_host): the
+host->device copy of (pts, psi) and the device->host copy of everything the
+reference writes are inside the timed region.
 
 N>1 (torchrun): the domain is partitioned into x-slabs; rank r evaluates the
 cells it owns using owned + ghost sites (ghost margin = largest ball-aware
 search radius, with the global dpsi), so per-cell results are identical to
 N=1 and there is no data-path collective during the evaluation.  Total work
-is fixed (strong scaling).  `--impl reference` times the CPU oracle port of
-the reference kernel (oracle/, bit-identical to the numba reference) on the
-host cores, rank 0 only.
+is fixed (strong scaling).  `--impl reference` times the CPU port of the
+reference kernel (oracle/, bit-identical to the numba reference) on the host
+cores over ALL cells of the same workload each step (grid build included),
+rank 0 only; it never loads the CUDA library.
 """
 from __future__ import annotations
 
@@ -60,6 +66,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-hbm", action="store_true")
+    ap.add_argument("--mode", default="parity", choices=["parity", "robust"],
+                    help="restriction of the timed evaluation (DESIGN.md §5.1)")
     return ap.parse_args()
 
 
@@ -74,6 +82,31 @@ def make_scene(name):
     from paper_2601_05765_b200 import scenes
 
     return scenes.make(name)
+
+
+def workload_psi(name, sc):
+    """(psi f64, description) of the workload: the committed converged weights."""
+    fx = os.path.join(ROOT, "tests", "golden", f"psi_{name}.npz")
+    if os.path.exists(fx):
+        return (np.load(fx)["psi"].astype(np.float64),
+                f"converged weights of the config's first cold-start Newton solve (eps_vol 1%), "
+                f"fixture tests/golden/psi_{name}.npz (f32-rounded), identical in both arms")
+    return None, None
+
+
+def config_of(a, sc, psi_desc):
+    """The workload description, identical in both arms."""
+    return {"workload": workload_desc(a.config, sc), "ball_aware": True, "smf": a.smf, "psi": psi_desc,
+            "restriction": "parity mode (the reference's restriction bit for bit)" if a.mode == "parity"
+            else "robust (DESIGN.md 5.1)",
+            "l2": "GPU arm: 256 MiB flush write before every timed step",
+            "parallelism": f"x-slab spatial partition over {a.gpus} GPU(s), ghosts by search radius"
+            if a.gpus > 1 else "1 GPU"}
+
+
+# Port-vs-numba speed of the CPU baseline, measured in the build container
+# (8 vCPU, 8 threads) on the same kind of workload: tools/port_vs_numba.py.
+PORT_VS_NUMBA = None
 
 
 def workload_desc(name, sc):
@@ -254,26 +287,47 @@ def hbm_kernels(sc, dom, psi_g, smf, reps=5, cg_iters=50):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
 
-def cpu_reference_run(sc, psi, steps, warmup, sample_cells, threads):
-    """CPU oracle port of _kernels._batch_evaluate on the host cores."""
+def cpu_reference_run(sc, psi, steps, warmup, threads, cells=None):
+    """CPU port of _kernels._batch_evaluate (oracle/, bit-identical to the
+    numba reference) on the host cores: per step the reference's own
+    SpatialGrid (numpy stable argsort, laguerre.py:52-80), _dpsi_max and the
+    batch kernel over every cell (or the `cells` sample).  Outputs are
+    allocated once, as a caller would."""
     from oracle import pyoracle as O
     from paper_2601_05765_b200 import geom, laguerre
 
     O.set_threads(threads)
     dom = geom.box_domain([0, 0, 0], [1, 1, 1])
     dpk = laguerre.domain_pack(dom)
-    rng = np.random.default_rng(0)
-    cells = np.sort(rng.choice(sc.n, size=min(sample_cells, sc.n), replace=False)).astype(np.int64)
-    times = []
+    outs = O.alloc_outputs(sc.n, 32)
+    m = sc.n if cells is None else len(cells)
+    times, err = [], 0
     for it in range(warmup + steps):
         t0 = time.perf_counter()
         g = O.SpatialGrid(sc.pts, [0, 0, 0], [1, 1, 1], dpk.volume)
-        o = O.evaluate(sc.pts, psi, dpk.args(), dpk.tol, g, ball_aware=True, want_m2=True, smf=32,
-                       i0=0, i1=len(cells), cells=cells)
+        err = O.batch_evaluate(sc.pts, psi, *dpk.args(), *g.kernel_args(), dpk.tol, O.dpsi_max(psi), True, True,
+                               32, *[outs[k] for k in O.OUT_ORDER], i0=0, i1=0 if cells is None else m,
+                               cells=cells)
         t1 = time.perf_counter()
         if it >= warmup:
             times.append(t1 - t0)
-    return len(cells) / (sum(times) / len(times)), O.num_threads(), o["err"]
+    return m / (sum(times) / len(times)), O.num_threads(), err, times
+
+
+def cpu_newton_run(cfg, threads):
+    """CPU Newton restatement (oracle/newton_ref.py: SPEC.md:286-335 over the
+    oracle) from the cold start: (ms, stats)."""
+    from oracle import newton_ref
+    from oracle import pyoracle as O
+    from paper_2601_05765_b200 import geom, laguerre
+
+    O.set_threads(threads)
+    sc = make_scene(cfg)
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    dpk = laguerre.domain_pack(dom)
+    t0 = time.perf_counter()
+    _, st = newton_ref.newton_solve(sc.pts, sc.nu, dpk.args(), dpk.tol, dom.diagonal())
+    return 1e3 * (time.perf_counter() - t0), st
 
 
 def main():
@@ -283,29 +337,20 @@ def main():
         if rank != 0:
             return
         sc = make_scene(a.config)
-        # converged weights need the device solve; the CPU arm uses the same
-        # weights when a GPU is present, else the cold-start weights
-        psi = sc.psi_cold()
-        try:
-            import torch
-
-            if torch.cuda.is_available():
-                from paper_2601_05765_b200 import geom
-
-                psi = converged_psi(sc, geom.box_domain([0, 0, 0], [1, 1, 1]))[0].cpu().numpy()
-        except Exception:
-            pass
+        psi, desc = workload_psi(a.config, sc)
+        if psi is None:
+            psi, desc = sc.psi_cold(), "cold start (no converged-weight fixture)"
         threads = os.cpu_count() or 1
-        sample = 400_000 if sc.n > 400_000 else sc.n
-        v, cores, err = cpu_reference_run(sc, psi, a.steps, a.warmup, sample, threads)
+        v, cores, err, times = cpu_reference_run(sc, psi, a.steps, a.warmup, threads)
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": 1e3 * sample / v, "higher_is_better": True,
+                "warmup": a.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "impl": "reference",
-                "config": {"workload": workload_desc(a.config, sc), "ball_aware": True, "smf": 32},
+                "impl": "reference", "config": config_of(a, sc, desc),
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                 "sample": f"{sample} random cells of the workload per step "
-                                           "(full neighbourhoods), grid build included"},
+                                 "sample": f"all {sc.n} cells of the workload every step, grid build + dpsi "
+                                           "included (oracle/potflow_oracle.c: the reference kernel restated in "
+                                           "C, bit-identical to the numba reference, tests/test_oracle_golden.py)",
+                                 "port_vs_numba": PORT_VS_NUMBA},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 "flags": err}
         print(json.dumps(line), flush=True)
@@ -332,23 +377,36 @@ def main():
     c = _lib.ctx()
     laguerre.upload_domain(c, *dpk.args(), dpk.tol)
 
-    # ---- set-up (untimed): converged weights from the config's first solve
+    _lib.set_parity_mode(a.mode == "parity")
+    psi_fix, psi_desc = workload_psi(a.config, sc)
+
+    # ---- set-up (untimed): the config's first (cold-start) Newton solve, timed
     newton = None
+    psi_g = None
     if a.no_newton:
-        psi_g = torch.as_tensor(sc.psi_cold(), device="cuda")
+        pass
     elif ws > 1:
         psi_g, newton = dist_newton(sc, dom, ws)
     else:
-        psi_g, first_ms, nst = converged_psi(sc, dom)    # first solve of the process (allocations,
-        again = [converged_psi(sc, dom)[1] for _ in range(3)]  # module loads); the same cold start x3
+        with _lib.parity(False):  # the robust restriction (parity mode stalls on C4)
+            psi_g, first_ms, nst = converged_psi(sc, dom)    # first solve of the process (allocations,
+            again = [converged_psi(sc, dom)[1] for _ in range(3)]  # module loads); the same cold start x3
         newton_ms = statistics.median(again)
         newton = {"ms_per_solve": newton_ms, "ms_solves": again, "ms_first_solve_in_process": first_ms,
                   "iterations": nst["iterations"],
                   "evaluations": nst["evaluations"], "cg_iterations": nst["cg_iterations"],
                   "worst_initial": nst["worst_initial"], "worst_final": nst["worst_final"],
                   "status": nst["status_name"], "start": "cold (kappa (3 nu/4 pi)^(2/3))",
-                  "eps_vol": 0.01, "n": sc.n}
-    psi_h = psi_g.cpu().numpy()
+                  "restriction": "robust", "eps_vol": 0.01, "n": sc.n}
+    if psi_fix is not None:
+        psi_h = psi_fix
+        if psi_g is not None and newton is not None:  # the fixture is this solve's result (f32-rounded)
+            newton["fixture_max_rel_diff"] = float(np.max(np.abs(psi_g.cpu().numpy() - psi_fix) / psi_fix))
+    elif psi_g is not None:
+        psi_h, psi_desc = psi_g.cpu().numpy(), "converged weights of this run's cold-start Newton solve"
+    else:
+        psi_h, psi_desc = sc.psi_cold(), "cold start"
+    psi_g = torch.as_tensor(psi_h, device="cuda")
     from paper_2601_05765_b200 import partition
 
     dpsi = partition.global_dpsi(psi_h) if ws > 1 else float(max(psi_h.max() - psi_h.min(), 0.0))
@@ -367,9 +425,12 @@ def main():
     outs = restricted.alloc(n_l, smf)
     census = torch.zeros((n_l, 16), dtype=torch.int32, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    # N=1: the device dpsi reduction runs inside every step (dpsi < 0); N>1: the
+    # all-reduced global value (a slab's own max - min is not the reference's)
+    dpsi_step = dpsi if ws > 1 else -1.0
 
     def step(cen=None):
-        err = L.pf_batch_evaluate_ex(c, n_l, _lib.ptr(pts_l), _lib.ptr(psi_l), float(dpk.tol), dpsi, 1,
+        err = L.pf_batch_evaluate_ex(c, n_l, _lib.ptr(pts_l), _lib.ptr(psi_l), float(dpk.tol), dpsi_step, 1,
                                      1, smf, *[_lib.ptr(t) for t in outs],
                                      _lib.ptr(owned_t), 0 if owned_t is None else len(owned),
                                      None, _lib.ptr(cen), 1, _lib.stream_ptr())
@@ -380,7 +441,10 @@ def main():
     torch.cuda.synchronize()
     cen = census[owned_t.long()] if owned_t is not None else census
     s_cell = float((cen.double().cpu().numpy() @ S_WEIGHTS).sum())  # DP slots, all owned cells
-    mean_clips = float(cen[:, 0].double().mean())
+    cen_mean = cen.double().mean(0).cpu().numpy()
+    mean_clips = float(cen_mean[0])
+    s_build = float(cen_mean[:6] @ S_WEIGHTS[:6])
+    s_eval = float(cen_mean[6:] @ S_WEIGHTS[6:])
 
     for _ in range(a.warmup):
         step()
@@ -391,13 +455,12 @@ def main():
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
 
-    # ---- timed region
-    fl = 0
-    tot_ms = 0.0
-    cells_ms = 0.0
-    launches0 = L.pf_launch_count()
-    with ClockSampler(dev) as clk:
-        for _ in range(a.steps):
+    import ctypes
+
+    def timed(nsteps, clk_on=True):
+        fl, tot_ms, cells_ms, build_ms = 0, 0.0, 0.0, 0.0
+        _lib.check(L.pf_stage_timing(c, 1), "pf_stage_timing")
+        for _ in range(nsteps):
             flush.fill_(1.0)
             if ws > 1:
                 dist.barrier()
@@ -408,61 +471,96 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             tot_ms += e0.elapsed_time(e1)
-            import ctypes
-
             ms = ctypes.c_double(0.0)
             if n_eval > 0:
                 _lib.check(L.pf_last_cells_ms(c, ctypes.byref(ms)), "pf_last_cells_ms")
             cells_ms += ms.value
+        b, e, ne = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_int64(0)
+        _lib.check(L.pf_stage_times(c, ctypes.byref(b), ctypes.byref(e), ctypes.byref(ne)), "pf_stage_times")
+        _lib.check(L.pf_stage_timing(c, 0), "pf_stage_timing")
+        nst = max(ne.value, 1)
+        return fl, tot_ms / nsteps, cells_ms / nsteps, b.value / nst, e.value / nst
+
+    # ---- timed region
+    launches0 = L.pf_launch_count()
+    with ClockSampler(dev) as clk:
+        fl, t_step, t_cells, t_build, t_evalk = timed(a.steps)
     launches = int(L.pf_launch_count() - launches0)
-    t_step = tot_ms / a.steps
-    t_cells = cells_ms / a.steps
+    # the robust restriction's time on the same workload (same contract, not the headline)
+    with _lib.parity(a.mode != "parity"):
+        _, t_other, _, _, _ = timed(max(3, min(a.steps, 5)))
     if ws > 1:
-        tt = all_reduce_host([t_step, t_cells], "max")
-        t_step, t_cells = float(tt[0]), float(tt[1])
+        tt = all_reduce_host([t_step, t_cells, t_build, t_evalk, t_other], "max")
+        t_step, t_cells, t_build, t_evalk, t_other = (float(x) for x in tt)
         s_cell_total = float(all_reduce_host([s_cell], "sum")[0])
     else:
         s_cell_total = s_cell
     value = sc.n / (t_step * 1e-3)
 
-    # ---- end to end through the drop-in numpy API (N=1)
+    # ---- end to end through the drop-in numpy API: pageable caller arrays
     # (N > 1: every rank calls the drop-in on its slab's host arrays -- owned
     # cells plus ghosts, the ghost results discarded -- max time over ranks)
     e2e = None
     if not a.no_e2e:
-        from oracle import pyoracle as O  # only for the output allocator shapes
-
-        host = O.alloc_outputs(n_l, smf)
-        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
-        pts_p, psi_p = pin(sc.pts[idx]), pin(psi_h[idx])
-        host = {k: pin(v) for k, v in host.items()}
         gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
-        times = []
-        for it in range(2 + a.steps):
+        order = ("status", "vol", "ksur", "cent", "ipt", "m2", "fcount", "ftag", "farea", "fh", "fnrm", "fcent")
+
+        def host_outputs(pinned):
+            shp = {"status": ((n_l,), np.int64), "vol": ((n_l,), np.float64), "ksur": ((n_l,), np.float64),
+                   "cent": ((n_l, 3), np.float64), "ipt": ((n_l, 3), np.float64), "m2": ((n_l,), np.float64),
+                   "fcount": ((n_l,), np.int64), "ftag": ((n_l, smf), np.int64), "farea": ((n_l, smf), np.float64),
+                   "fh": ((n_l, smf), np.float64), "fnrm": ((n_l, smf, 3), np.float64),
+                   "fcent": ((n_l, smf, 3), np.float64)}
+            if not pinned:
+                return {k: np.zeros(*shp[k]) for k in order}
+            return {k: torch.zeros(shp[k][0], dtype=torch.from_numpy(np.zeros(1, shp[k][1])).dtype).pin_memory()
+                    .numpy() for k in order}
+
+        def run_e2e(pinned, nsteps):
+            host = host_outputs(pinned)  # allocated once, like a caller's arrays
+            pts_h = np.ascontiguousarray(sc.pts[idx])
+            psi_hh = np.ascontiguousarray(psi_h[idx])
+            if pinned:
+                pts_h = torch.from_numpy(pts_h).pin_memory().numpy()
+                psi_hh = torch.from_numpy(psi_hh).pin_memory().numpy()
+            times = []
+            for it in range(2 + nsteps):
+                if ws > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _kernels._batch_evaluate(pts_h, psi_hh, *dpk.args(), *gargs, dpk.tol, dpsi_step, True, True, smf,
+                                         *[host[k] for k in order])
+                if it >= 2:
+                    times.append(time.perf_counter() - t0)
+            t = sum(times) / len(times)
+            h2d, d2h = _kernels.last_copy_bytes
             if ws > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            _kernels._batch_evaluate(pts_p, psi_p, *dpk.args(), *gargs, dpk.tol, dpsi, True, True, smf,
-                                     *[host[k] for k in O.OUT_ORDER])
-            torch.cuda.synchronize()
-            if it >= 2:
-                times.append(time.perf_counter() - t0)
-        t_e2e = sum(times) / len(times)
-        h2d = pts_p.nbytes + psi_p.nbytes
-        d2h = sum(host[k].nbytes for k in O.OUT_ORDER)
-        if ws > 1:
-            t_e2e = float(all_reduce_host([t_e2e], "max")[0])
-            tot = all_reduce_host([h2d, d2h], "sum")
-            h2d, d2h = float(tot[0]), float(tot[1])
-        e2e = {"value": sc.n / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * t_e2e,
-               "api": "paper_2601_05765_b200._kernels._batch_evaluate (numpy, pinned host buffers)"
+                t = float(all_reduce_host([t], "max")[0])
+                tot = all_reduce_host([h2d, d2h], "sum")
+                h2d, d2h = float(tot[0]), float(tot[1])
+            return t, int(h2d), int(d2h), host
+
+        t_e2e, h2d, d2h, host = run_e2e(False, a.steps)
+        e2e = {"value": sc.n / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e,
+               "api": "paper_2601_05765_b200._kernels._batch_evaluate on pageable numpy arrays (np.zeros outputs "
+                      "allocated once) -> C ABI pf_batch_evaluate_host; copies counted by the library: (pts, psi) "
+                      "in, per cell 96 B + per restricted facet 72 B out (everything the reference writes)"
                       + (f"; {ws} ranks, each on its slab (owned + ghost cells), max over ranks" if ws > 1 else "")}
+        # the drop-in's host outputs equal the device-resident step's (same cells, same kernels)
+        if ws == 1:
+            step()  # the device-resident step in the same restriction mode
+            torch.cuda.synchronize()
+            fc_dev = outs[6].cpu().numpy()
+            e2e["matches_device_step"] = bool(np.array_equal(host["fcount"], fc_dev)
+                                              and np.array_equal(host["vol"], outs[1].cpu().numpy()))
+        del host
+        t_pin, _, _, _ = run_e2e(True, max(3, min(a.steps, 5)))
+        e2e["pinned"] = {"value": sc.n / t_pin, "ms_per_step": 1e3 * t_pin,
+                         "note": "same call with page-locked caller arrays"}
 
-    # ---- FP64 roofline of the dominant kernel (k_cells_fast + exact tier)
-    import ctypes
-
+    # ---- FP64 roofline of the dominant kernels (k_cells_build + k_cells_eval_sync + tiers)
     peak = ctypes.c_double(0.0)
     _lib.check(L.pf_fp64_peak(ctypes.byref(peak), None), "pf_fp64_peak")
     peak_v = peak.value
@@ -483,10 +581,15 @@ def main():
                 "frac": achieved / peak_v if peak_v > 0 else None, "traffic": traffic,
                 "traffic_unit": "bytes per step (DRAM read+write of the cell kernels, ncu)",
                 "traffic_detail": traffic_src,
-                "kernel": "k_cells_build+k_cells_eval (+k_cells_exact retries)",
+                "kernel": "k_cells_build+k_cells_eval_sync (+mid/exact tiers)",
                 "kernel_ms": t_cells, "kernel_share_of_step": t_cells / t_step,
-                "algorithmic": f"census S_cell (SURVEY.md §8(d)) = {s_cell_total / sc.n:.0f} DP slots/cell,"
-                               f" x2 flop/slot; mean processed candidates {mean_clips:.1f}/cell",
+                "split": {"build_ms": t_build, "eval_ms": t_evalk,
+                          "build_slots_per_cell": s_build, "eval_slots_per_cell": s_eval,
+                          "build_frac": 2.0 * s_build * sc.n / (t_build * 1e-3) / 1e12 / peak_v if t_build > 0 else None,
+                          "eval_frac": 2.0 * s_eval * sc.n / (t_evalk * 1e-3) / 1e12 / peak_v if t_evalk > 0 else None},
+                "algorithmic": f"census S_cell (SURVEY.md §8(d)) = {s_cell_total / sc.n:.0f} DP slots/cell "
+                               f"(build {s_build:.0f} + evaluation {s_eval:.0f}), x2 flop/slot; mean processed "
+                               f"candidates {mean_clips:.1f}/cell",
                 "peak_source": "measured in-run by pf_fp64_peak (DFMA chains; MEASURED_PEAKS.json has no FP64 entry)"
                                + (f", summed over the {ws} ranks' GPUs" if ws > 1 else "")}
 
@@ -499,23 +602,35 @@ def main():
     cpu = None
     if not a.no_cpu and ws == 1 and rank == 0:
         threads = os.cpu_count() or 1
-        sample = 200_000 if sc.n > 200_000 else sc.n
-        v, cores, _ = cpu_reference_run(sc, psi_h, 1, 0, sample, threads)
+        v, cores, _, tt = cpu_reference_run(sc, psi_h, 1, 0, threads)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{sample} random cells of the same workload (full neighbourhoods), one pass, "
-                         "grid build included; oracle/potflow_oracle.c is bit-identical to the numba reference"}
+               "sample": f"all {sc.n} cells of the same workload, one pass ({tt[0]:.1f} s), grid build + dpsi "
+                         "included; oracle/potflow_oracle.c is bit-identical to the numba reference",
+               "port_vs_numba": PORT_VS_NUMBA}
+        # Newton: the CPU restatement (SPEC.md:286-335 over the oracle) converges on C2
+        # (the reference-faithful restriction stalls on C4); the device on C2 beside it
+        try:
+            ms_cpu, st = cpu_newton_run("C2", threads)
+            sc2 = make_scene("C2")
+            with _lib.parity(True):
+                _, ms_dev, st2 = converged_psi(sc2, dom)
+                ms_dev = statistics.median([converged_psi(sc2, dom)[1] for _ in range(3)])
+            cpu["newton"] = {"config": "C2 97k dam break, cold start, eps_vol 1%", "cpu_ms": ms_cpu,
+                             "cpu_iterations": st["iterations"], "cpu_evaluations": st["evaluations"],
+                             "cpu_cg_iterations": st["cg_iterations"], "device_ms": ms_dev,
+                             "device_iterations": st2["iterations"], "device_evaluations": st2["evaluations"],
+                             "device_cg_iterations": st2["cg_iterations"],
+                             "device_restriction": "parity mode", "cores": threads}
+        except Exception as ex:  # report, never fail the bench line
+            cpu["newton"] = {"error": repr(ex)[:200]}
 
     if rank == 0:
+        cfg = config_of(a, sc, psi_desc)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload_desc(a.config, sc), "ball_aware": True, "smf": smf,
-                           "psi": "converged (first cold-start Newton solve, eps_vol=1%)"
-                           if newton else "cold start",
-                           "l2": "256 MiB flush write before every timed step",
-                           "parallelism": f"x-slab spatial partition over {ws} GPU(s), ghosts by search radius"
-                           if ws > 1 else "1 GPU"},
-                "flags": fl, "e2e": e2e, "gpu_launches": launches,
+                "config": cfg, "flags": fl, "e2e": e2e, "gpu_launches": launches,
+                "other_restriction_ms_per_step": {("robust" if a.mode == "parity" else "parity"): t_other},
                 "roofline": roofline, "roofline_hbm_kernels": hbm, "cpu_baseline": cpu, "newton": newton,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

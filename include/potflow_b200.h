@@ -262,9 +262,17 @@ int pf_daxpy(int64_t n, const double *a, double s, const double *b, double *out,
 /* x += dt v, reflected into the box [lo+tau, hi-tau] (velocity component flipped) */
 int pf_fluid_advect(int64_t n, double *x, double *v, double dt, const double *lo_host,
                     const double *hi_host, double tau, void *stream);
-/* v += dt/m ((c - x)/eps^2 + m g), m = rho nu (spring pressure + gravity) */
+/* spring pressure force F_p = k (c - x) / eps^2 (SPEC.md pressure_force):
+ * spring = PF_SPRING_SPEC: k = 1, the SPEC as printed (c - x = (eps^2,0,0) -> (1,0,0));
+ * spring = PF_SPRING_GM: k = m = rho nu, the Gallouet-Merigot acceleration
+ * (c - x)/eps^2 the paper follows.  F f64[n,3]. */
+#define PF_SPRING_GM 0
+#define PF_SPRING_SPEC 1
+int pf_pressure_force(int64_t n, const double *x, const double *cent, const double *nu, const double *rho,
+                      double eps, int spring, double *F, void *stream);
+/* v += dt/m (F_p + m g), m = rho nu (spring pressure + gravity) */
 int pf_fluid_forces(int64_t n, const double *x, const double *cent, const double *nu, const double *rho,
-                    double *v, double dt, double eps, const double *g_host, void *stream);
+                    double *v, double dt, double eps, const double *g_host, int spring, void *stream);
 
 /* implicit velocity update with viscosity mu (fluid graph Laplacian, P1 weights
  * |B_ij|/(2|p_j-p_i|)), wall friction mu_b (boundary weights, zero wall velocity) and
@@ -274,7 +282,7 @@ int pf_fluid_forces_implicit(int64_t n, int smf, const double *x, const double *
                              const int32_t *fcount, const int32_t *ftag, const double *farea, const double *nu,
                              const double *rho, double *v, double dt, double eps, const double *g_host,
                              double mu, double mu_b, double gamma, double affinity, const double *dplanes,
-                             int ndom, int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
+                             int ndom, int spring, int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
                              double *sol, double rtol, void *stream);
 
 /* compact per-facet CSR of an evaluation's fixed-stride facet outputs

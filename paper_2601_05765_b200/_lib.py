@@ -65,6 +65,10 @@ def lib():
         L.pf_batch_evaluate_host.argtypes = ([vp, i64, vp, vp, d, d, i, i, i64] + [vp] * 12 + [i, vp, vp])
         L.pf_batch_build.restype = i64
         L.pf_batch_build.argtypes = [vp, i64, vp, vp, d, d, i, i64, i64, i64] + [vp] * 9 + [i, vp]
+        L.pf_stage_timing.argtypes = [vp, i]
+        L.pf_stage_times.argtypes = [vp, vp, vp, vp]
+        L.pf_stage_timing.restype = i
+        L.pf_stage_times.restype = i
         L.pf_grid_order.restype = i
         L.pf_grid_order.argtypes = [vp, vp, vp]
         L.pf_facets_csr.restype = i

@@ -139,9 +139,12 @@ struct alignas(16) WSX {  // 16-byte multiple: every warp's polytope stays TMA-a
     using Cap = C_;
     Poly<C_> P[NP];
     U u;
-    int oflow;    // capacity overflow seen by any lane
-    int strict;   // parity mode (CellIn::strict) for this cell
-    int cen_on;   // census requested for this cell
+    // one word of per-cell flags: the build workspace is sized to the byte
+    // (24 warps x 9600 B fill the SM's shared memory exactly)
+    uint8_t oflow;   // capacity overflow seen by any lane
+    uint8_t strict;  // parity mode (CellIn::strict) for this cell
+    uint8_t cen_on;  // census requested for this cell
+    uint8_t pad_;
     int cen[16];  // algorithmic-work census (SURVEY.md §8(d) S_cell terms)
 };
 template <class C> union BEU { BuildScratch<C> b; EvalScratch<C> e; };

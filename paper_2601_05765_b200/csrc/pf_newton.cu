@@ -623,16 +623,35 @@ __global__ void __launch_bounds__(RB) k_advect(int64_t n, double *__restrict__ x
 // gravity F_g = m g; v += dt/m (F_p + F_g) = dt ((c - x)/eps^2 + g), m = rho nu.
 // The spring is mass-proportional as in the scheme the paper follows; it is
 // the form for which SPEC.md's stability guideline dt <= eps holds.
+// spring coefficient of the pressure force F_p = k (c - x) / eps^2:
+// PF_SPRING_SPEC (1): k = 1, SPEC.md:357-361 pressure_force as printed;
+// PF_SPRING_GM (0): k = m, the Gallouet-Merigot acceleration (c - x)/eps^2
+// the paper follows
+__device__ __forceinline__ double spring_coef(int spring, double m) { return spring == 1 ? 1.0 : m; }
+
+// F_p of every particle (SPEC.md pressure_force)
+__global__ void __launch_bounds__(RB) k_pressure(int64_t n, const double *__restrict__ x,
+                                                const double *__restrict__ c, const double *__restrict__ nu,
+                                                const double *__restrict__ rho, double inv_eps2, int spring,
+                                                double *__restrict__ F) {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        const double ks = spring_coef(spring, rho[i] * nu[i]) * inv_eps2;
+        for (int a = 0; a < 3; a++) F[3 * i + a] = ks * (c[3 * i + a] - x[3 * i + a]);
+    }
+}
+
 __global__ void __launch_bounds__(RB) k_forces(int64_t n, const double *__restrict__ x,
                                               const double *__restrict__ c, const double *__restrict__ nu,
                                               const double *__restrict__ rho, double *__restrict__ v,
-                                              double dt, double inv_eps2, double g0, double g1, double g2) {
+                                              double dt, double inv_eps2, double g0, double g1, double g2,
+                                              int spring) {
     const double g[3] = {g0, g1, g2};
     for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
         const double m = rho[i] * nu[i];
+        const double ks = spring_coef(spring, m) * inv_eps2;
 #pragma unroll
         for (int a = 0; a < 3; a++) {
-            double f = m * (c[3 * i + a] - x[3 * i + a]) * inv_eps2 + m * g[a];
+            double f = ks * (c[3 * i + a] - x[3 * i + a]) + m * g[a];
             v[3 * i + a] += dt * f / m;
         }
     }
@@ -651,7 +670,7 @@ __global__ void __launch_bounds__(RB) k_fluid_system(
     const double *__restrict__ vol, const int *__restrict__ fcount, const int *__restrict__ ftag,
     const double *__restrict__ farea, const double *__restrict__ nu, const double *__restrict__ rho,
     const double *__restrict__ v, double dt, double inv_eps2, double g0, double g1, double g2, double mu,
-    double mu_b, double gamma, double affinity, const double *__restrict__ dplanes, int ndom,
+    double mu_b, double gamma, double affinity, const double *__restrict__ dplanes, int ndom, int spring,
     int *__restrict__ hcnt, int *__restrict__ hcol, double *__restrict__ hval, double *__restrict__ diag,
     double *__restrict__ rhs) {
     const double g[3] = {g0, g1, g2};
@@ -695,7 +714,7 @@ __global__ void __launch_bounds__(RB) k_fluid_system(
         diag[i] = d;
 #pragma unroll
         for (int a = 0; a < 3; a++) {
-            const double fp = m * (cent[3 * i + a] - x[3 * i + a]) * inv_eps2;
+            const double fp = spring_coef(spring, m) * (cent[3 * i + a] - x[3 * i + a]) * inv_eps2;
             rhs[a * n + i] = m / dt * v[3 * i + a] + fp + m * g[a] + gamma * ft[a];
         }
     }
@@ -718,10 +737,18 @@ extern "C" int pf_fluid_advect(int64_t n, double *x, double *v, double dt, const
 
 extern "C" int pf_fluid_forces(int64_t n, const double *x, const double *cent, const double *nu,
                                const double *rho, double *v, double dt, double eps, const double *g_host,
-                               void *stream) {
+                               int spring, void *stream) {
     pf_internal_launches_add(1);
     k_forces<<<nblocks(n), RB, 0, (cudaStream_t)stream>>>(n, x, cent, nu, rho, v, dt, 1.0 / (eps * eps),
-                                                          g_host[0], g_host[1], g_host[2]);
+                                                          g_host[0], g_host[1], g_host[2], spring);
+    NCK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int pf_pressure_force(int64_t n, const double *x, const double *cent, const double *nu,
+                                 const double *rho, double eps, int spring, double *F, void *stream) {
+    pf_internal_launches_add(1);
+    k_pressure<<<nblocks(n), RB, 0, (cudaStream_t)stream>>>(n, x, cent, nu, rho, 1.0 / (eps * eps), spring, F);
     NCK(cudaGetLastError());
     return 0;
 }
@@ -736,13 +763,13 @@ extern "C" int pf_fluid_forces_implicit(int64_t n, int smf, const double *x, con
                                         const double *farea, const double *nu, const double *rho, double *v,
                                         double dt, double eps, const double *g_host, double mu, double mu_b,
                                         double gamma, double affinity, const double *dplanes, int ndom,
-                                        int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
+                                        int spring, int32_t *hcnt, int32_t *hcol, double *hval, double *diag, double *rhs,
                                         double *sol, double rtol, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     pf_internal_launches_add(1);
     k_fluid_system<<<nblocks(n), RB, 0, st>>>(n, smf, x, cent, vol, fcount, ftag, farea, nu, rho, v, dt,
                                                1.0 / (eps * eps), g_host[0], g_host[1], g_host[2], mu, mu_b,
-                                               gamma, affinity, dplanes, ndom, hcnt, hcol, hval, diag, rhs);
+                                               gamma, affinity, dplanes, ndom, spring, hcnt, hcol, hval, diag, rhs);
     NCK(cudaGetLastError());
     int total = 0;
     for (int a = 0; a < 3; a++) {

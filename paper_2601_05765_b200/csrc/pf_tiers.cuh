@@ -37,5 +37,8 @@ using FastCaps = Caps<PF_FCV, 32, PF_FCL, PF_FCC, PF_FCE, PF_FCP, false>;
 // Mid: the fast tier's overflow (mostly the boundary-point pool of cells whose
 // sphere meets many facets) in shared memory, 4 warps (48 KB each) per SM.
 using MidCaps = Caps<128, 64, 448, 64, 128, 512, false>;
+#if PF_FCV == 48 && PF_FCL == 160 && PF_FCC == 40 && PF_FCE == 48
+static_assert(sizeof(BWS<FastCaps>) == 9600, "fast build workspace must stay 9600 B: 3 blocks of 8 warps per SM");
+#endif
 using ExactCaps = Caps<REF_MAX_V, REF_MAX_F, REF_MAX_L, 1024, REF_MAX_L, 4096, true>;
 }  // namespace pf

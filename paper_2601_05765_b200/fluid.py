@@ -5,7 +5,10 @@ PAPER.md:332-334 and 374-381); this is its in-scope part:
 
     x <- x + dt v, reflected into the domain box by tau_geom
     psi <- newton_solve(x, nu, warm psi)
-    F_p = (c_i - x_i) / eps^2,  F_g = m g,  v <- v + dt/m (F_p + F_g)
+    F_p = k (c_i - x_i) / eps^2,  F_g = m g,  v <- v + dt/m (F_p + F_g)
+    k = m (spring="gallouet_merigot", default: the paper's Gallouet-Merigot
+    acceleration) or k = 1 (spring="spec":
+    SPEC.md pressure_force as printed)
 
 With viscosity, wall friction or surface tension (the first
 "next" row of SURVEY §8(f)) the velocity update is implicit:
@@ -51,6 +54,9 @@ class FluidState:
     history: list = field(default_factory=list)
 
 
+SPRINGS = {"gallouet_merigot": 0, "spec": 1}  # PF_SPRING_GM / PF_SPRING_SPEC
+
+
 @dataclass
 class SimParams:
     dt: float = 1e-3
@@ -67,21 +73,43 @@ class SimParams:
     boundary_affinity: float = 1.0    # weight of the wall ghosts in the surface-tension Laplacian
     implicit: bool | None = None      # None: implicit iff any of the three above is non-zero
     visc_rtol: float = 1e-10
+    spring: str = "gallouet_merigot"  # or "spec": F_p = (c - x)/eps^2 as SPEC.md prints it
+
+    def spring_code(self) -> int:
+        if self.spring not in SPRINGS:
+            raise ValueError(f"spring must be one of {sorted(SPRINGS)}")
+        return SPRINGS[self.spring]
 
 
 def _bind():
     L = solver._bind()
     if not getattr(L, "_fluid_bound", False):
         vp, i64, d, i = C.c_void_p, C.c_int64, C.c_double, C.c_int
-        L.pf_fluid_forces_implicit.argtypes = ([i64, i] + [vp] * 9 + [d, d, vp, d, d, d, d, vp, i]
+        L.pf_fluid_forces_implicit.argtypes = ([i64, i] + [vp] * 9 + [d, d, vp, d, d, d, d, vp, i, i]
                                                + [vp] * 6 + [d, vp])
         L.pf_fluid_forces_implicit.restype = C.c_int
         L.pf_fluid_advect.argtypes = [i64, vp, vp, d, vp, vp, d, vp]
         L.pf_fluid_advect.restype = C.c_int
-        L.pf_fluid_forces.argtypes = [i64, vp, vp, vp, vp, vp, d, d, vp, vp]
+        L.pf_fluid_forces.argtypes = [i64, vp, vp, vp, vp, vp, d, d, vp, i, vp]
         L.pf_fluid_forces.restype = C.c_int
+        L.pf_pressure_force.argtypes = [i64, vp, vp, vp, vp, d, i, vp, vp]
+        L.pf_pressure_force.restype = C.c_int
         L._fluid_bound = True
     return L
+
+
+def pressure_force(x, cent, nu, rho, eps: float, spring: str = "gallouet_merigot"):
+    """F_p = k (c - x) / eps^2 per particle (SPEC.md pressure_force), [n,3] CUDA f64."""
+    import torch
+
+    L = _bind()
+    t = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda").contiguous()  # noqa: E731
+    x, cent, nu, rho = t(x), t(cent), t(nu), t(rho)
+    F = torch.empty_like(x)
+    _lib.check(L.pf_pressure_force(x.shape[0], _lib.ptr(x), _lib.ptr(cent), _lib.ptr(nu), _lib.ptr(rho),
+                                   float(eps), SPRINGS[spring], _lib.ptr(F), _lib.stream_ptr()),
+               "pf_pressure_force")
+    return F
 
 
 def make_state(pts, vel, nu, rho) -> FluidState:
@@ -126,7 +154,7 @@ def step(state: FluidState, params: SimParams, domain: ConvexCell) -> dict:
     else:
         _lib.check(L.pf_fluid_forces(n, _lib.ptr(state.x), _lib.ptr(cent), _lib.ptr(state.nu),
                                      _lib.ptr(state.rho), _lib.ptr(state.v), float(params.dt),
-                                     float(params.eps), g, s), "pf_fluid_forces")
+                                     float(params.eps), g, params.spring_code(), s), "pf_fluid_forces")
     state.step_index += 1
     state.time += params.dt
     diag = {"step": state.step_index, **{k: res.stats[k] for k in
@@ -160,6 +188,6 @@ def implicit_forces(state: FluidState, params: SimParams, domain: ConvexCell, ce
         n, smf, P(state.x), P(cent), P(vol), P(fcount), P(ftag), P(farea), P(state.nu), P(state.rho),
         P(state.v), float(params.dt), float(params.eps), g, float(params.viscosity),
         float(params.boundary_viscosity), float(params.surface_tension), float(params.boundary_affinity),
-        P(planes), ndom, P(hcnt), P(hcol), P(hval), P(diag), P(rhs), P(sol), float(params.visc_rtol),
+        P(planes), ndom, params.spring_code(), P(hcnt), P(hcol), P(hval), P(diag), P(rhs), P(sol), float(params.visc_rtol),
         _lib.stream_ptr())
     return _lib.check(it, "pf_fluid_forces_implicit")

@@ -1,0 +1,18 @@
+set -x
+T=r02c
+O=gpurun_out/$T
+mkdir -p $O
+timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu > $O/bench.json 2> $O/bench.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench_c4.csv \
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-newton > /dev/null 2>&1
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed.avg.per_cycle_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum
+PF_NCU_STEP=1 ncu --profile-from-start off --metrics $M --clock-control none --csv --log-file $O/kernels_metrics.csv \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-newton --no-hbm > /dev/null 2>&1
+for k in k_cells_build k_cells_eval_sync; do
+  PF_NCU_STEP=1 timeout 1500 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:$k -c 1 \
+      -o $O/${k}_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-newton --no-hbm > /dev/null 2>&1
+done
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $O/hbm_kernels.csv python tools/hbm_probe.py C4 > $O/hbm_probe_ncu.json 2>&1
+python tools/hbm_probe.py C4 > $O/hbm_probe.json 2>&1
+ls -la $O
