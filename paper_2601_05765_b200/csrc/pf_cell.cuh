@@ -293,7 +293,12 @@ PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
 // ---------------------------------------------------------------------------
 template <class W>
 PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B, int wa, double nx,
-                  double ny, double nz, double dd, int tag, double tol) {
+                  double ny, double nz, double dd, int tag, double tol, double px, double py, double pz,
+                  double *rfar2) {
+    // *rfar2 (on CLIP_CUT): max_v |v - p|^2 over B's vertices, from the kept and
+    // the new vertices as they are produced (the reference's rfar pass,
+    // _kernels.py:1341-1354, same terms and order per vertex; -1 when a dropped
+    // vertex makes a full pass necessary)
     using C = typename W::Cap;
     BuildScratch<C> &S = ws->u.b;
     const uint8_t *lfa = S.lf[wa];
@@ -309,6 +314,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
     int K = 0;
     double s_reg = 0.0;
     int vmap_reg = 0xffff;
+    double rmax = 0.0;  // this lane's share of max |v - p|^2 over B's vertices
     if (nv <= 32) {
         const int v = L;
         if (v < nv) {
@@ -322,7 +328,9 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         const unsigned m = pfw::ballot(keep);
         if (keep) {
             vmap_reg = pfw::popc(m & lt);
-            B.x[vmap_reg] = A.x[v]; B.y[vmap_reg] = A.y[v]; B.z[vmap_reg] = A.z[v];
+            const double ax = A.x[v], ay = A.y[v], az = A.z[v];
+            B.x[vmap_reg] = ax; B.y[vmap_reg] = ay; B.z[vmap_reg] = az;
+            rmax = sq(ax - px) + sq(ay - py) + sq(az - pz);
         }
         if (v < nv) S.vmap[v] = (uint16_t)vmap_reg;
         K = pfw::popc(m);
@@ -350,7 +358,10 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
             if (keep) {
                 int idx = K + pfw::popc(m & lt);
                 S.vmap[v] = (uint16_t)idx;
-                B.x[idx] = A.x[v]; B.y[idx] = A.y[v]; B.z[idx] = A.z[v];
+                const double ax = A.x[v], ay = A.y[v], az = A.z[v];
+                B.x[idx] = ax; B.y[idx] = ay; B.z[idx] = az;
+                const double d2 = sq(ax - px) + sq(ay - py) + sq(az - pz);
+                if (d2 > rmax) rmax = d2;
             } else if (v < nv) {
                 S.vmap[v] = 0xffff;
             }
@@ -453,9 +464,12 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
             if (id < C::CV) {
                 double sa = S.sd[a], sb = S.sd[b];
                 double t = sa / (sa - sb);
-                B.x[id] = A.x[a] + t * (A.x[b] - A.x[a]);
-                B.y[id] = A.y[a] + t * (A.y[b] - A.y[a]);
-                B.z[id] = A.z[a] + t * (A.z[b] - A.z[a]);
+                const double nxv = A.x[a] + t * (A.x[b] - A.x[a]);
+                const double nyv = A.y[a] + t * (A.y[b] - A.y[a]);
+                const double nzv = A.z[a] + t * (A.z[b] - A.z[a]);
+                B.x[id] = nxv; B.y[id] = nyv; B.z[id] = nzv;
+                const double d2 = sq(nxv - px) + sq(nyv - py) + sq(nzv - pz);
+                if (d2 > rmax) rmax = d2;
             }
         }
         NFirst += pfw::popc(m);
@@ -605,6 +619,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
     // 5. drop unreferenced vertices (_kernels.py:297-315).  A kept vertex can
     // only lose all its facets if some dropped facet emitted 1-2 entries.
     if (!small_facet) {
+        *rfar2 = pfw::max_d_inl(rmax);
         if (L == 0) {
             B.nv = NVB; B.nf = NF2; B.nl = NL2;
             if (ws->cen_on) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += NVB; }
@@ -643,6 +658,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         for (int k = L; k < NL2; k += 32) B.lv[k] = (uint16_t)(S.vmap[B.lv[k]] - 2);
         nref = base;
     }
+    *rfar2 = -1.0;
     if (L == 0) {
         B.nv = nref; B.nf = NF2; B.nl = NL2;
         if (ws->cen_on) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += nref; }
@@ -920,6 +936,9 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
         for (int c = pfw::lane(); c < nc; c += 32) {
             const double D2 = S.cd2[c];
             const double D = sqrt(D2);
+            // the serial loop below needs only D (its stop test, _kernels.py:1309)
+            // and whether the site is coincident: D replaces D^2, -1 marks it
+            S.cd2[c] = D2 <= tol * tol ? -1.0 : D;
             if (D2 <= tol * tol) continue;
             const int sl = S.cord[c];
             const double psij = S.cw[sl];
@@ -938,13 +957,13 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
             // candidate c into registers; the warp syncs before any lane acts on
             // it (a lane that runs ahead must not overwrite the shared scratch
             // -- next shell's gather, evaluation workspace -- under a slower lane)
-            const double D2 = S.cd2[c];
+            const double Dc = S.cd2[c];  // sqrt(d^2), or -1 for a coincident site
             const int j = S.cj[c];
             const int sl = S.cord[c];
             const double nxc = S.cx[sl], nyc = S.cy[sl], nzc = S.cz[sl], ddc = S.cw[sl];
             pfw::sync();
-            if (sqrt(D2) >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
-            if (D2 <= tol * tol) {
+            if (Dc >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
+            if (Dc < 0.0) {
                 const double psij = ddc;  // coincident site: the slot kept its weight
                 if (psij > psii || (psij == psii && j < i)) { *which_out = which; *nclips = ncl; return 1; }
                 continue;
@@ -959,12 +978,13 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
                 if (ws->cen_on && pfw::lane() == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += ws->P[which].nv; }
                 continue;
             }
-            int st = clip(ws, ws->P[which], ws->P[1 - which], which, nxc, nyc, nzc, ddc, j, tol);
+            double rfar2;
+            int st = clip(ws, ws->P[which], ws->P[1 - which], which, nxc, nyc, nzc, ddc, j, tol, px, py, pz, &rfar2);
             if (st == CLIP_EMPTY) { *which_out = which; *nclips = ncl; return 1; }
             if (st == CLIP_OVERFLOW) { *which_out = which; *nclips = ncl; return 3; }
             if (st == CLIP_CUT) {
                 which = 1 - which;
-                rfar = poly_rfar(ws->P[which], px, py, pz);
+                rfar = rfar2 >= 0.0 ? sqrt(rfar2) : poly_rfar(ws->P[which], px, py, pz);
                 stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
                 if (ball_aware && br < stop_r) stop_r = br;
             }

@@ -12,6 +12,8 @@
 // (row = cell, stride smf, int32 columns, f64 values); assembly compacts each
 // row to its site facets.  All reductions are two-level with a fixed block
 // count, so every number is bitwise reproducible run to run.
+#include <cooperative_groups.h>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -276,6 +278,243 @@ __global__ void __launch_bounds__(RB) k_pdir(int64_t n, const double *__restrict
         p[i] = z[i] + beta * p[i];
 }
 
+// ---- Jacobi-PCG as ONE cooperative persistent kernel ----------------------
+// Every block owns a contiguous range of rows; per iteration three grid-wide
+// barriers: after the SpMV (p.Ap), after the update (r.z, r.r), after the new
+// search direction.  Every block reduces the per-block partials itself in one
+// fixed order, so all blocks take the same (bitwise reproducible) decisions
+// and the host is not involved until the solve ends.  z = D^-1 r is never
+// stored (recomputed from r, diag: the same bits).  Bytes per row and
+// iteration: ELL row (12 per entry) + hcnt + 5 vector reads + 2 writes in
+// the SpMV/update + 3 reads and 1 write for the direction.
+// ELL (stride smf, hcnt used slots) -> CSR (row_ptr, col, val) for the iterations
+__global__ void k_csr_total(int64_t n, const int *__restrict__ hcnt, int *__restrict__ rp) {
+    rp[n] = rp[n - 1] + hcnt[n - 1];
+}
+__global__ void __launch_bounds__(RB) k_csr_fill(int64_t n, int smf, const int *__restrict__ hcnt,
+                                                const int *__restrict__ hcol, const double *__restrict__ hval,
+                                                const int *__restrict__ rp, int *__restrict__ ccol,
+                                                double *__restrict__ cval) {
+    // 4 lanes per row, many rows in flight (the copy is latency-bound)
+    const int sub = threadIdx.x & 3;
+    for (int64_t i = (blockIdx.x * (int64_t)RB + threadIdx.x) >> 2; i < n; i += ((int64_t)gridDim.x * RB) >> 2) {
+        const int c = hcnt[i], o = rp[i];
+        for (int k = sub; k < c; k += 4) {
+            ccol[o + k] = hcol[i * smf + k];
+            cval[o + k] = hval[i * smf + k];
+        }
+    }
+}
+constexpr int CG_T = 1024;
+__device__ __forceinline__ void all_reduce2(const double *__restrict__ part, int G, double *a_out,
+                                            double *b_out, double *sh) {
+    // fixed order: lane l sums part[l], part[l+32], ...; then a fixed shuffle tree
+    if (threadIdx.x < 32) {
+        double a = 0.0, b = 0.0;
+        for (int k = threadIdx.x; k < G; k += 32) { a += part[k]; b += part[G + k]; }
+        for (int m = 16; m > 0; m >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, m);
+            b += __shfl_xor_sync(0xffffffffu, b, m);
+        }
+        if (threadIdx.x == 0) { sh[0] = a; sh[1] = b; }
+    }
+    __syncthreads();
+    *a_out = sh[0];
+    *b_out = sh[1];
+    __syncthreads();
+}
+__device__ __forceinline__ double block_sum_all(double v, double *sh) {
+    // block sum with the result in every thread (fixed tree)
+    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        double s = l < (int)(blockDim.x >> 5) ? sh[l] : 0.0;
+        for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+        if (l == 0) sh[32] = s;
+    }
+    __syncthreads();
+    const double r = sh[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(CG_T, 1)
+    k_pcg_coop(int64_t n, int smf, const int *__restrict__ hcnt, const int *__restrict__ hcol,
+               const double *__restrict__ hval, const double *__restrict__ diag, const double *__restrict__ b,
+               double *__restrict__ x, double *__restrict__ r, double *__restrict__ p, double *__restrict__ Ap,
+               double *__restrict__ partA, double *__restrict__ partB, double rtol, int max_iter,
+               int *__restrict__ out_it, const int *__restrict__ rp) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[40];
+    const int G = gridDim.x;
+    const int64_t R = (n + G - 1) / G;
+    const int64_t lo = blockIdx.x * R, hi = lo + R < n ? lo + R : n;
+    // init: x = 0, r = b, p = z = D^-1 b
+    double rz_p = 0.0, bb_p = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
+        const double bi = b[i], zi = bi / diag[i];
+        x[i] = 0.0; r[i] = bi; p[i] = zi;
+        rz_p += bi * zi;
+        bb_p += bi * bi;
+    }
+    rz_p = block_sum_all(rz_p, sh);
+    bb_p = block_sum_all(bb_p, sh);
+    if (threadIdx.x == 0) { partB[blockIdx.x] = rz_p; partB[G + blockIdx.x] = bb_p; }
+    grid.sync();
+    double rz, bb;
+    all_reduce2(partB, G, &rz, &bb, sh);
+    int it = 0;
+    if (bb > 0.0) {
+        const int sub = threadIdx.x & 3;
+        for (;;) {
+            // A: Ap = H p on the block's rows (4 lanes per row), partial p.Ap
+            double pap = 0.0;
+            for (int64_t i0 = lo; i0 < hi; i0 += CG_T / 4) {
+                const int64_t i = i0 + (threadIdx.x >> 2);
+                double s = 0.0;
+                const bool row = i < hi;
+                if (row) {  // CSR row [rp[i], rp[i+1]): contiguous, no ELL padding fetched
+                    const int k0 = rp[i], k1 = rp[i + 1];
+#pragma unroll 4
+                    for (int k = k0 + sub; k < k1; k += 4) s += hval[k] * p[hcol[k]];
+                }
+                s += __shfl_xor_sync(0xffffffffu, s, 1);
+                s += __shfl_xor_sync(0xffffffffu, s, 2);
+                if (row && sub == 0) {
+                    const double pi = p[i];
+                    s += diag[i] * pi;
+                    Ap[i] = s;
+                    pap += pi * s;
+                }
+            }
+            pap = block_sum_all(pap, sh);
+            if (threadIdx.x == 0) { partA[blockIdx.x] = pap; partA[G + blockIdx.x] = 0.0; }
+            grid.sync();
+            double pAp, dummy;
+            all_reduce2(partA, G, &pAp, &dummy, sh);
+            const double alpha = pAp != 0.0 ? rz / pAp : 0.0;
+            // B: x += alpha p, r -= alpha Ap, partial r.z (z = r / diag) and r.r
+            double rzn = 0.0, rr = 0.0;
+            for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
+                const double ri = r[i] - alpha * Ap[i];
+                x[i] = x[i] + alpha * p[i];
+                r[i] = ri;
+                const double zi = ri / diag[i];
+                rzn += ri * zi;
+                rr += ri * ri;
+            }
+            rzn = block_sum_all(rzn, sh);
+            rr = block_sum_all(rr, sh);
+            if (threadIdx.x == 0) { partB[blockIdx.x] = rzn; partB[G + blockIdx.x] = rr; }
+            grid.sync();
+            double rz_new, rr_all;
+            all_reduce2(partB, G, &rz_new, &rr_all, sh);
+            const double beta = rz != 0.0 ? rz_new / rz : 0.0;
+            rz = rz_new;
+            it++;
+            if (sqrt(rr_all) <= rtol * sqrt(bb) || it >= max_iter || !(rz_new == rz_new)) break;
+            // C: p = z + beta p
+            for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) p[i] = r[i] / diag[i] + beta * p[i];
+            grid.sync();
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *out_it = it;
+}
+
+// Same iteration with two barriers: the new search direction p = z + beta p
+// is formed where it is consumed -- by the SpMV, for its own rows and for
+// every gathered column (r, diag and the previous p are gathered instead of
+// p alone) -- and written to the other of two p buffers.  Bitwise the same
+// numbers as k_pcg_coop (same formula per entry).
+__global__ void __launch_bounds__(CG_T, 1)
+    k_pcg_coop2(int64_t n, const double *__restrict__ hval, const int *__restrict__ hcol,
+                const int *__restrict__ rp, const double *__restrict__ diag, const double *__restrict__ b,
+                double *__restrict__ x, double *__restrict__ r, double *__restrict__ pa, double *__restrict__ pb,
+                double *__restrict__ Ap, double *__restrict__ partA, double *__restrict__ partB, double rtol,
+                int max_iter, int *__restrict__ out_it) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[40];
+    const int G = gridDim.x;
+    const int64_t R = (n + G - 1) / G;
+    const int64_t lo = blockIdx.x * R, hi = lo + R < n ? lo + R : n;
+    double rz_p = 0.0, bb_p = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
+        const double bi = b[i], zi = bi / diag[i];
+        x[i] = 0.0; r[i] = bi; pa[i] = 0.0;
+        rz_p += bi * zi;
+        bb_p += bi * bi;
+    }
+    rz_p = block_sum_all(rz_p, sh);
+    bb_p = block_sum_all(bb_p, sh);
+    if (threadIdx.x == 0) { partB[blockIdx.x] = rz_p; partB[G + blockIdx.x] = bb_p; }
+    grid.sync();
+    double rz, bb;
+    all_reduce2(partB, G, &rz, &bb, sh);
+    int it = 0;
+    double beta = 0.0;  // p_0 = z_0 = z_0 + 0 * (p = 0)
+    double *pold = pa, *pnew = pb;
+    if (bb > 0.0) {
+        const int sub = threadIdx.x & 3;
+        for (;;) {
+            double pap = 0.0;
+            for (int64_t i0 = lo; i0 < hi; i0 += CG_T / 4) {
+                const int64_t i = i0 + (threadIdx.x >> 2);
+                double s = 0.0;
+                const bool row = i < hi;
+                if (row) {
+                    const int k0 = rp[i], k1 = rp[i + 1];
+#pragma unroll 4
+                    for (int k = k0 + sub; k < k1; k += 4) {
+                        const int j = hcol[k];
+                        s += hval[k] * (r[j] / diag[j] + beta * pold[j]);
+                    }
+                }
+                s += __shfl_xor_sync(0xffffffffu, s, 1);
+                s += __shfl_xor_sync(0xffffffffu, s, 2);
+                if (row && sub == 0) {
+                    const double di = diag[i];
+                    const double pi = r[i] / di + beta * pold[i];
+                    pnew[i] = pi;
+                    s += di * pi;
+                    Ap[i] = s;
+                    pap += pi * s;
+                }
+            }
+            pap = block_sum_all(pap, sh);
+            if (threadIdx.x == 0) { partA[blockIdx.x] = pap; partA[G + blockIdx.x] = 0.0; }
+            grid.sync();
+            double pAp, dummy;
+            all_reduce2(partA, G, &pAp, &dummy, sh);
+            const double alpha = pAp != 0.0 ? rz / pAp : 0.0;
+            double rzn = 0.0, rr = 0.0;
+            for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
+                const double ri = r[i] - alpha * Ap[i];
+                x[i] = x[i] + alpha * pnew[i];
+                r[i] = ri;
+                const double zi = ri / diag[i];
+                rzn += ri * zi;
+                rr += ri * ri;
+            }
+            rzn = block_sum_all(rzn, sh);
+            rr = block_sum_all(rr, sh);
+            if (threadIdx.x == 0) { partB[blockIdx.x] = rzn; partB[G + blockIdx.x] = rr; }
+            grid.sync();
+            double rz_new, rr_all;
+            all_reduce2(partB, G, &rz_new, &rr_all, sh);
+            beta = rz != 0.0 ? rz_new / rz : 0.0;
+            rz = rz_new;
+            it++;
+            if (sqrt(rr_all) <= rtol * sqrt(bb) || it >= max_iter || !(rz_new == rz_new)) break;
+            double *t = pold; pold = pnew; pnew = t;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *out_it = it;
+}
+
 __global__ void __launch_bounds__(RB) k_axpy_to(int64_t n, const double *__restrict__ a, double s,
                                                const double *__restrict__ b, double *__restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
@@ -357,7 +596,7 @@ int ws_alloc(int64_t n, int smf) {
     rc |= dalloc(&w.farea_t, &w.c[14], E); rc |= dalloc(&w.hcnt, &w.c[15], N);
     rc |= dalloc(&w.hcol, &w.c[16], E); rc |= dalloc(&w.fcount, &w.c[17], N); rc |= dalloc(&w.ftag, &w.c[18], E);
     rc |= dalloc(&w.fcount_t, &w.c[19], N); rc |= dalloc(&w.ftag_t, &w.c[20], E);
-    rc |= dalloc(&w.part, &w.c[21], 3 * NPART); rc |= dalloc(&w.sc, &w.c[22], 16);
+    rc |= dalloc(&w.part, &w.c[21], 4 * NPART); rc |= dalloc(&w.sc, &w.c[22], 16);
     rc |= dalloc(&w.red, &w.c[23], 16);
     rc |= dalloc(&w.cent, &w.ccap[0], 3 * N); rc |= dalloc(&w.cent_t, &w.ccap[1], 3 * N);
     if (!w.ic) NCK(cudaMalloc(&w.ic, 4 * sizeof(int)));
@@ -434,32 +673,73 @@ int pf_pcg(int64_t n, int smf, const int32_t *hcnt, const int32_t *hcol, const d
     cudaStream_t st = (cudaStream_t)stream;
     if (ws_alloc(n, smf)) return -1;
     NewtonWS &w = g_ws;
-    int nb = nblocks(n);
-    NCK(cudaMemsetAsync(w.ic, 0, 4 * sizeof(int), st));
-    pf_internal_launches_add(2);
-    k_pcg_init<<<nb, RB, 0, st>>>(n, b, diag, x, w.r, w.z, w.p, w.part);
-    k_sum2<<<1, 1024, 0, st>>>(w.part, nb, w.sc + 0, w.sc + 5);
-    int host_ic[2] = {0, 0};
-    double bb = 0.0;
-    NCK(cudaMemcpyAsync(&bb, w.sc + 5, sizeof(double), cudaMemcpyDeviceToHost, st));
-    NCK(cudaStreamSynchronize(st));
-    if (!(bb > 0.0)) return 0;
-    const int batch = 8;
-    while (true) {
-        for (int t = 0; t < batch; t++) {
-            pf_internal_launches_add(5);
-            k_spmv<<<nb, SPMV_T, 0, st>>>(n, smf, hcnt, hcol, hval, diag, w.p, w.Ap, w.part, w.ic);
-            k_alpha<<<1, 1024, 0, st>>>(w.part, nb, w.sc, w.ic);
-            k_update<<<nb, RB, 0, st>>>(n, diag, x, w.r, w.z, w.p, w.Ap, w.sc, w.part, w.ic);
-            k_beta<<<1, 1024, 0, st>>>(w.part, nb, w.sc, w.ic, rtol, max_iter);
-            k_pdir<<<nb, RB, 0, st>>>(n, w.z, w.p, w.sc, w.ic);
-        }
-        NCK(cudaMemcpyAsync(host_ic, w.ic, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-        NCK(cudaStreamSynchronize(st));
-        if (host_ic[0]) break;
+    if (n <= 0) return 0;
+    static int coop_blocks = 0;
+    if (!coop_blocks) {
+        int dev = 0, nsm = 0, per = 0;
+        NCK(cudaGetDevice(&dev));
+        NCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        NCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_coop, CG_T, 0));
+        coop_blocks = nsm * std::max(1, std::min(per, 2));
     }
-    NCK(cudaGetLastError());
-    return host_ic[1];
+    // CSR copy of the matrix (12 B per entry: the ELL rows' padding would be
+    // fetched with every iteration's SpMV)
+    static int *rp = nullptr, *ccol = nullptr;
+    static double *cval = nullptr;
+    static size_t rp_c = 0, ce_c = 0;
+    static void *cub_tmp = nullptr;
+    static size_t cub_c = 0;
+    if (dalloc(&rp, &rp_c, (size_t)n + 1)) return -1;
+    {
+        size_t need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, hcnt, rp, (int)n + 1, st);
+        if (need > cub_c) {
+            if (cub_tmp) cudaFree(cub_tmp);
+            NCK(cudaMalloc(&cub_tmp, need));
+            cub_c = need;
+        }
+        // rp[n] = sum of hcnt[0..n): scan n+1 entries of hcnt with a zero appended
+        NCK(cudaMemsetAsync(rp + n, 0, sizeof(int), st));
+        NCK(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_c, hcnt, rp, (int)n, st));
+        pf_internal_launches_add(2);
+        k_csr_total<<<1, 1, 0, st>>>(n, hcnt, rp);
+    }
+    int nnz = 0;
+    NCK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NCK(cudaStreamSynchronize(st));
+    if (dalloc(&ccol, &ce_c, (size_t)nnz + 1)) return -1;
+    {
+        static size_t cv_c = 0;
+        if (dalloc(&cval, &cv_c, (size_t)nnz + 1)) return -1;
+    }
+    pf_internal_launches_add(1);
+    k_csr_fill<<<(int)std::min<int64_t>((n + 63) / 64, 148 * 64), RB, 0, st>>>(n, smf, hcnt, hcol, hval, rp, ccol, cval);
+    int G = (int)std::min<int64_t>(coop_blocks, (n + CG_T / 4 - 1) / (CG_T / 4));
+    if (G > NPART) G = NPART;
+    int64_t nn = n;
+    int smf_ = smf, mi = max_iter;
+    double rt = rtol;
+    double *partA = w.part, *partB = w.part + 2 * NPART;  // part holds 4 * NPART
+    void *args[] = {&nn, &smf_, (void *)&hcnt, (void *)&ccol, (void *)&cval, (void *)&diag, (void *)&b, &x, &w.r,
+                    &w.p, &w.Ap, &partA, &partB, &rt, &mi, &w.ic, (void *)&rp};
+    pf_internal_launches_add(1);
+    static int fused = -1;
+    if (fused < 0) {
+        const char *e = getenv("PF_CG_FUSED");
+        fused = e ? atoi(e) : 1;
+    }
+    if (fused) {
+        double *pb = w.z;  // the second direction buffer (z is never stored)
+        void *args2[] = {&nn, (void *)&cval, (void *)&ccol, (void *)&rp, (void *)&diag, (void *)&b, &x, &w.r,
+                         &w.p, &pb, &w.Ap, &partA, &partB, &rt, &mi, &w.ic};
+        NCK(cudaLaunchCooperativeKernel((const void *)k_pcg_coop2, G, CG_T, args2, 0, st));
+    } else {
+        NCK(cudaLaunchCooperativeKernel((const void *)k_pcg_coop, G, CG_T, args, 0, st));
+    }
+    int it = 0;
+    NCK(cudaMemcpyAsync(&it, w.ic, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NCK(cudaStreamSynchronize(st));
+    return it;
 }
 
 }  // extern "C"

@@ -548,6 +548,91 @@ __global__ void __launch_bounds__(EXACT_WARPS * 32)
     }
 }
 
+// kNN with a shared-memory workspace (k <= 64): warp per query, 8 warps per
+// block, all SMs busy; the query's shells are gathered and (d^2, j)-sorted as
+// in the cell build.  k > 64 (or a shell of > 64 candidates tied at one
+// distance) falls back to k_knn's reference-capacity workspace.
+using KnnCaps = Caps<8, 8, 8, 64, 8, 8, false>;
+using KnnWS = BWS<KnnCaps>;
+constexpr int KNN_WARPS = 8;
+__global__ void __launch_bounds__(KNN_WARPS * 32)
+    k_knn_fast(CellIn in, int64_t nq, const double *__restrict__ q, int k, double t0,
+               int64_t *__restrict__ out_idx, int *__restrict__ fallback, int *__restrict__ nfall) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    KnnWS *ws = (KnnWS *)(smem + (size_t)wid * sizeof(KnnWS));
+    const int64_t nw = (int64_t)gridDim.x * KNN_WARPS;
+    for (int64_t t = blockIdx.x * (int64_t)KNN_WARPS + wid; t < nq; t += nw) {
+        const double qx = q[3 * t], qy = q[3 * t + 1], qz = q[3 * t + 2];
+        double tlo = -1.0, thi = t0;
+        int got = 0;
+        bool fail = false;
+        for (;;) {
+            bool all = false;
+            const int nc = gather_shell<true>(ws, in, -1, qx, qy, qz, tlo, thi, &all);
+            if (nc > KnnCaps::CC) {
+                const double base = tlo > 0.0 ? tlo : 0.0;
+                const double nt = base + (thi - base) * 0.25;
+                if (!(nt > base) || !(nt < thi)) { fail = true; break; }
+                thi = nt;
+                continue;
+            }
+            sort_candidates(ws, nc);
+            const int take = nc < k - got ? nc : k - got;
+            for (int c = lane; c < take; c += 32) out_idx[t * k + got + c] = ws->u.b.cj[c];
+            got += take;
+            __syncwarp();
+            if (got >= k || all) break;
+            tlo = thi;
+            thi = thi * 4.0;
+        }
+        if (fail && lane == 0) fallback[atomicAdd(nfall, 1)] = (int)t;
+        if (!fail && got < k)
+            for (int c = got + lane; c < k; c += 32) out_idx[t * k + c] = -1;
+        __syncwarp();
+    }
+}
+
+// queries that overflowed the fast kNN workspace, with the exact-tier workspace
+__global__ void __launch_bounds__(EXACT_WARPS * 32)
+    k_knn_list(CellIn in, const int *__restrict__ list, const int *__restrict__ nlist, const double *__restrict__ q,
+               int k, double t0, WS<ExactCaps> *__restrict__ wsbase, int64_t *__restrict__ out_idx) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WS<ExactCaps> *ws = wsbase + (size_t)blockIdx.x * EXACT_WARPS + wid;
+    const int nw = gridDim.x * EXACT_WARPS;
+    for (int u = blockIdx.x * EXACT_WARPS + wid; u < *nlist; u += nw) {
+        const int64_t t = list[u];
+        const double qx = q[3 * t], qy = q[3 * t + 1], qz = q[3 * t + 2];
+        double tlo = -1.0, thi = t0;
+        int got = 0;
+        for (;;) {
+            bool all = false;
+            int nc = gather_shell<true>(ws, in, -1, qx, qy, qz, tlo, thi, &all);
+            if (nc > ExactCaps::CC) {
+                double base = tlo > 0.0 ? tlo : 0.0;
+                double nt = base + (thi - base) * 0.25;
+                if (!(nt > base) || !(nt < thi)) {
+                    for (int c = got + lane; c < k; c += 32) out_idx[t * k + c] = -1;
+                    break;
+                }
+                thi = nt;
+                continue;
+            }
+            sort_candidates(ws, nc);
+            int take = nc < k - got ? nc : k - got;
+            for (int c = lane; c < take; c += 32) out_idx[t * k + got + c] = ws->u.b.cj[c];
+            got += take;
+            __syncwarp();
+            if (got >= k || all) {
+                for (int c = got + lane; c < k; c += 32) out_idx[t * k + c] = -1;
+                break;
+            }
+            tlo = thi;
+            thi = thi * 4.0;
+        }
+    }
+}
+
 void fill_cellin(pf_ctx *c, CellIn &in, int64_t n, const double *pts, const double *psi, double tol,
                  double dpsi, int ball_aware, int want_m2) {
     memset(&in, 0, sizeof in);
@@ -1272,9 +1357,28 @@ int64_t pf_knn(pf_ctx *c, int64_t n, const double *pts, int64_t nq, const double
     fill_cellin(c, in, n, pts, nullptr, c->tol, 0.0, 1, 0);
     double h = std::max(c->gh[0], std::max(c->gh[1], c->gh[2]));
     double r0 = h * std::cbrt((double)k);
-    g_launches++;
-    k_knn<<<c->exact_warps / EXACT_WARPS, EXACT_WARPS * 32, 0, st>>>(in, nq, queries, (int)k, r0 * r0,
-                                                                   c->exact_ws, out_idx);
+    if (k > KnnCaps::CC) {
+        g_launches++;
+        k_knn<<<c->exact_warps / EXACT_WARPS, EXACT_WARPS * 32, 0, st>>>(in, nq, queries, (int)k, r0 * r0,
+                                                                       c->exact_ws, out_idx);
+    } else {
+        static int knn_blocks = 0;
+        const int smem = (int)(KNN_WARPS * sizeof(KnnWS));
+        if (!knn_blocks) {
+            CK(cudaFuncSetAttribute(k_knn_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            int per = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_knn_fast, KNN_WARPS * 32, smem));
+            knn_blocks = c->nsm * std::max(per, 1);
+        }
+        if (ensure(&c->retry_list, &c->retry_cap, (size_t)nq + 1)) return -1;
+        CK(cudaMemsetAsync(c->counters + 2, 0, sizeof(int), st));
+        const int64_t want = (nq + KNN_WARPS - 1) / KNN_WARPS;
+        g_launches += 2;
+        k_knn_fast<<<(int)std::min<int64_t>(knn_blocks, want), KNN_WARPS * 32, smem, st>>>(
+            in, nq, queries, (int)k, r0 * r0, out_idx, c->retry_list, c->counters + 2);
+        k_knn_list<<<c->exact_warps / EXACT_WARPS, EXACT_WARPS * 32, 0, st>>>(
+            in, c->retry_list, c->counters + 2, queries, (int)k, r0 * r0, c->exact_ws, out_idx);
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return k;
