@@ -381,31 +381,34 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
     #pragma unroll 1
     for (int k0 = 0; k0 < nl; k0 += 32) {
         const int k = k0 + L;
-        int cr = 0, em = 0, f = 0, a = 0, b = 0;
+        bool ina = false, cr = false;
+        int f = 0, a = 0, b = 0;
         if (k < nl) {
             f = lfa[k];
             const int kn = k + 1 == A.lp[f + 1] ? A.lp[f] : k + 1;
             a = A.lv[k];
             b = A.lv[kn];
             const double sa = S.sd[a], sb = S.sd[b];
-            const bool ina = sa <= tol, inb = sb <= tol;
-            const bool c = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
-            S.ecls[k] = (uint8_t)((ina ? 1 : 0) | (c ? 2 : 0));
-            cr = c ? 1 : 0;
-            em = (ina ? 1 : 0) + cr;
+            const bool inb = sb <= tol;
+            ina = sa <= tol;
+            cr = ina ? (!inb && sa < -tol) : (inb && sb < -tol);
+            S.ecls[k] = (uint8_t)((ina ? 1 : 0) | (cr ? 2 : 0));
         }
-        int tot;
-        const int pk = pfw::excl_scan_inl((em << 16) | cr, L, &tot);
+        // both prefix counts from two ballots (an entry emits its inside tail
+        // vertex and/or its crossing vertex)
+        const unsigned mi = pfw::ballot(ina), mc = pfw::ballot(cr);
         if (k < nl) {
-            const int pcr = NE + (pk & 0xffff), pem = NEm + (pk >> 16);
+            const int pc = pfw::popc(mc & lt);
+            const int pcr = NE + pc, pem = NEm + pfw::popc(mi & lt) + pc;
             if (cr && pcr < C::CE) { S.ea[pcr] = (uint16_t)a; S.eb[pcr] = (uint16_t)b; }
             S.epos[k] = (uint16_t)pem;
             S.cpos[k] = pcr;
             if (k == A.lp[f]) S.fscan0[f] = (uint16_t)pem;
+            const int em = (ina ? 1 : 0) + (cr ? 1 : 0);
             if (em) pfw::atom_add(&S.fk[f], em);
         }
-        NE += tot & 0xffff;
-        NEm += tot >> 16;
+        NE += pfw::popc(mc);
+        NEm += pfw::popc(mi) + pfw::popc(mc);
     }
     pfw::sync();
     // 3b. prefix sums in facet order: kept-facet indices and loop bases
