@@ -274,16 +274,29 @@ def hbm_kernels(sc, dom, psi_g, smf, reps=5, cg_iters=50):
     torch.cuda.synchronize()
     t_it = e0.elapsed_time(e1) / max(it, 1)
     nnz = int(hcnt.sum())
+    # exact k-nearest sites of every site (k = 16, the _knn drop-in's kernel)
+    knn = torch.empty((n, 16), dtype=torch.int64, device="cuda")
+    L.pf_knn(c, n, _lib.ptr(pts), n, _lib.ptr(pts), 16, _lib.ptr(knn), 0, s)
+    torch.cuda.synchronize()
+    e0.record()
+    L.pf_knn(c, n, _lib.ptr(pts), n, _lib.ptr(pts), 16, _lib.ptr(knn), 0, s)
+    e1.record()
+    torch.cuda.synchronize()
+    t_knn = e0.elapsed_time(e1)
     gb_grid = 68.0 * n / (t_grid * 1e-3) / 1e9
     gb_cg = (12.0 * nnz + 108.0 * n) / (t_it * 1e-3) / 1e9
+    gb_knn = 152.0 * n / (t_knn * 1e-3) / 1e9
     mk = lambda gbs, ms, by, note: {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",  # noqa: E731
                                     "frac": gbs / peak if peak else None, "ms": ms, "algorithmic_bytes": by,
                                     "note": note}
     return {"grid_counting_sort": mk(gb_grid, t_grid, 68 * n, "68 B/site (SURVEY §8(d)); 6 small kernels + 1 host "
                                      "read of the bucket-size sum"),
             "pcg_iteration": mk(gb_cg, t_it, int(12 * nnz + 108 * n),
-                                f"12 nnz + 108 n bytes, nnz={nnz}; 5 kernels per iteration (SpMV 8 lanes/row, "
-                                "2 single-block reductions, 2 vector updates), host check every 8"),
+                                f"12 nnz + 108 n bytes, nnz={nnz}; one cooperative kernel on a SELL-32 copy of the "
+                                f"Hessian (2 grid barriers per iteration), {it} iterations per call incl. the "
+                                "SELL repack and the final host read"),
+            "knn": mk(gb_knn, t_knn, 152 * n, "every site's 16 nearest sites: 24 B query + 128 B result per site "
+                      "(candidate positions are L2-resident); warp per query, shell gather + rank sort"),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
 

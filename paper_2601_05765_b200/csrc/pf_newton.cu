@@ -146,172 +146,52 @@ __global__ void __launch_bounds__(RB) k_hessian(int64_t n, int smf, const double
     }
 }
 
-// ---- Jacobi PCG (device scalars; `done` short-circuits after convergence) ----
-// sc: [0] rz, [1] pAp, [2] rr, [3] alpha, [4] beta, [5] bb, [6] rr_new, [7] rz_new
-// ic: [0] done flag, [1] iterations
-
-__global__ void __launch_bounds__(RB) k_pcg_init(int64_t n, const double *__restrict__ b,
-                                                const double *__restrict__ diag, double *__restrict__ x,
-                                                double *__restrict__ r, double *__restrict__ z,
-                                                double *__restrict__ p, double *__restrict__ part) {
-    __shared__ double sh[32];
-    double rz = 0.0, bb = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        double bi = b[i], zi = bi / diag[i];
-        x[i] = 0.0;
-        r[i] = bi;
-        z[i] = zi;
-        p[i] = zi;
-        rz += bi * zi;
-        bb += bi * bi;
-    }
-    double a = block_sum(rz, sh), c = block_sum(bb, sh);
-    if (threadIdx.x == 0) { part[blockIdx.x] = a; part[NPART + blockIdx.x] = c; }
-}
-
-__global__ void k_sum2(const double *__restrict__ part, int nb, double *out0, double *out1) {
-    __shared__ double sh[32];
-    double a = 0.0, b = 0.0;
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) { a += part[k]; b += part[NPART + k]; }
-    a = block_sum(a, sh);
-    b = block_sum(b, sh);
-    if (threadIdx.x == 0) { *out0 = a; if (out1) *out1 = b; }
-}
-
-// Ap = H p and partial p.Ap
-constexpr int SPMV_T = 1024;  // SpMV block: 128 rows in flight per block (latency-bound gathers)
-__global__ void __launch_bounds__(SPMV_T) k_spmv(int64_t n, int smf, const int *__restrict__ hcnt,
-                                            const int *__restrict__ hcol, const double *__restrict__ hval,
-                                            const double *__restrict__ diag, const double *__restrict__ p,
-                                            double *__restrict__ Ap, double *__restrict__ part,
-                                            const int *__restrict__ ic) {
-    if (ic[0]) return;
-    __shared__ double sh[32];
-    double acc = 0.0;
-    // 4 lanes per row, loads unrolled: a row's ELL slots are read as contiguous
-    // segments and its gathers p[col] are in flight together (thread-per-row
-    // walked them one dependent load at a time; 8 lanes per row: 5% slower)
-    const int sub = threadIdx.x & 3;
-    const int64_t rows_per_pass = (int64_t)gridDim.x * (SPMV_T / 4);
-    for (int64_t i = blockIdx.x * (int64_t)(SPMV_T / 4) + (threadIdx.x >> 2); i - (threadIdx.x >> 2) < n;
-         i += rows_per_pass) {
-        double s = 0.0;
-        const bool row = i < n;
-        if (row) {
-            const int c = hcnt[i];
-            const int *col = hcol + i * smf;
-            const double *val = hval + i * smf;
-            #pragma unroll 4
-            for (int k = sub; k < c; k += 4) s += val[k] * p[col[k]];
-        }
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (row && sub == 0) {
-            s += diag[i] * p[i];
-            Ap[i] = s;
-            acc += p[i] * s;
-        }
-    }
-    acc = block_sum(acc, sh);
-    if (threadIdx.x == 0) part[blockIdx.x] = acc;
-}
-
-__global__ void k_alpha(const double *__restrict__ part, int nb, double *sc, const int *ic) {
-    if (ic[0]) return;
-    __shared__ double sh[32];
-    double a = 0.0;
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) a += part[k];
-    a = block_sum(a, sh);
-    if (threadIdx.x == 0) {
-        sc[1] = a;
-        sc[3] = a != 0.0 ? sc[0] / a : 0.0;
-    }
-}
-
-// x += alpha p ; r -= alpha Ap ; z = r / diag ; partial r.z and r.r
-__global__ void __launch_bounds__(RB) k_update(int64_t n, const double *__restrict__ diag,
-                                              double *__restrict__ x, double *__restrict__ r,
-                                              double *__restrict__ z, const double *__restrict__ p,
-                                              const double *__restrict__ Ap, const double *__restrict__ sc,
-                                              double *__restrict__ part, const int *__restrict__ ic) {
-    if (ic[0]) return;
-    __shared__ double sh[32];
-    const double alpha = sc[3];
-    double rz = 0.0, rr = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        double xi = x[i] + alpha * p[i];
-        double ri = r[i] - alpha * Ap[i];
-        double zi = ri / diag[i];
-        x[i] = xi;
-        r[i] = ri;
-        z[i] = zi;
-        rz += ri * zi;
-        rr += ri * ri;
-    }
-    double a = block_sum(rz, sh), c = block_sum(rr, sh);
-    if (threadIdx.x == 0) { part[blockIdx.x] = a; part[NPART + blockIdx.x] = c; }
-}
-
-// beta, convergence test ||r|| <= rtol ||b||, iteration count
-__global__ void k_beta(const double *__restrict__ part, int nb, double *sc, int *ic, double rtol,
-                       int max_iter) {
-    if (ic[0]) return;
-    __shared__ double sh[32];
-    double a = 0.0, b = 0.0;
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) { a += part[k]; b += part[NPART + k]; }
-    a = block_sum(a, sh);
-    b = block_sum(b, sh);
-    if (threadIdx.x == 0) {
-        sc[4] = sc[0] != 0.0 ? a / sc[0] : 0.0;
-        sc[0] = a;
-        sc[2] = b;
-        ic[1] += 1;
-        if (sqrt(b) <= rtol * sqrt(sc[5]) || ic[1] >= max_iter || !(a == a)) ic[0] = 1;
-    }
-}
-
-__global__ void __launch_bounds__(RB) k_pdir(int64_t n, const double *__restrict__ z, double *__restrict__ p,
-                                            const double *__restrict__ sc, const int *__restrict__ ic) {
-    if (ic[0]) return;
-    const double beta = sc[4];
-    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
-        p[i] = z[i] + beta * p[i];
-}
-
-// ---- Jacobi-PCG as ONE cooperative persistent kernel ----------------------
-// Every block owns a contiguous range of rows; per iteration three grid-wide
-// barriers: after the SpMV (p.Ap), after the update (r.z, r.r), after the new
-// search direction.  Every block reduces the per-block partials itself in one
-// fixed order, so all blocks take the same (bitwise reproducible) decisions
-// and the host is not involved until the solve ends.  z = D^-1 r is never
-// stored (recomputed from r, diag: the same bits).  Bytes per row and
-// iteration: ELL row (12 per entry) + hcnt + 5 vector reads + 2 writes in
-// the SpMV/update + 3 reads and 1 write for the direction.
-// ELL (stride smf, hcnt used slots) -> CSR (row_ptr, col, val) for the iterations
-__global__ void k_csr_total(int64_t n, const int *__restrict__ hcnt, int *__restrict__ rp) {
-    rp[n] = rp[n - 1] + hcnt[n - 1];
-}
-__global__ void __launch_bounds__(RB) k_csr_fill(int64_t n, int smf, const int *__restrict__ hcnt,
-                                                const int *__restrict__ hcol, const double *__restrict__ hval,
-                                                const int *__restrict__ rp, int *__restrict__ ccol,
-                                                double *__restrict__ cval) {
-    // 4 lanes per row, many rows in flight (the copy is latency-bound)
-    const int sub = threadIdx.x & 3;
-    for (int64_t i = (blockIdx.x * (int64_t)RB + threadIdx.x) >> 2; i < n; i += ((int64_t)gridDim.x * RB) >> 2) {
-        const int c = hcnt[i], o = rp[i];
-        for (int k = sub; k < c; k += 4) {
-            ccol[o + k] = hcol[i * smf + k];
-            cval[o + k] = hval[i * smf + k];
+// ---- Jacobi-PCG: one cooperative persistent kernel on a SELL-32 copy -------
+// The iterations read the Hessian as SELL-32 (Kreutzer et al.): slices of 32
+// consecutive rows, each slice column-major and padded to its longest row, so
+// a warp reads a slice's values and columns as fully coalesced 256 B / 128 B
+// lines and every lane (= row) has its gathers for several entries in
+// flight.  Matrix loads carry the evict-first (streaming) hint, so the
+// vectors (x, r, z, two direction buffers, Ap, diag: 7 x 8 B per row, 112 MB
+// at 2M rows) stay resident in the 126 MB L2 while the matrix streams past.
+//
+// Per iteration two grid-wide barriers:
+//   A  p = z + beta p_old (formed where it is consumed: for the own row and
+//      for every gathered column), Ap = H p, partial p.Ap        | grid.sync
+//   B  x += alpha p, r -= alpha Ap, z = r / diag, partial r.z, r.r | grid.sync
+// Every block reduces the per-block partials itself in one fixed order, so
+// all blocks take the same (bitwise reproducible) decisions and the host is
+// not involved until the solve ends.
+constexpr int SELL_C = 32;
+__global__ void __launch_bounds__(RB) k_sell_pack(int64_t n, int smf, const int *__restrict__ hcnt,
+                                                 const int *__restrict__ hcol, const double *__restrict__ hval,
+                                                 int *__restrict__ scol, double *__restrict__ sval,
+                                                 int *__restrict__ swid) {
+    const int l = threadIdx.x & 31;
+    const int64_t ns = (n + SELL_C - 1) / SELL_C;
+    const int64_t wstride = ((int64_t)gridDim.x * RB) >> 5;
+    for (int64_t s = (blockIdx.x * (int64_t)RB + threadIdx.x) >> 5; s < ns; s += wstride) {
+        const int64_t i = s * SELL_C + l;
+        const int c = i < n ? hcnt[i] : 0;
+        const int w = __reduce_max_sync(0xffffffffu, c);
+        if (l == 0) swid[s] = w;
+        const size_t base = (size_t)s * SELL_C * smf + l;
+        const int pad = (int)(i < n ? i : s * SELL_C);  // padding gathers the own row's entry (cached)
+        for (int m = 0; m < w; m++) {
+            const bool on = m < c;
+            scol[base + (size_t)m * SELL_C] = on ? hcol[i * smf + m] : pad;
+            sval[base + (size_t)m * SELL_C] = on ? hval[i * smf + m] : 0.0;
         }
     }
 }
-constexpr int CG_T = 1024;
+
+constexpr int CG_T = 512;
 __device__ __forceinline__ void all_reduce2(const double *__restrict__ part, int G, double *a_out,
                                             double *b_out, double *sh) {
     // fixed order: lane l sums part[l], part[l+32], ...; then a fixed shuffle tree
     if (threadIdx.x < 32) {
         double a = 0.0, b = 0.0;
-        for (int k = threadIdx.x; k < G; k += 32) { a += part[k]; b += part[G + k]; }
+        for (int k = threadIdx.x; k < G; k += 32) { a += __ldcg(part + k); b += __ldcg(part + G + k); }
         for (int m = 16; m > 0; m >>= 1) {
             a += __shfl_xor_sync(0xffffffffu, a, m);
             b += __shfl_xor_sync(0xffffffffu, b, m);
@@ -340,23 +220,27 @@ __device__ __forceinline__ double block_sum_all(double v, double *sh) {
     return r;
 }
 
-__global__ void __launch_bounds__(CG_T, 1)
-    k_pcg_coop(int64_t n, int smf, const int *__restrict__ hcnt, const int *__restrict__ hcol,
-               const double *__restrict__ hval, const double *__restrict__ diag, const double *__restrict__ b,
-               double *__restrict__ x, double *__restrict__ r, double *__restrict__ p, double *__restrict__ Ap,
-               double *__restrict__ partA, double *__restrict__ partB, double rtol, int max_iter,
-               int *__restrict__ out_it, const int *__restrict__ rp) {
+__global__ void __launch_bounds__(CG_T, 2)
+    k_pcg_sell(int64_t n, int smf, const int *__restrict__ scol, const double *__restrict__ sval,
+               const int *__restrict__ swid, const double *__restrict__ diag, const double *__restrict__ b,
+               double *__restrict__ x, double *__restrict__ r, double *__restrict__ z, double *__restrict__ pa,
+               double *__restrict__ pb, double *__restrict__ Ap, double *__restrict__ part, double rtol,
+               int max_iter, int *__restrict__ out_it) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[40];
     const int G = gridDim.x;
-    const int64_t R = (n + G - 1) / G;
-    const int64_t lo = blockIdx.x * R, hi = lo + R < n ? lo + R : n;
-    // init: x = 0, r = b, p = z = D^-1 b
+    const int64_t ns = (n + SELL_C - 1) / SELL_C;
+    // this block's slices [s0, s1) and rows [lo, hi)
+    const int64_t s0 = ns * blockIdx.x / G, s1 = ns * (blockIdx.x + 1) / G;
+    const int64_t lo = s0 * SELL_C, hi = s1 * SELL_C < n ? s1 * SELL_C : n;
+    const int wib = threadIdx.x >> 5, nwb = CG_T >> 5, l = threadIdx.x & 31;
+    double *partA = part, *partB = part + 2 * G;
+    // x = 0, r = b, z = D^-1 b, p_old = 0 (beta = 0: p_0 = z_0)
     double rz_p = 0.0, bb_p = 0.0;
     for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
         const double bi = b[i], zi = bi / diag[i];
-        x[i] = 0.0; r[i] = bi; p[i] = zi;
+        x[i] = 0.0; r[i] = bi; z[i] = zi; pa[i] = 0.0;
         rz_p += bi * zi;
         bb_p += bi * bi;
     }
@@ -367,121 +251,42 @@ __global__ void __launch_bounds__(CG_T, 1)
     double rz, bb;
     all_reduce2(partB, G, &rz, &bb, sh);
     int it = 0;
-    if (bb > 0.0) {
-        const int sub = threadIdx.x & 3;
-        for (;;) {
-            // A: Ap = H p on the block's rows (4 lanes per row), partial p.Ap
-            double pap = 0.0;
-            for (int64_t i0 = lo; i0 < hi; i0 += CG_T / 4) {
-                const int64_t i = i0 + (threadIdx.x >> 2);
-                double s = 0.0;
-                const bool row = i < hi;
-                if (row) {  // CSR row [rp[i], rp[i+1]): contiguous, no ELL padding fetched
-                    const int k0 = rp[i], k1 = rp[i + 1];
-#pragma unroll 4
-                    for (int k = k0 + sub; k < k1; k += 4) s += hval[k] * p[hcol[k]];
-                }
-                s += __shfl_xor_sync(0xffffffffu, s, 1);
-                s += __shfl_xor_sync(0xffffffffu, s, 2);
-                if (row && sub == 0) {
-                    const double pi = p[i];
-                    s += diag[i] * pi;
-                    Ap[i] = s;
-                    pap += pi * s;
-                }
-            }
-            pap = block_sum_all(pap, sh);
-            if (threadIdx.x == 0) { partA[blockIdx.x] = pap; partA[G + blockIdx.x] = 0.0; }
-            grid.sync();
-            double pAp, dummy;
-            all_reduce2(partA, G, &pAp, &dummy, sh);
-            const double alpha = pAp != 0.0 ? rz / pAp : 0.0;
-            // B: x += alpha p, r -= alpha Ap, partial r.z (z = r / diag) and r.r
-            double rzn = 0.0, rr = 0.0;
-            for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
-                const double ri = r[i] - alpha * Ap[i];
-                x[i] = x[i] + alpha * p[i];
-                r[i] = ri;
-                const double zi = ri / diag[i];
-                rzn += ri * zi;
-                rr += ri * ri;
-            }
-            rzn = block_sum_all(rzn, sh);
-            rr = block_sum_all(rr, sh);
-            if (threadIdx.x == 0) { partB[blockIdx.x] = rzn; partB[G + blockIdx.x] = rr; }
-            grid.sync();
-            double rz_new, rr_all;
-            all_reduce2(partB, G, &rz_new, &rr_all, sh);
-            const double beta = rz != 0.0 ? rz_new / rz : 0.0;
-            rz = rz_new;
-            it++;
-            if (sqrt(rr_all) <= rtol * sqrt(bb) || it >= max_iter || !(rz_new == rz_new)) break;
-            // C: p = z + beta p
-            for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) p[i] = r[i] / diag[i] + beta * p[i];
-            grid.sync();
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *out_it = it;
-}
-
-// Same iteration with two barriers: the new search direction p = z + beta p
-// is formed where it is consumed -- by the SpMV, for its own rows and for
-// every gathered column (r, diag and the previous p are gathered instead of
-// p alone) -- and written to the other of two p buffers.  Bitwise the same
-// numbers as k_pcg_coop (same formula per entry).
-__global__ void __launch_bounds__(CG_T, 1)
-    k_pcg_coop2(int64_t n, const double *__restrict__ hval, const int *__restrict__ hcol,
-                const int *__restrict__ rp, const double *__restrict__ diag, const double *__restrict__ b,
-                double *__restrict__ x, double *__restrict__ r, double *__restrict__ pa, double *__restrict__ pb,
-                double *__restrict__ Ap, double *__restrict__ partA, double *__restrict__ partB, double rtol,
-                int max_iter, int *__restrict__ out_it) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double sh[40];
-    const int G = gridDim.x;
-    const int64_t R = (n + G - 1) / G;
-    const int64_t lo = blockIdx.x * R, hi = lo + R < n ? lo + R : n;
-    double rz_p = 0.0, bb_p = 0.0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
-        const double bi = b[i], zi = bi / diag[i];
-        x[i] = 0.0; r[i] = bi; pa[i] = 0.0;
-        rz_p += bi * zi;
-        bb_p += bi * bi;
-    }
-    rz_p = block_sum_all(rz_p, sh);
-    bb_p = block_sum_all(bb_p, sh);
-    if (threadIdx.x == 0) { partB[blockIdx.x] = rz_p; partB[G + blockIdx.x] = bb_p; }
-    grid.sync();
-    double rz, bb;
-    all_reduce2(partB, G, &rz, &bb, sh);
-    int it = 0;
-    double beta = 0.0;  // p_0 = z_0 = z_0 + 0 * (p = 0)
+    double beta = 0.0;
     double *pold = pa, *pnew = pb;
     if (bb > 0.0) {
-        const int sub = threadIdx.x & 3;
         for (;;) {
+            // A: p = z + beta p_old, Ap = H p (lane per row of a slice), partial p.Ap
             double pap = 0.0;
-            for (int64_t i0 = lo; i0 < hi; i0 += CG_T / 4) {
-                const int64_t i = i0 + (threadIdx.x >> 2);
-                double s = 0.0;
-                const bool row = i < hi;
-                if (row) {
-                    const int k0 = rp[i], k1 = rp[i + 1];
-#pragma unroll 4
-                    for (int k = k0 + sub; k < k1; k += 4) {
-                        const int j = hcol[k];
-                        s += hval[k] * (r[j] / diag[j] + beta * pold[j]);
-                    }
+            for (int64_t s = s0 + wib; s < s1; s += nwb) {
+                const int64_t i = s * SELL_C + l;
+                const int w = swid[s];
+                const int *__restrict__ cc = scol + (size_t)s * SELL_C * smf + l;
+                const double *__restrict__ vv = sval + (size_t)s * SELL_C * smf + l;
+                double acc = 0.0;
+                int m = 0;
+                for (; m + 4 <= w; m += 4) {  // four entries' loads and gathers in flight
+                    const int c0 = __ldcs(cc), c1 = __ldcs(cc + SELL_C), c2 = __ldcs(cc + 2 * SELL_C),
+                              c3 = __ldcs(cc + 3 * SELL_C);
+                    const double v0 = __ldcs(vv), v1 = __ldcs(vv + SELL_C), v2 = __ldcs(vv + 2 * SELL_C),
+                                 v3 = __ldcs(vv + 3 * SELL_C);
+                    const double q0 = z[c0] + beta * pold[c0], q1 = z[c1] + beta * pold[c1];
+                    const double q2 = z[c2] + beta * pold[c2], q3 = z[c3] + beta * pold[c3];
+                    acc += v0 * q0; acc += v1 * q1; acc += v2 * q2; acc += v3 * q3;
+                    cc += 4 * SELL_C; vv += 4 * SELL_C;
                 }
-                s += __shfl_xor_sync(0xffffffffu, s, 1);
-                s += __shfl_xor_sync(0xffffffffu, s, 2);
-                if (row && sub == 0) {
+                for (; m < w; m++) {
+                    const int c0 = __ldcs(cc);
+                    const double v0 = __ldcs(vv);
+                    acc += v0 * (z[c0] + beta * pold[c0]);
+                    cc += SELL_C; vv += SELL_C;
+                }
+                if (i < n) {
                     const double di = diag[i];
-                    const double pi = r[i] / di + beta * pold[i];
+                    const double pi = z[i] + beta * pold[i];
                     pnew[i] = pi;
-                    s += di * pi;
-                    Ap[i] = s;
-                    pap += pi * s;
+                    acc += di * pi;
+                    Ap[i] = acc;
+                    pap += pi * acc;
                 }
             }
             pap = block_sum_all(pap, sh);
@@ -490,12 +295,14 @@ __global__ void __launch_bounds__(CG_T, 1)
             double pAp, dummy;
             all_reduce2(partA, G, &pAp, &dummy, sh);
             const double alpha = pAp != 0.0 ? rz / pAp : 0.0;
+            // B: x += alpha p, r -= alpha Ap, z = r / diag, partial r.z and r.r
             double rzn = 0.0, rr = 0.0;
             for (int64_t i = lo + threadIdx.x; i < hi; i += CG_T) {
                 const double ri = r[i] - alpha * Ap[i];
                 x[i] = x[i] + alpha * pnew[i];
                 r[i] = ri;
                 const double zi = ri / diag[i];
+                z[i] = zi;
                 rzn += ri * zi;
                 rr += ri * ri;
             }
@@ -667,7 +474,9 @@ int pf_newton_hessian(int64_t n, int smf, const double *pts, const double *psi, 
     return 0;
 }
 
-// Jacobi-PCG on the ELL Hessian; returns the iteration count (>= 0)
+// Jacobi-PCG on the ELL Hessian; returns the iteration count (>= 0).  The
+// matrix is repacked as SELL-32 (k_sell_pack) for the iterations, which run
+// in one cooperative kernel (k_pcg_sell); one host read at the end.
 int pf_pcg(int64_t n, int smf, const int32_t *hcnt, const int32_t *hcol, const double *hval,
            const double *diag, const double *b, double *x, double rtol, int max_iter, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -679,63 +488,31 @@ int pf_pcg(int64_t n, int smf, const int32_t *hcnt, const int32_t *hcol, const d
         int dev = 0, nsm = 0, per = 0;
         NCK(cudaGetDevice(&dev));
         NCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        NCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_coop, CG_T, 0));
-        coop_blocks = nsm * std::max(1, std::min(per, 2));
+        NCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_sell, CG_T, 0));
+        coop_blocks = nsm * std::max(1, std::min(per, 4));
     }
-    // CSR copy of the matrix (12 B per entry: the ELL rows' padding would be
-    // fetched with every iteration's SpMV)
-    static int *rp = nullptr, *ccol = nullptr;
-    static double *cval = nullptr;
-    static size_t rp_c = 0, ce_c = 0;
-    static void *cub_tmp = nullptr;
-    static size_t cub_c = 0;
-    if (dalloc(&rp, &rp_c, (size_t)n + 1)) return -1;
-    {
-        size_t need = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, need, hcnt, rp, (int)n + 1, st);
-        if (need > cub_c) {
-            if (cub_tmp) cudaFree(cub_tmp);
-            NCK(cudaMalloc(&cub_tmp, need));
-            cub_c = need;
-        }
-        // rp[n] = sum of hcnt[0..n): scan n+1 entries of hcnt with a zero appended
-        NCK(cudaMemsetAsync(rp + n, 0, sizeof(int), st));
-        NCK(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_c, hcnt, rp, (int)n, st));
-        pf_internal_launches_add(2);
-        k_csr_total<<<1, 1, 0, st>>>(n, hcnt, rp);
-    }
-    int nnz = 0;
-    NCK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int), cudaMemcpyDeviceToHost, st));
-    NCK(cudaStreamSynchronize(st));
-    if (dalloc(&ccol, &ce_c, (size_t)nnz + 1)) return -1;
-    {
-        static size_t cv_c = 0;
-        if (dalloc(&cval, &cv_c, (size_t)nnz + 1)) return -1;
-    }
+    const int64_t ns = (n + SELL_C - 1) / SELL_C;
+    static int *scol = nullptr, *swid = nullptr;
+    static double *sval = nullptr, *pb = nullptr;
+    static size_t scol_c = 0, sval_c = 0, swid_c = 0, pb_c = 0;
+    const size_t E = (size_t)ns * SELL_C * smf;
+    if (dalloc(&scol, &scol_c, E) || dalloc(&sval, &sval_c, E) || dalloc(&swid, &swid_c, (size_t)ns) ||
+        dalloc(&pb, &pb_c, (size_t)n))
+        return -1;
     pf_internal_launches_add(1);
-    k_csr_fill<<<(int)std::min<int64_t>((n + 63) / 64, 148 * 64), RB, 0, st>>>(n, smf, hcnt, hcol, hval, rp, ccol, cval);
-    int G = (int)std::min<int64_t>(coop_blocks, (n + CG_T / 4 - 1) / (CG_T / 4));
+    k_sell_pack<<<(int)std::min<int64_t>((ns * 32 + RB - 1) / RB, 148 * 32), RB, 0, st>>>(n, smf, hcnt, hcol, hval,
+                                                                                         scol, sval, swid);
+    NCK(cudaGetLastError());
+    int G = (int)std::min<int64_t>(coop_blocks, ns);
     if (G > NPART) G = NPART;
     int64_t nn = n;
     int smf_ = smf, mi = max_iter;
     double rt = rtol;
-    double *partA = w.part, *partB = w.part + 2 * NPART;  // part holds 4 * NPART
-    void *args[] = {&nn, &smf_, (void *)&hcnt, (void *)&ccol, (void *)&cval, (void *)&diag, (void *)&b, &x, &w.r,
-                    &w.p, &w.Ap, &partA, &partB, &rt, &mi, &w.ic, (void *)&rp};
+    double *part = w.part;  // 4 * NPART doubles
+    void *args[] = {&nn, &smf_, (void *)&scol, (void *)&sval, (void *)&swid, (void *)&diag, (void *)&b, &x,
+                    &w.r, &w.z, &w.p, &pb, &w.Ap, &part, &rt, &mi, &w.ic};
     pf_internal_launches_add(1);
-    static int fused = -1;
-    if (fused < 0) {
-        const char *e = getenv("PF_CG_FUSED");
-        fused = e ? atoi(e) : 1;
-    }
-    if (fused) {
-        double *pb = w.z;  // the second direction buffer (z is never stored)
-        void *args2[] = {&nn, (void *)&cval, (void *)&ccol, (void *)&rp, (void *)&diag, (void *)&b, &x, &w.r,
-                         &w.p, &pb, &w.Ap, &partA, &partB, &rt, &mi, &w.ic};
-        NCK(cudaLaunchCooperativeKernel((const void *)k_pcg_coop2, G, CG_T, args2, 0, st));
-    } else {
-        NCK(cudaLaunchCooperativeKernel((const void *)k_pcg_coop, G, CG_T, args, 0, st));
-    }
+    NCK(cudaLaunchCooperativeKernel((const void *)k_pcg_sell, G, CG_T, args, 0, st));
     int it = 0;
     NCK(cudaMemcpyAsync(&it, w.ic, sizeof(int), cudaMemcpyDeviceToHost, st));
     NCK(cudaStreamSynchronize(st));
