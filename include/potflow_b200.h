@@ -255,6 +255,18 @@ int pf_cg1_spmv_dots(int nrows, const int32_t *rows, int smf, const int32_t *hcn
 int pf_cg1_step(int nrows, const int32_t *rows, const double *diag, double *x, double *r, double *u,
                 const double *w, double *p, double *s, const double *red_dev, double *sc_dev, int first,
                 void *stream);
+/* the same iteration with the convergence test on the device, so the host
+ * reads one flag per batch of iterations instead of one scalar per iteration:
+ * sc_dev[3] = ||b||^2, [4] done flag, [5] iterations (zero sc_dev[3..5] before the
+ * first iteration).  step_conv applies the test of pf_pcg (||r|| <= rtol ||b||,
+ * it >= max_iter, non-finite) to the all-reduced r.r and skips the update once
+ * done; spmv_dots_c skips its work once done. */
+int pf_cg1_spmv_dots_c(int nrows, const int32_t *rows, int smf, const int32_t *hcnt, const int32_t *hcol,
+                       const double *hval, const double *diag, const double *u, const double *r, double *w,
+                       double *out3_dev, const double *sc_dev, void *stream);
+int pf_cg1_step_conv(int nrows, const int32_t *rows, const double *diag, double *x, double *r, double *u,
+                     const double *w, double *p, double *s, const double *red_dev, double *sc_dev, double rtol,
+                     int max_iter, void *stream);
 /* out = a + s b (n entries) */
 int pf_daxpy(int64_t n, const double *a, double s, const double *b, double *out, void *stream);
 

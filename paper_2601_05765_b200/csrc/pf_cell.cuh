@@ -372,11 +372,8 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
 
     // 3a. lane per loop entry (edge a -> b of facet f): classification,
     // crossing entries in walk order (= entry order) and the facet's emitted
-    // loop length (_kernels.py:160-228); one scan of both counts
+    // loop length (_kernels.py:160-228); both prefix counts from ballots
     const int nl = A.nl;
-    #pragma unroll 1
-    for (int f = L; f < nf; f += 32) S.fk[f] = 0;
-    pfw::sync();
     int NE = 0, NEm = 0;
     #pragma unroll 1
     for (int k0 = 0; k0 < nl; k0 += 32) {
@@ -405,7 +402,9 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
             S.cpos[k] = pcr;
             if (k == A.lp[f]) S.fscan0[f] = (uint16_t)pem;
             const int em = (ina ? 1 : 0) + (cr ? 1 : 0);
-            if (em) pfw::atom_add(&S.fk[f], em);
+            // the facet's last entry records where its emission ends (3b
+            // subtracts where it starts): no zeroing pass, no atomics
+            if (k + 1 == A.lp[f + 1]) S.fk[f] = pem + em;
         }
         NE += pfw::popc(mc);
         NEm += pfw::popc(mi) + pfw::popc(mc);
@@ -419,7 +418,8 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         int f = f0 + L;
         int kk = 0, keep = 0;
         if (f < nf) {
-            kk = S.fk[f];
+            kk = S.fk[f] - S.fscan0[f];
+            S.fk[f] = kk;
             keep = kk >= 3;
         }
         small_facet |= pfw::any(kk >= 1 && kk <= 2);

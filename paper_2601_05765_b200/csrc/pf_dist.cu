@@ -226,8 +226,14 @@ __global__ void __launch_bounds__(DB) k_cg1_spmv_dots(int nrows, const int *__re
                                                       const double *__restrict__ hval,
                                                       const double *__restrict__ diag, const double *__restrict__ u,
                                                       const double *__restrict__ r, double *__restrict__ w,
-                                                      double *__restrict__ part) {
+                                                      double *__restrict__ part,
+                                                      const double *__restrict__ sc = nullptr) {
     double v[3] = {0.0, 0.0, 0.0};
+    if (sc && sc[4] != 0.0) {  // converged (device-side test): partials of zero, no work
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 3; k++) part[k * DNB + blockIdx.x] = 0.0;
+        return;
+    }
     const int op[3] = {0, 0, 0};
     for (int t = blockIdx.x * DB + threadIdx.x; t < nrows; t += DNB * DB) {
         const int64_t i = rows[t];
@@ -261,12 +267,41 @@ __global__ void k_cg1_scalars(const double *__restrict__ red, double *__restrict
     sc[0] = g; sc[1] = alpha; sc[2] = beta;
 }
 
+// the same with the convergence test of pf_pcg on the device (sc[3] = b.b,
+// sc[4] = done, sc[5] = iterations); red = all-reduced (r.u, w.u, r.r)
+__global__ void k_cg1_scalars_conv(const double *__restrict__ red, double *__restrict__ sc, double rtol,
+                                   int max_iter) {
+    if (sc[4] != 0.0) return;
+    const int it = (int)sc[5];
+    const double rr = red[2];
+    if (it == 0) {
+        sc[3] = rr;
+        if (!(rr > 0.0)) { sc[4] = 1.0; return; }
+    } else if (sqrt(rr) <= rtol * sqrt(sc[3]) || it >= max_iter || !isfinite(rr)) {
+        sc[4] = 1.0;
+        return;
+    }
+    const double g = red[0], dl = red[1];
+    double beta = 0.0, alpha;
+    if (it == 0) {
+        alpha = dl != 0.0 ? g / dl : 0.0;
+    } else {
+        beta = sc[0] != 0.0 ? g / sc[0] : 0.0;
+        const double den = dl - (sc[1] != 0.0 ? beta * g / sc[1] : 0.0);
+        alpha = den != 0.0 ? g / den : 0.0;
+    }
+    sc[0] = g; sc[1] = alpha; sc[2] = beta;
+    sc[5] = it + 1;
+}
+
 // p = u + beta p; s = w + beta s; x += alpha p; r -= alpha s; u = r / diag
 __global__ void __launch_bounds__(DB) k_cg1_update(int nrows, const int *__restrict__ rows,
                                                    const double *__restrict__ diag, double *__restrict__ x,
                                                    double *__restrict__ r, double *__restrict__ u,
                                                    const double *__restrict__ w, double *__restrict__ p,
-                                                   double *__restrict__ s, const double *__restrict__ sc) {
+                                                   double *__restrict__ s, const double *__restrict__ sc,
+                                                   int conv = 0) {
+    if (conv && sc[4] != 0.0) return;
     const double alpha = sc[1], beta = sc[2];
     for (int t = blockIdx.x * DB + threadIdx.x; t < nrows; t += DNB * DB) {
         const int i = rows[t];
@@ -394,6 +429,29 @@ int pf_cg1_step(int nrows, const int32_t *rows, const double *diag, double *x, d
     pf_internal_launches_add(2);
     k_cg1_scalars<<<1, 1, 0, st>>>(red_dev, sc_dev, first);
     k_cg1_update<<<DNB, DB, 0, st>>>(nrows, rows, diag, x, r, u, w, p, s, sc_dev);
+    DCK(cudaGetLastError());
+    return 0;
+}
+
+int pf_cg1_spmv_dots_c(int nrows, const int32_t *rows, int smf, const int32_t *hcnt, const int32_t *hcol,
+                       const double *hval, const double *diag, const double *u, const double *r, double *w,
+                       double *out3_dev, const double *sc_dev, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (part_alloc()) return -1;
+    pf_internal_launches_add(2);
+    k_cg1_spmv_dots<<<DNB, DB, 0, st>>>(nrows, rows, smf, hcnt, hcol, hval, diag, u, r, w, g_part, sc_dev);
+    k_finish<3><<<1, DB, 0, st>>>(g_part, out3_dev, 0, 0, 0, 0);
+    DCK(cudaGetLastError());
+    return 0;
+}
+
+int pf_cg1_step_conv(int nrows, const int32_t *rows, const double *diag, double *x, double *r, double *u,
+                     const double *w, double *p, double *s, const double *red_dev, double *sc_dev, double rtol,
+                     int max_iter, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    pf_internal_launches_add(2);
+    k_cg1_scalars_conv<<<1, 1, 0, st>>>(red_dev, sc_dev, rtol, max_iter);
+    k_cg1_update<<<DNB, DB, 0, st>>>(nrows, rows, diag, x, r, u, w, p, s, sc_dev, 1);
     DCK(cudaGetLastError());
     return 0;
 }

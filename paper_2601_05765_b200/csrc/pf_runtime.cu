@@ -1,6 +1,7 @@
 // pf_runtime.cu -- device runtime of the partial-OT hot path for sm_100a:
 // grid build (counting sort), weight reductions, the two-tier warp-per-cell
 // evaluation kernels, batched kNN, and the C ABI of include/potflow_b200.h.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -118,6 +119,17 @@ struct pf_ctx {
     // parity mode: restrict the facets exactly as the reference does, including
     // its spurious-entry and long-arc outcomes; 0 = robust default
     int strict = 0;
+    // grid build: bucket size cached across calls (the cell results do not depend
+    // on the bucket layout), refreshed from an asynchronous read of the mean ball
+    // radius; bucket counts known to be zero (the scatter consumes them)
+    double h_cache = 0.0;
+    int64_t h_cache_n = -1;
+    double *h_pinned = nullptr;
+    cudaEvent_t h_ev = nullptr;
+    bool h_pending = false;
+    int64_t bcount_zero = -1;  // bcount[0..bcount_zero] is all zeros
+    int grid_coop_blocks = 0;
+    int *grid_part = nullptr;
 };
 
 // ---------------------------------------------------------------------------
@@ -275,6 +287,143 @@ __global__ void k_grid_export(const int *__restrict__ bstart, int ncell, const i
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
     for (int64_t c = t; c <= ncell; c += st) bs64[c] = bstart[c];
     for (int64_t i = t; i < n; i += st) sid64[i] = sid[i];
+}
+
+// The whole counting sort as ONE cooperative kernel (three grid barriers):
+//   1. bucket id of every site, histogram (shared counts start at zero)
+//   2. exclusive scan of the counts: per-block chunk sums, every block adds the
+//      sums of the blocks before it, then scans its chunk
+//   3. scatter, the counts serving as decrementing cursors (they end at zero,
+//      so the next build needs no memset)
+//   4. per bucket (by its first slot: work ~ n, not ~ the bucket count): order
+//      by site index (== numpy's stable argsort) and write the SoA copy
+constexpr int GRID_T = 1024;
+__global__ void __launch_bounds__(GRID_T, 1) k_grid_coop(const double *__restrict__ pts, int64_t n, double lo0,
+                                                       double lo1, double lo2, double ih0, double ih1, double ih2,
+                                                       int g0, int g1, int g2, int64_t ncell, int *__restrict__ bid,
+                                                       int *__restrict__ bcount, int *__restrict__ bstart,
+                                                       int *__restrict__ sid, double *__restrict__ sx,
+                                                       double *__restrict__ sy, double *__restrict__ sz,
+                                                       int *__restrict__ part) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int sh[33];
+    const int64_t T = (int64_t)gridDim.x * GRID_T, t0 = blockIdx.x * (int64_t)GRID_T + threadIdx.x;
+    for (int64_t i = t0; i < n; i += T) {
+        const int a = bucket_coord(pts[3 * i], lo0, ih0, g0);
+        const int b = bucket_coord(pts[3 * i + 1], lo1, ih1, g1);
+        const int c = bucket_coord(pts[3 * i + 2], lo2, ih2, g2);
+        const int l = (a * g1 + b) * g2 + c;
+        bid[i] = l;
+        atomicAdd(&bcount[l], 1);
+    }
+    grid.sync();
+    // chunk of this block over the ncell + 1 counts (bcount[ncell] == 0), in
+    // tiles of GRID_T x 8 counts read as two int4 per thread (enough loads in
+    // flight to stream the counts; the arrays carry 16 ints of padding)
+    const int64_t m = ncell + 1, G = gridDim.x;
+    const int64_t C8 = ((m + G - 1) / G + 7) & ~(int64_t)7;
+    const int64_t c0 = C8 * blockIdx.x < m ? C8 * blockIdx.x : m, c1 = c0 + C8 < m ? c0 + C8 : m;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int TILE = GRID_T * 8;
+    int loc = 0;
+    for (int64_t base = c0; base < c1; base += TILE) {
+        const int64_t k = base + 8 * (int64_t)threadIdx.x;
+        if (k < c1) {
+            const int4 u0 = *(const int4 *)(bcount + k), u1 = *(const int4 *)(bcount + k + 4);
+            const int v[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+            for (int e = 0; e < 8; e++) loc += k + e < c1 ? v[e] : 0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+    if (lane == 0) sh[w] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int k = 0; k < GRID_T / 32; k++) s += sh[k];
+        part[blockIdx.x] = s;
+    }
+    grid.sync();
+    // offset of this chunk: sum of the preceding blocks' chunk sums
+    int off = 0;
+    for (int k = threadIdx.x; k < blockIdx.x; k += GRID_T) off += __ldcg(part + k);
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+    __syncthreads();
+    if (lane == 0) sh[w] = off;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int k = 0; k < GRID_T / 32; k++) s += sh[k];
+        sh[32] = s;
+    }
+    __syncthreads();
+    int run = sh[32];
+    __syncthreads();
+    for (int64_t base = c0; base < c1; base += TILE) {
+        const int64_t k = base + 8 * (int64_t)threadIdx.x;
+        int v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (k < c1) {
+            const int4 u0 = *(const int4 *)(bcount + k), u1 = *(const int4 *)(bcount + k + 4);
+            v[0] = u0.x; v[1] = u0.y; v[2] = u0.z; v[3] = u0.w; v[4] = u1.x; v[5] = u1.y; v[6] = u1.z; v[7] = u1.w;
+#pragma unroll
+            for (int e = 0; e < 8; e++) v[e] = k + e < c1 ? v[e] : 0;
+        }
+        int tsum = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) { const int t = v[e]; v[e] = tsum; tsum += t; }
+        int x = tsum;  // inclusive warp scan of the thread sums
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) sh[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int s2 = sh[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, s2, o);
+                if (lane >= o) s2 += y;
+            }
+            sh[lane] = s2;
+        }
+        __syncthreads();
+        const int tb = run + (w > 0 ? sh[w - 1] : 0) + x - tsum;
+        if (k < c1) {
+            if (k + 8 <= c1) {
+                *(int4 *)(bstart + k) = make_int4(tb + v[0], tb + v[1], tb + v[2], tb + v[3]);
+                *(int4 *)(bstart + k + 4) = make_int4(tb + v[4], tb + v[5], tb + v[6], tb + v[7]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; e++)
+                    if (k + e < c1) bstart[k + e] = tb + v[e];
+            }
+        }
+        run += sh[31];
+        __syncthreads();
+    }
+    grid.sync();
+    for (int64_t i = t0; i < n; i += T) {
+        const int l = bid[i];
+        sid[bstart[l] + atomicSub(&bcount[l], 1) - 1] = (int)i;
+    }
+    grid.sync();
+    for (int64_t k = t0; k < n; k += T) {
+        const int l = bid[sid[k]];
+        const int a = bstart[l];
+        if (k != a) continue;
+        const int b = bstart[l + 1];
+        for (int q = a + 1; q < b; q++) {
+            const int v = sid[q];
+            int j = q - 1;
+            while (j >= a && sid[j] > v) { sid[j + 1] = sid[j]; j--; }
+            sid[j + 1] = v;
+        }
+        for (int q = a; q < b; q++) {
+            const int i = sid[q];
+            sx[q] = pts[3 * i]; sy[q] = pts[3 * i + 1]; sz[q] = pts[3 * i + 2];
+        }
+    }
 }
 
 // cells of the fast tier: shared-memory workspace, one warp per cell, cells
@@ -812,15 +961,36 @@ int grid_build(pf_ctx *c, int64_t n, const double *pts, const double *psi, doubl
     for (int a = 0; a < 3; a++) ext[a] = std::max(c->dhi[a] - c->dlo[a], 1e-300);
     double H = cell_size;
     if (!(H > 0.0)) {
+        // bucket edge = mean ball radius (~ half the ball-aware search radius).
+        // The cell results do not depend on the bucket layout, so
+        // the edge is cached per site count and refreshed from an asynchronous
+        // read: only the first build of a run waits for the device.
         H = 0.0;
         if (psi && n > 0) {
-            CK(cudaMemsetAsync(c->dscal + 3, 0, sizeof(double), st));
-            g_launches++;
-            k_sum_sqrt<<<c->nsm * 4, 256, 0, st>>>(psi, n, c->dscal + 3);
-            double sum = 0.0;
-            CK(cudaMemcpyAsync(&sum, c->dscal + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            H = sum / (double)n;  // mean ball radius ~ half the ball-aware search radius
+            if (!c->h_pinned) {
+                CK(cudaMallocHost(&c->h_pinned, sizeof(double)));
+                CK(cudaEventCreateWithFlags(&c->h_ev, cudaEventDisableTiming));
+            }
+            if (c->h_pending && c->h_cache_n == n && cudaEventQuery(c->h_ev) == cudaSuccess) {
+                c->h_cache = *c->h_pinned / (double)n;
+                c->h_pending = false;
+            }
+            const bool have = c->h_cache_n == n && c->h_cache > 0.0;
+            if (!c->h_pending || !have) {
+                CK(cudaMemsetAsync(c->dscal + 3, 0, sizeof(double), st));
+                g_launches++;
+                k_sum_sqrt<<<c->nsm * 4, 256, 0, st>>>(psi, n, c->dscal + 3);
+                CK(cudaMemcpyAsync(c->h_pinned, c->dscal + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
+                CK(cudaEventRecord(c->h_ev, st));
+                c->h_pending = true;
+            }
+            if (!have) {
+                CK(cudaEventSynchronize(c->h_ev));
+                c->h_cache = *c->h_pinned / (double)n;
+                c->h_cache_n = n;
+                c->h_pending = false;
+            }
+            H = c->h_cache;
         }
         if (!(H > 0.0)) H = 0.5 * std::cbrt(c->dvol / (double)std::max<int64_t>(n, 1));
     }
@@ -840,37 +1010,29 @@ int grid_build(pf_ctx *c, int64_t n, const double *pts, const double *psi, doubl
         c->gih[a] = 1.0 / c->gh[a];
     }
     const int64_t ncell = (int64_t)g[0] * g[1] * g[2];
+    const size_t bcap0 = c->bcount_cap;
     if (ensure(&c->sx, &c->sx_cap, n) || ensure(&c->sy, &c->sy_cap, n) || ensure(&c->sz, &c->sz_cap, n) ||
         ensure(&c->sid, &c->sid_cap, n) || ensure(&c->bid, &c->bid_cap, n) ||
-        ensure(&c->bcount, &c->bcount_cap, ncell + 1) || ensure(&c->bstart, &c->bstart_cap, ncell + 1))
+        ensure(&c->bcount, &c->bcount_cap, ncell + 17) || ensure(&c->bstart, &c->bstart_cap, ncell + 17))
         return -1;
-    int64_t nblk = (ncell + 1 + SCAN_B - 1) / SCAN_B;
-    if (nblk > SCAN_B) return set_err("grid too large for the two-level scan");
-    if (ensure(&c->scan_tmp, &c->scan_tmp_cap, 2 * nblk + 2)) return -1;
-    CK(cudaMemsetAsync(c->bcount, 0, (ncell + 1) * sizeof(int), st));
-    int gb = (int)std::min<int64_t>(c->nsm * 8, (n + 255) / 256 + 1);
-    if (n > 0) {
-        g_launches++;
-        k_grid_bucket<<<gb, 256, 0, st>>>(pts, n, c->glo[0], c->glo[1], c->glo[2], c->gih[0], c->gih[1],
-                                          c->gih[2], g[0], g[1], g[2], c->bid, c->bcount);
+    if (c->bcount_cap != bcap0) c->bcount_zero = -1;  // reallocated
+    if (!c->grid_coop_blocks) {
+        int per = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_grid_coop, GRID_T, 0));
+        c->grid_coop_blocks = c->nsm * std::max(1, std::min(per, 2));
+        CK(cudaMalloc(&c->grid_part, sizeof(int) * c->grid_coop_blocks));
     }
+    if (c->bcount_zero < ncell) {  // first build on this buffer (later builds leave it zeroed)
+        CK(cudaMemsetAsync(c->bcount, 0, (ncell + 1) * sizeof(int), st));
+        c->bcount_zero = ncell;
+    }
+    int64_t nn = n, nc = ncell;
+    double lo0 = c->glo[0], lo1 = c->glo[1], lo2 = c->glo[2], ih0 = c->gih[0], ih1 = c->gih[1], ih2 = c->gih[2];
+    int g0 = g[0], g1 = g[1], g2 = g[2];
+    void *args[] = {(void *)&pts, &nn, &lo0, &lo1, &lo2, &ih0, &ih1, &ih2, &g0, &g1, &g2, &nc,
+                    &c->bid, &c->bcount, &c->bstart, &c->sid, &c->sx, &c->sy, &c->sz, &c->grid_part};
     g_launches++;
-    k_scan_blocks<<<(int)nblk, SCAN_T, 0, st>>>(c->bcount, c->bstart, ncell + 1, c->scan_tmp);
-    if (nblk > 1) {
-        g_launches++;
-        k_scan_blocks<<<1, SCAN_T, 0, st>>>(c->scan_tmp, c->scan_tmp + nblk + 1, nblk, nullptr);
-        g_launches++;
-        k_scan_add<<<(int)nblk, 256, 0, st>>>(c->bstart, ncell + 1, c->scan_tmp + nblk + 1);
-    }
-    CK(cudaMemsetAsync(c->bcount, 0, (ncell + 1) * sizeof(int), st));
-    if (n > 0) {
-        g_launches++;
-        k_grid_scatter<<<gb, 256, 0, st>>>(c->bid, n, c->bstart, c->bcount, c->sid);
-        g_launches++;
-        k_grid_finish<<<(int)std::min<int64_t>(c->nsm * 8, (ncell + 255) / 256), 256, 0, st>>>(
-            (int)ncell, c->bstart, c->sid, pts, c->sx, c->sy, c->sz);
-    }
-    CK(cudaGetLastError());
+    CK(cudaLaunchCooperativeKernel((const void *)k_grid_coop, c->grid_coop_blocks, GRID_T, args, 0, st));
     c->grid_n = n;
     c->grid_pts = pts;
     return 0;
@@ -979,9 +1141,11 @@ int pf_ctx_destroy(pf_ctx *c) {
     if (!c) return 0;
     void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
                     c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
-                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2, c->csr_cnt, c->csr_off};
+                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2, c->csr_cnt, c->csr_off, c->grid_part};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    if (c->h_ev) cudaEventDestroy(c->h_ev);
     delete c;
     return 0;
 }

@@ -113,7 +113,9 @@ def _bind():
         L.pf_cg1_init.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.pf_cg1_spmv_dots.argtypes = [i, vp, i, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.pf_cg1_step.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, vp]
-        for name in ("pf_cg1_init", "pf_cg1_spmv_dots", "pf_cg1_step"):
+        L.pf_cg1_spmv_dots_c.argtypes = [i, vp, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pf_cg1_step_conv.argtypes = [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, d, i, vp]
+        for name in ("pf_cg1_init", "pf_cg1_spmv_dots", "pf_cg1_step", "pf_cg1_spmv_dots_c", "pf_cg1_step_conv"):
             getattr(L, name).restype = i
         for name in ("pf_evaluate_lean_cells", "pf_rows_gradient", "pf_rows_hessian", "pf_dcg_init",
                      "pf_dcg_spmv", "pf_dcg_update", "pf_dcg_pdir", "pf_daxpy"):
@@ -140,9 +142,10 @@ class CudaOps:
         f8, i4 = dict(dtype=torch.float64, **dev), dict(dtype=torch.int32, **dev)
         self.n = n = len(pts_local)
         self.smf, self.ball_aware, self.tau = smf, int(ball_aware), float(tau_psi)
-        self.pts = torch.as_tensor(np.ascontiguousarray(pts_local), **f8)
-        self.nu = torch.as_tensor(np.ascontiguousarray(nu_local), **f8)
-        self.rows = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.int32), **i4)
+        # numpy arrays or tensors (the exchange data plane hands over device tensors)
+        self.pts = torch.as_tensor(pts_local, **f8).contiguous()
+        self.nu = torch.as_tensor(nu_local, **f8).contiguous()
+        self.rows = torch.as_tensor(rows, **i4).contiguous()
         self.nrows = len(rows)
         self.psi = torch.zeros(n, **f8)
         self.psi_t = torch.zeros(n, **f8)
@@ -308,6 +311,30 @@ class CudaOps:
                                     self.p(v["s"]), self.p(red), self.p(self.cg1_sc), int(first), self._s()),
                  "pf_cg1_step")
 
+    # device-side convergence (one host read per batch of iterations)
+    def cg1_conv_reset(self):
+        self.cg1_sc.zero_()
+
+    def cg1_spmv_dots_c(self):
+        v = self.v
+        out = self.torch.zeros(3, dtype=self.torch.float64, device="cuda")
+        self.chk(self.L.pf_cg1_spmv_dots_c(self.nrows, self.p(self.rows), self.smf, self.p(self.hcnt),
+                                           self.p(self.hcol), self.p(self.hval), self.p(v["diag"]),
+                                           self.p(v["z"]), self.p(v["r"]), self.p(v["Ap"]), self.p(out),
+                                           self.p(self.cg1_sc), self._s()), "pf_cg1_spmv_dots_c")
+        return out
+
+    def cg1_step_conv(self, red, rtol: float, max_iter: int):
+        v = self.v
+        self.chk(self.L.pf_cg1_step_conv(self.nrows, self.p(self.rows), self.p(v["diag"]), self.p(v["x"]),
+                                         self.p(v["r"]), self.p(v["z"]), self.p(v["Ap"]), self.p(v["p"]),
+                                         self.p(v["s"]), self.p(red), self.p(self.cg1_sc), float(rtol),
+                                         int(max_iter), self._s()), "pf_cg1_step_conv")
+
+    def cg1_status(self):
+        sc = self.cg1_sc[4:6].cpu()
+        return bool(sc[0] != 0.0), int(sc[1])
+
     def vec(self, name):
         return self.v[name]
 
@@ -347,12 +374,13 @@ class DistNewton:
     def __init__(self, pts: np.ndarray, nu: np.ndarray, domain, group=None, smf: int = 32,
                  ball_aware: bool = True, slack: float = 1.5, ops_factory=None, axis_lo=None,
                  axis_hi=None, cg: str = "single"):
-        self.pts = np.ascontiguousarray(pts, dtype=np.float64)
-        self.nu = np.ascontiguousarray(nu, dtype=np.float64)
+        self.pts = None if pts is None else np.ascontiguousarray(pts, dtype=np.float64)
+        self.nu = None if nu is None else np.ascontiguousarray(nu, dtype=np.float64)
         self.domain = domain
         self.comm = Comm(group)
         self.smf, self.ball_aware, self.slack = smf, ball_aware, slack
         self.cg = cg  # "single": one all-reduce per CG iteration; "classic": two
+        self.cg_batch = 8  # CG iterations per host convergence read (device-side test)
         # slab boundaries: x-quantiles of the sites (balanced) unless given
         self.lo, self.hi = axis_lo, axis_hi
         self.tau = 1e-12 * domain.diagonal() ** 2
@@ -403,16 +431,12 @@ class DistNewton:
         for _ in range(8):
             if self._margin_ok(dpsi, trial):
                 break
-            # weights outgrew the ghost layer: re-partition from the global
-            # weights, with the margin sized for the weights being evaluated
-            # (the trial weights psi + alpha x on a damping trial)
-            psi_g = self._gather_global(self.ops.psi_host(False))
-            x_g = self._gather_global(self.ops.vec("x").cpu().numpy()) if trial else None
-            self._partition(psi_g, dpsi, psi_g + self._alpha * x_g if trial else None)
+            # weights outgrew the ghost layer: re-partition, with the margin
+            # sized for the weights being evaluated (the trial weights
+            # psi + alpha x on a damping trial)
+            self._repartition(dpsi, trial)
             self.repartitions += 1
             if trial:
-                l2g = self.slab.local_to_global
-                self.ops.vec("x").copy_(self.ops.torch.as_tensor(x_g[l2g]))
                 self.ops.trial(self._alpha)
             dpsi = self._dpsi(trial)
         else:
@@ -422,12 +446,42 @@ class DistNewton:
         st = [float(v) for v in st.cpu()]
         return st[0], -st[1], -st[2]
 
+    def _repartition(self, dpsi: float, trial: bool):
+        """Re-partition from the all-gathered global weights (replicated mode)."""
+        psi_g = self._gather_global(self.ops.psi_host(False))
+        x_g = self._gather_global(self.ops.vec("x").cpu().numpy()) if trial else None
+        self._partition(psi_g, dpsi, psi_g + self._alpha * x_g if trial else None)
+        if trial:
+            self.ops.vec("x").copy_(self.ops.torch.as_tensor(x_g[self.slab.local_to_global]))
+
+    def _start(self, psi_init):
+        """Initial weights (cold: the free balls' (3 nu / 4 pi)^(2/3)) and the
+        first partition; returns whether the start is cold."""
+        cold = psi_init is None
+        psi0 = (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0) if cold else np.asarray(psi_init, np.float64)
+        lo_, hi_ = float(psi0.min()), float(psi0.max())
+        self._partition(psi0, max(hi_ - lo_, 0.0))
+        return cold
+
     # --- Jacobi-PCG ---------------------------------------------------------
     def _pcg1(self, rtol: float, max_iter: int = 10000) -> int:
         """Single-reduction Jacobi-PCG (Chronopoulos & Gear): per iteration one halo
-        exchange of u = D^-1 r and ONE all-reduce of (r.u, w.u, r.r), w = A u."""
+        exchange of u = D^-1 r and ONE all-reduce of (r.u, w.u, r.r), w = A u.
+        With a backend that tests convergence on the device (cg1_step_conv) the
+        iterations are stream-ordered and the host reads one flag per
+        ``cg_batch`` iterations (iterations past convergence are no-ops)."""
         o, c = self.ops, self.comm
         o.cg1_init()
+        if self.cg_batch > 1 and hasattr(o, "cg1_step_conv"):
+            o.cg1_conv_reset()
+            while True:
+                for _ in range(self.cg_batch):
+                    c.exchange(o.vec("z"), self.plan, self.idx_send, self.idx_recv)
+                    red = c.all_reduce(o.cg1_spmv_dots_c(), "sum")
+                    o.cg1_step_conv(red, rtol, max_iter)
+                done, it = o.cg1_status()
+                if done:
+                    return it
         bb, it = 0.0, 0
         while True:
             c.exchange(o.vec("z"), self.plan, self.idx_send, self.idx_recv)
@@ -466,13 +520,8 @@ class DistNewton:
               max_newton: int = 100) -> DistResult:
         S = dict(status=0, iterations=0, evaluations=0, cg_iterations=0, damping_halvings=0,
                  init_doublings=0, worst_initial=0.0, worst_final=0.0, last_alpha=0.0)
-        cold = psi_init is None
-        psi0 = (np.zeros(len(self.pts)) if cold else np.asarray(psi_init, dtype=np.float64))
-        if cold:
-            psi0 = (3.0 * self.nu / (4.0 * np.pi)) ** (2.0 / 3.0)
-        lo_, hi_ = float(psi0.min()), float(psi0.max())
-        self._partition(psi0, max(hi_ - lo_, 0.0))
         self._alpha = 1.0
+        cold = self._start(psi_init)
         if cold:
             kappa = 1.0
             while True:
@@ -547,3 +596,80 @@ class DistNewton:
         own = self.slab.owned_local
         return DistResult(psi_owned=self.ops.owned("psi"), owned_global=self.slab.local_to_global[own],
                           stats=S)
+
+
+class DistNewtonLocal(DistNewton):
+    """The same partitioned solve with no replicated arrays: every rank passes
+    only the sites it owns (global ids, positions, volumes as tensors on its
+    device, gid order) and the x-slab cuts.  The local set (owned + ghosts)
+    and the CG halo plan come from ``halo.SlabComm.ghosts`` (all-to-alls of
+    the owned rows within each peer's margin); a re-partition re-exchanges the
+    ghosts with a wider margin from the owned weights -- nothing is gathered.
+    Per-cell results and the Newton iterations equal ``DistNewton``'s
+    (tests/test_halo_gloo.py)."""
+
+    def __init__(self, gid, pts, nu, domain, cuts, group=None, smf: int = 32, ball_aware: bool = True,
+                 slack: float = 1.5, ops_factory=None, cg: str = "single"):
+        import torch
+
+        from . import halo
+
+        super().__init__(None, None, domain, group=group, smf=smf, ball_aware=ball_aware, slack=slack,
+                         ops_factory=ops_factory, cg=cg)
+        self.torch = torch
+        self.halo = halo
+        self.gid = torch.as_tensor(gid, dtype=torch.int64)
+        dev = self.gid.device
+        self.own_pts = torch.as_tensor(pts, dtype=torch.float64, device=dev).contiguous()
+        self.own_nu = torch.as_tensor(nu, dtype=torch.float64, device=dev).contiguous()
+        self.sc = halo.SlabComm(cuts, self.comm)
+
+    def _exchange(self, psi_own, dpsi: float, psi_plan_own=None, x_own=None):
+        t = self.torch
+        dev = self.gid.device
+        psi_own = t.as_tensor(psi_own, dtype=t.float64, device=dev)
+        plan = psi_own if psi_plan_own is None else t.as_tensor(psi_plan_own, dtype=t.float64, device=dev)
+        margin = self.halo.ghost_margin(plan.cpu().numpy(), dpsi, self.slack)
+        fields = {"pts": self.own_pts, "nu": self.own_nu, "psi": psi_own}
+        if x_own is not None:
+            fields["x"] = t.as_tensor(x_own, dtype=t.float64, device=dev)
+        loc = self.sc.ghosts(self.gid, fields, margin)
+        owned = loc.owned.cpu().numpy().astype(np.int32)
+        self.slab = partition.Slab(self.comm.rank, self.comm.world, loc.lo, loc.hi, loc.gid.cpu().numpy(),
+                                   owned, margin)
+        self.plan = loc.plan
+        lp = loc.fields["pts"] if dev.type == "cuda" else loc.fields["pts"].numpy()
+        ln = loc.fields["nu"] if dev.type == "cuda" else loc.fields["nu"].numpy()
+        self.ops = self.ops_factory(lp, ln, owned)
+        self.ops.set_psi(loc.fields["psi"] if dev.type == "cuda" else loc.fields["psi"].numpy())
+        if x_own is not None:
+            self.ops.vec("x").copy_(loc.fields["x"])
+        self.idx_send = {q: self.ops.index(ix) for q, ix in self.plan.send.items()}
+        self.idx_recv = {q: self.ops.index(ix) for q, ix in self.plan.recv.items()}
+        self.halo_entries = self.plan.volume()
+
+    def _partition(self, psi, dpsi, psi_plan=None):
+        self._exchange(psi, dpsi, psi_plan)
+
+    def _repartition(self, dpsi: float, trial: bool):
+        psi_own = self.ops.owned("psi")
+        x_own = self.ops.owned("x") if trial else None
+        self._exchange(psi_own, dpsi, psi_own + self._alpha * x_own if trial else None, x_own)
+
+    def _start(self, psi_init):
+        t = self.torch
+        cold = psi_init is None
+        if cold:
+            psi0 = (3.0 * self.own_nu / (4.0 * np.pi)) ** (2.0 / 3.0)
+        else:
+            psi0 = t.as_tensor(psi_init, dtype=t.float64, device=self.gid.device)
+        if psi0.numel():
+            mm = t.stack([-psi0.min(), psi0.max()])
+        else:
+            mm = t.tensor([-np.inf, -np.inf], dtype=t.float64, device=psi0.device)
+        if self.comm.gloo and mm.is_cuda:
+            mm = mm.cpu()
+        mm = self.comm.all_reduce(mm, "max")
+        lo_, hi_ = -float(mm[0]), float(mm[1])
+        self._partition(psi0, max(hi_ - lo_, 0.0) if np.isfinite(hi_) else 0.0)
+        return cold

@@ -170,6 +170,34 @@ class NumpyOps:
         self._n("r")[r] -= alpha * s[r]
         self._n("z")[r] = self._n("r")[r] / self._n("diag")[r]
 
+    # device-side convergence variant (dist_solver.CudaOps.cg1_step_conv)
+    def cg1_conv_reset(self):
+        self.conv = [0.0, 0]  # done, iterations
+        self.bb = 0.0
+
+    def cg1_spmv_dots_c(self):
+        if self.conv[0]:
+            return torch.zeros(3, dtype=torch.float64)
+        return self.cg1_spmv_dots()
+
+    def cg1_step_conv(self, red, rtol, max_iter):
+        if self.conv[0]:
+            return
+        it, rr = self.conv[1], float(red[2])
+        if it == 0:
+            self.bb = rr
+            if not rr > 0.0:
+                self.conv[0] = 1.0
+                return
+        elif np.sqrt(rr) <= rtol * np.sqrt(self.bb) or it >= max_iter or not np.isfinite(rr):
+            self.conv[0] = 1.0
+            return
+        self.cg1_step(red, it == 0)
+        self.conv[1] = it + 1
+
+    def cg1_status(self):
+        return bool(self.conv[0]), int(self.conv[1])
+
     def vec(self, name):
         return self.v[name]
 
@@ -182,3 +210,36 @@ class NumpyOps:
     def owned(self, name):
         src = self.psi if name == "psi" else self._n(name)
         return src[self.rows].copy()
+
+
+def _result(self):
+    o = self.slots[0]
+    r = self.rows
+    return {"vol": torch.as_tensor(o["vol"][r]), "cent": torch.as_tensor(np.ascontiguousarray(o["cent"][r]))}
+
+
+NumpyOps.result = _result
+
+
+class NumpyParticleOps:
+    """numpy restatement of pf_fluid_advect / pf_fluid_forces (csrc/pf_newton.cu
+    k_advect, k_forces) on CPU tensors, for the distributed fluid step tests."""
+
+    def advect(self, x, v, dt, lo, hi, tau):
+        X, V = x.numpy(), v.numpy()
+        lo_ = np.asarray(lo, np.float64) + tau
+        hi_ = np.asarray(hi, np.float64) - tau
+        p = X + dt * V
+        below, above = p < lo_, p > hi_
+        p = np.where(below, lo_ + (lo_ - p), p)
+        V[below] = -V[below]
+        above = p > hi_
+        p = np.where(above, hi_ - (p - hi_), p)
+        V[above] = -V[above]
+        X[:] = np.minimum(np.maximum(p, lo_), hi_)
+
+    def forces(self, x, cent, nu, rho, v, dt, eps, g, spring):
+        m = (rho * nu).numpy()[:, None]
+        ks = (m if spring == 0 else np.ones_like(m)) * (1.0 / (eps * eps))
+        f = ks * (cent.numpy() - x.numpy()) + m * np.asarray(g, np.float64)[None, :]
+        v.numpy()[:] += dt * f / m
