@@ -195,9 +195,16 @@ def dist_newton(sc, dom, ws):
     import torch
     import torch.distributed as dist
 
-    from paper_2601_05765_b200 import dist_solver
+    from paper_2601_05765_b200 import dist_solver, partition
 
-    solver = dist_solver.DistNewton(sc.pts, sc.nu, dom)
+    # exchange data plane: every rank starts from the sites of its own slab
+    # (ghosts and the CG halo plan come from all-to-alls, halo.SlabComm)
+    rank = dist.get_rank()
+    cuts = partition.slab_cuts(sc.pts[:, 0], ws)
+    gid = np.nonzero(partition.slab_owner(sc.pts[:, 0], ws, cuts=cuts) == rank)[0]
+    dev = "cuda"
+    solver = dist_solver.DistNewtonLocal(torch.as_tensor(gid, device=dev), torch.as_tensor(sc.pts[gid], device=dev),
+                                         torch.as_tensor(sc.nu[gid], device=dev), dom, cuts)
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -216,8 +223,8 @@ def dist_newton(sc, dom, ws):
               "cg_iterations": st["cg_iterations"], "worst_initial": st["worst_initial"],
               "worst_final": st["worst_final"], "status": st["status_name"],
               "start": "cold (kappa (3 nu/4 pi)^(2/3))", "eps_vol": 0.01, "n": sc.n,
-              "partition": f"{ws} x-slabs, halo {st['halo_entries']} entries/rank, "
-                           f"{st['repartitions']} re-partitions"}
+              "partition": f"{ws} x-slabs (owned sites per rank, ghosts by all-to-all), halo "
+                           f"{st['halo_entries']} entries/rank, {st['repartitions']} re-partitions"}
     return torch.as_tensor(psi, device="cuda"), newton
 
 
@@ -425,8 +432,16 @@ def main():
     dpsi = partition.global_dpsi(psi_h) if ws > 1 else float(max(psi_h.max() - psi_h.min(), 0.0))
 
     if ws > 1:
-        slab = partition.slab_partition(sc.pts, psi_h, dpsi, ws, rank)
-        idx, owned = slab.local_to_global, slab.owned_local
+        # exchange data plane: owned sites of this rank's slab, ghosts from the
+        # other ranks' owned sites within this rank's search radius (all-to-all)
+        from paper_2601_05765_b200 import dist_solver, halo
+
+        cuts = partition.slab_cuts(sc.pts[:, 0], ws)
+        gid = np.nonzero(partition.slab_owner(sc.pts[:, 0], ws, cuts=cuts) == rank)[0]
+        sl = halo.SlabComm(cuts, dist_solver.Comm())
+        loc = sl.ghosts(torch.as_tensor(gid, device="cuda"), {"pts": torch.as_tensor(sc.pts[gid], device="cuda")},
+                        halo.ghost_margin(psi_h[gid], dpsi, 1.0))
+        idx, owned = loc.gid.cpu().numpy(), loc.owned.cpu().numpy().astype(np.int32)
     else:
         idx, owned = np.arange(sc.n), None
     pts_l = torch.as_tensor(np.ascontiguousarray(sc.pts[idx]), device="cuda")

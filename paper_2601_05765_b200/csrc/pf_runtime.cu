@@ -20,6 +20,12 @@
 
 using namespace pf;
 
+// the block-synchronous evaluation kernel lives in pf_eval.cu
+int pf_internal_eval_sync_attr();
+int pf_internal_eval_sync(const CellIn &in, const CellOut &out, int count, const Poly<FastCaps> *gpoly,
+                          const uint8_t *stage, int *retry_list, int *counters, unsigned long long *err, int nsm,
+                          cudaStream_t st);
+
 namespace {
 
 thread_local std::string g_err;
@@ -289,14 +295,14 @@ __global__ void k_grid_export(const int *__restrict__ bstart, int ncell, const i
     for (int64_t i = t; i < n; i += st) sid64[i] = sid[i];
 }
 
-// The whole counting sort as ONE cooperative kernel (three grid barriers):
+// The whole counting sort as ONE cooperative kernel (four grid barriers):
 //   1. bucket id of every site, histogram (shared counts start at zero)
 //   2. exclusive scan of the counts: per-block chunk sums, every block adds the
 //      sums of the blocks before it, then scans its chunk
 //   3. scatter, the counts serving as decrementing cursors (they end at zero,
 //      so the next build needs no memset)
 //   4. per bucket (by its first slot: work ~ n, not ~ the bucket count): order
-//      by site index (== numpy's stable argsort) and write the SoA copy
+//      by site index (== numpy's stable argsort); then the SoA copy
 constexpr int GRID_T = 1024;
 __global__ void __launch_bounds__(GRID_T, 1) k_grid_coop(const double *__restrict__ pts, int64_t n, double lo0,
                                                        double lo1, double lo2, double ih0, double ih1, double ih2,
@@ -403,11 +409,20 @@ __global__ void __launch_bounds__(GRID_T, 1) k_grid_coop(const double *__restric
         __syncthreads();
     }
     grid.sync();
-    for (int64_t i = t0; i < n; i += T) {
-        const int l = bid[i];
-        sid[bstart[l] + atomicSub(&bcount[l], 1) - 1] = (int)i;
+    // scatter, four sites per thread in flight
+    for (int64_t i0 = t0; i0 < n; i0 += 4 * T) {
+        int l[4], st[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) l[u] = i0 + u * T < n ? bid[i0 + u * T] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++) st[u] = l[u] >= 0 ? bstart[l[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (l[u] >= 0) sid[st[u] + atomicSub(&bcount[l[u]], 1) - 1] = (int)(i0 + u * T);
     }
     grid.sync();
+    // order each bucket by site index (its first slot's thread; most buckets
+    // hold one or two sites)
     for (int64_t k = t0; k < n; k += T) {
         const int l = bid[sid[k]];
         const int a = bstart[l];
@@ -419,10 +434,20 @@ __global__ void __launch_bounds__(GRID_T, 1) k_grid_coop(const double *__restric
             while (j >= a && sid[j] > v) { sid[j + 1] = sid[j]; j--; }
             sid[j + 1] = v;
         }
-        for (int q = a; q < b; q++) {
-            const int i = sid[q];
-            sx[q] = pts[3 * i]; sy[q] = pts[3 * i + 1]; sz[q] = pts[3 * i + 2];
-        }
+    }
+    grid.sync();
+    // SoA copy of the positions in bucket order, four slots per thread in flight
+    for (int64_t k0 = t0; k0 < n; k0 += 4 * T) {
+        int i[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) i[u] = k0 + u * T < n ? sid[k0 + u * T] : -1;
+        double px[4], py[4], pz[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (i[u] >= 0) { px[u] = pts[3 * i[u]]; py[u] = pts[3 * i[u] + 1]; pz[u] = pts[3 * i[u] + 2]; }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (i[u] >= 0) { sx[k0 + u * T] = px[u]; sy[k0 + u * T] = py[u]; sz[k0 + u * T] = pz[u]; }
     }
 }
 
@@ -532,94 +557,8 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }
 
-// Block-synchronous evaluation: blocks of SYNC_WARPS warps (2 per SM), one
-// cell per warp per round; the warps run each phase of the evaluation
-// together (__syncthreads between phases), so the SM's instruction caches
-// hold one phase at a time instead of the whole ~90 KB of evaluation code
-// (measured: the unsynchronised kernel spends half its stall samples on
-// instruction fetch).
-#ifndef PF_SYNC_WARPS
-#define PF_SYNC_WARPS 8
-#endif
-#ifndef PF_SYNC_BLOCKS
-#define PF_SYNC_BLOCKS 2
-#endif
-constexpr int SYNC_WARPS = PF_SYNC_WARPS;
-constexpr int SYNC_BLOCKS = PF_SYNC_BLOCKS;  // blocks per SM
-__global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
-    k_cells_eval_sync(CellIn in, CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
-                      const uint8_t *__restrict__ stage, int *__restrict__ retry_list,
-                      int *__restrict__ counters, unsigned long long *__restrict__ err) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    EWS<FastCaps> *ws = (EWS<FastCaps> *)(smem + (size_t)wid * sizeof(EWS<FastCaps>));
-    int fl = 0;
-    const bool tma = !PF_NO_TMA_LOAD;
-    unsigned phase = 0;
-    if (tma && lane == 0) mbar_init(&ws->u.e.mbar);
-    __syncwarp();
-    for (int base = blockIdx.x * SYNC_WARPS; base < count; base += gridDim.x * SYNC_WARPS) {
-        const int t = base + wid;
-        int i = -1;
-        if (t < count) {
-            i = in.cells ? in.cells[t] : in.g.sid[t];
-            if (stage[i] != 1) i = -1;
-        }
-        const bool act = i >= 0;
-        {
-            // next round's polytope into L2 while this round computes
-            const int tn = t + gridDim.x * SYNC_WARPS;
-            if (tn < count) {
-                const int inext = in.cells ? in.cells[tn] : in.g.sid[tn];
-                const char *pp = (const char *)(gpoly + inext);
-                const int nlines = (int)((sizeof(Poly<FastCaps>) + 127) / 128);
-                if (lane < nlines) asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + 128 * lane));
-            }
-        }
-        double px = 0.0, py = 0.0, pz = 0.0, psi = 0.0;
-        CellRes res;
-        EvalState st;
-        st.done = 1;
-        if (act) {
-            if (tma) poly_load_tma(gpoly + i, ws->P[0], &ws->u.e.mbar, phase);
-            else poly_load(gpoly + i, ws->P[0]);
-            if (lane == 0) {
-                ws->oflow = 0;
-                ws->strict = in.strict;
-                ws->cen_on = out.census16 != nullptr;
-                for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
-            }
-            __syncwarp();
-            px = in.pts[3 * i]; py = in.pts[3 * i + 1]; pz = in.pts[3 * i + 2];
-            psi = in.psi[i];
-            eval_setup(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
-        }
-        __syncthreads();
-        if (!st.done) eval_restrict(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
-        __syncthreads();
-        if (!st.done) eval_integrals(ws, ws->P[0], px, py, pz, psi, in.tol, in.want_m2, &res, &st);
-        __syncthreads();
-        if (!st.done) eval_interior(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
-        for (int a = 0; a < 4; a++) {
-            const bool need = !st.done && st.attempt < 4;
-            if (!__syncthreads_or(need)) break;
-            if (need) eval_patch_attempt(ws, ws->P[0], px, py, pz, psi, in.tol, &res, &st);
-        }
-        __syncthreads();
-        if (!st.done) eval_final(ws, ws->P[0], px, py, pz, psi, in.want_m2, &res, &st);
-        if (act) {
-            const int r = eval_write(ws, in, out, i, 0, res);
-            if (r & FLAG_RETRY) {
-                if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
-            } else {
-                cell_finish(ws, out, i, r);
-                fl |= r & 7;
-            }
-        }
-        __syncthreads();
-    }
-    if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
-}
+// Block-synchronous evaluation kernel: pf_eval.cu (its own translation unit,
+// launched through pf_internal_eval_sync).
 
 // cells that overflowed the fast tier: larger capacities, still in shared memory;
 // their own overflow is queued for the exact tier
@@ -842,9 +781,7 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
                                 (int)(BUILD_WARPS * sizeof(BWS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(EWS<FastCaps>))));
-        CK(cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(SYNC_WARPS * sizeof(EWS<FastCaps>))));
-        CK(cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        if (pf_internal_eval_sync_attr()) return -1;
         CK(cudaFuncSetAttribute(k_cells_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(MID_WARPS * sizeof(WS<MidCaps>))));
         c->mid = !getenv("PF_NO_MID");
@@ -922,9 +859,9 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
         if (sev) CK(cudaEventRecord(sev[1], st));
         g_launches++;
         if (c->eval_sync) {
-            const int64_t sb = std::min<int64_t>(c->nsm * SYNC_BLOCKS, (count + SYNC_WARPS - 1) / SYNC_WARPS);
-            k_cells_eval_sync<<<(int)sb, SYNC_WARPS * 32, SYNC_WARPS * sizeof(EWS<FastCaps>), st>>>(
-                in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
+            if (pf_internal_eval_sync(in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err,
+                                      c->nsm, st))
+                return -1;
         } else {
             k_cells_eval<<<(int)eblocks, FAST_WARPS * 32, FAST_WARPS * sizeof(EWS<FastCaps>), st>>>(
                 in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);

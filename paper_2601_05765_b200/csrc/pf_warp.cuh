@@ -9,10 +9,10 @@
 
 #if defined(__CUDACC__) && !defined(PF_EMU)
 #define PF_DEV __device__ __forceinline__
-#define PF_DEVNI __device__ __noinline__
+#define PF_DEVNI static __device__ __noinline__
 // out-of-line device function: one copy of the code however many call sites
 // (the cell kernel is instruction-cache bound)
-#define PF_NOINL __device__ __noinline__
+#define PF_NOINL static __device__ __noinline__
 #define PF_FULL 0xffffffffu
 namespace pfw {
 PF_DEV int lane() { return threadIdx.x & 31; }

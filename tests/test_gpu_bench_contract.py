@@ -29,3 +29,26 @@ def test_bench_json_line_contract():
     assert r["bound"] in ("fp64", "hbm", "tensor") and 0 < r["frac"] < 1 and r["peak"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+
+
+def test_bench_two_ranks_one_line():
+    """The torchrun launch the driver uses at N > 1 (two ranks sharing the box's
+    GPU over gloo here): rank 0 prints one line, the partitioned Newton solve
+    runs on the exchange data plane."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, PF_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+                          "--config", "C2", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu", "--no-hbm"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["newton"]["status"] == "converged" and "all-to-all" in d["newton"]["partition"]

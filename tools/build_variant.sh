@@ -14,6 +14,11 @@ else
   rm -rf $SRC; git -C $ROOT worktree prune
   git -C $ROOT worktree add -f --detach $SRC $REF >/dev/null 2>&1
 fi
-make -s -C $SRC/paper_2601_05765_b200/csrc -B OUT=$OUT NVFLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -Xptxas -v $*" > /tmp/ptxas_$NAME.log 2>&1 || { cat /tmp/ptxas_$NAME.log | tail -20; exit 1; }
+# own object directory; extra flags (e.g. -DPF_X=1, EVAL_FMAD=true) through the Makefile
+MK=(); EX=()
+for a in "$@"; do case "$a" in *=*) if [[ "$a" == -* ]]; then EX+=("$a"); else MK+=("$a"); fi;; *) EX+=("$a");; esac; done
+make -s -j6 -C $SRC/paper_2601_05765_b200/csrc OBJDIR=/tmp/pf_obj_$NAME PTXAS_OUT=/tmp/ptxas_$NAME OUT=$OUT \
+    EXTRA="${EX[*]}" "${MK[@]}" > /tmp/make_$NAME.log 2>&1 || { tail -20 /tmp/make_$NAME.log; exit 1; }
+rm -rf /tmp/pf_obj_$NAME
 if [ "$REF" != "-" ]; then git -C $ROOT worktree remove --force $SRC; fi
 echo built $OUT
