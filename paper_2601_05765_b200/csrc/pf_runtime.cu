@@ -652,7 +652,35 @@ __global__ void __launch_bounds__(KNN_WARPS * 32)
     const int64_t nw = (int64_t)gridDim.x * KNN_WARPS;
     for (int64_t t = blockIdx.x * (int64_t)KNN_WARPS + wid; t < nq; t += nw) {
         const double qx = q[3 * t], qy = q[3 * t + 1], qz = q[3 * t + 2];
-        double tlo = -1.0, thi = t0;
+        // first shell sized from the local site density (the 3x3x3 buckets
+        // around q) for ~2k candidates: one gather for most queries
+        double thi = t0;
+        {
+            const GridView &g = in.g;
+            const int bx = bucket_coord(qx, g.lo[0], g.ih[0], g.gn[0]);
+            const int by = bucket_coord(qy, g.lo[1], g.ih[1], g.gn[1]);
+            const int bz = bucket_coord(qz, g.lo[2], g.ih[2], g.gn[2]);
+            int cnt = 0, nb = 0;
+            if (lane < 27) {
+                const int x = bx + lane / 9 - 1, y = by + (lane / 3) % 3 - 1, z = bz + lane % 3 - 1;
+                if (x >= 0 && y >= 0 && z >= 0 && x < g.gn[0] && y < g.gn[1] && z < g.gn[2]) {
+                    const int l = (x * g.gn[1] + y) * g.gn[2] + z;
+                    cnt = g.bstart[l + 1] - g.bstart[l];
+                    nb = 1;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                nb += __shfl_xor_sync(0xffffffffu, nb, o);
+            }
+            if (cnt > 0) {
+                const double vb = 1.0 / (g.ih[0] * g.ih[1] * g.ih[2]);  // bucket volume
+                const double rho = cnt / (nb * vb);
+                const double r3 = 2.0 * k / (4.1887902047863905 * rho);
+                thi = cbrt(r3 * r3);
+            }
+        }
+        double tlo = -1.0;
         int got = 0;
         bool fail = false;
         for (;;) {
