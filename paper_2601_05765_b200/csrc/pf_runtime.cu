@@ -3,6 +3,7 @@
 // evaluation kernels, batched kNN, and the C ABI of include/potflow_b200.h.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -136,6 +137,13 @@ struct pf_ctx {
     int64_t bcount_zero = -1;  // bcount[0..bcount_zero] is all zeros
     int grid_coop_blocks = 0;
     int *grid_part = nullptr;
+    // evaluation order sorted by polytope size (PF_EVAL_SORT, default on)
+    int eval_sort = -1;
+    uint8_t *ekey = nullptr, *ekey2 = nullptr;
+    int *eidx = nullptr, *eidx2 = nullptr;
+    size_t ekey_cap = 0, ekey2_cap = 0, eidx_cap = 0, eidx2_cap = 0;
+    void *esort_tmp = nullptr;
+    size_t esort_cap = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -490,7 +498,7 @@ constexpr int BUILD_WARPS = PF_BUILD_WARPS;
 __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
     k_cells_build(CellIn in, CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
                   uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
-                  unsigned long long *__restrict__ err) {
+                  unsigned long long *__restrict__ err, uint8_t *__restrict__ ekey, int *__restrict__ eidx) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     BWS<FastCaps> *ws = (BWS<FastCaps> *)(smem + (size_t)wid * sizeof(BWS<FastCaps>));
@@ -505,11 +513,19 @@ __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
             poly_store_tma(ws->P[which], gpoly + i);
             if (lane == 0) {
                 stage[i] = 1;
+                if (ekey) {  // evaluation order: larger polytopes first (sort key ascending)
+                    const int nl = ws->P[which].nl;
+                    ekey[t] = (uint8_t)(254 - (nl < 254 ? nl : 254));
+                    eidx[t] = i;
+                }
                 if (out.census16)
                     for (int k = 0; k < 16; k++) out.census16[(size_t)i * 16 + k] = ws->cen[k];
             }
         } else {
-            if (lane == 0) stage[i] = 0;
+            if (lane == 0) {
+                stage[i] = 0;
+                if (ekey) { ekey[t] = 255; eidx[t] = i; }  // nothing to evaluate: last
+            }
             if (r & FLAG_RETRY) {
                 if (lane == 0) retry_list[atomicAdd(&counters[0], 1)] = i;
             } else {
@@ -880,14 +896,41 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
     if (c->split && count > 0) {
         if (ensure(&c->gpoly, &c->gpoly_cap, (size_t)n) || ensure(&c->stage, &c->stage_cap, (size_t)n))
             return -1;
+        if (c->eval_sort < 0) {
+            const char *e = getenv("PF_EVAL_SORT");
+            c->eval_sort = !(e && e[0] == '0');
+        }
+        const bool sorted = c->eval_sort && c->eval_sync && count > 4096;
+        if (sorted && (ensure(&c->ekey, &c->ekey_cap, (size_t)count) || ensure(&c->ekey2, &c->ekey2_cap, (size_t)count) ||
+                       ensure(&c->eidx, &c->eidx_cap, (size_t)count) || ensure(&c->eidx2, &c->eidx2_cap, (size_t)count)))
+            return -1;
         g_launches++;
         k_cells_build<<<(int)bblocks, BUILD_WARPS * 32, BUILD_WARPS * sizeof(BWS<FastCaps>), st>>>(
-            in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err);
+            in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err,
+            sorted ? c->ekey : nullptr, sorted ? c->eidx : nullptr);
         CK(cudaGetLastError());
         if (sev) CK(cudaEventRecord(sev[1], st));
         g_launches++;
         if (c->eval_sync) {
-            if (pf_internal_eval_sync(in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err,
+            CellIn ein = in;
+            int ecount = (int)count;
+            if (sorted) {
+                // The 8 warps of an evaluation block run every phase in lockstep,
+                // so a round costs its largest cell: similar cells share rounds.
+                size_t need = 0;
+                cub::DeviceRadixSort::SortPairs(nullptr, need, c->ekey, c->ekey2, c->eidx, c->eidx2, ecount, 0, 8, st);
+                if (need > c->esort_cap) {
+                    if (c->esort_tmp) cudaFree(c->esort_tmp);
+                    CK(cudaMalloc(&c->esort_tmp, need));
+                    c->esort_cap = need;
+                }
+                CK(cub::DeviceRadixSort::SortPairs(c->esort_tmp, need, c->ekey, c->ekey2, c->eidx, c->eidx2, ecount,
+                                                   0, 8, st));
+                g_launches += 2;
+                ein.cells = c->eidx2;
+                ein.ncells = ecount;
+            }
+            if (pf_internal_eval_sync(ein, out, ecount, c->gpoly, c->stage, c->retry_list, c->counters, c->err,
                                       c->nsm, st))
                 return -1;
         } else {
@@ -1106,7 +1149,8 @@ int pf_ctx_destroy(pf_ctx *c) {
     if (!c) return 0;
     void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
                     c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
-                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2, c->csr_cnt, c->csr_off, c->grid_part};
+                    c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2, c->csr_cnt, c->csr_off, c->grid_part,
+                    c->ekey, c->ekey2, c->eidx, c->eidx2, c->esort_tmp};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
