@@ -14,6 +14,10 @@
 
 using namespace pf;
 
+// the cell kernels read their CellIn / CellOut parameters in place (param
+// space) instead of from a local-memory copy (C4: 103.4 -> 100.4 ms)
+#define PF_KPARAM const __grid_constant__
+
 extern int pf_internal_set_err(const char *msg);
 extern unsigned long long pf_internal_launches_add(unsigned long long k);
 
@@ -37,7 +41,7 @@ namespace {
 constexpr int SYNC_WARPS = PF_SYNC_WARPS;
 constexpr int SYNC_BLOCKS = PF_SYNC_BLOCKS;  // blocks per SM
 __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
-    k_cells_eval_sync(CellIn in, CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
+    k_cells_eval_sync(PF_KPARAM CellIn in, PF_KPARAM CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
                       const uint8_t *__restrict__ stage, int *__restrict__ retry_list,
                       int *__restrict__ counters, unsigned long long *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem[];

@@ -21,6 +21,10 @@
 
 using namespace pf;
 
+// the cell kernels read their CellIn / CellOut parameters in place (param
+// space) instead of from a local-memory copy (C4: 103.4 -> 100.4 ms)
+#define PF_KPARAM const __grid_constant__
+
 // the block-synchronous evaluation kernel lives in pf_eval.cu
 int pf_internal_eval_sync_attr();
 int pf_internal_eval_sync(const CellIn &in, const CellOut &out, int count, const Poly<FastCaps> *gpoly,
@@ -496,7 +500,7 @@ constexpr int BUILD_WARPS = PF_BUILD_WARPS;
 #define PF_BUILD_MINB 3
 #endif
 __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
-    k_cells_build(CellIn in, CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
+    k_cells_build(PF_KPARAM CellIn in, PF_KPARAM CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
                   uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
                   unsigned long long *__restrict__ err, uint8_t *__restrict__ ekey, int *__restrict__ eidx) {
     extern __shared__ __align__(16) unsigned char smem[];
