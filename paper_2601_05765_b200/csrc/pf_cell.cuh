@@ -134,9 +134,10 @@ struct alignas(16) EvalScratch {  // 16-byte multiple: the evaluation workspaces
 
 // per-warp workspaces.  WS: both phases (fused and reference-capacity
 // kernels); BWS / EWS: what the split build / evaluate kernels need.
-template <class C_, int NP, class U>
+template <class C_, int NP, class U, bool CEN_ = true>
 struct alignas(16) WSX {  // 16-byte multiple: every warp's polytope stays TMA-aligned
     using Cap = C_;
+    static constexpr bool CEN = CEN_;  // census code compiled in (the timed kernels leave it out)
     Poly<C_> P[NP];
     U u;
     // one word of per-cell flags: the build workspace is sized to the byte
@@ -153,6 +154,12 @@ template <class C> struct EU { EvalScratch<C> e; };
 template <class C> using WS = WSX<C, 2, BEU<C>>;
 template <class C> using BWS = WSX<C, 2, BU<C>>;
 template <class C> using EWS = WSX<C, 1, EU<C>>;
+// the same without the census code: the split kernels' timed instantiations
+template <class C> using BWSN = WSX<C, 2, BU<C>, false>;
+template <class C> using EWSN = WSX<C, 1, EU<C>, false>;
+// census requested for this cell (never, where the workspace leaves it out)
+template <class W>
+PF_DEV bool cen_on(const W *ws) { return W::CEN && ws->cen_on; }
 
 
 // census slots:
@@ -217,12 +224,33 @@ struct CellOut {
 };
 
 PF_DEV double sq(double x) { return x * x; }
+// the evaluation's phases and their single-call-site helpers inlined into the
+// kernel (each has one call site per kernel, so the code does not grow; the
+// phase-synchronous kernel keeps its instruction-cache footprint): C4
+// evaluation 41.4 -> 38.0 ms.  PF_EVAL_INL=0: out of line.
+#ifndef PF_EVAL_INL
+#define PF_EVAL_INL 1
+#endif
+#if PF_EVAL_INL
+#define PF_PHASE PF_DEV
+#else
+#define PF_PHASE PF_NOINL
+#endif
 // one out-of-line copy of the (long) double-precision atan2
 PF_NOINL double atan2_ool(double y, double x) { return atan2(y, x); }
-// out-of-line IEEE division / square root: same bits as the inline operators,
-// one copy of the code (the evaluation kernel is instruction-cache bound)
+// IEEE division / square root inline (PF_MATH_INL=0: one out-of-line copy
+// each; inline measured faster once the evaluation phases were inlined: C4
+// evaluation 38.0 -> 36.7 ms)
+#ifndef PF_MATH_INL
+#define PF_MATH_INL 1
+#endif
+#if PF_MATH_INL
+PF_DEV double ddiv(double a, double b) { return a / b; }
+PF_DEV double dsqrt(double x) { return sqrt(x); }
+#else
 PF_NOINL double ddiv(double a, double b) { return a / b; }
 PF_NOINL double dsqrt(double x) { return sqrt(x); }
+#endif
 
 // _kernels.py:59-80
 PF_DEV void perp_basis_inl(double nx, double ny, double nz, double *e) {
@@ -276,16 +304,20 @@ PF_DEV bool ang_lt(double xu, double yu, double xv, double yv) {
     return xu > 0.0;  // 0 before pi in the upper half
 }
 
-// max_v |v - p| (the running "rfar" of _kernels.py:1230-1237, 1341-1354)
+// max_v |v - p|^2 and max_v |v - p| (the running "rfar" of _kernels.py:1230-1237, 1341-1354)
 template <class C>
-PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
+PF_DEV double poly_rfar2(const Poly<C> &A, double px, double py, double pz) {
     double m = 0.0;
     #pragma unroll 1
     for (int v = pfw::lane(); v < A.nv; v += 32) {
         double d2 = sq(A.x[v] - px) + sq(A.y[v] - py) + sq(A.z[v] - pz);
         if (d2 > m) m = d2;
     }
-    return sqrt(pfw::max_d_inl(m));
+    return pfw::max_d_inl(m);
+}
+template <class C>
+PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
+    return sqrt(poly_rfar2(A, px, py, pz));
 }
 
 // ---------------------------------------------------------------------------
@@ -306,7 +338,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
     const int L = pfw::lane();
     const unsigned lt = pfw::lanemask_lt();
     const int nv = A.nv, nf = A.nf;
-    if (ws->cen_on && L == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += nv; }
+    if (cen_on(ws) && L == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += nv; }
 
     // 1. classify vertices (_kernels.py:121-134) and 2. keep the inside
     // ones in order (_kernels.py:137-147); one pass when nv <= 32 (the signed
@@ -478,7 +510,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         NFirst += pfw::popc(m);
     }
     const int NVB = K + NFirst;
-    if (ws->cen_on && L == 0) ws->cen[CEN_NEWV] += NFirst;
+    if (cen_on(ws) && L == 0) ws->cen[CEN_NEWV] += NFirst;
     if (NVB > C::CV || NFk > C::CF || NLk > C::CL) {
         if (!C::EXACT && L == 0) ws->oflow = 1;
         pfw::sync();
@@ -625,7 +657,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         *rfar2 = pfw::max_d_inl(rmax);
         if (L == 0) {
             B.nv = NVB; B.nf = NF2; B.nl = NL2;
-            if (ws->cen_on) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += NVB; }
+            if (cen_on(ws)) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += NVB; }
         }
         pfw::sync();
         return CLIP_CUT;
@@ -664,7 +696,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
     *rfar2 = -1.0;
     if (L == 0) {
         B.nv = nref; B.nf = NF2; B.nl = NL2;
-        if (ws->cen_on) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += nref; }
+        if (cen_on(ws)) { ws->cen[CEN_NFV] += ncp; ws->cen[CEN_CUTS]++; ws->cen[CEN_RFAR] += nref; }
     }
     pfw::sync();
     return CLIP_CUT;
@@ -865,7 +897,15 @@ PF_DEV double cell_slack(const GridView &g, double px, double py, double pz, dou
 // later shells (t_lo > 0) out of line: the first shell -- the only one of most
 // cells at converged weights -- keeps the lean single-run gather
 template <class W>
-PF_NOINL int gather_later(W *ws, const CellIn &in, int self, double px, double py, double pz, double t_lo,
+#ifndef PF_GATHER_INL
+#define PF_GATHER_INL 0
+#endif
+#if PF_GATHER_INL
+PF_DEV
+#else
+PF_NOINL
+#endif
+int gather_later(W *ws, const CellIn &in, int self, double px, double py, double pz, double t_lo,
                           double t_hi, bool *all_sites) {
     return gather_shell<true>(ws, in, self, px, py, pz, t_lo, t_hi, all_sites);
 }
@@ -875,7 +915,15 @@ PF_NOINL int gather_later(W *ws, const CellIn &in, int self, double px, double p
 // returns 0 ok / 1 empty / 3 overflow; *which = buffer holding the cell
 // ---------------------------------------------------------------------------
 template <class W>
-PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
+#ifndef PF_BUILD_CELL_INL
+#define PF_BUILD_CELL_INL 1  // build_cell inlined into its kernels (out of line: C4 build 49.7 -> 57.8 ms)
+#endif
+#if PF_BUILD_CELL_INL
+PF_DEV
+#else
+PF_NOINL
+#endif
+int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
     using C = typename W::Cap;
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const double psii = in.psi[i];
@@ -907,7 +955,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
     #pragma unroll 1
     for (;;) {
         bool all_sites = false;
-        if (ws->cen_on && pfw::lane() == 0) ws->cen[CEN_GATH]++;
+        if (cen_on(ws) && pfw::lane() == 0) ws->cen[CEN_GATH]++;
         int nc = t_lo > 0.0 ? gather_later(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites)
                             : gather_shell<false>(ws, in, i, px, py, pz, t_lo, t_hi, &all_sites);
         if (nc > C::CC) {
@@ -978,7 +1026,7 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
             // s > tol.  Skip it (exact: the margin dwarfs the rounding of s, h
             // and rfar).  Same census as the classification.
             if (ddc - (nxc * px + nyc * py + nzc * pz) > rfar * (1.0 + 1e-12) + 1e-12) {
-                if (ws->cen_on && pfw::lane() == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += ws->P[which].nv; }
+                if (cen_on(ws) && pfw::lane() == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += ws->P[which].nv; }
                 continue;
             }
             double rfar2;
@@ -987,8 +1035,14 @@ PF_NOINL int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *ncl
             if (st == CLIP_OVERFLOW) { *which_out = which; *nclips = ncl; return 3; }
             if (st == CLIP_CUT) {
                 which = 1 - which;
-                rfar = rfar2 >= 0.0 ? sqrt(rfar2) : poly_rfar(ws->P[which], px, py, pz);
-                stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
+                // rfar and the stop radius from max |v - p|^2 as two independent
+                // square roots (the reference squares the rounded rfar; the stop
+                // radius only has to bound the cutting sites, which it does with a
+                // margin of tol over the ulps: a site at the boundary leaves every
+                // vertex within rounding of its plane)
+                if (rfar2 < 0.0) rfar2 = poly_rfar2(ws->P[which], px, py, pz);
+                rfar = sqrt(rfar2);
+                stop_r = rfar + sqrt(rfar2 + dpsi_s);
                 if (ball_aware && br < stop_r) stop_r = br;
             }
         }
@@ -1057,7 +1111,7 @@ PF_DEV int twin_facet(const EvalScratch<C> &E, const Poly<C> &P, int f, int a, i
 // Returns 0, 1 on a facet with more than MAX_P boundary points (the
 // reference's kind -1), 2 on pool overflow.
 template <class W>
-PF_NOINL int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                           double psi, double R, double tol) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -1359,7 +1413,7 @@ PF_DEV bool seg_last(int key) {
 // (cross, dot), instead of 2 atan2 + 8 sin/cos per arc.  Agrees with the
 // reference to rounding.
 template <class W>
-PF_NOINL void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                              double tol) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -1544,7 +1598,7 @@ PF_NOINL int conn_circle(const EvalScratch<C> &E, int i, int j, bool arc, double
 // (from the end tangent of pred(q) -> q and the start tangent of its own
 // connector).  Per facet: E.fpa = the clamped patch area, E.funs = unstable.
 template <class W>
-PF_NOINL void ring_patches(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE void ring_patches(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                            double psi, double R, double tol, double cx, double cy, double cz) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -1665,7 +1719,7 @@ struct EvalState {
 
 // _kernels.py:1008-1026: defaults, vertex-in-ball flags, twin-facet table
 template <class W>
-PF_NOINL void eval_setup(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE void eval_setup(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                          double psi, double tol, CellRes *res, EvalState *st) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -1708,7 +1762,7 @@ PF_NOINL void eval_setup(W *ws, const Poly<typename W::Cap> &P, double px, doubl
 
 // restriction of every facet (_kernels.py:1027-1040)
 template <class W>
-PF_NOINL void eval_restrict(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE void eval_restrict(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                             double psi, double tol, CellRes *res, EvalState *st) {
     const int rst = restrict_all(ws, P, px, py, pz, psi, st->R, tol);
     if (rst == 2) {
@@ -1724,7 +1778,7 @@ PF_NOINL void eval_restrict(W *ws, const Poly<typename W::Cap> &P, double px, do
 
 // facet integrals, full-ball / empty decision (_kernels.py:1041-1092)
 template <class W>
-PF_NOINL void eval_integrals(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE void eval_integrals(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                              double psi, double tol, int want_m2, CellRes *res, EvalState *st) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -1753,7 +1807,7 @@ PF_NOINL void eval_integrals(W *ws, const Poly<typename W::Cap> &P, double px, d
         }
     }
     pfw::sync();
-    if (ws->cen_on) {
+    if (cen_on(ws)) {
         int cross = 0, seg = 0, arc = 0, bp = 0, proj = 0, fc = 0;
         #pragma unroll 1
         for (int f = L; f < nf; f += 32) fc += E.fkind[f] == RF_FULLCIRCLE;
@@ -1804,7 +1858,7 @@ PF_NOINL void eval_integrals(W *ws, const Poly<typename W::Cap> &P, double px, d
 // interior point (_kernels.py:723-816): ray per restricted facet, lane per
 // facet; the ray midpoints and margins reuse the facet-frame slots
 template <class W>
-PF_NOINL void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                             double psi, double tol, CellRes *res, EvalState *st) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -1905,7 +1959,7 @@ PF_NOINL void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, do
 
 // one attempt of the occluded areas with perturb-and-retry (_kernels.py:1100-1128)
 template <class W>
-PF_NOINL void eval_patch_attempt(W *ws, const Poly<typename W::Cap> &P, double px, double py,
+PF_PHASE void eval_patch_attempt(W *ws, const Poly<typename W::Cap> &P, double px, double py,
                                  double pz, double psi, double tol, CellRes *res, EvalState *st) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -1945,7 +1999,7 @@ PF_NOINL void eval_patch_attempt(W *ws, const Poly<typename W::Cap> &P, double p
 
 // K, volume, centroid, second moment (_kernels.py:1130-1170)
 template <class W>
-PF_NOINL void eval_final(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
+PF_PHASE void eval_final(W *ws, const Poly<typename W::Cap> &P, double px, double py, double pz,
                          double psi, int want_m2, CellRes *res, EvalState *st) {
     using C = typename W::Cap;
     EvalScratch<C> &E = ws->u.e;
@@ -2051,8 +2105,9 @@ PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, 
         ws->oflow = 0;
         ws->strict = in.strict;
         ws->cen_on = out.census16 != nullptr;
+        if (W::CEN)
 #pragma unroll 1
-        for (int k = 0; k < 16; k++) ws->cen[k] = 0;
+            for (int k = 0; k < 16; k++) ws->cen[k] = 0;
     }
     pfw::sync();
     int nclips;
@@ -2093,7 +2148,7 @@ PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, 
 
 // Phase B: evaluate the polytope in ws->P[which] and write the outputs.
 template <class W>
-PF_NOINL int eval_write(W *ws, const CellIn &in, const CellOut &out, int i, int which, CellRes r);
+PF_PHASE int eval_write(W *ws, const CellIn &in, const CellOut &out, int i, int which, CellRes r);
 template <class W>
 PF_DEV int cell_phase_eval(W *ws, const CellIn &in, const CellOut &out, int i, int which) {
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
@@ -2103,7 +2158,7 @@ PF_DEV int cell_phase_eval(W *ws, const CellIn &in, const CellOut &out, int i, i
 }
 // write one evaluated cell's outputs (_kernels.py:1441-1474); returns its flags
 template <class W>
-PF_NOINL int eval_write(W *ws, const CellIn &in, const CellOut &out, int i, int which, CellRes r) {
+PF_PHASE int eval_write(W *ws, const CellIn &in, const CellOut &out, int i, int which, CellRes r) {
     const int L = pfw::lane();
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const Poly<typename W::Cap> &P = ws->P[which];
@@ -2147,7 +2202,7 @@ PF_NOINL int eval_write(W *ws, const CellIn &in, const CellOut &out, int i, int 
             }
             nk += pfw::popc(m);
         }
-        if (ws->cen_on && L == 0) { ws->cen[CEN_RFAC] += nk; ws->cen[CEN_RFAC_NF] += nk * P.nf; }
+        if (cen_on(ws) && L == 0) { ws->cen[CEN_RFAC] += nk; ws->cen[CEN_RFAC_NF] += nk * P.nf; }
         if (nk > smf) { nk = smf; flags |= FLAG_OVERFLOW; }
     }
 
@@ -2253,7 +2308,7 @@ PF_DEV void poly_load(const Poly<C> *g, Poly<C> &A) {
 template <class W>
 PF_DEV void cell_finish(W *ws, const CellOut &out, int i, int r) {
     if (!(r & FLAG_RETRY) && pfw::lane() == 0) {
-        if (out.census16)
+        if (W::CEN && out.census16)
 #pragma unroll 1
             for (int k = 0; k < 16; k++) out.census16[(size_t)i * 16 + k] = k < CEN_N ? ws->cen[k] : 0;
         if (out.flags) out.flags[i] = r;

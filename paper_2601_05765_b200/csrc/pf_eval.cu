@@ -40,22 +40,37 @@ namespace {
 #endif
 constexpr int SYNC_WARPS = PF_SYNC_WARPS;
 constexpr int SYNC_BLOCKS = PF_SYNC_BLOCKS;  // blocks per SM
+// EW: EWSN<FastCaps> (timed: no census code) or EWS<FastCaps> (the census pass)
+template <class EW>
 __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
     k_cells_eval_sync(PF_KPARAM CellIn in, PF_KPARAM CellOut out, int count, const Poly<FastCaps> *__restrict__ gpoly,
                       const uint8_t *__restrict__ stage, int *__restrict__ retry_list,
                       int *__restrict__ counters, unsigned long long *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    EWS<FastCaps> *ws = (EWS<FastCaps> *)(smem + (size_t)wid * sizeof(EWS<FastCaps>));
+    EW *ws = (EW *)(smem + (size_t)wid * sizeof(EW));
     int fl = 0;
     const bool tma = !PF_NO_TMA_LOAD;
     unsigned phase = 0;
     if (tma && lane == 0) mbar_init(&ws->u.e.mbar);
     __syncwarp();
+#ifndef PF_EVAL_PIPE_IDX
+#define PF_EVAL_PIPE_IDX 1  // next round's cell index and stage byte loaded a round ahead
+#endif
+    int i_nx = -1;  // this warp's next cell (or -1), loaded during the previous round
+    if (PF_EVAL_PIPE_IDX) {
+        const int t0 = blockIdx.x * SYNC_WARPS + wid;
+        if (t0 < count) {
+            const int i0 = in.cells ? in.cells[t0] : in.g.sid[t0];
+            i_nx = stage[i0] == 1 ? i0 : -1;
+        }
+    }
     for (int base = blockIdx.x * SYNC_WARPS; base < count; base += gridDim.x * SYNC_WARPS) {
         const int t = base + wid;
         int i = -1;
-        if (t < count) {
+        if (PF_EVAL_PIPE_IDX) {
+            i = i_nx;
+        } else if (t < count) {
             i = in.cells ? in.cells[t] : in.g.sid[t];
             if (stage[i] != 1) i = -1;
         }
@@ -63,11 +78,13 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
         {
             // next round's polytope into L2 while this round computes
             const int tn = t + gridDim.x * SYNC_WARPS;
+            i_nx = -1;
             if (tn < count) {
                 const int inext = in.cells ? in.cells[tn] : in.g.sid[tn];
                 const char *pp = (const char *)(gpoly + inext);
                 const int nlines = (int)((sizeof(Poly<FastCaps>) + 127) / 128);
                 if (lane < nlines) asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + 128 * lane));
+                if (PF_EVAL_PIPE_IDX) i_nx = stage[inext] == 1 ? inext : -1;
             }
         }
         double px = 0.0, py = 0.0, pz = 0.0, psi = 0.0;
@@ -81,7 +98,8 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
                 ws->oflow = 0;
                 ws->strict = in.strict;
                 ws->cen_on = out.census16 != nullptr;
-                for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
+                if (EW::CEN)
+                    for (int k = 0; k < 16; k++) ws->cen[k] = out.census16 ? out.census16[(size_t)i * 16 + k] : 0;
             }
             __syncwarp();
             px = in.pts[3 * i]; py = in.pts[3 * i + 1]; pz = in.pts[3 * i + 2];
@@ -118,10 +136,13 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
 }  // namespace
 
 int pf_internal_eval_sync_attr() {
-    cudaError_t e = cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(SYNC_WARPS * sizeof(EWS<FastCaps>)));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_cells_eval_sync, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    static_assert(sizeof(EWSN<FastCaps>) == sizeof(EWS<FastCaps>), "one launch shape for both evaluation kernels");
+    cudaError_t e = cudaSuccess;
+    for (const void *kf : {(const void *)k_cells_eval_sync<EWSN<FastCaps>>, (const void *)k_cells_eval_sync<EWS<FastCaps>>}) {
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SYNC_WARPS * sizeof(EWS<FastCaps>)));
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
     if (e != cudaSuccess) {
         char b[256];
         snprintf(b, sizeof b, "pf_eval.cu: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -135,8 +156,9 @@ int pf_internal_eval_sync(const CellIn &in, const CellOut &out, int count, const
                           cudaStream_t st) {
     const int64_t sb = std::min<int64_t>((int64_t)nsm * SYNC_BLOCKS, (count + SYNC_WARPS - 1) / SYNC_WARPS);
     if (sb <= 0) return 0;
-    k_cells_eval_sync<<<(int)sb, SYNC_WARPS * 32, SYNC_WARPS * sizeof(EWS<FastCaps>), st>>>(
-        in, out, count, gpoly, stage, retry_list, counters, err);
+    auto ke = out.census16 ? k_cells_eval_sync<EWS<FastCaps>> : k_cells_eval_sync<EWSN<FastCaps>>;
+    ke<<<(int)sb, SYNC_WARPS * 32, SYNC_WARPS * sizeof(EWS<FastCaps>), st>>>(in, out, count, gpoly, stage, retry_list,
+                                                                             counters, err);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         char b[256];

@@ -499,13 +499,15 @@ constexpr int BUILD_WARPS = PF_BUILD_WARPS;
 #ifndef PF_BUILD_MINB
 #define PF_BUILD_MINB 3
 #endif
+// BW: BWSN<FastCaps> (timed: no census code) or BWS<FastCaps> (the census pass)
+template <class BW>
 __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
     k_cells_build(PF_KPARAM CellIn in, PF_KPARAM CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
                   uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
                   unsigned long long *__restrict__ err, uint8_t *__restrict__ ekey, int *__restrict__ eidx) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    BWS<FastCaps> *ws = (BWS<FastCaps> *)(smem + (size_t)wid * sizeof(BWS<FastCaps>));
+    BW *ws = (BW *)(smem + (size_t)wid * sizeof(BW));
     const int nw = gridDim.x * BUILD_WARPS;
     int fl = 0;
     for (int t = blockIdx.x * BUILD_WARPS + wid; t < count; t += nw) {
@@ -522,7 +524,7 @@ __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
                     ekey[t] = (uint8_t)(254 - (nl < 254 ? nl : 254));
                     eidx[t] = i;
                 }
-                if (out.census16)
+                if (BW::CEN && out.census16)
                     for (int k = 0; k < 16; k++) out.census16[(size_t)i * 16 + k] = ws->cen[k];
             }
         } else {
@@ -825,8 +827,10 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        CK(cudaFuncSetAttribute(k_cells_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(BUILD_WARPS * sizeof(BWS<FastCaps>))));
+        static_assert(sizeof(BWSN<FastCaps>) == sizeof(BWS<FastCaps>), "one launch shape for both build kernels");
+        for (const void *kf : {(const void *)k_cells_build<BWSN<FastCaps>>, (const void *)k_cells_build<BWS<FastCaps>>})
+            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(BUILD_WARPS * sizeof(BWS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(FAST_WARPS * sizeof(EWS<FastCaps>))));
         if (pf_internal_eval_sync_attr()) return -1;
@@ -837,13 +841,14 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
             const char *e = getenv("PF_EVAL_SYNC");
             c->eval_sync = !(e && e[0] == '0');
         }
-        for (const void *kf : {(const void *)k_cells_build, (const void *)k_cells_eval})
+        for (const void *kf : {(const void *)k_cells_build<BWSN<FastCaps>>, (const void *)k_cells_build<BWS<FastCaps>>,
+                               (const void *)k_cells_eval})
             CK(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         c->split = getenv("PF_FUSED") ? 0 : 1;
         int nb = 0, nbb = 0, nbe = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cells_fast, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(WS<FastCaps>)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, k_cells_build, BUILD_WARPS * 32,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, k_cells_build<BWSN<FastCaps>>, BUILD_WARPS * 32,
                                                          BUILD_WARPS * sizeof(BWS<FastCaps>)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbe, k_cells_eval, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(EWS<FastCaps>)));
@@ -909,7 +914,8 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
                        ensure(&c->eidx, &c->eidx_cap, (size_t)count) || ensure(&c->eidx2, &c->eidx2_cap, (size_t)count)))
             return -1;
         g_launches++;
-        k_cells_build<<<(int)bblocks, BUILD_WARPS * 32, BUILD_WARPS * sizeof(BWS<FastCaps>), st>>>(
+        auto kb = out.census16 ? k_cells_build<BWS<FastCaps>> : k_cells_build<BWSN<FastCaps>>;
+        kb<<<(int)bblocks, BUILD_WARPS * 32, BUILD_WARPS * sizeof(BWS<FastCaps>), st>>>(
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err,
             sorted ? c->ekey : nullptr, sorted ? c->eidx : nullptr);
         CK(cudaGetLastError());

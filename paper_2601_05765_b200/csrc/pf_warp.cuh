@@ -44,20 +44,28 @@ PF_DEV int __builtin_ctz_pf(unsigned m) { return __ffs(m) - 1; }
 // provided by tests/emu/emu_warp.h
 #endif
 
+#ifndef PF_WARP_INL
+#define PF_WARP_INL 0
+#endif
+#if PF_WARP_INL
+#define PF_WRED PF_DEV
+#else
+#define PF_WRED PF_NOINL
+#endif
 namespace pfw {
 // exact (order-independent) warp reductions
-PF_NOINL double max_d(double v) {
+PF_WRED double max_d(double v) {
     for (int m = 16; m > 0; m >>= 1) {
         double o = shfl_xor(v, m);
         v = o > v ? o : v;
     }
     return v;
 }
-PF_NOINL double sum_d(double v) {
+PF_WRED double sum_d(double v) {
     for (int m = 16; m > 0; m >>= 1) v += shfl_xor(v, m);
     return v;
 }
-PF_NOINL int sum_i(int v) {
+PF_WRED int sum_i(int v) {
     for (int m = 16; m > 0; m >>= 1) v += shfl_xor(v, m);
     return v;
 }
@@ -70,7 +78,7 @@ PF_DEV int max_i(int v) {
 }
 // inclusive sum over lanes [first, lane] (first = start of this lane's run of
 // a segmented reduction); fixed shuffle tree, so the result is deterministic
-PF_NOINL double seg_sum_d(double v, int first) {
+PF_WRED double seg_sum_d(double v, int first) {
     for (int o = 1; o < 32; o <<= 1) {
         double y = shfl(v, (lane() - o) & 31);
         if (lane() - o >= first) v += y;
@@ -96,7 +104,7 @@ PF_DEV double max_d_inl(double v) {
     return v;
 }
 // exclusive prefix over lanes of an int
-PF_NOINL int excl_scan_i(int v, int *total) {
+PF_WRED int excl_scan_i(int v, int *total) {
     int x = v;
     for (int o = 1; o < 32; o <<= 1) {
         int y = shfl(x, (lane() - o) & 31);
