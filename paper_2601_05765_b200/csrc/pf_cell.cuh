@@ -237,7 +237,23 @@ PF_DEV double sq(double x) { return x * x; }
 #define PF_PHASE PF_NOINL
 #endif
 // one out-of-line copy of the (long) double-precision atan2
+#ifndef PF_ATAN2_INL
+#define PF_ATAN2_INL 0
+#endif
+#if PF_ATAN2_INL
+PF_DEV double atan2_ool(double y, double x) { return atan2(y, x); }
+#else
 PF_NOINL double atan2_ool(double y, double x) { return atan2(y, x); }
+#endif
+// the evaluation's multi-call-site helpers (PF_HELPER_INL=1: inline)
+#ifndef PF_HELPER_INL
+#define PF_HELPER_INL 0
+#endif
+#if PF_HELPER_INL
+#define PF_HELPER PF_DEV
+#else
+#define PF_HELPER PF_NOINL
+#endif
 // IEEE division / square root inline (PF_MATH_INL=0: one out-of-line copy
 // each; inline measured faster once the evaluation phases were inlined: C4
 // evaluation 38.0 -> 36.7 ms)
@@ -269,7 +285,7 @@ PF_DEV void perp_basis_inl(double nx, double ny, double nz, double *e) {
     e[4] = nz * e1x - nx * e1z;
     e[5] = nx * e1y - ny * e1x;
 }
-PF_NOINL void perp_basis(double nx, double ny, double nz, double *e) { perp_basis_inl(nx, ny, nz, e); }
+PF_HELPER void perp_basis(double nx, double ny, double nz, double *e) { perp_basis_inl(nx, ny, nz, e); }
 
 template <class C>
 PF_DEV void load_domain(Poly<C> &A, const CellIn &in) {
@@ -1361,7 +1377,7 @@ PF_PHASE int restrict_all(W *ws, const Poly<typename W::Cap> &P, double px, doub
 #define PF_SWEEP_AMBIG 1e-6
 // (never called in parity mode: the reference keeps the wrapped sweep)
 template <class C>
-PF_NOINL bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
+PF_HELPER bool long_arc_impossible(const Poly<C> &P, int f, double qx, double qy, double qz,
                                 double dx, double dy, double dz, double rc, double tol) {
     double dn = dsqrt(dx * dx + dy * dy + dz * dz);
     if (!(dn > 0.0)) return false;
@@ -1494,7 +1510,7 @@ PF_PHASE void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, d
 }
 
 // _kernels.py:819-835
-PF_NOINL void project_from(double cx, double cy, double cz, double yx, double yy, double yz,
+PF_HELPER void project_from(double cx, double cy, double cz, double yx, double yy, double yz,
                          double px, double py, double pz, double psi, double *o) {
     double dx = yx - cx, dy = yy - cy, dz = yz - cz;
     double a = dx * dx + dy * dy + dz * dz;
@@ -1556,7 +1572,7 @@ PF_DEV bool ccw_le(const double *a, const double *b, const double *c, const doub
 // keeps that order, so the test can only fail when the sweep is within
 // rounding of 0 or pi: it is evaluated when sin^2 of the sweep is < 1e-6.
 template <class C>
-PF_NOINL int conn_circle(const EvalScratch<C> &E, int i, int j, bool arc, double nfx, double nfy,
+PF_HELPER int conn_circle(const EvalScratch<C> &E, int i, int j, bool arc, double nfx, double nfy,
                          double nfz, double sf, double cx, double cy, double cz, double px,
                          double py, double pz, double psi, double *m, double *ee, bool *uns) {
     if (arc) {

@@ -44,8 +44,10 @@ PF_DEV int __builtin_ctz_pf(unsigned m) { return __ffs(m) - 1; }
 // provided by tests/emu/emu_warp.h
 #endif
 
+// the warp reductions inline (PF_WARP_INL=0: one out-of-line copy each;
+// inline measured faster: C4 evaluation 36.6 -> 34.1 ms)
 #ifndef PF_WARP_INL
-#define PF_WARP_INL 0
+#define PF_WARP_INL 1
 #endif
 #if PF_WARP_INL
 #define PF_WRED PF_DEV
