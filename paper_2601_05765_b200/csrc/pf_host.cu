@@ -23,6 +23,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -176,14 +178,23 @@ class Pool {
     bool stop_ = false;
 };
 
+// host timeline of one call (PF_HOST_TRACE=1: printed to stderr; dev tool)
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 // completion count of one range's scatter tasks
 struct Job {
     std::mutex m;
     std::condition_variable cv;
     int left = 0;
+    double t_copied = 0.0, t_done = 0.0;  // trace
     void done() {
         std::lock_guard<std::mutex> g(m);
-        if (--left == 0) cv.notify_all();
+        if (--left == 0) {
+            t_done = now_ms();
+            cv.notify_all();
+        }
     }
     void wait() {
         std::unique_lock<std::mutex> l(m);
@@ -362,6 +373,9 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
     }
     cudaStream_t st = h->comp;
     void *sv = (void *)st;
+    static const bool trace = getenv("PF_HOST_TRACE") != nullptr;
+    const double t_start = trace ? now_ms() : 0.0;
+    std::vector<double> t_kern(K, 0.0);
     const std::vector<int64_t> bnd = range_bounds(n, K);
     int64_t h2d = 0, d2h = 0;
     // inputs (the caller's pageable arrays)
@@ -431,6 +445,7 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
         const int slot = k % RING;
         if (k >= RING) jobs[k - RING].wait();  // slot free
         HCK(cudaEventSynchronize(h->ev_tot[k]));
+        if (trace) t_kern[k] = now_ms();
         const int64_t F = h->totals[k];
         const size_t dn = (size_t)m * DENSE_W, fn = (size_t)F * FACET_W;
         if (ensure_pinned(&h->ring[slot], &h->ring_c[slot], dn + fn)) return -1;
@@ -454,6 +469,7 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
         h->pool->submit([=, &o]() {
             cudaSetDevice(dev);
             cudaEventSynchronize(ev);
+            if (trace) job->t_copied = now_ms();
             int64_t acc = 0;
             for (int64_t t = 0; t < m; t++) {
                 o[t] = (int32_t)acc;
@@ -481,6 +497,13 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
     HCK(cudaStreamSynchronize(st));
     HCK(cudaStreamSynchronize(h->copy));
     d2h += (int64_t)sizeof e;
+    if (trace) {
+        fprintf(stderr, "[pf_host] K=%d threads=%d total %.2f ms; per range (ms from start): kernels+pack done / copied / scattered\n",
+                K, T, now_ms() - t_start);
+        for (int k = 0; k < K; k++)
+            fprintf(stderr, "[pf_host] %2d %8.2f %8.2f %8.2f\n", k, t_kern[k] - t_start, jobs[k].t_copied - t_start,
+                    jobs[k].t_done - t_start);
+    }
     h->last_h2d = h2d;
     h->last_d2h = d2h;
     if (h2d_bytes) *h2d_bytes = h2d;
