@@ -57,15 +57,37 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
 #ifndef PF_EVAL_PIPE_IDX
 #define PF_EVAL_PIPE_IDX 1  // next round's cell index and stage byte loaded a round ahead
 #endif
+#ifndef PF_DYN_EVAL
+#define PF_DYN_EVAL 1  // rounds handed out from a global counter (0: grid stride)
+#endif
+    // Rounds of SYNC_WARPS consecutive work items: with PF_DYN_EVAL each block
+    // takes its next round from counters[3] (one round ahead, so the next
+    // round's cells can be prefetched), and the kernel ends with the work, not
+    // with the block whose fixed share was the heaviest.
+    __shared__ int s_round;
+    int base, nb;  // this round's and the next round's first work item
+    if (PF_DYN_EVAL) {
+        __shared__ int s_first[2];
+        if (threadIdx.x == 0) {
+            s_first[0] = atomicAdd(&counters[3], SYNC_WARPS);
+            s_first[1] = atomicAdd(&counters[3], SYNC_WARPS);
+        }
+        __syncthreads();
+        base = s_first[0];
+        nb = s_first[1];
+    } else {
+        base = blockIdx.x * SYNC_WARPS;
+        nb = base + gridDim.x * SYNC_WARPS;
+    }
     int i_nx = -1;  // this warp's next cell (or -1), loaded during the previous round
     if (PF_EVAL_PIPE_IDX) {
-        const int t0 = blockIdx.x * SYNC_WARPS + wid;
+        const int t0 = base + wid;
         if (t0 < count) {
             const int i0 = in.cells ? in.cells[t0] : in.g.sid[t0];
             i_nx = stage[i0] == 1 ? i0 : -1;
         }
     }
-    for (int base = blockIdx.x * SYNC_WARPS; base < count; base += gridDim.x * SYNC_WARPS) {
+    while (base < count) {
         const int t = base + wid;
         int i = -1;
         if (PF_EVAL_PIPE_IDX) {
@@ -77,7 +99,7 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
         const bool act = i >= 0;
         {
             // next round's polytope into L2 while this round computes
-            const int tn = t + gridDim.x * SYNC_WARPS;
+            const int tn = nb + wid;
             i_nx = -1;
             if (tn < count) {
                 const int inext = in.cells ? in.cells[tn] : in.g.sid[tn];
@@ -128,7 +150,10 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
                 fl |= r & 7;
             }
         }
+        if (PF_DYN_EVAL && threadIdx.x == 0) s_round = atomicAdd(&counters[3], SYNC_WARPS);  // the round after next
         __syncthreads();
+        base = nb;
+        nb = PF_DYN_EVAL ? s_round : nb + gridDim.x * SYNC_WARPS;
     }
     if (lane == 0 && fl) atomicOr(err, (unsigned long long)fl);
 }

@@ -39,6 +39,7 @@
 
 extern unsigned long long pf_internal_launches_add(unsigned long long k);
 extern int pf_internal_set_err(const char *msg);
+extern void pf_internal_keep_weights(pf_ctx *c, int on);
 
 namespace {
 
@@ -235,6 +236,8 @@ struct HostPath {
     size_t cub_c = 0;
     int64_t *err = nullptr;
     // pinned
+    double *in_stage = nullptr;  // inputs (pts, psi) staged by the worker pool
+    size_t in_stage_c = 0;
     double *ring[RING] = {nullptr, nullptr, nullptr};
     size_t ring_c[RING] = {0, 0, 0};
     int32_t *totals = nullptr;  // per-range facet totals (pinned)
@@ -259,7 +262,7 @@ HostPath *host_path(pf_ctx *c) {
 int ensure_events(HostPath *h, int K) {
     while ((int)h->ev_tot.size() < K) {
         cudaEvent_t a, b;
-        HCK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        HCK(cudaEventCreate(&a));  // timed: PF_HOST_TRACE reads it
         HCK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
         h->ev_tot.push_back(a);
         h->ev_copy.push_back(b);
@@ -376,16 +379,58 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
     static const bool trace = getenv("PF_HOST_TRACE") != nullptr;
     const double t_start = trace ? now_ms() : 0.0;
     std::vector<double> t_kern(K, 0.0);
+    double t_staged = 0.0, t_queued = 0.0;
+    cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // trace: stream start, inputs on device, grid + ranges sorted
+    if (trace) {
+        for (auto &e : tev) HCK(cudaEventCreate(&e));
+        HCK(cudaEventRecord(tev[0], st));
+    }
     const std::vector<int64_t> bnd = range_bounds(n, K);
     int64_t h2d = 0, d2h = 0;
-    // inputs (the caller's pageable arrays)
-    HCK(cudaMemcpyAsync(h->pts, pts_h, n3 * sizeof(double), cudaMemcpyHostToDevice, st));
-    HCK(cudaMemcpyAsync(h->psi, psi_h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    // inputs (the caller's pageable arrays): the worker pool copies pieces into
+    // pinned staging, each piece's H2D is queued as soon as it is staged
+    // (a pageable cudaMemcpy stages through one driver buffer: C4 ~5 ms -> ~1.5 ms)
+    {
+        if (ensure_pinned(&h->in_stage, &h->in_stage_c, n3 + n)) return -1;
+        constexpr int PIECES = 16;
+        const size_t tot = n3 + n;
+        std::vector<Job> staged(PIECES);
+        double *stg = h->in_stage;
+        for (int q = 0; q < PIECES; q++) {
+            const size_t a = tot * q / PIECES, b = tot * (q + 1) / PIECES;
+            staged[q].left = 1;
+            Job *job = &staged[q];
+            h->pool->submit([=]() {
+                // [0, n3) = pts, [n3, n3 + n) = psi
+                if (a < n3) memcpy(stg + a, pts_h + a, (std::min(b, n3) - a) * sizeof(double));
+                if (b > n3) {
+                    const size_t a2 = std::max(a, n3);
+                    memcpy(stg + a2, psi_h + (a2 - n3), (b - a2) * sizeof(double));
+                }
+                job->done();
+            });
+        }
+        for (int q = 0; q < PIECES; q++) {
+            const size_t a = tot * q / PIECES, b = tot * (q + 1) / PIECES;
+            staged[q].wait();
+            if (a < n3)
+                HCK(cudaMemcpyAsync(h->pts + a, stg + a, (std::min(b, n3) - a) * sizeof(double),
+                                    cudaMemcpyHostToDevice, st));
+            if (b > n3) {
+                const size_t a2 = std::max(a, n3);
+                HCK(cudaMemcpyAsync(h->psi + (a2 - n3), stg + a2, (b - a2) * sizeof(double), cudaMemcpyHostToDevice,
+                                    st));
+            }
+        }
+    }
     HCK(cudaMemcpyAsync(h->bnd, bnd.data(), (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     h2d += (int64_t)((n3 + n) * sizeof(double));
     HCK(cudaMemsetAsync(h->err, 0, sizeof(int64_t), st));
+    if (trace) {
+        t_staged = now_ms();
+        HCK(cudaEventRecord(tev[1], st));
+    }
     if (pf_grid_build(ctx, n, h->pts, h->psi, 0.0, sv)) return -1;
-    if (dpsi_max < 0.0 && pf_dpsi_max(ctx, n, h->psi, nullptr, sv)) return -1;
     if (pf_grid_order(ctx, h->order, sv)) return -1;
     // cells of each index range in bucket order: stable radix sort by range id
     if (K > 1) {
@@ -406,6 +451,7 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
     } else {
         HCK(cudaMemcpyAsync(h->cells, h->order, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     }
+    if (trace) HCK(cudaEventRecord(tev[2], st));
     // per range: cell kernels, pack, facet total
     size_t scan_need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_need, h->cnt, h->off, (int)n + 1, st);
@@ -414,6 +460,12 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
         HCK(cudaMalloc(&h->cub_tmp, scan_need));
         h->cub_c = scan_need;
     }
+    // one (grid, psi) for all ranges: dpsi and the slack bounds computed by the first
+    struct KeepWeights {
+        pf_ctx *c;
+        explicit KeepWeights(pf_ctx *c_) : c(c_) { pf_internal_keep_weights(c, 1); }
+        ~KeepWeights() { pf_internal_keep_weights(c, 0); }
+    } keep(ctx);
     for (int k = 0; k < K; k++) {
         const int64_t i0 = bnd[k], m = bnd[k + 1] - bnd[k];
         if (m <= 0) { h->totals[k] = 0; continue; }
@@ -434,6 +486,7 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
         HCK(cudaMemcpyAsync(h->totals + k, off + m, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         HCK(cudaEventRecord(h->ev_tot[k], st));
     }
+    if (trace) t_queued = now_ms();
     // host: follow the ranges -- D2H of exactly the staged bytes into a pinned
     // ring slot, then the worker pool scatters it into the caller's arrays
     std::vector<Job> jobs(K);
@@ -498,8 +551,15 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
     HCK(cudaStreamSynchronize(h->copy));
     d2h += (int64_t)sizeof e;
     if (trace) {
-        fprintf(stderr, "[pf_host] K=%d threads=%d total %.2f ms; per range (ms from start): kernels+pack done / copied / scattered\n",
-                K, T, now_ms() - t_start);
+        float g_in = 0.f, g_grid = 0.f, g_r0 = 0.f;
+        cudaEventElapsedTime(&g_in, tev[0], tev[1]);
+        cudaEventElapsedTime(&g_grid, tev[1], tev[2]);
+        cudaEventElapsedTime(&g_r0, tev[2], h->ev_tot[0]);
+        fprintf(stderr, "[pf_host] K=%d threads=%d total %.2f ms; host: inputs staged %.2f, all queued %.2f; "
+                "device: inputs %.2f, grid+sort %.2f, range 0 %.2f\n", K, T, now_ms() - t_start, t_staged - t_start,
+                t_queued - t_start, g_in, g_grid, g_r0);
+        for (auto &e : tev) cudaEventDestroy(e);
+        fprintf(stderr, "[pf_host] per range (ms from start): kernels+pack done / copied / scattered\n");
         for (int k = 0; k < K; k++)
             fprintf(stderr, "[pf_host] %2d %8.2f %8.2f %8.2f\n", k, t_kern[k] - t_start, jobs[k].t_copied - t_start,
                     jobs[k].t_done - t_start);

@@ -88,6 +88,10 @@ struct pf_ctx {
     size_t bcount_cap = 0, bstart_cap = 0;
     double *smax = nullptr;  // per super-bucket max weight (build_cell's local slack)
     size_t smax_cap = 0;
+    // a caller evaluating one (grid, psi) in several cell subsets (the host
+    // drop-in's index ranges) computes the weight range and the super-bucket
+    // maxima once: pf_internal_keep_weights
+    bool keep_w = false, have_dpsi = false, have_smax = false;
     int *csr_cnt = nullptr, *csr_off = nullptr;  // pf_facets_csr scratch
     size_t csr_cnt_cap = 0, csr_off_cap = 0;
     double *cslack = nullptr;  // per-site weight slack
@@ -496,6 +500,9 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 4)
 #define PF_BUILD_WARPS 8
 #endif
 constexpr int BUILD_WARPS = PF_BUILD_WARPS;
+#ifndef PF_DYN_BUILD
+#define PF_DYN_BUILD 1
+#endif
 #ifndef PF_BUILD_MINB
 #define PF_BUILD_MINB 3
 #endif
@@ -508,9 +515,19 @@ __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     BW *ws = (BW *)(smem + (size_t)wid * sizeof(BW));
-    const int nw = gridDim.x * BUILD_WARPS;
     int fl = 0;
-    for (int t = blockIdx.x * BUILD_WARPS + wid; t < count; t += nw) {
+    // cells handed out one at a time from a global counter (counters[2]): the
+    // kernel ends when the last cell does, not when the unluckiest of the
+    // warps' fixed shares does (PF_DYN_BUILD=0: grid stride)
+    const int nw = gridDim.x * BUILD_WARPS;
+    int t = PF_DYN_BUILD ? 0 : blockIdx.x * BUILD_WARPS + wid;
+    for (;;) {
+        if (PF_DYN_BUILD) {
+            int tt = 0;
+            if (lane == 0) tt = atomicAdd(&counters[2], 1);
+            t = __shfl_sync(0xffffffffu, tt, 0);
+        }
+        if (t >= count) break;
         const int i = in.cells ? in.cells[t] : in.g.sid[t];
         int which = 0;
         poly_store_tma_wait();  // the previous cell's bulk store has read its buffer
@@ -540,6 +557,7 @@ __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
             }
         }
         __syncwarp();
+        if (!PF_DYN_BUILD) t += nw;
     }
     // drain the last bulk store: it still reads this warp's shared memory
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -880,10 +898,14 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
         if (const char *e = getenv("PF_SUPER_F")) in.g.sf = std::max(1, atoi(e));  // development experiment
         for (int a = 0; a < 3; a++) in.g.sgn[a] = (in.g.gn[a] + in.g.sf - 1) / in.g.sf;
         const size_t ns = (size_t)in.g.sgn[0] * in.g.sgn[1] * in.g.sgn[2];
-        if (ensure(&c->smax, &c->smax_cap, ns)) return -1;
-        g_launches++;
-        k_super_max<<<(int)std::min<size_t>((ns + 255) / 256, (size_t)c->nsm * 8), 256, 0, st>>>(in.g, in.psi, c->smax);
-        CK(cudaGetLastError());
+        if (!(c->keep_w && c->have_smax)) {
+            if (ensure(&c->smax, &c->smax_cap, ns)) return -1;
+            g_launches++;
+            k_super_max<<<(int)std::min<size_t>((ns + 255) / 256, (size_t)c->nsm * 8), 256, 0, st>>>(in.g, in.psi,
+                                                                                                      c->smax);
+            CK(cudaGetLastError());
+            c->have_smax = c->keep_w;
+        }
         in.g.smax = c->smax;
         if (ensure(&c->cslack, &c->cslack_cap, (size_t)n)) return -1;
         g_launches++;
@@ -1327,7 +1349,10 @@ int64_t pf_batch_evaluate_ex(pf_ctx *c, int64_t n, const double *pts, const doub
     if (rebuild_grid || c->grid_n != n || c->grid_pts != pts) {
         if (grid_build(c, n, pts, psi, 0.0, st)) return -1;
     }
-    if (dpsi_max < 0.0 && dpsi_dev(c, n, psi, st)) return -1;
+    if (dpsi_max < 0.0 && !(c->keep_w && c->have_dpsi)) {
+        if (dpsi_dev(c, n, psi, st)) return -1;
+        c->have_dpsi = c->keep_w;
+    }
     if (ensure(&c->census, &c->census_cap, (size_t)n + 1)) return -1;
     CellIn in;
     fill_cellin(c, in, n, pts, psi, tol, dpsi_max, ball_aware, want_m2);
@@ -1444,7 +1469,10 @@ int pf_batch_evaluate_async(pf_ctx *c, int64_t n, const double *pts, const doubl
     if (rebuild_grid || c->grid_n != n || c->grid_pts != pts) {
         if (grid_build(c, n, pts, psi, 0.0, st)) return -1;
     }
-    if (dpsi_max < 0.0 && dpsi_dev(c, n, psi, st)) return -1;
+    if (dpsi_max < 0.0 && !(c->keep_w && c->have_dpsi)) {
+        if (dpsi_dev(c, n, psi, st)) return -1;
+        c->have_dpsi = c->keep_w;
+    }
     if (ensure(&c->census, &c->census_cap, (size_t)n + 1)) return -1;
     CellIn in;
     fill_cellin(c, in, n, pts, psi, tol, dpsi_max, ball_aware, want_m2);
@@ -1604,3 +1632,11 @@ int pf_facets_csr(pf_ctx *c, int64_t n, int64_t smf, const int64_t *fcount, cons
 
 unsigned long long pf_internal_launches_add(unsigned long long k) { return g_launches += k; }
 int pf_internal_set_err(const char *msg) { return set_err("%s", msg); }
+// between keep_weights(c, 1) and keep_weights(c, 0) the weights and the grid
+// do not change: the first evaluation computes dpsi and the super-bucket
+// maxima, the later ones reuse them
+void pf_internal_keep_weights(pf_ctx *c, int on) {
+    c->keep_w = on != 0;
+    c->have_dpsi = false;
+    c->have_smax = false;
+}
