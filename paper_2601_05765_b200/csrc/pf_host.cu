@@ -57,7 +57,7 @@ namespace {
 constexpr int DENSE_W = 12;  // doubles per cell record
 constexpr int FACET_W = 9;   // doubles per facet record
 constexpr int FLAG_BUILD_OVERFLOW = 512;
-constexpr int RING = 3;      // pinned staging slots in flight
+constexpr int RING = 4;      // pinned staging slots in flight
 
 // ---------------------------------------------------------------------------
 // device side
@@ -238,8 +238,8 @@ struct HostPath {
     // pinned
     double *in_stage = nullptr;  // inputs (pts, psi) staged by the worker pool
     size_t in_stage_c = 0;
-    double *ring[RING] = {nullptr, nullptr, nullptr};
-    size_t ring_c[RING] = {0, 0, 0};
+    double *ring[RING] = {};
+    size_t ring_c[RING] = {};
     int32_t *totals = nullptr;  // per-range facet totals (pinned)
     int totals_c = 0;
     cudaStream_t comp = nullptr, copy = nullptr;
@@ -351,7 +351,9 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
         HCK(cudaMalloc(&h->err, sizeof(int64_t)));
         HCK(cudaGetDevice(&h->device));
         const unsigned hw = std::thread::hardware_concurrency();
-        h->pool = new Pool((int)std::max(1u, std::min(hw ? hw : 4u, 16u)));
+        // one core left to the thread that follows the ranges and queues the
+        // copies (with every core scattering it was descheduled for ms at a time)
+        h->pool = new Pool((int)std::max(1u, std::min(hw ? hw - 1 : 4u, 16u)));
     }
     const int K = (int)std::max<int64_t>(1, std::min<int64_t>(chunks > 0 ? chunks : 16, std::min<int64_t>(n, 64)));
     const size_t n3 = 3 * (size_t)n, nf = (size_t)n * smf;
