@@ -618,6 +618,11 @@ def main():
                 "algorithmic": f"census S_cell (SURVEY.md §8(d)) = {s_cell_total / sc.n:.0f} DP slots/cell "
                                f"(build {s_build:.0f} + evaluation {s_eval:.0f}), x2 flop/slot; mean processed "
                                f"candidates {mean_clips:.1f}/cell",
+                "census_per_cell": {k: round(float(v), 2) for k, v in zip(
+                    ("clips", "vertex_tests", "new_vertices", "new_facet_vertices", "rfar_updates", "cuts",
+                     "loop_entries", "sphere_crossings", "restricted_facets", "restricted_facets_x_nf",
+                     "segment_pieces", "arc_pieces", "boundary_points", "projected_points", "full_circles",
+                     "candidate_shells"), cen_mean)},
                 "peak_source": "measured in-run by pf_fp64_peak (DFMA chains; MEASURED_PEAKS.json has no FP64 entry)"
                                + (f", summed over the {ws} ranks' GPUs" if ws > 1 else "")}
 

@@ -202,6 +202,84 @@ def knn(grid: SpatialGrid, q, k: int, domain: ConvexCell | None = None) -> np.nd
                      domain)[0].cpu().numpy()
 
 
+def build_cell(i: int, sites, domain: ConvexCell, grid=None, ball_aware: bool = False):
+    """Laguerre cell of site i inside the domain; None when the cell is empty
+    (reference laguerre.py:148-183, same arguments and errors).
+
+    The device builds the cell from the sites within a radius r of p_i, in
+    their global index order (so the (d^2, j) candidate order and the
+    coincident-site rule are the reference's) with the GLOBAL weight range
+    max psi - min psi, the reference's security-radius slack.  The result is the
+    reference's cell once r covers every site the build can process: the
+    ball-aware radius sqrt(psi_i) + sqrt(psi_i + dpsi) in ball-aware mode; in
+    full mode the subset cell's own security radius rfar + sqrt(rfar^2 +
+    dpsi) (beyond it no site can cut), else r grows and the cell is rebuilt.
+    ``grid`` is accepted for signature compatibility."""
+    from . import _kernels as _k
+    from .geom import unpack_cell
+
+    if isinstance(sites, (list, tuple)) and len(sites) and isinstance(sites[0], Site):
+        pts, psi, _, _ = sites_to_arrays(sites)
+    else:
+        pts, psi = sites
+        pts = np.asarray(pts, dtype=np.float64).reshape(-1, 3)
+        psi = np.asarray(psi, dtype=np.float64)
+    n = len(pts)
+    i = int(i)
+    if not 0 <= i < n:
+        raise IndexError(f"site index {i} out of range for {n} sites")
+    dp = domain_pack(domain)
+    dpsi = float(max(psi.max() - psi.min(), 0.0))
+    d2 = np.sum((pts - pts[i]) ** 2, axis=1)
+    psii = float(psi[i])
+    if ball_aware and psii > 0.0:
+        r = (np.sqrt(psii) + np.sqrt(psii + dpsi)) * (1.0 + 1e-9)
+    else:
+        # full mode: start from the distance that holds ~64 sites, grow as needed
+        r = float(np.sqrt(np.partition(d2, min(64, n - 1))[min(64, n - 1)])) * 1.5 + 1e-12
+    gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
+    while True:
+        sub = np.nonzero(d2 <= r * r)[0]  # increasing global indices, contains i
+        m, li = len(sub), int(np.searchsorted(sub, i))
+        smv, smf, sml = 128, 64, 512
+        while True:  # the reference's capacities, reached by doubling strides as build_diagram_packed
+            status = np.zeros(m, dtype=np.int64)
+            nv, nf, nl = (np.zeros(m, dtype=np.int64) for _ in range(3))
+            verts, planes = np.zeros((m, smv, 3)), np.zeros((m, smf, 4))
+            tags, lp, lv = (np.zeros((m, smf), dtype=np.int64), np.zeros((m, smf + 1), dtype=np.int64),
+                            np.zeros((m, sml), dtype=np.int64))
+            _k._batch_build(pts[sub], psi[sub], *dp.args(), *gargs, dp.tol, dpsi, ball_aware, smv, smf, sml,
+                            status, nv, nf, nl, verts, planes, tags, lp, lv)
+            if status[li] != 3 or (smv, smf, sml) == (_k.MAX_V, _k.MAX_F, _k.MAX_L):
+                break
+            smv, smf, sml = min(2 * smv, _k.MAX_V), min(2 * smf, _k.MAX_F), min(2 * sml, _k.MAX_L)
+        st = int(status[li])
+        if st == 3:
+            raise RuntimeError("cell exceeded kernel buffer capacity")
+        if st == 1:
+            return None
+        done = (ball_aware and psii > 0.0) or m == n
+        if not done:
+            v = verts[li, :int(nv[li])]
+            rfar = float(np.sqrt(np.max(np.sum((v - pts[i]) ** 2, axis=1))))
+            need = rfar + np.sqrt(rfar * rfar + dpsi)
+            done = need * (1.0 + 1e-9) <= r
+            r = max(2.0 * r, need * 1.01)
+        if done:
+            nfi = int(nf[li])
+            t = np.zeros(_k.MAX_F, dtype=np.int64)
+            t[:nfi] = np.where(tags[li, :nfi] >= 0, sub[np.maximum(tags[li, :nfi], 0)], tags[li, :nfi])
+            lpi = np.zeros(_k.MAX_F + 1, dtype=np.int64)
+            lpi[:nfi + 1] = lp[li, :nfi + 1]
+            vi = np.zeros((_k.MAX_V, 3))
+            vi[:int(nv[li])] = verts[li, :int(nv[li])]
+            pli = np.zeros((_k.MAX_F, 4))
+            pli[:nfi] = planes[li, :nfi]
+            lvi = np.zeros(_k.MAX_L, dtype=np.int64)
+            lvi[:int(nl[li])] = lv[li, :int(nl[li])]
+            return unpack_cell(vi, np.array([nv[li], nfi, nl[li]]), pli, t, lpi, lvi)
+
+
 class PackedDiagram:
     """All unrestricted Laguerre cells in fixed-stride packed storage
     (laguerre.py:186-222 of the reference; host numpy arrays)."""

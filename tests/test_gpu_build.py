@@ -43,3 +43,33 @@ def test_build_diagram_packed_matches_reference(golden, mode):
         cells = laguerre.build_diagram((golden["bb_pts"], golden["bb_psi"]), dom)
         vol = sum(geom.cell_volume_convex(c) for c in cells if c is not None)
         assert abs(vol - 1.0) < 1e-9
+
+
+@pytest.mark.parametrize("mode", ["ba", "full"])
+def test_single_cell_build_matches_reference(golden, mode):
+    """laguerre.build_cell (reference laguerre.py:148-183): the cell of one
+    site, from the sites near it, equals the reference's packed cell of the
+    whole-diagram build bit for bit (vertices, planes, tags, loops)."""
+    from paper_2601_05765_b200 import geom, laguerre
+
+    dom = geom.box_domain([0, 0, 0], [1, 1, 1])
+    pts, psi = golden["bb_pts"], golden["bb_psi"]
+    st = golden[f"bb_{mode}_status"]
+    rng = np.random.default_rng(5)
+    picks = list(rng.choice(len(pts), 12, replace=False)) + [int(np.argmax(psi)), int(np.argmin(psi))]
+    for i in picks:
+        c = laguerre.build_cell(int(i), (pts, psi), dom, ball_aware=(mode == "ba"))
+        if st[i] == 1:
+            assert c is None
+            continue
+        g = {k: golden[f"bb_{mode}_{k}"][i] for k in KEYS}
+        want = geom.unpack_cell(g["verts"], np.array([g["nv"], g["nf"], g["nl"]]), g["planes"], g["tags"],
+                                g["lp"], g["lv"])
+        assert np.array_equal(c.vertices, want.vertices)
+        assert len(c.facets) == len(want.facets)
+        for fc, fw in zip(c.facets, want.facets):
+            assert fc.tag == fw.tag
+            assert np.array_equal(fc.plane.n, fw.plane.n) and fc.plane.d == fw.plane.d
+            assert np.array_equal(fc.loop, fw.loop)
+    with pytest.raises(IndexError):
+        laguerre.build_cell(len(pts), (pts, psi), dom)

@@ -21,7 +21,8 @@ def region_map(fname):
         return {}
     lines = open(p).read().splitlines()
     out, cur, step = {}, fname, None
-    fn_re = re.compile(r"^(?:template <[^>]*>\s*)?(?:PF_DEV|PF_NOINL|__global__|__device__)[^(]*?(\w+)\(")
+    fn_re = re.compile(r"^(?:template <[^>]*>\s*)?(?:(?:PF_DEV|PF_NOINL|PF_PHASE|PF_HELPER|PF_WRED|__global__|__device__)[^(]*?"
+                       r"|(?:int|void|double|bool|unsigned) )(\w+)\(")
     step_re = re.compile(r"^\s*// (\d[a-e]?)\. ")
     for i, ln in enumerate(lines, 1):
         m = fn_re.match(ln)
