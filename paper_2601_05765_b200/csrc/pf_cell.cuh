@@ -199,6 +199,12 @@ struct CellIn {
     int strict;     // parity mode: the reference's restriction outcomes bit for bit
     double t_init;  // first shell radius^2 when not ball-aware
     const double *cslack;  // optional: per-cell weight slack (cell_slack), ball-aware only
+    // optional, full (non-ball-aware) mode: the PF_HEAVY heaviest sites
+    // (indices, weights in descending order) and, in heavy_psi[nheavy], the
+    // largest weight of all other sites (build_cell: heavy-site phase)
+    const int *heavy_idx;
+    const double *heavy_psi;
+    int nheavy;
     const int *cells;  // optional: evaluate only these cells (original indices)
     int ncells;
 };
@@ -932,7 +938,9 @@ int gather_later(W *ws, const CellIn &in, int self, double px, double py, double
 // build the Laguerre cell of site i (_kernels.py:1197-1355)
 // returns 0 ok / 1 empty / 3 overflow; *which = buffer holding the cell
 // ---------------------------------------------------------------------------
-template <class W>
+// HV: compile the full-mode heavy-site phase in (the ball-aware build kernel
+// leaves it out: the extra paths cost the lean kernel ~25%)
+template <class W, bool HV = true>
 #ifndef PF_BUILD_CELL_INL
 #define PF_BUILD_CELL_INL 1  // build_cell inlined into its kernels (out of line: C4 build 49.7 -> 57.8 ms)
 #endif
@@ -964,7 +972,39 @@ int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
 
     // weight slack of the security radius: the per-cell bound of cell_slack()
     // when the runtime computed it, else the reference's global one
-    const double dpsi_s = (ball_aware && in.cslack) ? in.cslack[i] : dpsi;
+    double dpsi_s = (ball_aware && in.cslack) ? in.cslack[i] : dpsi;
+
+    // Full mode with the heavy-site list (in.heavy_*): a site j can only cut
+    // while |p_j - p_i| < rfar + sqrt(rfar^2 + psi_j - psi_i), so the slack
+    // splits into the ordinary sites' (largest weight outside the list) and
+    // that of the heavy sites not processed yet (lane k holds heavy site k).
+    // The (d^2, j)-ordered stream of all sites stops at the ordinary radius;
+    // the heavy sites beyond it follow in (d^2, j) order.  Everything skipped
+    // is a site that leaves the polytope untouched at its turn (rfar only
+    // shrinks), so the cuts and their order are the reference's -- without
+    // the n - 1 candidates one huge weight makes every cell visit
+    // (SURVEY.md §8(f) row 2).
+    const bool heavy = HV && !ball_aware && in.heavy_idx != nullptr && in.nheavy > 0;
+    const int Lh = pfw::lane();
+    int hk = -1;
+    double hw = 0.0;
+    unsigned unseen = 0;
+    double slack_rest = dpsi;
+    if (heavy) {
+        if (Lh < in.nheavy) { hk = in.heavy_idx[Lh]; hw = in.heavy_psi[Lh]; }
+        unseen = pfw::ballot(Lh < in.nheavy && hk != i);  // the cell's own site is no candidate
+        const double pr = in.heavy_psi[in.nheavy] - psii;
+        slack_rest = pr > 0.0 ? (pr < dpsi ? pr : dpsi) : 0.0;
+    }
+    // the slack over the ordinary sites and the unprocessed heavy ones
+    auto heavy_slack = [&]() {
+        double sl = ((unseen >> Lh) & 1u) ? hw - psii : -1e300;
+        sl = pfw::max_d_inl(sl);
+        sl = sl > slack_rest ? sl : slack_rest;
+        return sl > 0.0 ? (sl < dpsi ? sl : dpsi) : 0.0;
+    };
+    if (heavy) dpsi_s = heavy_slack();
+    bool to_heavy = false;  // the ordinary stream is done: heavy-site phase
 
     double t_lo = -1.0;
     double t_hi = ball_aware ? br * br * (1.0 + 1e-14) : in.t_init;
@@ -1021,6 +1061,7 @@ int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
         pfw::sync();
         double stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
         if (ball_aware && br < stop_r) stop_r = br;
+        double r_rest = heavy ? rfar + sqrt(rfar * rfar + slack_rest) : stop_r;
         #pragma unroll 1
         for (int c = 0; c < nc; c++) {
             // candidate c into registers; the warp syncs before any lane acts on
@@ -1032,6 +1073,17 @@ int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
             const double nxc = S.cx[sl], nyc = S.cy[sl], nzc = S.cz[sl], ddc = S.cw[sl];
             pfw::sync();
             if (Dc >= stop_r) { *which_out = which; *nclips = ncl; return 0; }
+            if (heavy) {
+                const unsigned hm = pfw::ballot(hk == j) & unseen;
+                if (hm) {  // a heavy site in the stream: processed here, at its turn
+                    unseen &= ~hm;
+                    dpsi_s = heavy_slack();
+                    stop_r = rfar + sqrt(rfar * rfar + dpsi_s);
+                } else if (Dc >= r_rest) {  // no ordinary site can cut any more
+                    to_heavy = true;
+                    break;
+                }
+            }
             if (Dc < 0.0) {
                 const double psij = ddc;  // coincident site: the slot kept its weight
                 if (psij > psii || (psij == psii && j < i)) { *which_out = which; *nclips = ncl; return 1; }
@@ -1062,9 +1114,11 @@ int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
                 rfar = sqrt(rfar2);
                 stop_r = rfar + sqrt(rfar2 + dpsi_s);
                 if (ball_aware && br < stop_r) stop_r = br;
+                if (heavy) r_rest = rfar + sqrt(rfar2 + slack_rest);
             }
         }
-        if (all_sites) break;
+        if (to_heavy || all_sites) break;
+        if (heavy) stop_r = r_rest;  // the shells only carry the ordinary stream
         if (sqrt(t_hi) >= stop_r) break;
         // next shell: sized for ~0.7 CC candidates from the density seen so far
         // (volume x 8 at most), and never past the stop radius -- the shells
@@ -1077,6 +1131,60 @@ int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
         t_hi = t_hi * (cf * cf);
         const double tstop = stop_r * stop_r * (1.0 + 1e-12);
         if (t_hi > tstop) t_hi = tstop;
+    }
+    // heavy-site phase: the unprocessed heavy sites in (d^2, j) order, each
+    // with the stream's tests and the bisector plane of _kernels.py:1325-1330
+    if (heavy && unseen) {
+        double hx = 0.0, hy = 0.0, hz = 0.0, hd2 = 0.0;
+        if ((unseen >> Lh) & 1u) {
+            hx = in.pts[3 * hk]; hy = in.pts[3 * hk + 1]; hz = in.pts[3 * hk + 2];
+            hd2 = sq(hx - px) + sq(hy - py) + sq(hz - pz);
+        }
+        #pragma unroll 1
+        while (unseen) {
+            // the unprocessed heavy site first in (d^2, j) order
+            int m = -1;
+            #pragma unroll 1
+            for (unsigned u = unseen; u; u &= u - 1) {
+                const int k = __builtin_ctz_pf(u);
+                const double dk = pfw::shfl(hd2, k);
+                const int jk = pfw::shfl(hk, k);
+                if (m < 0) { m = k; continue; }
+                const double dm = pfw::shfl(hd2, m);
+                const int jm = pfw::shfl(hk, m);
+                if (dk < dm || (dk == dm && jk < jm)) m = k;
+            }
+            const double D2 = pfw::shfl(hd2, m);
+            const int j = pfw::shfl(hk, m);
+            const double psij = pfw::shfl(hw, m);
+            const double cx = pfw::shfl(hx, m), cy = pfw::shfl(hy, m), cz = pfw::shfl(hz, m);
+            const double D = sqrt(D2);
+            // the remaining heavy sites are at least this far: none can cut
+            if (D2 > tol * tol && D >= rfar + sqrt(rfar * rfar + dpsi_s)) break;
+            unseen &= ~(1u << m);
+            dpsi_s = heavy_slack();
+            if (D2 <= tol * tol) {
+                if (psij > psii || (psij == psii && j < i)) { *which_out = which; *nclips = ncl; return 1; }
+                continue;
+            }
+            ncl++;
+            const double nxc = (cx - px) / D, nyc = (cy - py) / D, nzc = (cz - pz) / D;
+            const double hij = 0.5 * (D2 + psii - psij) / D;
+            const double ddc = (nxc * px + nyc * py + nzc * pz) + hij;
+            if (ddc - (nxc * px + nyc * py + nzc * pz) > rfar * (1.0 + 1e-12) + 1e-12) {
+                if (cen_on(ws) && pfw::lane() == 0) { ws->cen[CEN_CLIPS]++; ws->cen[CEN_TESTS] += ws->P[which].nv; }
+                continue;
+            }
+            double rfar2;
+            int st = clip(ws, ws->P[which], ws->P[1 - which], which, nxc, nyc, nzc, ddc, j, tol, px, py, pz, &rfar2);
+            if (st == CLIP_EMPTY) { *which_out = which; *nclips = ncl; return 1; }
+            if (st == CLIP_OVERFLOW) { *which_out = which; *nclips = ncl; return 3; }
+            if (st == CLIP_CUT) {
+                which = 1 - which;
+                if (rfar2 < 0.0) rfar2 = poly_rfar2(ws->P[which], px, py, pz);
+                rfar = sqrt(rfar2);
+            }
+        }
     }
     *which_out = which;
     *nclips = ncl;
@@ -2116,7 +2224,7 @@ PF_NOINL int write_packed(W *ws, const CellOut &out, int i, int st, int which) {
     return 0;
 }
 
-template <class W>
+template <class W, bool HV = true>
 PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, int *which) {
     const int L = pfw::lane();
     if (L == 0) {
@@ -2129,7 +2237,7 @@ PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, 
     }
     pfw::sync();
     int nclips;
-    int st = build_cell(ws, in, i, which, &nclips);
+    int st = build_cell<W, HV>(ws, in, i, which, &nclips);
     if (ws->oflow) {
         pfw::sync();
         if (!W::Cap::EXACT) return FLAG_RETRY;

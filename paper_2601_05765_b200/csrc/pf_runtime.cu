@@ -92,6 +92,12 @@ struct pf_ctx {
     // drop-in's index ranges) computes the weight range and the super-bucket
     // maxima once: pf_internal_keep_weights
     bool keep_w = false, have_dpsi = false, have_smax = false;
+    // full mode: the heaviest sites by one descending radix sort of (psi, index)
+    double *hv_keys = nullptr;  // [n + 1]: sorted weights, then -1e300
+    int *hv_iota = nullptr, *hv_vals = nullptr;
+    size_t hv_cap = 0;
+    void *hv_tmp = nullptr;
+    size_t hv_tmp_cap = 0;
     int *csr_cnt = nullptr, *csr_off = nullptr;  // pf_facets_csr scratch
     size_t csr_cnt_cap = 0, csr_off_cap = 0;
     double *cslack = nullptr;  // per-site weight slack
@@ -506,8 +512,9 @@ constexpr int BUILD_WARPS = PF_BUILD_WARPS;
 #ifndef PF_BUILD_MINB
 #define PF_BUILD_MINB 3
 #endif
-// BW: BWSN<FastCaps> (timed: no census code) or BWS<FastCaps> (the census pass)
-template <class BW>
+// BW: BWSN<FastCaps> (timed: no census code) or BWS<FastCaps> (the census pass);
+// HV: full mode (the heavy-site phase compiled in) or ball-aware
+template <class BW, bool HV>
 __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
     k_cells_build(PF_KPARAM CellIn in, PF_KPARAM CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
                   uint8_t *__restrict__ stage, int *__restrict__ retry_list, int *__restrict__ counters,
@@ -531,7 +538,7 @@ __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
         const int i = in.cells ? in.cells[t] : in.g.sid[t];
         int which = 0;
         poly_store_tma_wait();  // the previous cell's bulk store has read its buffer
-        int r = cell_phase_build(ws, in, out, i, &which);
+        int r = cell_phase_build<BW, HV>(ws, in, out, i, &which);
         if (r < 0) {
             poly_store_tma(ws->P[which], gpoly + i);
             if (lane == 0) {
@@ -829,6 +836,14 @@ __global__ void k_super_max(GridView g, const double *__restrict__ psi, double *
     }
 }
 
+// 0..n-1 and the sentinel weight after the sorted ones (the heavy-site list)
+enum { PF_HEAVY = 8 };
+__global__ void k_iota_tail(int *__restrict__ iota, int64_t n, double *__restrict__ tail) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        iota[t] = (int)t;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *tail = -1e300;
+}
+
 // per-site weight slack (pf_cell.cuh cell_slack), thread per evaluated cell
 // (the cells of a subset call only: chunked callers pay it once in total)
 __global__ void k_cell_slack(CellIn in, int64_t count, double *__restrict__ slack) {
@@ -846,7 +861,10 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
                                 (int)(FAST_WARPS * sizeof(WS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_fast, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         static_assert(sizeof(BWSN<FastCaps>) == sizeof(BWS<FastCaps>), "one launch shape for both build kernels");
-        for (const void *kf : {(const void *)k_cells_build<BWSN<FastCaps>>, (const void *)k_cells_build<BWS<FastCaps>>})
+        for (const void *kf : {(const void *)k_cells_build<BWSN<FastCaps>, false>,
+                               (const void *)k_cells_build<BWS<FastCaps>, false>,
+                               (const void *)k_cells_build<BWSN<FastCaps>, true>,
+                               (const void *)k_cells_build<BWS<FastCaps>, true>})
             CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)(BUILD_WARPS * sizeof(BWS<FastCaps>))));
         CK(cudaFuncSetAttribute(k_cells_eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -859,14 +877,16 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
             const char *e = getenv("PF_EVAL_SYNC");
             c->eval_sync = !(e && e[0] == '0');
         }
-        for (const void *kf : {(const void *)k_cells_build<BWSN<FastCaps>>, (const void *)k_cells_build<BWS<FastCaps>>,
-                               (const void *)k_cells_eval})
+        for (const void *kf : {(const void *)k_cells_build<BWSN<FastCaps>, false>,
+                               (const void *)k_cells_build<BWS<FastCaps>, false>,
+                               (const void *)k_cells_build<BWSN<FastCaps>, true>,
+                               (const void *)k_cells_build<BWS<FastCaps>, true>, (const void *)k_cells_eval})
             CK(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         c->split = getenv("PF_FUSED") ? 0 : 1;
         int nb = 0, nbb = 0, nbe = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cells_fast, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(WS<FastCaps>)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, k_cells_build<BWSN<FastCaps>>, BUILD_WARPS * 32,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, k_cells_build<BWSN<FastCaps>, false>, BUILD_WARPS * 32,
                                                          BUILD_WARPS * sizeof(BWS<FastCaps>)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbe, k_cells_eval, FAST_WARPS * 32,
                                                          FAST_WARPS * sizeof(EWS<FastCaps>)));
@@ -914,6 +934,35 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
         CK(cudaGetLastError());
         in.cslack = c->cslack;
     }
+    if (!in.ball_aware && count > 0 && !getenv("PF_NO_HEAVY")) {
+        // full mode: the PF_HEAVY heaviest sites for build_cell's heavy-site phase
+        const size_t nn = (size_t)n;
+        if (c->hv_cap < nn + 1) {
+            for (void *p : {(void *)c->hv_keys, (void *)c->hv_iota, (void *)c->hv_vals})
+                if (p) cudaFree(p);
+            CK(cudaMalloc(&c->hv_keys, (nn + 1) * sizeof(double)));
+            CK(cudaMalloc(&c->hv_iota, nn * sizeof(int)));
+            CK(cudaMalloc(&c->hv_vals, nn * sizeof(int)));
+            c->hv_cap = nn + 1;
+        }
+        g_launches++;
+        k_iota_tail<<<(int)std::min<int64_t>((n + 255) / 256, (int64_t)c->nsm * 8), 256, 0, st>>>(c->hv_iota, n,
+                                                                                                 c->hv_keys + n);
+        size_t need = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, need, in.psi, c->hv_keys, c->hv_iota, c->hv_vals, (int)n,
+                                                  0, 64, st);
+        if (need > c->hv_tmp_cap) {
+            if (c->hv_tmp) cudaFree(c->hv_tmp);
+            CK(cudaMalloc(&c->hv_tmp, need));
+            c->hv_tmp_cap = need;
+        }
+        CK(cub::DeviceRadixSort::SortPairsDescending(c->hv_tmp, need, in.psi, c->hv_keys, c->hv_iota, c->hv_vals,
+                                                     (int)n, 0, 64, st));
+        g_launches += 4;
+        in.heavy_idx = c->hv_vals;
+        in.heavy_psi = c->hv_keys;
+        in.nheavy = (int)std::min<int64_t>(PF_HEAVY, n);
+    }
     cudaEvent_t *sev = nullptr;
     if (c->stage_on && c->split && count > 0) {
         if (c->stage_n == c->stage_ev.size()) {
@@ -936,7 +985,8 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
                        ensure(&c->eidx, &c->eidx_cap, (size_t)count) || ensure(&c->eidx2, &c->eidx2_cap, (size_t)count)))
             return -1;
         g_launches++;
-        auto kb = out.census16 ? k_cells_build<BWS<FastCaps>> : k_cells_build<BWSN<FastCaps>>;
+        auto kb = in.ball_aware ? (out.census16 ? k_cells_build<BWS<FastCaps>, false> : k_cells_build<BWSN<FastCaps>, false>)
+                                : (out.census16 ? k_cells_build<BWS<FastCaps>, true> : k_cells_build<BWSN<FastCaps>, true>);
         kb<<<(int)bblocks, BUILD_WARPS * 32, BUILD_WARPS * sizeof(BWS<FastCaps>), st>>>(
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err,
             sorted ? c->ekey : nullptr, sorted ? c->eidx : nullptr);
@@ -1182,7 +1232,8 @@ int pf_ctx_destroy(pf_ctx *c) {
     void *ptrs[] = {c->dv, c->dp, c->dt, c->dlp, c->dlv, c->sx, c->sy, c->sz, c->sid, c->bid,
                     c->bcount, c->bstart, c->scan_tmp, c->dscal, c->mm, c->retry_list, c->counters,
                     c->err, c->census, c->exact_ws, c->gpoly, c->stage, c->smax, c->cslack, c->retry_list2, c->csr_cnt, c->csr_off, c->grid_part,
-                    c->ekey, c->ekey2, c->eidx, c->eidx2, c->esort_tmp};
+                    c->ekey, c->ekey2, c->eidx, c->eidx2, c->esort_tmp, c->hv_keys, c->hv_iota, c->hv_vals,
+                    c->hv_tmp};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);

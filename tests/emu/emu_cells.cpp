@@ -225,6 +225,21 @@ int64_t pfemu_evaluate(int n, const double *pts, const double *psi,
         for (int i = 0; i < n; i++) cslack[i] = cell_slack(in.g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], psi[i], dpsi);
         in.cslack = cslack.data();
     }
+    // full mode: the heaviest sites (pf_runtime.cu launch_cells, PF_HEAVY = 8)
+    std::vector<int> hv_idx;
+    std::vector<double> hv_psi;
+    if (!ball_aware && n > 0 && !getenv("PF_NO_HEAVY")) {
+        std::vector<int> o(n);
+        for (int i = 0; i < n; i++) o[i] = i;
+        std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return psi[a] > psi[b]; });
+        const int nh = std::min(8, n);
+        hv_idx.assign(o.begin(), o.begin() + nh);
+        for (int k = 0; k < nh; k++) hv_psi.push_back(psi[o[k]]);
+        hv_psi.push_back(n > nh ? psi[o[nh]] : -1e300);
+        in.heavy_idx = hv_idx.data();
+        in.heavy_psi = hv_psi.data();
+        in.nheavy = nh;
+    }
     CellOut out;
     memset(&out, 0, sizeof(out));
     out.status = status; out.vol = vol; out.ksur = ksur; out.cent = cent; out.ipt = ipt; out.m2 = m2;

@@ -73,3 +73,57 @@ def test_single_cell_build_matches_reference(golden, mode):
             assert np.array_equal(fc.loop, fw.loop)
     with pytest.raises(IndexError):
         laguerre.build_cell(len(pts), (pts, psi), dom)
+
+
+def test_full_mode_heavy_weights_match_oracle(golden):
+    """Full mode with a few huge weights (the n - 1-candidate pathology of
+    SURVEY §8(f) row 2): the device's heavy-site phase gives the reference's
+    packed cells bit for bit (oracle = the bit-identical C restatement), and
+    in a fraction of the time the global security radius would take."""
+    import os
+    import sys
+    import time
+
+    import torch
+
+    from conftest import ROOT
+    from paper_2601_05765_b200 import _kernels
+
+    sys.path.insert(0, ROOT)
+    from oracle import pyoracle as O
+
+    rng = np.random.default_rng(21)
+    n = 4000
+    pts = rng.random((n, 3))
+    psi = np.full(n, (0.6 * (1.0 / n) ** (1.0 / 3.0)) ** 2)
+    psi[[5, 1234, 2999]] = (0.3, 0.12, 0.05)
+    dpsi = float(psi.max() - psi.min())
+    dom, tol = golden_domain(golden), float(golden["dom_unit_tol"])
+    smv, smf, sml = 512, 160, 2048  # the reference's capacities: the heavy sites' cells are large
+
+    def arrays():
+        return [np.zeros(n, np.int64) for _ in range(4)] + [
+            np.zeros((n, smv, 3)), np.zeros((n, smf, 4)), np.zeros((n, smf), np.int64),
+            np.zeros((n, smf + 1), np.int64), np.zeros((n, sml), np.int64)]
+
+    ref = arrays()
+    g = O.SpatialGrid(pts, [0, 0, 0], [1, 1, 1], 1.0)
+    err_ref = O.batch_build(pts, psi, *dom, *g.kernel_args(), tol, dpsi, False, smv, smf, sml, *ref)
+    gargs = (None, None, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1, 1, 1.0)
+    times = {}
+    for mode in ("heavy", "global"):
+        if mode == "global":
+            os.environ["PF_NO_HEAVY"] = "1"
+        try:
+            dev = arrays()
+            for rep in range(2):  # second call timed
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                assert _kernels._batch_build(pts, psi, *dom, *gargs, tol, dpsi, False, smv, smf, sml, *dev) == err_ref
+                torch.cuda.synchronize()
+                times[mode] = time.perf_counter() - t0
+        finally:
+            os.environ.pop("PF_NO_HEAVY", None)
+        for k, a, b in zip(KEYS, dev, ref):
+            assert np.array_equal(a, b), (mode, k)
+    assert times["heavy"] < times["global"]
