@@ -344,6 +344,111 @@ PF_DEV double poly_rfar(const Poly<C> &A, double px, double py, double pz) {
     return sqrt(poly_rfar2(A, px, py, pz));
 }
 
+// the clip's rare paths (more than 32 vertices, dropped vertices) as helper
+// functions; out of line (PF_COLD_OOL=1) measured slower (C4 build 47.5 ->
+// 51.1 ms, the calls' register traffic), so they are inlined
+#ifndef PF_COLD_OOL
+#define PF_COLD_OOL 0
+#endif
+#if PF_COLD_OOL
+#define PF_COLD PF_NOINL
+#else
+#define PF_COLD PF_DEV
+#endif
+// clip step 1-2 for polytopes of more than 32 vertices (rare: out of line, so
+// the common single-chunk path keeps its registers).  Returns CLIP_UNTOUCHED /
+// CLIP_EMPTY, or -1 with *K and this lane's *rmax share.
+template <class W>
+PF_COLD int clip_classify_wide(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B, double nx,
+                               double ny, double nz, double dd, double tol, double px, double py, double pz,
+                               int *K_out, double *rmax_out) {
+    using C = typename W::Cap;
+    BuildScratch<C> &S = ws->u.b;
+    const int L = pfw::lane();
+    const unsigned lt = pfw::lanemask_lt();
+    const int nv = A.nv;
+    int K = 0;
+    double rmax = 0.0;
+    int n_out = 0;
+    #pragma unroll 1
+    for (int v0 = 0; v0 < nv; v0 += 32) {
+        int v = v0 + L;
+        bool out = false;
+        if (v < nv) {
+            double sv = nx * A.x[v] + ny * A.y[v] + nz * A.z[v] - dd;
+            S.sd[v] = sv;
+            out = sv > tol;
+        }
+        n_out += pfw::popc(pfw::ballot(out));
+    }
+    if (n_out == 0) return CLIP_UNTOUCHED;
+    if (nv - n_out == 0) return CLIP_EMPTY;
+    pfw::sync();
+    #pragma unroll 1
+    for (int v0 = 0; v0 < nv; v0 += 32) {
+        int v = v0 + L;
+        bool keep = v < nv && S.sd[v] <= tol;
+        unsigned m = pfw::ballot(keep);
+        if (keep) {
+            int idx = K + pfw::popc(m & lt);
+            S.vmap[v] = (uint16_t)idx;
+            const double ax = A.x[v], ay = A.y[v], az = A.z[v];
+            B.x[idx] = ax; B.y[idx] = ay; B.z[idx] = az;
+            const double d2 = sq(ax - px) + sq(ay - py) + sq(az - pz);
+            if (d2 > rmax) rmax = d2;
+        } else if (v < nv) {
+            S.vmap[v] = 0xffff;
+        }
+        K += pfw::popc(m);
+    }
+    *K_out = K;
+    *rmax_out = rmax;
+    return -1;
+}
+
+// clip step 5 (_kernels.py:297-315): drop the vertices no loop references
+// any more (rare: only after a dropped facet emitted 1-2 entries); returns
+// the vertex count
+template <class W>
+PF_COLD int clip_drop_unreferenced(W *ws, Poly<typename W::Cap> &B, int NVB, int NL2) {
+    using C = typename W::Cap;
+    BuildScratch<C> &S = ws->u.b;
+    const int L = pfw::lane();
+    const unsigned lt = pfw::lanemask_lt();
+    #pragma unroll 1
+    for (int v = L; v < NVB; v += 32) S.vmap[v] = 0;
+    pfw::sync();
+    #pragma unroll 1
+    for (int k = L; k < NL2; k += 32) S.vmap[B.lv[k]] = 1;
+    pfw::sync();
+    int nref = 0;
+    #pragma unroll 1
+    for (int v0 = 0; v0 < NVB; v0 += 32) {
+        int v = v0 + L;
+        nref += pfw::popc(pfw::ballot(v < NVB && S.vmap[v] == 1));
+    }
+    if (nref != NVB) {
+        int base = 0;
+        #pragma unroll 1
+        for (int v0 = 0; v0 < NVB; v0 += 32) {
+            int v = v0 + L;
+            bool r = v < NVB && S.vmap[v] == 1;
+            unsigned m = pfw::ballot(r);
+            double x = 0, y = 0, z = 0;
+            int dst = base + pfw::popc(m & lt);
+            if (r) { x = B.x[v]; y = B.y[v]; z = B.z[v]; }
+            pfw::sync();
+            if (r) { B.x[dst] = x; B.y[dst] = y; B.z[dst] = z; S.vmap[v] = (uint16_t)(dst + 2); }
+            base += pfw::popc(m);
+            pfw::sync();
+        }
+        #pragma unroll 1
+        for (int k = L; k < NL2; k += 32) B.lv[k] = (uint16_t)(S.vmap[B.lv[k]] - 2);
+        nref = base;
+    }
+    return nref;
+}
+
 // ---------------------------------------------------------------------------
 // clip A by n.x <= dd into B (_kernels.py:109-319), warp-cooperative
 // ---------------------------------------------------------------------------
@@ -391,38 +496,8 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         if (v < nv) S.vmap[v] = (uint16_t)vmap_reg;
         K = pfw::popc(m);
     } else {
-        int n_out = 0;
-        #pragma unroll 1
-        for (int v0 = 0; v0 < nv; v0 += 32) {
-            int v = v0 + L;
-            bool out = false;
-            if (v < nv) {
-                double sv = nx * A.x[v] + ny * A.y[v] + nz * A.z[v] - dd;
-                S.sd[v] = sv;
-                out = sv > tol;
-            }
-            n_out += pfw::popc(pfw::ballot(out));
-        }
-        if (n_out == 0) return CLIP_UNTOUCHED;
-        if (nv - n_out == 0) return CLIP_EMPTY;
-        pfw::sync();
-        #pragma unroll 1
-        for (int v0 = 0; v0 < nv; v0 += 32) {
-            int v = v0 + L;
-            bool keep = v < nv && S.sd[v] <= tol;
-            unsigned m = pfw::ballot(keep);
-            if (keep) {
-                int idx = K + pfw::popc(m & lt);
-                S.vmap[v] = (uint16_t)idx;
-                const double ax = A.x[v], ay = A.y[v], az = A.z[v];
-                B.x[idx] = ax; B.y[idx] = ay; B.z[idx] = az;
-                const double d2 = sq(ax - px) + sq(ay - py) + sq(az - pz);
-                if (d2 > rmax) rmax = d2;
-            } else if (v < nv) {
-                S.vmap[v] = 0xffff;
-            }
-            K += pfw::popc(m);
-        }
+        const int r = clip_classify_wide(ws, A, B, nx, ny, nz, dd, tol, px, py, pz, &K, &rmax);
+        if (r >= 0) return r;
     }
     pfw::sync();
 
@@ -686,37 +761,7 @@ PF_DEV int clip(W *ws, const Poly<typename W::Cap> &A, Poly<typename W::Cap> &B,
         pfw::sync();
         return CLIP_CUT;
     }
-    #pragma unroll 1
-    for (int v = L; v < NVB; v += 32) S.vmap[v] = 0;
-    pfw::sync();
-    #pragma unroll 1
-    for (int k = L; k < NL2; k += 32) S.vmap[B.lv[k]] = 1;
-    pfw::sync();
-    int nref = 0;
-    #pragma unroll 1
-    for (int v0 = 0; v0 < NVB; v0 += 32) {
-        int v = v0 + L;
-        nref += pfw::popc(pfw::ballot(v < NVB && S.vmap[v] == 1));
-    }
-    if (nref != NVB) {
-        int base = 0;
-        #pragma unroll 1
-        for (int v0 = 0; v0 < NVB; v0 += 32) {
-            int v = v0 + L;
-            bool r = v < NVB && S.vmap[v] == 1;
-            unsigned m = pfw::ballot(r);
-            double x = 0, y = 0, z = 0;
-            int dst = base + pfw::popc(m & lt);
-            if (r) { x = B.x[v]; y = B.y[v]; z = B.z[v]; }
-            pfw::sync();
-            if (r) { B.x[dst] = x; B.y[dst] = y; B.z[dst] = z; S.vmap[v] = (uint16_t)(dst + 2); }
-            base += pfw::popc(m);
-            pfw::sync();
-        }
-        #pragma unroll 1
-        for (int k = L; k < NL2; k += 32) B.lv[k] = (uint16_t)(S.vmap[B.lv[k]] - 2);
-        nref = base;
-    }
+    const int nref = clip_drop_unreferenced(ws, B, NVB, NL2);
     *rfar2 = -1.0;
     if (L == 0) {
         B.nv = nref; B.nf = NF2; B.nl = NL2;
