@@ -983,8 +983,9 @@ int gather_later(W *ws, const CellIn &in, int self, double px, double py, double
 // build the Laguerre cell of site i (_kernels.py:1197-1355)
 // returns 0 ok / 1 empty / 3 overflow; *which = buffer holding the cell
 // ---------------------------------------------------------------------------
-// HV: compile the full-mode heavy-site phase in (the ball-aware build kernel
-// leaves it out: the extra paths cost the lean kernel ~25%)
+// HV: the general build (full mode with the heavy-site phase, packed
+// outputs); HV = false is the ball-aware evaluation build, compiled without
+// the other modes' paths (the heavy-site phase alone cost it ~25%)
 template <class W, bool HV = true>
 #ifndef PF_BUILD_CELL_INL
 #define PF_BUILD_CELL_INL 1  // build_cell inlined into its kernels (out of line: C4 build 49.7 -> 57.8 ms)
@@ -998,7 +999,7 @@ int build_cell(W *ws, const CellIn &in, int i, int *which_out, int *nclips) {
     using C = typename W::Cap;
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     const double psii = in.psi[i];
-    const bool ball_aware = in.ball_aware != 0;  // hoisted: `in` is in local memory
+    const bool ball_aware = !HV || in.ball_aware != 0;  // hoisted: `in` is in local memory
     const double tol = in.tol, dpsi = in.dpsi_ptr ? *in.dpsi_ptr : in.dpsi;
     load_domain(ws->P[0], in);
     #pragma unroll 1
@@ -2289,7 +2290,7 @@ PF_DEV int cell_phase_build(W *ws, const CellIn &in, const CellOut &out, int i, 
         st = 3;
     }
     if (out.census && L == 0) out.census[i] = nclips;
-    if (out.pk_status) return write_packed(ws, out, i, st, *which);
+    if (HV && out.pk_status) return write_packed(ws, out, i, st, *which);
     const double px = in.pts[3 * i], py = in.pts[3 * i + 1], pz = in.pts[3 * i + 2];
     if (st == 3) {
         if (L == 0) {

@@ -513,7 +513,7 @@ constexpr int BUILD_WARPS = PF_BUILD_WARPS;
 #define PF_BUILD_MINB 3
 #endif
 // BW: BWSN<FastCaps> (timed: no census code) or BWS<FastCaps> (the census pass);
-// HV: full mode (the heavy-site phase compiled in) or ball-aware
+// HV: the general build (full mode, packed outputs) or the ball-aware evaluation build
 template <class BW, bool HV>
 __global__ void __launch_bounds__(BUILD_WARPS * 32, PF_BUILD_MINB)
     k_cells_build(PF_KPARAM CellIn in, PF_KPARAM CellOut out, int count, Poly<FastCaps> *__restrict__ gpoly,
@@ -985,7 +985,7 @@ int launch_cells(pf_ctx *c, const CellIn &in_, const CellOut &out, int64_t n, cu
                        ensure(&c->eidx, &c->eidx_cap, (size_t)count) || ensure(&c->eidx2, &c->eidx2_cap, (size_t)count)))
             return -1;
         g_launches++;
-        auto kb = in.ball_aware ? (out.census16 ? k_cells_build<BWS<FastCaps>, false> : k_cells_build<BWSN<FastCaps>, false>)
+        auto kb = (in.ball_aware && !out.pk_status) ? (out.census16 ? k_cells_build<BWS<FastCaps>, false> : k_cells_build<BWSN<FastCaps>, false>)
                                 : (out.census16 ? k_cells_build<BWS<FastCaps>, true> : k_cells_build<BWSN<FastCaps>, true>);
         kb<<<(int)bblocks, BUILD_WARPS * 32, BUILD_WARPS * sizeof(BWS<FastCaps>), st>>>(
             in, out, (int)count, c->gpoly, c->stage, c->retry_list, c->counters, c->err,
