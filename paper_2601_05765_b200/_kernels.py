@@ -97,10 +97,13 @@ def _chunk_bounds(n: int, K: int) -> np.ndarray:
     """Index-range boundaries [0 = b_0 <= ... <= b_K = n] of the host drop-in's
     ranges (pf_batch_evaluate_host's range_bounds, pf_host.cu): equal, except
     the last three shrink (1/2, 1/4, 1/8 of one) so the work left after the
-    last kernel is short."""
+    last kernel is short, and with K >= 10 the first two (1/4, 1/2) so the
+    host's scatter starts early."""
     wts = np.ones(K)
     if K >= 6:
         wts[-3:] = (0.5, 0.25, 0.125)
+    if K >= 10:
+        wts[:2] = (0.25, 0.5)
     bnd = np.rint(np.concatenate([[0.0], np.cumsum(wts)]) / wts.sum() * n).astype(np.int64)
     bnd[0], bnd[-1] = 0, n
     return bnd

@@ -281,10 +281,13 @@ int ensure_pinned(double **p, size_t *cap, size_t count) {
 }
 
 // index-range boundaries: equal ranges, the last three shrinking (1/2, 1/4,
-// 1/8 of one) so the work left after the last kernel is short
+// 1/8 of one) so the work left after the last kernel is short, and with
+// K >= 10 the first two (1/4, 1/2) so the host's scatter -- host-memory
+// bound, about as fast as the device produces -- starts early
 std::vector<int64_t> range_bounds(int64_t n, int K) {
     std::vector<double> w(K, 1.0);
     if (K >= 6) { w[K - 3] = 0.5; w[K - 2] = 0.25; w[K - 1] = 0.125; }
+    if (K >= 10) { w[0] = 0.25; w[1] = 0.5; }  // the first copy (and the host's scatter) starts early
     double tot = 0.0;
     for (double x : w) tot += x;
     std::vector<int64_t> b(K + 1, 0);
