@@ -323,15 +323,29 @@ void scatter_rows(int64_t i0, int64_t r0, int64_t r1, const double *dense, const
             if (m2) m2[i] = r[9];
         }
         const int64_t nk = fc < 0 ? 0 : (fc > smf ? smf : fc);
-        for (int64_t s = 0; s < nk; s++, fo++) {
-            const double *f = fac + fo * FACET_W;
-            const int64_t a = i * smf + s;
-            if (ftag) memcpy(&ftag[a], &f[0], 8);
-            if (farea) farea[a] = f[1];
-            if (fh) fh[a] = f[2];
-            if (fnrm) { fnrm[3 * a] = f[3]; fnrm[3 * a + 1] = f[4]; fnrm[3 * a + 2] = f[5]; }
-            if (fcent) { fcent[3 * a] = f[6]; fcent[3 * a + 1] = f[7]; fcent[3 * a + 2] = f[8]; }
-        }
+        // one contiguous run per output array (five write streams at a time
+        // instead of interleaving them per facet)
+        const double *f = fac + fo * FACET_W;
+        const int64_t a0 = i * smf;
+        if (ftag)
+            for (int64_t s = 0; s < nk; s++) memcpy(&ftag[a0 + s], &f[s * FACET_W], 8);
+        if (farea)
+            for (int64_t s = 0; s < nk; s++) farea[a0 + s] = f[s * FACET_W + 1];
+        if (fh)
+            for (int64_t s = 0; s < nk; s++) fh[a0 + s] = f[s * FACET_W + 2];
+        if (fnrm)
+            for (int64_t s = 0; s < nk; s++) {
+                fnrm[3 * (a0 + s)] = f[s * FACET_W + 3];
+                fnrm[3 * (a0 + s) + 1] = f[s * FACET_W + 4];
+                fnrm[3 * (a0 + s) + 2] = f[s * FACET_W + 5];
+            }
+        if (fcent)
+            for (int64_t s = 0; s < nk; s++) {
+                fcent[3 * (a0 + s)] = f[s * FACET_W + 6];
+                fcent[3 * (a0 + s) + 1] = f[s * FACET_W + 7];
+                fcent[3 * (a0 + s) + 2] = f[s * FACET_W + 8];
+            }
+        fo += nk;
     }
 }
 

@@ -258,7 +258,9 @@ def build_cell(i: int, sites, domain: ConvexCell, grid=None, ball_aware: bool = 
             raise RuntimeError("cell exceeded kernel buffer capacity")
         if st == 1:
             return None
-        done = (ball_aware and psii > 0.0) or m == n
+        # ball-aware: the subset holds every site within the stop radius (psi_i > 0) or
+        # the build processes none (psi_i <= 0: the domain cell, _kernels.py:1239-1248)
+        done = ball_aware or m == n
         if not done:
             v = verts[li, :int(nv[li])]
             rfar = float(np.sqrt(np.max(np.sum((v - pts[i]) ** 2, axis=1))))
