@@ -343,6 +343,18 @@ int pf_sample_surface(pf_ctx *ctx, int64_t n, const double *pts, const double *p
                       const int64_t *cell, const int64_t *max_tries, uint64_t seed, double *x, double *normal,
                       int32_t *status, void *stream);
 
+/* cell-to-cell traversal of m rays (f64[m, 6]: origin, unit direction) through the
+ * unrestricted power diagram (cell_nf i32[n], planes f64[n, smf, 4] (n.x <= d), tags
+ * i32[n, smf] (site >= 0, domain face < 0): pf_batch_build in full mode), SPEC.md renderer
+ * `traverse` (§6): per ray up to max_seg pieces (cell, t_enter, t_exit, fluid), each
+ * power-cell span split at the chord of the cell's ball; mode 0 Volume (to the domain exit),
+ * 1 SurfaceOnly (up to the first exit through a sphere patch).  status: 0 ok, 1 the ray
+ * misses the domain, 2 the 8n-crossing guard or max_seg was reached. */
+int pf_traverse(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double psimax, int smf,
+                const int32_t *cell_nf, const double *planes, const int32_t *tags, int64_t m, const double *rays,
+                int mode, int max_seg, int32_t *out_cell, double *out_t0, double *out_t1, uint8_t *out_fluid,
+                int32_t *count, int32_t *status, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

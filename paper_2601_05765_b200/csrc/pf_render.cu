@@ -40,6 +40,7 @@ namespace {
     } while (0)
 
 struct Grid {
+    const double *pts;  // [n, 3] original order
     const double *sx, *sy, *sz;
     const int *sid, *bstart;
     int gn[3];
@@ -387,6 +388,151 @@ __global__ void k_sample(Grid g, const double *__restrict__ pts, const double *_
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// traverse (SPEC renderer `traverse`, PAPER §6 "load the current cell's
+// neighbors and iteratively intersect facets facing the ray ... until the
+// closest facet is the domain boundary"): thread per ray, walking the
+// unrestricted power diagram (packed cells of pf_batch_build in full mode).
+// The fluid is the union of V_i ∩ B_i, so within the power cell i the fluid
+// part of the ray is its chord of the ball B_i: every cell span is split into
+// air / fluid / air pieces.  SurfaceOnly stops after the first fluid piece that
+// leaves through the sphere.  Consecutive pieces share their end points.
+// ---------------------------------------------------------------------------
+// power-nearest site of x (lowest index on ties): cube searches of growing
+// half width r until no site outside can be nearer in power distance
+__device__ int power_nearest(const Grid &g, const double *__restrict__ psi, double psimax, const double *x) {
+    const double hmin = fmin(g.h[0], fmin(g.h[1], g.h[2]));
+    double r = hmin;
+    int best = -1;
+    double bd = 1e300;
+    for (int it = 0; it < 64; it++) {
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; a++) {
+            lo[a] = (int)floor((x[a] - r - g.lo[a]) / g.h[a]);
+            hi[a] = (int)floor((x[a] + r - g.lo[a]) / g.h[a]);
+            lo[a] = lo[a] < 0 ? 0 : (lo[a] >= g.gn[a] ? g.gn[a] - 1 : lo[a]);
+            hi[a] = hi[a] < 0 ? 0 : (hi[a] >= g.gn[a] ? g.gn[a] - 1 : hi[a]);
+        }
+        for (int bx = lo[0]; bx <= hi[0]; bx++)
+            for (int by = lo[1]; by <= hi[1]; by++)
+                for (int bz = lo[2]; bz <= hi[2]; bz++) {
+                    const int lin = (bx * g.gn[1] + by) * g.gn[2] + bz;
+                    for (int s = g.bstart[lin]; s < g.bstart[lin + 1]; s++) {
+                        const int i = g.sid[s];
+                        const double dx = x[0] - g.sx[s], dy = x[1] - g.sy[s], dz = x[2] - g.sz[s];
+                        const double pd = dx * dx + dy * dy + dz * dz - psi[i];
+                        if (pd < bd || (pd == bd && i < best)) { bd = pd; best = i; }
+                    }
+                }
+        const bool all = lo[0] == 0 && lo[1] == 0 && lo[2] == 0 && hi[0] == g.gn[0] - 1 && hi[1] == g.gn[1] - 1 &&
+                         hi[2] == g.gn[2] - 1;
+        if (all) break;
+        if (best >= 0) {
+            // a site at distance > r has power distance > r^2 - psimax
+            const double need = bd + psimax;
+            if (need <= r * r) break;
+            r = fmax(2.0 * r, sqrt(fmax(need, 0.0)) * (1.0 + 1e-12));
+        } else {
+            r *= 2.0;
+        }
+    }
+    return best;
+}
+
+__global__ void k_traverse(Grid g, const double *__restrict__ psi, double psimax, const double *__restrict__ dp,
+                           int dnf, int smf, const int32_t *__restrict__ cnf, const double *__restrict__ planes,
+                           const int32_t *__restrict__ tags, int64_t m, const double *__restrict__ rays, int mode,
+                           int max_seg, int64_t max_steps, int32_t *__restrict__ out_cell, double *__restrict__ out_t0,
+                           double *__restrict__ out_t1, uint8_t *__restrict__ out_fluid, int32_t *__restrict__ count,
+                           int32_t *__restrict__ status) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+        const double o[3] = {rays[6 * r], rays[6 * r + 1], rays[6 * r + 2]};
+        const double d[3] = {rays[6 * r + 3], rays[6 * r + 4], rays[6 * r + 5]};
+        int nseg = 0, st = 0;
+        // the ray inside the (convex) domain: [t0, t1]
+        double t0 = 0.0, t1 = 1e300;
+        bool miss = false;
+        for (int f = 0; f < dnf && !miss; f++) {
+            const double nd = dp[4 * f] * d[0] + dp[4 * f + 1] * d[1] + dp[4 * f + 2] * d[2];
+            const double gap = dp[4 * f + 3] - (dp[4 * f] * o[0] + dp[4 * f + 1] * o[1] + dp[4 * f + 2] * o[2]);
+            if (fabs(nd) < 1e-300) { if (gap < 0.0) miss = true; continue; }
+            const double t = gap / nd;
+            if (nd > 0.0) t1 = fmin(t1, t); else t0 = fmax(t0, t);
+        }
+        if (miss || !(t0 < t1)) {
+            count[r] = 0;
+            status[r] = 1;
+            continue;
+        }
+        const double tm0 = t0 + 1e-9 * (t1 - t0);  // just inside the entry face
+        const double x0[3] = {o[0] + tm0 * d[0], o[1] + tm0 * d[1], o[2] + tm0 * d[2]};
+        int i = power_nearest(g, psi, psimax, x0);
+        int prev = -1;
+        double tin = t0;
+        for (int64_t step = 0; i >= 0; step++) {
+            if (step >= max_steps) { st = 2; break; }
+            // exit through the nearest facet facing the ray (not the one entered by)
+            double tout = t1;
+            int next = -1;
+            const int nfi = cnf[i];
+            for (int f = 0; f < nfi; f++) {
+                const double *pl = planes + ((int64_t)i * smf + f) * 4;
+                const int tg = tags[(int64_t)i * smf + f];
+                if (tg >= 0 && tg == prev) continue;
+                const double nd = pl[0] * d[0] + pl[1] * d[1] + pl[2] * d[2];
+                if (!(nd > 1e-300)) continue;
+                double t = (pl[3] - (pl[0] * o[0] + pl[1] * o[1] + pl[2] * o[2])) / nd;
+                if (t < tin) t = tin;
+                if (t < tout || (t == tout && tg >= 0 && (next < 0 || tg < next))) { tout = t; next = tg; }
+            }
+            if (tout >= t1) { tout = t1; next = -1; }
+            // the span's pieces: air / fluid (the chord of B_i) / air
+            double ta = 1e300, tb = -1e300;  // chord of the ball B(p_i, sqrt(psi_i))
+            bool stop = false;
+            {
+                const double *pp = g.pts + 3 * (int64_t)i;
+                const double wx = o[0] - pp[0], wy = o[1] - pp[1], wz = o[2] - pp[2];
+                const double b = d[0] * wx + d[1] * wy + d[2] * wz;
+                const double c = wx * wx + wy * wy + wz * wz - psi[i];
+                const double disc = b * b - c;
+                if (psi[i] > 0.0 && disc > 0.0) {
+                    const double sq = sqrt(disc);
+                    ta = -b - sq;
+                    tb = -b + sq;
+                }
+            }
+            const double fa = fmax(tin, ta), fb = fmin(tout, tb);
+            double cut[4];
+            int np = 0;
+            cut[np++] = tin;
+            if (fa < fb) {
+                if (fa > tin) cut[np++] = fa;
+                if (fb < tout) cut[np++] = fb;
+            }
+            cut[np++] = tout;
+            for (int k = 0; k + 1 < np; k++) {
+                const double a = cut[k], bq = cut[k + 1];
+                if (!(bq > a)) continue;  // a zero-length span (an edge or vertex crossing)
+                const bool fl = fa < fb && a >= fa && bq <= fb;
+                if (nseg >= max_seg) { st = 2; stop = true; break; }
+                const int64_t q = r * (int64_t)max_seg + nseg++;
+                out_cell[q] = i;
+                out_t0[q] = a;
+                out_t1[q] = bq;
+                out_fluid[q] = fl ? 1 : 0;
+                if (mode == 1 && fl && bq < tout) { stop = true; break; }  // surface exit
+            }
+            if (stop || next < 0) break;
+            prev = i;
+            i = next;
+            tin = tout;
+        }
+        count[r] = nseg;
+        status[r] = st;
+    }
+}
+
 }  // namespace
 
 // defined in pf_runtime.cu
@@ -398,6 +544,7 @@ static int render_grid(pf_ctx *ctx, int64_t n, const double *pts, const double *
                        Grid &g, void *stream) {
     if (pf_grid_build(ctx, n, pts, psi, 0.0, stream)) return -1;
     if (pf_internal_grid_view(ctx, &g.sx, &g.sy, &g.sz, &g.sid, &g.bstart, g.gn, g.lo, g.h)) return -1;
+    g.pts = pts;
     const double hmin = fmin(g.h[0], fmin(g.h[1], g.h[2]));
     g.reach = (int)ceil((rmax + extra) / hmin);
     if (g.reach < 1) g.reach = 1;
@@ -492,6 +639,30 @@ extern "C" int pf_sample_surface(pf_ctx *ctx, int64_t n, const double *pts, cons
         pf_internal_launches_add(1);
         k_sample<<<(int)((m + 127) / 128 < 8192 ? (m + 127) / 128 : 8192), 128, 0, st>>>(
             g, pts, psi, m, cell, max_tries, dp, dnf, seed, x, normal, status);
+        RCK(cudaGetLastError());
+    }
+    RCK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+extern "C" int pf_traverse(pf_ctx *ctx, int64_t n, const double *pts, const double *psi, double psimax, int smf,
+                           const int32_t *cell_nf, const double *planes, const int32_t *tags, int64_t m,
+                           const double *rays, int mode, int max_seg, int32_t *out_cell, double *out_t0,
+                           double *out_t1, uint8_t *out_fluid, int32_t *count, int32_t *status, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) return pf_internal_set_err("pf_traverse: empty scene");
+    if (smf <= 0 || max_seg <= 0) return pf_internal_set_err("pf_traverse: bad strides");
+    Grid g;
+    if (render_grid(ctx, n, pts, psi, 0.0, 0.0, g, stream)) return -1;
+    const double *dp = nullptr;
+    int dnf = 0;
+    double tol = 0.0;
+    if (pf_internal_domain_view(ctx, &dp, &dnf, &tol)) return -1;
+    if (m > 0) {
+        pf_internal_launches_add(1);
+        k_traverse<<<(int)((m + 127) / 128 < 8192 ? (m + 127) / 128 : 8192), 128, 0, st>>>(
+            g, psi, psimax, dp, dnf, smf, cell_nf, planes, tags, m, rays, mode, max_seg, 8 * n + 8, out_cell, out_t0,
+            out_t1, out_fluid, count, status);
         RCK(cudaGetLastError());
     }
     RCK(cudaStreamSynchronize(st));

@@ -50,8 +50,9 @@ def _bind():
         L.pf_render_smooth.argtypes = [vp, i64, vp, vp, dbl, dbl, dbl, vp, ci, ci, vp, vp, vp, vp]
         L.pf_smooth_sdf.argtypes = [vp, i64, vp, vp, dbl, dbl, i64, vp, vp, vp]
         L.pf_sample_surface.argtypes = [vp, i64, vp, vp, dbl, i64, vp, vp, C.c_uint64, vp, vp, vp, vp]
+        L.pf_traverse.argtypes = [vp, i64, vp, vp, dbl, ci, vp, vp, vp, i64, vp, ci, ci, vp, vp, vp, vp, vp, vp, vp]
         for f in ("pf_render_first_hit", "pf_render_depth", "pf_render_smooth", "pf_smooth_sdf",
-                  "pf_sample_surface"):
+                  "pf_sample_surface", "pf_traverse"):
             getattr(L, f).restype = C.c_int
         L._render_bound = True
     return L
@@ -101,6 +102,86 @@ def depth(pts, psi, cam: Camera, domain=None):
                                  cp.ctypes.data_as(C.c_void_p), cam.width, cam.height, _lib.ptr(out),
                                  _lib.stream_ptr()), "pf_render_depth")
     return out
+
+
+class Traversal:
+    """Per-ray pieces of a cell-to-cell traversal (SPEC renderer `traverse`):
+    piece k < count[r] of ray r covers [t0[r, k], t1[r, k]] in power cell
+    cell[r, k], inside the fluid when fluid[r, k]; consecutive pieces share
+    end points.  status[r]: 0 ok, 1 the ray misses the domain, 2 the
+    TraversalLoop guard (8 n facet crossings) or the piece capacity."""
+
+    def __init__(self, cell, t0, t1, fluid, count, status):
+        self.cell, self.t0, self.t1, self.fluid, self.count, self.status = cell, t0, t1, fluid, count, status
+
+    def path(self, r: int):
+        """[(cell id, t_enter, t_exit, in_fluid)] of ray r."""
+        k = int(self.count[r])
+        return [(int(self.cell[r, q]), float(self.t0[r, q]), float(self.t1[r, q]), bool(self.fluid[r, q]))
+                for q in range(k)]
+
+    def fluid_length(self):
+        """In-fluid path length of every ray (SPEC Depth before normalisation)."""
+        ln = (self.t1 - self.t0) * self.fluid
+        k = np.arange(self.cell.shape[1])[None, :] < self.count[:, None]
+        return (ln * k).sum(axis=1)
+
+
+def traverse(pts, psi, origins, dirs, mode: str = "volume", max_segments: int = 256, domain=None,
+             diagram=None) -> Traversal:
+    """Cell-to-cell traversal of rays through the unrestricted power diagram
+    (SPEC.md renderer `traverse`; §6: "load the current cell's
+    neighbors and iteratively intersect facets facing the ray" until the
+    domain boundary; "we explore the empty part of the domain through the
+    unrestricted Laguerre diagram").  Within power cell i the fluid part of a
+    ray is its chord of the ball B_i.  mode "volume" runs to the domain exit,
+    "surface" stops after the first exit through a sphere patch.  ``diagram``:
+    a laguerre.PackedDiagram in full mode (built here when None)."""
+    import torch
+
+    from .geom import box_domain
+    from .laguerre import build_diagram_packed
+
+    dom = domain if domain is not None else box_domain([0, 0, 0], [1, 1, 1])
+    pts_h = np.ascontiguousarray(_host_np(pts), np.float64).reshape(-1, 3)
+    psi_h = np.ascontiguousarray(_host_np(psi), np.float64).reshape(-1)
+    if diagram is None:
+        diagram = build_diagram_packed((pts_h, psi_h), dom, ball_aware=False)
+    L = _bind()
+    p, w, _ = _prep(pts_h, psi_h, dom)
+    smf = int(diagram.planes.shape[1])
+    nf = torch.as_tensor(np.where(diagram.status == 0, diagram.nf, 0).astype(np.int32), device="cuda")
+    planes = torch.as_tensor(np.ascontiguousarray(diagram.planes), dtype=torch.float64, device="cuda")
+    tags = torch.as_tensor(np.ascontiguousarray(diagram.tags).astype(np.int32), device="cuda")
+    o = np.asarray(_host_np(origins), np.float64).reshape(-1, 3)
+    d = np.asarray(_host_np(dirs), np.float64).reshape(-1, 3)
+    d = d / np.linalg.norm(d, axis=1, keepdims=True)
+    rays = torch.as_tensor(np.ascontiguousarray(np.concatenate([o, d], axis=1)), device="cuda")
+    m = rays.shape[0]
+    cell = torch.empty((m, max_segments), dtype=torch.int32, device="cuda")
+    t0 = torch.empty((m, max_segments), dtype=torch.float64, device="cuda")
+    t1 = torch.empty((m, max_segments), dtype=torch.float64, device="cuda")
+    fl = torch.empty((m, max_segments), dtype=torch.uint8, device="cuda")
+    cnt = torch.empty(m, dtype=torch.int32, device="cuda")
+    st = torch.empty(m, dtype=torch.int32, device="cuda")
+    psimax = float(psi_h.max()) if len(psi_h) else 0.0
+    _lib.check(L.pf_traverse(_lib.ctx(), p.shape[0], _lib.ptr(p), _lib.ptr(w), psimax, smf, _lib.ptr(nf),
+                             _lib.ptr(planes), _lib.ptr(tags), m, _lib.ptr(rays), 1 if mode == "surface" else 0,
+                             int(max_segments), _lib.ptr(cell), _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(fl),
+                             _lib.ptr(cnt), _lib.ptr(st), _lib.stream_ptr()), "pf_traverse")
+    return Traversal(cell.cpu().numpy(), t0.cpu().numpy(), t1.cpu().numpy(), fl.cpu().numpy().astype(bool),
+                     cnt.cpu().numpy(), st.cpu().numpy())
+
+
+def _host_np(x):
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            return x.detach().cpu().numpy()
+    except ImportError:
+        pass
+    return np.asarray(x)
 
 
 def default_blend(psi) -> float:
