@@ -48,13 +48,22 @@ class Comm:
         self.rank = dist.get_rank(group) if self.on else 0
         self.world = dist.get_world_size(group) if self.on else 1
         self.gloo = self.on and dist.get_backend(group) == "gloo"
+        # PF_DIST_FORCE_COLLECTIVES=1: issue the collectives even with one rank
+        # (tests: drives the NCCL path on a one-GPU box)
+        import os
+
+        self.force = self.on and os.environ.get("PF_DIST_FORCE_COLLECTIVES") == "1"
+
+    def active(self) -> bool:
+        """Whether the exchanges and reductions go through torch.distributed."""
+        return self.on and (self.world > 1 or self.force)
 
     def _staged(self, t):
         return t.cpu() if (self.gloo and t.is_cuda) else t
 
     def all_reduce(self, t, op="sum"):
         """In-place all-reduce of a small tensor (sum or max)."""
-        if not self.on or self.world == 1:
+        if not self.active():
             return t
         d = self.dist
         s = self._staged(t)
@@ -65,7 +74,7 @@ class Comm:
 
     def exchange(self, vec, plan: partition.HaloPlan, idx_send: dict, idx_recv: dict):
         """Fill the ghost entries of `vec` (local-length) from their owners."""
-        if not self.on or self.world == 1 or (not plan.send and not plan.recv):
+        if not self.active() or (not plan.send and not plan.recv):
             return vec
         import torch
 
@@ -86,7 +95,7 @@ class Comm:
         return self.dist.get_global_rank(self.group, q) if self.group is not None else q
 
     def all_gather_objects(self, obj):
-        if not self.on or self.world == 1:
+        if not self.active():
             return [obj]
         out = [None] * self.world
         self.dist.all_gather_object(out, obj, group=self.group)

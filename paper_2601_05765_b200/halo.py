@@ -92,7 +92,7 @@ class SlabComm:
         """Exchange one row block per peer; returns (received rows stacked in
         source-rank order, rows received from each source)."""
         t = self.torch
-        if not self.comm.on or self.world == 1:
+        if not self.comm.active():
             return parts[self.rank], [int(parts[self.rank].shape[0]) if q == self.rank else 0
                                       for q in range(self.world)]
         d = self.comm.dist
@@ -123,7 +123,7 @@ class SlabComm:
             parts.append(self._pack(gid, fields, rows))
         keep = t.nonzero(own == self.rank).flatten()
         got, _ = self._alltoall(parts, width, gid.device)
-        rg, rf = self._unpack(got, layout, fields) if self.world > 1 and self.comm.on else \
+        rg, rf = self._unpack(got, layout, fields) if self.comm.active() else \
             (gid[:0], {k: v[:0] for k, v in fields.items()})
         g2 = t.cat([gid.index_select(0, keep), rg])
         order = t.argsort(g2)
@@ -133,7 +133,7 @@ class SlabComm:
 
     def margins(self, margin_mine: float) -> np.ndarray:
         t = self.torch
-        if not self.comm.on or self.world == 1:
+        if not self.comm.active():
             return np.array([margin_mine])
         dev = "cuda" if (not self.comm.gloo and t.cuda.is_available()) else "cpu"
         m = t.zeros(self.world, dtype=t.float64, device=dev)
@@ -161,7 +161,7 @@ class SlabComm:
             parts.append(self._pack(gid, fields, rows))
         got, cr = self._alltoall(parts, width, dev)
         no = int(gid.numel())
-        if self.world > 1 and self.comm.on:
+        if self.comm.active():
             rg, rf = self._unpack(got, layout, fields)
         else:
             rg, rf = gid[:0], {k: v[:0] for k, v in fields.items()}

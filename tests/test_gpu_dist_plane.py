@@ -98,3 +98,29 @@ def test_two_gpus_nccl(tmp_path):
     mp.start_processes(_worker, args=(2, _free_port(), str(tmp_path), "nccl"), nprocs=2, join=True,
                        start_method="spawn")
     _check(tmp_path, tmp_path / "single.npz")
+
+
+def _worker_one_nccl(rank, port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PF_DIST_FORCE_COLLECTIVES="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    _run(0, 1, out, "cuda")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_one_rank_nccl_collectives(tmp_path):
+    """The data plane's collectives (all_to_all_single of counts and rows for
+    the ghosts and the migration, the all-reduces of the Newton / PCG scalars)
+    over NCCL on the box's one GPU (PF_DIST_FORCE_COLLECTIVES: issued even
+    with one rank): same Newton and fluid results as without torch.distributed."""
+    _run(0, 1, str(tmp_path / "single.npz"), "cuda")
+    mp.start_processes(_worker_one_nccl, args=(_free_port(), str(tmp_path / "nccl.npz")), nprocs=1, join=True,
+                       start_method="spawn")
+    s, d = np.load(tmp_path / "single.npz"), np.load(tmp_path / "nccl.npz")
+    assert int(d["nit"]) == int(s["nit"]) and int(d["nev"]) == int(s["nev"])
+    assert list(d["it"]) == list(s["it"])
+    for k in ("npsi", "x", "v", "psi"):
+        assert np.array_equal(d[k], s[k]), k
