@@ -21,6 +21,8 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -349,6 +351,21 @@ void scatter_rows(int64_t i0, int64_t r0, int64_t r1, const double *dense, const
     }
 }
 
+// Transparent huge pages for the caller's output arrays (a hint; the
+// scatter writes ~1 KB per cell spread over five 0.5-1.5 GB arrays, so 4 KB
+// pages make it TLB bound).  Pages already faulted in keep their size until
+// khugepaged merges them; np.zeros arrays are faulted by our first call.
+void advise_huge(const void *p, size_t bytes) {
+    static const bool on = [] {
+        const char *e = getenv("PF_HOST_THP");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || !p || bytes < ((size_t)8 << 20)) return;
+    const uintptr_t pg = (uintptr_t)sysconf(_SC_PAGESIZE);
+    const uintptr_t a = ((uintptr_t)p + pg - 1) & ~(pg - 1), b = ((uintptr_t)p + bytes) & ~(pg - 1);
+    if (b > a) madvise((void *)a, b - a, MADV_HUGEPAGE);
+}
+
 }  // namespace
 
 extern "C" {
@@ -392,6 +409,12 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
         if (h->totals) cudaFreeHost(h->totals);
         HCK(cudaHostAlloc((void **)&h->totals, K * sizeof(int32_t), cudaHostAllocDefault));
         h->totals_c = K;
+    }
+    {
+        const size_t n1 = (size_t)n * 8, nf8 = (size_t)n * smf * 8;
+        advise_huge(status, n1); advise_huge(vol, n1); advise_huge(ksur, n1); advise_huge(m2, n1);
+        advise_huge(fcount, n1); advise_huge(cent, 3 * n1); advise_huge(ipt, 3 * n1); advise_huge(ftag, nf8);
+        advise_huge(farea, nf8); advise_huge(fh, nf8); advise_huge(fnrm, 3 * nf8); advise_huge(fcent, 3 * nf8);
     }
     cudaStream_t st = h->comp;
     void *sv = (void *)st;
