@@ -2420,6 +2420,28 @@ PF_DEV void mbar_init(unsigned long long *mb) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// the same in two halves: issue (every lane done with A), and wait
+template <class C>
+PF_DEV void poly_load_tma_issue(const Poly<C> *g, Poly<C> &A, unsigned long long *mb) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+    pfw::sync();
+    if (pfw::lane() == 0) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&A);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a),
+                     "r"((unsigned)sizeof(Poly<C>)) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(g), "r"((unsigned)sizeof(Poly<C>)), "r"(a) : "memory");
+    }
+}
+PF_DEV void poly_load_tma_wait(unsigned long long *mb, unsigned &phase) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(phase) : "memory");
+    phase ^= 1u;
+}
 template <class C>
 PF_DEV void poly_load_tma(const Poly<C> *g, Poly<C> &A, unsigned long long *mb, unsigned &phase) {
     static_assert(sizeof(Poly<C>) % 16 == 0, "bulk copy size");

@@ -79,6 +79,10 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
         base = blockIdx.x * SYNC_WARPS;
         nb = base + gridDim.x * SYNC_WARPS;
     }
+#ifndef PF_EARLY_TMA
+#define PF_EARLY_TMA 1
+#endif
+    bool issued = false;  // this round's polytope load was issued at the end of the last round
     int i_nx = -1;  // this warp's next cell (or -1), loaded during the previous round
     if (PF_EVAL_PIPE_IDX) {
         const int t0 = base + wid;
@@ -114,8 +118,14 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
         EvalState st;
         st.done = 1;
         if (act) {
-            if (tma) poly_load_tma(gpoly + i, ws->P[0], &ws->u.e.mbar, phase);
-            else poly_load(gpoly + i, ws->P[0]);
+            if (tma && PF_EARLY_TMA) {
+                if (!issued) poly_load_tma_issue(gpoly + i, ws->P[0], &ws->u.e.mbar);
+                poly_load_tma_wait(&ws->u.e.mbar, phase);
+            } else if (tma) {
+                poly_load_tma(gpoly + i, ws->P[0], &ws->u.e.mbar, phase);
+            } else {
+                poly_load(gpoly + i, ws->P[0]);
+            }
             if (lane == 0) {
                 ws->oflow = 0;
                 ws->strict = in.strict;
@@ -149,6 +159,13 @@ __global__ void __launch_bounds__(SYNC_WARPS * 32, SYNC_BLOCKS)
                 cell_finish(ws, out, i, r);
                 fl |= r & 7;
             }
+        }
+        // the next round's polytope, issued as soon as this warp is done with
+        // the buffer: the copy overlaps the round's barrier and the next setup
+        issued = false;
+        if (tma && PF_EARLY_TMA && PF_EVAL_PIPE_IDX && i_nx >= 0) {
+            poly_load_tma_issue(gpoly + i_nx, ws->P[0], &ws->u.e.mbar);
+            issued = true;
         }
         if (PF_DYN_EVAL && threadIdx.x == 0) s_round = atomicAdd(&counters[3], SYNC_WARPS);  // the round after next
         __syncthreads();
