@@ -389,7 +389,9 @@ int64_t pf_batch_evaluate_host(pf_ctx *ctx, int64_t n, const double *pts_h, cons
         // copies (with every core scattering it was descheduled for ms at a time)
         h->pool = new Pool((int)std::max(1u, std::min(hw ? hw - 1 : 4u, 16u)));
     }
-    const int K = (int)std::max<int64_t>(1, std::min<int64_t>(chunks > 0 ? chunks : 16, std::min<int64_t>(n, 64)));
+    // chunks <= 0: ~12k+ cells per range, 4 to 16 (_kernels.default_chunks)
+    const int64_t kdef = std::min<int64_t>(16, std::max<int64_t>(4, n / 12000));
+    const int K = (int)std::max<int64_t>(1, std::min<int64_t>(chunks > 0 ? chunks : kdef, std::min<int64_t>(n, 64)));
     const size_t n3 = 3 * (size_t)n, nf = (size_t)n * smf;
     if (dev_ensure(&h->pts, &h->pts_c, n3) || dev_ensure(&h->psi, &h->psi_c, n) ||
         dev_ensure(&h->status, &h->status_c, n) || dev_ensure(&h->vol, &h->vol_c, n) ||
