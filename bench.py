@@ -104,9 +104,19 @@ def config_of(a, sc, psi_desc):
             if a.gpus > 1 else "1 GPU"}
 
 
-# Port-vs-numba speed of the CPU baseline, measured in the build container
-# (8 vCPU, 8 threads) on the same kind of workload: tools/port_vs_numba.py.
-PORT_VS_NUMBA = None
+# Speed of the CPU baseline (the C port) against the real numba reference on the
+# same workload and threads, measured in the build container where the reference
+# exists (tools/port_vs_numba.py -> profiles/port_vs_numba.json; C4, 8 threads:
+# numba 59.0 s, port 29.0 s, all outputs bit-identical)
+try:
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "port_vs_numba.json")) as _f:
+        _pvn = json.load(_f)
+    PORT_VS_NUMBA = {"factor": round(_pvn["port_vs_numba"], 3), "config": _pvn["config"], "threads": _pvn["threads"],
+                     "numba_s": round(_pvn["numba_s"], 2), "port_s": round(_pvn["port_s"], 2),
+                     "outputs_identical": _pvn["outputs_identical"],
+                     "source": "profiles/port_vs_numba.json (tools/port_vs_numba.py, build container)"}
+except (OSError, ValueError, KeyError):
+    PORT_VS_NUMBA = None
 
 
 def workload_desc(name, sc):
