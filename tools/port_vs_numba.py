@@ -63,7 +63,7 @@ def main():
     res["outputs_identical"] = bool(all(np.array_equal(a, b) for a, b in zip(o_ref, o_port)))
     res["numba_cells_per_s"] = n / res["numba_s"]
     res["port_cells_per_s"] = n / res["port_s"]
-    out = os.path.join(ROOT, "profiles", "port_vs_numba.json")
+    out = os.path.join(ROOT, "profiles", "port_vs_numba.json" if cfg == "C4" else f"port_vs_numba_{cfg}.json")
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res))
 
