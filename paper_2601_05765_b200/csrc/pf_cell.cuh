@@ -254,6 +254,43 @@ PF_DEV double atan2_ool(double y, double x) { return atan2(y, x); }
 #else
 PF_NOINL double atan2_ool(double y, double x) { return atan2(y, x); }
 #endif
+// Branch-free atan2 for the value-only angles of the evaluation (arc sweeps,
+// Gauss-Bonnet turning angles): one division (the ratio, or its pi/4-reduced
+// form (mn - mx) / (mn + mx) when above tan(pi/8)) and a degree-10 polynomial
+// in t^2 (Chebyshev interpolant of atan(t)/t on [0, tan^2(pi/8)], 7e-17
+// relative); quadrant by selects, sign from y (so t < 0 tests and -0 behave as
+// atan2).  Within ~2 ulp of the library atan2, which keeps its branches for
+// the lanes' different quadrants; zeros / inf / nan go to the library.  The
+// wrap decisions of near-coincident arc end points keep the library atan2.
+#ifndef PF_FAST_ATAN2
+#define PF_FAST_ATAN2 1
+#endif
+PF_DEV double atan2_val(double y, double x) {
+#if PF_FAST_ATAN2
+    const double ax = fabs(x), ay = fabs(y);
+    const double mx = fmax(ax, ay), mn = fmin(ax, ay);
+    if (!(mx > 0.0) || !(mx < 1e300)) return atan2(y, x);
+    const bool red = mn > 0.41421356237309503 * mx;
+    const double t = (red ? mn - mx : mn) / (red ? mn + mx : mx);
+    const double z = t * t;
+    double p = 0.021135373157693246;
+    p = fma(p, z, -0.04348052215716462);
+    p = fma(p, z, 0.056883492268090106);
+    p = fma(p, z, -0.06640233930429408);
+    p = fma(p, z, 0.07689953496306857);
+    p = fma(p, z, -0.09090773074808414);
+    p = fma(p, z, 0.11111106180455946);
+    p = fma(p, z, -0.14285714180976467);
+    p = fma(p, z, 0.1999999999885511);
+    p = fma(p, z, -0.3333333333332844);
+    p = fma(p * z, t, t) + (red ? 0.78539816339744831 : 0.0);
+    if (ay > ax) p = 1.5707963267948966 - p;
+    if (x < 0.0) p = 3.1415926535897931 - p;
+    return copysign(p, y);
+#else
+    return atan2_ool(y, x);
+#endif
+}
 #ifndef PF_HELPER_INL
 #define PF_HELPER_INL 1
 #endif
@@ -1628,7 +1665,7 @@ PF_PHASE void ring_integrals(W *ws, const Poly<typename W::Cap> &P, double px, d
                 const double ir0 = q0 > 0.0 ? rsqrt_nr(q0) : 0.0, ir1 = q1 > 0.0 ? rsqrt_nr(q1) : 0.0;
                 const double c0 = q0 > 0.0 ? x0 * ir0 : 1.0, s0 = y0 * ir0;
                 const double c1 = q1 > 0.0 ? x1 * ir1 : 1.0, s1 = y1 * ir1;
-                double dth = atan2_ool(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
+                double dth = atan2_val(fma(x0, y1, -y0 * x1), fma(x0, x1, y0 * y1));
                 // end points (nearly) coincident: decide the wrap exactly as the
                 // reference does, from the two end-point angles (_kernels.py:696-700)
                 if (fabs(dth) < PF_SWEEP_AMBIG) dth = atan2_ool(y1, x1) - atan2_ool(y0, x0);
@@ -1690,7 +1727,7 @@ PF_DEV double dot3(const double *a, const double *b) { return fma(a[0], b[0], fm
 PF_DEV double ccw_angle(const double *a, const double *b, const double *m) {
     double c[3];
     cross3(a, b, c);
-    double t = atan2_ool(dot3(c, m), dot3(a, b));
+    double t = atan2_val(dot3(c, m), dot3(a, b));
     return t < 0.0 ? t + 2.0 * PF_PI : t;
 }
 PF_DEV void unit3(double *v) {
@@ -1845,7 +1882,7 @@ PF_PHASE void ring_patches(W *ws, const Poly<typename W::Cap> &P, double px, dou
             double cr[3];
             cross3(tin, tout, cr);
             const double nv[3] = {(prq[0] - px) * iR, (prq[1] - py) * iR, (prq[2] - pz) * iR};
-            const double th = atan2_ool(dot3(cr, nv), dot3(tin, tout));
+            const double th = atan2_val(dot3(cr, nv), dot3(tin, tout));
             if (fabs(th) > PF_PI - 1e-7) uns = true;
             term += th;
             unst = uns ? 1.0 : 0.0;
