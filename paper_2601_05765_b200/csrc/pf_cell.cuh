@@ -2111,7 +2111,7 @@ PF_PHASE void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, do
         if (t_hi - t_lo <= tol) continue;
         double tm = 0.5 * (t_lo + t_hi);
         double mx = ox + tm * dx, my = oy + tm * dy, mz = oz + tm * dz;
-        double mg = dsqrt(psi) - dsqrt(sq(mx - px) + sq(my - py) + sq(mz - pz));
+        double mg = st->R - dsqrt(sq(mx - px) + sq(my - py) + sq(mz - pz));  // st->R == dsqrt(psi)
         #pragma unroll 1
         for (int g = 0; g < nf; g++) {
             double d2 = P.d[g] - (P.nx[g] * mx + P.ny[g] * my + P.nz[g] * mz);
@@ -2147,7 +2147,7 @@ PF_PHASE void eval_interior(W *ws, const Poly<typename W::Cap> &P, double px, do
     if (ok) {
         double inv = ddiv(1.0, (double)nseg);
         double cx = sx * inv, cy = sy * inv, cz = sz * inv;
-        double mg = dsqrt(psi) - dsqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
+        double mg = st->R - dsqrt(sq(cx - px) + sq(cy - py) + sq(cz - pz));
         #pragma unroll 1
         for (int g = L; g < nf; g += 32) {
             double d2 = P.d[g] - (P.nx[g] * cx + P.ny[g] * cy + P.nz[g] * cz);
